@@ -1,0 +1,150 @@
+/*
+ * rhg_b200.h — C ABI of the B200-native threshold-RHG generator.
+ *
+ * Drop-in boundary for the reference's stats-only generator path
+ * (/root/reference/proj/include/rhg/):
+ *
+ *   reference                                            this ABI
+ *   ---------------------------------------------------  ----------------------------------
+ *   alpha_from_gamma              geometry.hpp:35-39      rhg_alpha_from_gamma
+ *   radial_const_from_avg_degree  geometry.hpp:26-33      rhg_radial_const_from_avg_degree
+ *   ModelParams(n,alpha,C,seed,P) geometry.hpp:49-67      rhg_params + rhg_params_validate
+ *   ModelParams::from_avg_degree  geometry.hpp:69-72      rhg_params_from_avg_degree
+ *   GenOptions                    generator.hpp:27-32     rhg_create(device) / rhg_shard
+ *   RunStats                      generator.hpp:34-46     rhg_run_stats
+ *   generate_stats(params, opts,  generator.hpp:219-291   rhg_generate_stats
+ *                  degrees*)
+ *   materialize_points / the      oracle.hpp:26-39,       rhg_sample_points (device sampler,
+ *     ChunkPointSource stream     sweep.hpp:102-151         points copied back in id order)
+ *   (parity hook, no ref. twin)                           rhg_count_edges_from_points
+ *
+ * Conventions: plain pointers and sizes, no exceptions across the ABI.
+ * Every call returns RHG_OK (0) or an error code; rhg_last_error() gives the
+ * thread-local message.  The reference's std::invalid_argument maps to
+ * RHG_INVALID_ARGUMENT, std::logic_error (sweep invariants) to RHG_INVARIANT.
+ * A context owns one CUDA device, one stream and its device buffers; it is
+ * not re-entrant.  There is no CPU fallback: without a usable sm_100 device
+ * rhg_create fails with RHG_CUDA.
+ */
+#ifndef RHG_B200_H
+#define RHG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RHG_ABI_VERSION 1
+
+enum {
+    RHG_OK = 0,
+    RHG_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    RHG_INVARIANT = 2,        /* std::logic_error in the reference      */
+    RHG_CUDA = 3,
+    RHG_NOMEM = 4
+};
+
+/* Graph identity: (n, alpha, C, seed, chunks) — geometry.hpp:47-56.
+ * R is derived (R = 2 ln n + C) and filled by rhg_params_validate. */
+typedef struct {
+    uint64_t n;
+    double alpha;
+    double C;
+    uint64_t seed;
+    uint32_t chunks;
+    double R; /* output of rhg_params_validate / from_avg_degree */
+} rhg_params;
+
+/* Which engines (angular chunks) this caller owns: rank r of `world` owns
+ * chunks [r*P/world, (r+1)*P/world) and the global-unit rows of slice r.
+ * {0, 1} = the whole graph (GenOptions default).  Partial results of all
+ * ranks sum (wrapping) to the whole-graph result. */
+typedef struct {
+    uint32_t rank;
+    uint32_t world;
+} rhg_shard;
+
+/* RunStats (generator.hpp:34-46) plus device timing. */
+typedef struct {
+    uint64_t n;
+    uint64_t edges;           /* total.edges                          */
+    uint64_t fingerprint;     /* total.fingerprint, wrapping Σ(u+v)   */
+    uint64_t comps;           /* total.comps (distance computations)  */
+    uint64_t global_vertices; /* n_G                                  */
+    uint64_t streaming_vertices; /* owned streaming points            */
+    uint64_t global_edges, global_comps; /* unit 0 share of this shard */
+    uint32_t annuli, first_streaming;
+    double R, r_G, cosh_R;
+    double device_ms;  /* CUDA-event time, first kernel -> counters ready   */
+    double sample_ms;  /* sampler kernels                                   */
+    double edges_ms;   /* cell index + edge kernels                         */
+    double host_ms;    /* host layout (binomial tree), uploads, launches     */
+    double seconds;    /* wall time of the whole call (RunStats.seconds)    */
+    uint64_t kernel_launches; /* kernels this call launched                 */
+    uint64_t device_bytes;    /* device memory held by the context          */
+} rhg_run_stats;
+
+/* Host point arrays in vertex-id order (n entries each; any may be NULL
+ * where a call documents it as optional). */
+typedef struct {
+    double* beta;       /* sorted begin angle (PointDraw.beta)         */
+    double* r;          /* radius                                       */
+    double* theta;      /* node angle in [0, 2pi)                       */
+    double* half_width; /* request half-width in the home annulus       */
+    double* coth_r;
+    double* inv_sinh_r;
+    double* cos_theta;
+    double* sin_theta;
+} rhg_points;
+
+const char* rhg_last_error(void);
+int rhg_abi_version(void);
+
+/* geometry.hpp:35-39 */
+int rhg_alpha_from_gamma(double gamma, double* alpha);
+/* geometry.hpp:26-33 */
+int rhg_radial_const_from_avg_degree(double d_bar, double alpha, double* C);
+/* geometry.hpp:57-67: validates and fills p->R */
+int rhg_params_validate(rhg_params* p);
+/* geometry.hpp:69-72 */
+int rhg_params_from_avg_degree(uint64_t n, double alpha, double d_bar, uint64_t seed, uint32_t chunks,
+                               rhg_params* out);
+
+typedef struct rhg_ctx rhg_ctx;
+int rhg_create(int device, rhg_ctx** out);
+void rhg_destroy(rhg_ctx* ctx);
+
+/* generator.hpp:219-291 generate_stats.  `degrees` (optional, u32[n],
+ * host) receives exact per-vertex degrees of the edges this shard emits. */
+int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, rhg_run_stats* out,
+                       uint32_t* degrees);
+
+/* The device sampler alone: all n points, id order, copied to host arrays
+ * (every field of `out` must be non-NULL).  Same streams as
+ * ChunkPointSource (sweep.hpp:102-151). */
+int rhg_sample_points(rhg_ctx* ctx, const rhg_params* params, rhg_points* out);
+
+/* Diagnostic: the raw std::mt19937_64 uniforms (x >> 11) * 2^-53 of every
+ * point's angle stream and radius stream (rng.hpp:58-69, seeds
+ * derive_seed(seed, {3|4, annulus, chunk})), in id order, n entries each.
+ * Integer-only, so bit-exact against the reference by construction. */
+int rhg_sample_uniforms(rhg_ctx* ctx, const rhg_params* params, double* u_angle, double* u_radius);
+
+/* Parity hook ("same points" mode): run the device edge kernels on a GIVEN
+ * point set (host arrays, id order; r may be NULL) instead of the device
+ * sampler.  With the reference's own points this must reproduce the
+ * reference's edges / fingerprint / comps bit for bit. */
+int rhg_count_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard,
+                                const rhg_points* pts, rhg_run_stats* out, uint32_t* degrees);
+
+/* Diagnostic (not part of the reference interface): measured non-FMA FP64
+ * DMUL+DADD instruction rate of `device` (the edge kernels' roofline
+ * denominator) and the dependent-DMUL latency in SM cycles. */
+int rhg_fp64_peak(int device, double* ops_per_s, double* dmul_latency_cycles, double* kernel_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RHG_B200_H */

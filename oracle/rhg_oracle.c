@@ -633,6 +633,7 @@ typedef struct {
     int stop, err;
     cstats st;
     uint32_t* degrees;
+    uint64_t* mat; /* optional [home annulus][node annulus] test counts */
 } engine;
 
 static void deg_add(uint32_t* d, uint64_t u, uint64_t v) {
@@ -798,6 +799,7 @@ static void match_node(engine* e, asweep* a, const ntok* nd) {
         }
         if (!act->local[i] && !nd->local) continue;
         ++e->st.comps;
+        if (e->mat) __atomic_fetch_add(&e->mat[(size_t)act->home[i] * e->L->count + nd->annulus], 1, __ATOMIC_RELAXED);
         const double lhs = act->cs[i] * nd->cs + act->sn[i] * nd->sn;
         const double rhs = act->coth[i] * nd->coth - cosh_R * act->inv[i] * nd->inv;
         if (lhs > rhs) {
@@ -888,6 +890,7 @@ typedef struct {
     uint32_t w, W;
     cstats st, gst;
     uint32_t* degrees;
+    uint64_t* mat;
     int err;
     char errmsg[256];
 } unit_job;
@@ -916,6 +919,7 @@ static void* unit_worker(void* arg) {
     for (uint32_t c = j->w; c < L->chunks; c += j->W) {
         engine e;
         engine_init(&e, L, j->P, c, j->degrees);
+        e.mat = j->mat;
         for (uint64_t g = 0; g < j->g_end; ++g) {
             /* global point g's home annulus */
             uint32_t home = 0;
@@ -946,6 +950,7 @@ static double now_s(void) {
     return ts.tv_sec + 1e-9 * ts.tv_nsec;
 }
 
+static uint64_t* g_mat = NULL; /* diagnostics only (orc_comps_matrix) */
 static int run_units(const layout_t* L, const pts_t* P, uint32_t threads, orc_stats* out, uint32_t* degrees) {
     const uint64_t nG = L->first_streaming < L->count ? L->id_base[(size_t)L->first_streaming * L->chunks] : L->n;
     const uint32_t ns = L->count - L->first_streaming;
@@ -959,7 +964,7 @@ static int run_units(const layout_t* L, const pts_t* P, uint32_t threads, orc_st
     unit_job* jobs = calloc(threads, sizeof(unit_job));
     for (uint32_t w = 0; w < threads; ++w) {
         jobs[w].L = L, jobs[w].P = P, jobs[w].g_end = nG, jobs[w].ghw = ghw, jobs[w].ns = ns, jobs[w].w = w,
-        jobs[w].W = threads, jobs[w].degrees = degrees;
+        jobs[w].W = threads, jobs[w].degrees = degrees, jobs[w].mat = g_mat;
         pthread_create(&th[w], NULL, unit_worker, &jobs[w]);
     }
     memset(out, 0, sizeof *out);
@@ -1027,5 +1032,17 @@ int orc_count_edges_from_points(uint64_t n, double alpha, double C, uint64_t see
     rc = run_units(&L, &P, threads, out, degrees);
     layout_free(&L);
     out->seconds = now_s() - t0;
+    return rc;
+}
+
+/* Diagnostics: distance computations per (request home annulus, node
+ * annulus) of the chunk sweeps; mat must hold annuli*annuli u64 (query the
+ * annulus count with orc_layout first).  Not thread-safe across calls. */
+int orc_comps_matrix(uint64_t n, double alpha, double C, uint64_t seed, uint32_t chunks, uint32_t threads,
+                     uint64_t* mat) {
+    orc_stats st;
+    g_mat = mat;
+    int rc = orc_generate_stats(n, alpha, C, seed, chunks, threads, &st, NULL);
+    g_mat = NULL;
     return rc;
 }

@@ -70,6 +70,10 @@ int orc_count_edges_from_points(uint64_t n, double alpha, double C, uint64_t see
                                 const double* cos_theta, const double* sin_theta, orc_stats* out,
                                 uint32_t* degrees);
 
+/* Diagnostics: chunk-sweep tests per (request home annulus, node annulus). */
+int orc_comps_matrix(uint64_t n, double alpha, double C, uint64_t seed, uint32_t chunks, uint32_t threads,
+                     uint64_t* mat);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,259 @@
+"""B200-native threshold random hyperbolic graph generator (sm_100a).
+
+Host-side mirror of the reference's stats-only generator interface
+(/root/reference/proj/include/rhg/geometry.hpp, generator.hpp): same names,
+same argument meaning, same exceptions (ValueError for the reference's
+std::invalid_argument, RuntimeError for std::logic_error).  All work runs in
+librhg_b200.so (C ABI, include/rhg_b200.h) on the GPU; there is no CPU path.
+
+    >>> import paper_1710_07565_b200 as rhg
+    >>> p = rhg.ModelParams.from_avg_degree(1 << 20, rhg.alpha_from_gamma(3.0), 16.0, seed=1, chunks=8)
+    >>> st = rhg.generate_stats(p)
+    >>> st.total.edges, st.total.fingerprint
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native
+from ._native import RhgCudaError, check, lib
+
+__all__ = ["alpha_from_gamma", "gamma_from_alpha", "radial_const_from_avg_degree", "radius_from_size",
+           "expected_avg_degree", "ModelParams", "GenOptions", "ChunkStats", "RunStats", "generate_stats",
+           "sample_points", "sample_uniforms", "fp64_peak", "count_edges_from_points", "Points", "RhgCudaError", "two_pi"]
+
+two_pi = 6.283185307179586476925286766559  # geometry.hpp:11
+
+
+def alpha_from_gamma(gamma: float) -> float:
+    """geometry.hpp:35-39 — raises ValueError unless gamma > 2."""
+    out = C.c_double()
+    check(lib().rhg_alpha_from_gamma(float(gamma), C.byref(out)))
+    return out.value
+
+
+def gamma_from_alpha(alpha: float) -> float:
+    """geometry.hpp:41-45."""
+    if not alpha > 0.5:
+        raise ValueError("gamma_from_alpha: alpha must be > 1/2")
+    return 2.0 * alpha + 1.0
+
+
+def radial_const_from_avg_degree(d_bar: float, alpha: float) -> float:
+    """geometry.hpp:26-33 — the C that yields average degree d_bar."""
+    out = C.c_double()
+    check(lib().rhg_radial_const_from_avg_degree(float(d_bar), float(alpha), C.byref(out)))
+    return out.value
+
+
+def radius_from_size(n: float, C_: float) -> float:
+    """geometry.hpp:14-17: R = 2 ln n + C."""
+    return 2.0 * math.log(n) + C_
+
+
+def expected_avg_degree(C_: float, alpha: float) -> float:
+    """geometry.hpp:20-23 (leading order)."""
+    q = alpha / (alpha - 0.5)
+    return 2.0 / math.pi * q * q * math.exp(-C_ / 2.0)
+
+
+class ModelParams:
+    """geometry.hpp:49-73: (n, alpha, C, seed, chunks) pin the graph; R derived."""
+
+    __slots__ = ("n", "alpha", "C", "R", "seed", "chunks")
+
+    def __init__(self, n: int, alpha: float, C_: float, seed: int, chunks: int):
+        p = _native.rhg_params(int(n), float(alpha), float(C_), int(seed), int(chunks), 0.0)
+        if int(n) < 0 or int(chunks) < 0 or int(chunks) >= 1 << 32:
+            raise ValueError("ModelParams: n and chunks must be non-negative integers")
+        check(lib().rhg_params_validate(C.byref(p)))
+        self.n, self.alpha, self.C, self.R, self.seed, self.chunks = p.n, p.alpha, p.C, p.R, p.seed, p.chunks
+
+    @classmethod
+    def from_avg_degree(cls, n: int, alpha: float, d_bar: float, seed: int, chunks: int) -> "ModelParams":
+        return cls(n, alpha, radial_const_from_avg_degree(d_bar, alpha), seed, chunks)
+
+    def _c(self) -> _native.rhg_params:
+        return _native.rhg_params(self.n, self.alpha, self.C, self.seed, self.chunks, self.R)
+
+    def __repr__(self):
+        return (f"ModelParams(n={self.n}, alpha={self.alpha!r}, C={self.C!r}, seed={self.seed}, "
+                f"chunks={self.chunks}, R={self.R!r})")
+
+
+@dataclass
+class GenOptions:
+    """generator.hpp:27-32.  `workers` and `cell_target` are accepted for
+    interface parity; neither changes the graph (the reference guarantees the
+    same).  `device` picks the GPU; `rank`/`world` select an engine shard
+    (chunks [rank*P/world, (rank+1)*P/world)) for multi-GPU runs."""
+    workers: int = 0
+    cell_target: int = 8
+    device: int = 0
+    rank: int = 0
+    world: int = 1
+
+
+@dataclass
+class ChunkStats:
+    """sweep.hpp:154-177 (totals only)."""
+    edges: int = 0
+    comps: int = 0
+    streaming_vertices: int = 0
+    fingerprint: int = 0
+
+
+@dataclass
+class RunStats:
+    """generator.hpp:34-46, plus device timing of this call."""
+    n: int = 0
+    global_vertices: int = 0
+    r_G: float = 0.0
+    total: ChunkStats = field(default_factory=ChunkStats)
+    seconds: float = 0.0
+    R: float = 0.0
+    annuli: int = 0
+    first_streaming: int = 0
+    global_edges: int = 0
+    global_comps: int = 0
+    device_ms: float = 0.0
+    sample_ms: float = 0.0
+    edges_ms: float = 0.0
+    host_ms: float = 0.0
+    kernel_launches: int = 0
+    device_bytes: int = 0
+    degrees: Optional[np.ndarray] = None
+
+    def avg_degree(self) -> float:
+        return 2.0 * self.total.edges / self.n if self.n else 0.0
+
+    def overestimation_ratio(self) -> float:
+        return self.total.comps / max(self.total.edges, 1)
+
+    @classmethod
+    def _from_c(cls, s: _native.rhg_run_stats) -> "RunStats":
+        return cls(n=s.n, global_vertices=s.global_vertices, r_G=s.r_G,
+                   total=ChunkStats(s.edges, s.comps, s.streaming_vertices, s.fingerprint), seconds=s.seconds,
+                   R=s.R, annuli=s.annuli, first_streaming=s.first_streaming, global_edges=s.global_edges,
+                   global_comps=s.global_comps, device_ms=s.device_ms, sample_ms=s.sample_ms, edges_ms=s.edges_ms,
+                   host_ms=s.host_ms, kernel_launches=s.kernel_launches, device_bytes=s.device_bytes)
+
+
+class _Context:
+    """One rhg_ctx (CUDA stream + device buffers) per device, reused."""
+
+    _lock = threading.Lock()
+    _ctx: dict = {}
+
+    @classmethod
+    def get(cls, device: int) -> C.c_void_p:
+        with cls._lock:
+            h = cls._ctx.get(device)
+            if h is None:
+                h = C.c_void_p()
+                check(lib().rhg_create(int(device), C.byref(h)))
+                cls._ctx[device] = h
+            return h
+
+    @classmethod
+    def release_all(cls):
+        with cls._lock:
+            for h in cls._ctx.values():
+                lib().rhg_destroy(h)
+            cls._ctx.clear()
+
+
+def _shard(opts: GenOptions) -> _native.rhg_shard:
+    return _native.rhg_shard(int(opts.rank), int(opts.world))
+
+
+def generate_stats(params: ModelParams, opts: GenOptions = GenOptions(), degrees: bool = False) -> RunStats:
+    """generator.hpp:219-291: edge count, wrapping Σ(u+v) fingerprint and
+    distance computations of the graph (or of this shard), on the GPU.  With
+    degrees=True, RunStats.degrees is the exact u32 per-vertex degree."""
+    ctx = _Context.get(opts.device)
+    st = _native.rhg_run_stats()
+    deg = np.zeros(params.n, np.uint32) if degrees else None
+    check(lib().rhg_generate_stats(ctx, C.byref(params._c()), C.byref(_shard(opts)), C.byref(st),
+                                   deg.ctypes.data_as(C.POINTER(C.c_uint32)) if degrees else None))
+    out = RunStats._from_c(st)
+    out.degrees = deg
+    return out
+
+
+@dataclass
+class Points:
+    """All n vertices in id order (PointDraw fields, sweep.hpp:89-97)."""
+    beta: np.ndarray
+    r: np.ndarray
+    theta: np.ndarray
+    half_width: np.ndarray
+    coth_r: np.ndarray
+    inv_sinh_r: np.ndarray
+    cos_theta: np.ndarray
+    sin_theta: np.ndarray
+
+    FIELDS = ("beta", "r", "theta", "half_width", "coth_r", "inv_sinh_r", "cos_theta", "sin_theta")
+
+    def _c(self) -> _native.rhg_points:
+        arrs = {}
+        for k in self.FIELDS:
+            a = getattr(self, k)
+            if a is None:
+                arrs[k] = None
+                continue
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                a = np.ascontiguousarray(a, np.float64)
+                setattr(self, k, a)
+            arrs[k] = a.ctypes.data_as(_native.P_f64)
+        return _native.rhg_points(*[arrs[k] for k in self.FIELDS])
+
+
+def sample_points(params: ModelParams, opts: GenOptions = GenOptions()) -> Points:
+    """The device sampler's point set (ChunkPointSource streams, sweep.hpp:102-141)."""
+    ctx = _Context.get(opts.device)
+    pts = Points(*[np.empty(params.n, np.float64) for _ in Points.FIELDS])
+    check(lib().rhg_sample_points(ctx, C.byref(params._c()), C.byref(pts._c())))
+    return pts
+
+
+def sample_uniforms(params: ModelParams, opts: GenOptions = GenOptions()):
+    """Raw MT19937-64 uniforms of every point's (angle, radius) streams, id order."""
+    ctx = _Context.get(opts.device)
+    ua, ur = np.empty(params.n, np.float64), np.empty(params.n, np.float64)
+    check(lib().rhg_sample_uniforms(ctx, C.byref(params._c()), ua.ctypes.data_as(_native.P_f64),
+                                    ur.ctypes.data_as(_native.P_f64)))
+    return ua, ur
+
+
+def fp64_peak(device: int = 0):
+    """Measured non-FMA FP64 DMUL+DADD rate (ops/s), dependent-DMUL latency (cycles), probe ms."""
+    a, b, c = C.c_double(), C.c_double(), C.c_double()
+    check(lib().rhg_fp64_peak(int(device), C.byref(a), C.byref(b), C.byref(c)))
+    return a.value, b.value, c.value
+
+
+def count_edges_from_points(params: ModelParams, points, opts: GenOptions = GenOptions(),
+                            degrees: bool = False) -> RunStats:
+    """Parity hook: run the device edge kernels on a given point set (any
+    object with the Points fields; r optional)."""
+    ctx = _Context.get(opts.device)
+    pts = Points(*[getattr(points, k, None) for k in Points.FIELDS])
+    for k in Points.FIELDS:
+        a = getattr(pts, k)
+        if k != "r" and (a is None or len(a) != params.n):
+            raise ValueError(f"count_edges_from_points: field {k} must have n entries")
+    st = _native.rhg_run_stats()
+    deg = np.zeros(params.n, np.uint32) if degrees else None
+    check(lib().rhg_count_edges_from_points(ctx, C.byref(params._c()), C.byref(_shard(opts)),
+                                            C.byref(pts._c()), C.byref(st),
+                                            deg.ctypes.data_as(C.POINTER(C.c_uint32)) if degrees else None))
+    out = RunStats._from_c(st)
+    out.degrees = deg
+    return out

@@ -1,0 +1,95 @@
+// Shared device definitions for the B200 (sm_100a) threshold-RHG kernels.
+//
+// Every arithmetic step that the reference performs in FP64 with plain
+// IEEE rounding and NO fused multiply-add (proj/CMakeLists.txt: -O3, no
+// -march) is written with __dmul_rn / __dadd_rn / __dsub_rn, which nvcc
+// never contracts into DFMA; the TUs are also compiled with --fmad=false.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rhgb {
+
+constexpr double kTwoPiD = 6.283185307179586476925286766559; // geometry.hpp:11
+constexpr double kPiD    = 3.14159265358979323846;           // M_PI
+
+// Per-annulus constants (partition.hpp:42-45) plus this shard's extended
+// point-array geometry for streaming annuli.
+struct AnnulusDev {
+    double lower, coth_lower, cris, cal, cau; // cris = cosh(R)/sinh(lower)
+    // streaming annuli only:
+    std::uint64_t off, halo, end;      // [off, halo) owned chunks, [halo, end) halo chunk
+    std::int64_t  dlt0, dlt1;          // id = idx + dlt0 (idx < halo) else idx + dlt1
+    double        cell_origin, cell_inv_w;
+    std::uint64_t cell_off;            // into the cell-start table
+    std::uint32_t ncells, pad;
+};
+
+// One sorted-uniform / radius stream pair = one (annulus, chunk) point
+// source (sweep.hpp:102-111), written to [out_off, out_off + count).
+struct StreamJob {
+    std::uint64_t out_off, count;
+    std::uint64_t seed_ang, seed_rad; // derive_seed(seed, {3|4, annulus, chunk})
+    double        a, b;               // chunk angular bounds (sweep.hpp:80-85)
+    std::uint32_t annulus, lift;      // lift: halo copy of chunk 0 seen from chunk P-1
+    std::uint32_t chunk, pad;
+};
+
+// Work list of the pair kernels: requests of annulus `a` (or the global
+// points, a = -1) against nodes of annulus `j`, in batches of 32 requests.
+struct PairJob {
+    std::uint64_t warp_begin;   // prefix over jobs
+    std::uint64_t req_off, req_end;
+    std::int32_t  a, j;
+};
+
+// A candidate list too long for one warp's inline pass (> kLongSeg nodes):
+// deferred to long_pairs_kernel, which splits it into kLongChunk-node chunks
+// spread evenly over the whole GPU.
+struct LongSeg {
+    double             cs, sn, coth, rci;
+    unsigned long long tkey, id, lo, hi;
+    std::uint64_t      c0, c1, chunk_base;
+    std::int32_t       j, same;
+};
+constexpr std::uint64_t kLongSeg   = 2048;
+constexpr std::uint64_t kLongChunk = 256;
+constexpr int           kCtrShift  = 40; // long counter: segments << 40 | chunks
+
+// A dense warp tile too large to run inline: 32 requests starting at p0 of
+// pair job `job` against nodes [u0, u1) of its target annulus.
+struct TileTask {
+    std::uint64_t p0, u0, u1;
+    std::int64_t  job;
+};
+
+struct Counters { // one per edge-producing kernel family
+    unsigned long long edges, fp, comps;
+};
+
+__device__ __forceinline__ double fmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double fadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double fsub(double a, double b) { return __dsub_rn(a, b); }
+
+// sweep.hpp:60-67 request_half_width_raw; acos branch via CUDA libm.
+__device__ __forceinline__ double request_half_width(double coth_r, double inv_r, double coth_b, double cris_b) {
+    const double arg = fsub(fmul(coth_r, coth_b), fmul(cris_b, inv_r));
+    if (arg <= -1.0) return kPiD;
+    if (arg >= 1.0) return 0.0;
+    return acos(arg);
+}
+// sweep.hpp:365-370 half_width_in
+__device__ __forceinline__ double half_width_in(const AnnulusDev& A, double coth_r, double inv_r) {
+    if (A.lower <= 0.0) return kPiD;
+    return request_half_width(coth_r, inv_r, A.coth_lower, A.cris);
+}
+
+// Order-preserving key of a non-negative double (window bounds are clamped
+// at +0 first; node angles are always >= +0): integer compares replace FP64
+// compares in the pair loops, keeping the FP64 pipe for the predicate.
+__device__ __forceinline__ unsigned long long nonneg_key(double x) {
+    return x > 0.0 ? static_cast<unsigned long long>(__double_as_longlong(x)) : 0ull;
+}
+
+} // namespace rhgb

@@ -1,0 +1,67 @@
+// Host-visible launch interfaces of the device kernels (sampler.cu, edges.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace rhgb {
+
+struct SamplerArgs {
+    const StreamJob*  jobs = nullptr;
+    int               njobs = 0;
+    const AnnulusDev* ann   = nullptr;
+    double            alpha = 1.0;
+    std::uint64_t     total = 0; // points (streaming extended arrays + global points)
+    double*           beta  = nullptr;
+    double*           hw    = nullptr;
+    double2*          rec0  = nullptr; // (lambda, theta)
+    double2*          rec1  = nullptr; // (cos theta, sin theta)
+    double2*          rec2  = nullptr; // (coth r, 1/sinh r)
+    double*           r_out = nullptr;             // optional: radius
+    double*           beta_unlifted_out = nullptr; // optional: raw beta
+};
+
+void launch_sampler(const SamplerArgs& a, cudaStream_t st, std::uint64_t* launches);
+void launch_frames_from_points(const SamplerArgs& a, cudaStream_t st, std::uint64_t* launches);
+void launch_mt_uniforms(const SamplerArgs& a, cudaStream_t st, std::uint64_t* launches);
+
+struct EdgeArgs {
+    const AnnulusDev* ann = nullptr;
+    int               count = 0, first_streaming = 0;
+    std::uint64_t     n_ext = 0;   // streaming extended points; global points follow
+    std::uint64_t     n_glob = 0;  // global points (ids 0..n_glob-1)
+    const double*     beta = nullptr;
+    const double*     hw   = nullptr;
+    const double2*    rec0 = nullptr;
+    const double2*    rec1 = nullptr;
+    const double2*    rec2 = nullptr;
+    std::uint64_t*    cellstart = nullptr;
+    unsigned long long* dmax_bits = nullptr; // per annulus, max half-width (bits)
+    double            cosh_R = 1.0;
+    double            chunk0_upper = 0.0; // chunk_upper_bound(0, P)
+    int               lift_part = 0;      // shard owns engine P-1 (halo = lifted chunk 0)
+    const PairJob*    stream_jobs = nullptr;
+    int               n_stream_jobs = 0;
+    std::uint64_t     stream_warps = 0;
+    const PairJob*    glob_jobs = nullptr;
+    int               n_glob_jobs = 0;
+    std::uint64_t     glob_warps = 0;
+    std::uint64_t     gg_tile_begin = 0, gg_tile_end = 0; // this shard's global-unit tiles
+    TileTask*         tasks = nullptr;
+    std::uint64_t     task_cap = 0;
+    unsigned long long* task_ctr = nullptr;
+    LongSeg*          long_segs = nullptr;
+    std::uint64_t     long_cap  = 0;
+    unsigned long long* long_ctr = nullptr;
+    Counters*         ctr = nullptr; // [0] streaming, [1] global requests, [2] global unit
+    unsigned int*     degrees = nullptr;
+};
+
+void launch_cell_index(const EdgeArgs& a, std::uint64_t ncells_total, cudaStream_t st, std::uint64_t* launches);
+void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches);
+
+constexpr int kGGTile = 128;
+
+} // namespace rhgb

@@ -1,0 +1,263 @@
+// Device point sampler (sm_100a): the reference's ChunkPointSource
+// (sweep.hpp:102-141) for every (annulus, chunk) stream of a shard.
+//
+//   S1 mt_uniforms_kernel   one warp per (stream, {angles, radii}): std::mt19937_64
+//                           seeded by derive_seed(seed,{3|4,i,c}) (rng.hpp:41-69),
+//                           312-word twist done warp-parallel in shared memory,
+//                           output (x >> 11) * 2^-53 written coalesced.
+//   S2 point_radial_kernel  per point: x_k = pow(U_k, 1/remaining) for the
+//                           sorted stream (rng.hpp:221), and the radius-only
+//                           attributes r, coth r, 1/sinh r, half-width
+//                           (partition.hpp:64-70, sweep.hpp:121-134).
+//   S3 sorted_chain_kernel  one thread per angle stream: the serial product
+//                           chain cur *= x_k, beta = a + w (1 - cur), clamp
+//                           (rng.hpp:218-229) — the only serial dependency.
+//   S4 point_angular_kernel per point: theta = beta + hw (mod 2pi), cos, sin,
+//                           engine-frame beta/lambda (sweep.hpp:135-139, 478-480).
+//
+// All exact-rounding steps use __dmul_rn/__dadd_rn (no FMA contraction).
+#include "device.cuh"
+#include "kernels.hpp"
+
+namespace rhgb {
+
+namespace {
+
+constexpr int kMtN = 312, kMtM = 156;
+
+__device__ __forceinline__ std::uint64_t mt_temper(std::uint64_t y) {
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    return y ^ (y >> 43);
+}
+__device__ __forceinline__ std::uint64_t mt_mix(std::uint64_t cur, std::uint64_t nxt, std::uint64_t far) {
+    const std::uint64_t x = (cur & 0xFFFFFFFF80000000ull) | (nxt & 0x7FFFFFFFull);
+    return far ^ (x >> 1) ^ ((x & 1ull) ? 0xB5026F5AA96619E9ull : 0ull);
+}
+
+// Warp-parallel regeneration of the 312-word state, equal to the sequential
+// in-place twist of [rand.predef] mersenne_twister_engine.
+__device__ __forceinline__ void mt_twist_warp(std::uint64_t* mt, int lane) {
+    std::uint64_t nv[5];
+    // words 0..155 read only old words
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = lane + 32 * k;
+        if (i < kMtN - kMtM) nv[k] = mt_mix(mt[i], mt[i + 1], mt[i + kMtM]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = lane + 32 * k;
+        if (i < kMtN - kMtM) mt[i] = nv[k];
+    }
+    __syncwarp();
+    // words 156..310 read new words i-156 and old words i, i+1
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = kMtN - kMtM + lane + 32 * k;
+        if (i < kMtN - 1) nv[k] = mt_mix(mt[i], mt[i + 1], mt[i - (kMtN - kMtM)]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = kMtN - kMtM + lane + 32 * k;
+        if (i < kMtN - 1) mt[i] = nv[k];
+    }
+    __syncwarp();
+    if (lane == 0) mt[kMtN - 1] = mt_mix(mt[kMtN - 1], mt[0], mt[kMtM - 1]);
+    __syncwarp();
+}
+
+constexpr int kMtWarps = 4;
+
+__global__ void __launch_bounds__(32 * kMtWarps) mt_uniforms_kernel(const StreamJob* __restrict__ jobs, int njobs,
+                                                                     double* __restrict__ u_ang,
+                                                                     double* __restrict__ u_rad) {
+    __shared__ std::uint64_t state[kMtWarps][kMtN];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gw   = blockIdx.x * kMtWarps + warp;
+    if (gw >= 2 * njobs) return;
+    const StreamJob& J   = jobs[gw >> 1];
+    const bool       ang = (gw & 1) == 0;
+    double*          out = (ang ? u_ang : u_rad) + J.out_off;
+    std::uint64_t*   mt  = state[warp];
+    if (J.count == 0) return;
+    if (lane == 0) { // [rand.predef] seeding recurrence (serial by definition)
+        std::uint64_t x = ang ? J.seed_ang : J.seed_rad;
+        mt[0]           = x;
+        for (int i = 1; i < kMtN; ++i) {
+            x     = 6364136223846793005ull * (x ^ (x >> 62)) + std::uint64_t(i);
+            mt[i] = x;
+        }
+    }
+    __syncwarp();
+    for (std::uint64_t base = 0; base < J.count; base += kMtN) {
+        mt_twist_warp(mt, lane);
+        const std::uint64_t left = J.count - base;
+        const int           nout = left < kMtN ? int(left) : kMtN;
+        for (int i = lane; i < nout; i += 32) out[base + i] = double(mt_temper(mt[i]) >> 11) * 0x1.0p-53;
+        __syncwarp();
+    }
+}
+
+__device__ __forceinline__ int find_job(const StreamJob* __restrict__ jobs, int njobs, std::uint64_t i) {
+    int lo = 0, hi = njobs - 1; // last job with out_off <= i
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (jobs[mid].out_off <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void point_radial_kernel(const StreamJob* __restrict__ jobs, int njobs, const AnnulusDev* __restrict__ ann,
+                                    double alpha, std::uint64_t total, double* __restrict__ u_ang,
+                                    double* __restrict__ hw_out, double2* __restrict__ rec2, double* __restrict__ r_out) {
+    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const StreamJob& J = jobs[find_job(jobs, njobs, i)];
+    const std::uint64_t k = i - J.out_off;
+    // rng.hpp:221: cur_max *= pow(U, 1.0 / remaining), remaining = count - k
+    const double rem = double(J.count - k);
+    u_ang[i]         = pow(u_ang[i], __ddiv_rn(1.0, rem));
+    // partition.hpp:64-70 radius_from_uniform
+    const AnnulusDev& A = ann[J.annulus];
+    const double      u = hw_out[i];
+    const double      c = fadd(A.cal, fmul(u, fsub(A.cau, A.cal)));
+    double            r = __ddiv_rn(acosh(c < 1.0 ? 1.0 : c), alpha);
+    r                   = r > 1e-12 ? r : 1e-12;
+    // sweep.hpp:125-134
+    const double ex   = exp(r);
+    const double mex  = __ddiv_rn(1.0, ex);
+    const double sh   = fmul(0.5, fsub(ex, mex));
+    const double coth = __ddiv_rn(fmul(0.5, fadd(ex, mex)), sh);
+    const double inv  = __ddiv_rn(1.0, sh);
+    hw_out[i]         = A.lower > 0.0 ? request_half_width(coth, inv, A.coth_lower, A.cris) : kPiD;
+    rec2[i]           = make_double2(coth, inv);
+    if (r_out) r_out[i] = r;
+}
+
+// rng.hpp:218-229.  One warp per stream: the 32 lanes stage the pow
+// factors (coalesced, next tile prefetched into registers), then every lane
+// runs the identical serial chain cur = fl(cur * x_k) over the tile — values
+// arrive by shuffle, so the loop-carried dependency is one DMUL per point —
+// and lane k%32 keeps beta_k for a coalesced store.
+__global__ void __launch_bounds__(128) sorted_chain_kernel(const StreamJob* __restrict__ jobs, int njobs,
+                                                           double* __restrict__ x) {
+    const int lane = threadIdx.x & 31;
+    const int w    = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (w >= njobs) return;
+    const StreamJob&    J = jobs[w];
+    double*             p = x + J.out_off;
+    const std::uint64_t n = J.count;
+    const double        a = J.a, b = J.b, wd = fsub(b, a);
+    const double        bmax = nextafter(b, a);
+    constexpr int       kQ   = 8; // tile = 32 * kQ points
+    double              cur  = 1.0;
+    double              nxt[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+        const std::uint64_t k = std::uint64_t(lane) + 32u * q;
+        nxt[q]                = k < n ? p[k] : 1.0;
+    }
+    for (std::uint64_t base = 0; base < n; base += 32 * kQ) {
+        double v[kQ], out[kQ];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) v[q] = nxt[q];
+        const std::uint64_t nb = base + 32 * kQ;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) { // prefetch the next tile while the chain runs
+            const std::uint64_t k = nb + std::uint64_t(lane) + 32u * q;
+            nxt[q]                = k < n ? p[k] : 1.0;
+        }
+        // past-the-end factors are 1.0: fl(cur * 1.0) == cur, so the tail
+        // needs no branch and the shuffles can all be hoisted.
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            double xs[32];
+#pragma unroll
+            for (int L = 0; L < 32; ++L) xs[L] = __shfl_sync(0xffffffffu, v[q], L);
+            double mine = 1.0;
+#pragma unroll
+            for (int L = 0; L < 32; ++L) {
+                cur  = fmul(cur, xs[L]);
+                mine = lane == L ? cur : mine;
+            }
+            const double y = fadd(a, fmul(wd, fsub(1.0, mine)));
+            out[q]         = y >= b ? bmax : y;
+        }
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            const std::uint64_t k = base + std::uint64_t(lane) + 32u * q;
+            if (k < n) p[k] = out[q];
+        }
+    }
+}
+
+// sweep.hpp:135-139 + 478-480: node angle, trig, engine-frame begin/centre.
+__global__ void point_angular_kernel(const StreamJob* __restrict__ jobs, int njobs, std::uint64_t total,
+                                     double* __restrict__ beta, const double* __restrict__ hw,
+                                     double2* __restrict__ rec0, double2* __restrict__ rec1,
+                                     double* __restrict__ theta_out) {
+    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const StreamJob& J  = jobs[find_job(jobs, njobs, i)];
+    const double     b0 = beta[i];
+    const double     h  = hw[i];
+    double           th = fadd(b0, h);
+    if (th >= kTwoPiD) th = fsub(th, kTwoPiD);
+    double s, c;
+    sincos(th, &s, &c);
+    const double bf = J.lift ? fadd(b0, kTwoPiD) : b0;
+    rec0[i]         = make_double2(fadd(bf, h), th);
+    rec1[i]         = make_double2(c, s);
+    if (theta_out) theta_out[i] = b0; // unlifted beta for point export
+    beta[i] = bf;
+}
+
+// "Same points" mode: given uploaded beta(unlifted)/hw/theta/cos/sin, build
+// the engine frames exactly as S4 does (no libm involved).
+__global__ void frames_from_points_kernel(const StreamJob* __restrict__ jobs, int njobs, std::uint64_t total,
+                                          double* __restrict__ beta, const double* __restrict__ hw,
+                                          double2* __restrict__ rec0) {
+    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const StreamJob& J  = jobs[find_job(jobs, njobs, i)];
+    const double     b0 = beta[i];
+    const double     bf = J.lift ? fadd(b0, kTwoPiD) : b0;
+    rec0[i].x           = fadd(bf, hw[i]);
+    beta[i]             = bf;
+}
+
+} // namespace
+
+void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
+    if (S.total == 0 || S.njobs == 0) return;
+    const int mt_blocks = (2 * S.njobs + kMtWarps - 1) / kMtWarps;
+    mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw);
+    const unsigned pblocks = unsigned((S.total + 255) / 256);
+    point_radial_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.beta, S.hw, S.rec2,
+                                                 S.r_out);
+    sorted_chain_kernel<<<(S.njobs + 3) / 4, 128, 0, st>>>(S.jobs, S.njobs, S.beta);
+    point_angular_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.total, S.beta, S.hw, S.rec0, S.rec1,
+                                                  S.beta_unlifted_out);
+    *launches += 4;
+}
+
+void launch_mt_uniforms(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
+    if (S.total == 0 || S.njobs == 0) return;
+    const int mt_blocks = (2 * S.njobs + kMtWarps - 1) / kMtWarps;
+    mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw);
+    *launches += 1;
+}
+
+void launch_frames_from_points(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
+    if (S.total == 0 || S.njobs == 0) return;
+    const unsigned pblocks = unsigned((S.total + 255) / 256);
+    frames_from_points_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.total, S.beta, S.hw, S.rec0);
+    *launches += 1;
+}
+
+} // namespace rhgb

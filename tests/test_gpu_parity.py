@@ -1,0 +1,156 @@
+"""Parity of the B200 path (through the C ABI) with the reference.
+
+* "same points" mode: the device edge kernels run on the reference's point
+  set (the oracle's points are bit-identical to the reference's — pinned in
+  test_oracle.py) and must reproduce the reference's golden edges,
+  fingerprint AND comps exactly, at every golden config that fits a test.
+* device sampler: the integer part (SplitMix seed path + MT19937-64 streams)
+  must be bit-exact; libm-derived attributes are compared with a stated
+  tolerance and their exact-mismatch rate is reported; the full device path
+  must equal the reference's edge rule (oracle) applied to the device's own
+  points, bit for bit.
+* shards: partial results of world in {2,3,4,7} engine shards sum to the whole.
+"""
+import numpy as np
+import pytest
+
+import paper_1710_07565_b200 as rhg
+
+pytestmark = pytest.mark.gpu
+
+
+def params_of(s):
+    return rhg.ModelParams(s["n"], s["alpha"], float.fromhex(s["C"]), s["seed"], s["P"])
+
+
+def triple(st):
+    return st.total.edges, st.total.fingerprint, st.total.comps
+
+
+def rows(golden, names, max_n):
+    return [s for s in golden["stats"] if s["name"] in names and s["n"] <= max_n]
+
+
+@pytest.mark.parametrize("names,max_n", [
+    ({"grid"}, 2000),
+    ({"n1", "n2", "more_chunks_than_points"}, 100),
+    ({"odd_P", "smoke"}, 20000),
+    ({"cfg1"}, 1 << 20),
+])
+def test_same_points_parity_golden(oracle, golden, names, max_n):
+    for s in rows(golden, names, max_n):
+        p = params_of(s)
+        pts = oracle.points(p.n, p.alpha, p.C, p.seed, p.chunks)
+        st = rhg.count_edges_from_points(p, pts)
+        assert triple(st) == (s["edges"], s["fingerprint"], s["comps"]), s
+        assert st.global_vertices == s["global_vertices"]
+
+
+def test_same_points_parity_cfg2(oracle, golden):
+    """configs[1] (n=2^24, d=64, gamma=2.2, seed=7) at P=64 — the bench config."""
+    s = rows(golden, {"cfg2"}, 1 << 24)[0]
+    p = params_of(s)
+    pts = oracle.points(p.n, p.alpha, p.C, p.seed, p.chunks)
+    st = rhg.count_edges_from_points(p, pts)
+    assert triple(st) == (s["edges"], s["fingerprint"], s["comps"])
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 7])
+def test_shards_sum_to_whole(oracle, world):
+    n, alpha, d, seed, P = 40000, 0.8, 12.0, 11, 14
+    p = rhg.ModelParams.from_avg_degree(n, alpha, d, seed, P)
+    pts = oracle.points(n, alpha, p.C, seed, P)
+    whole = oracle.generate_stats(n, alpha, p.C, seed, P)
+    acc = [0, 0, 0]
+    for r in range(world):
+        st = rhg.count_edges_from_points(p, pts, rhg.GenOptions(rank=r, world=world))
+        acc = [acc[0] + st.total.edges, (acc[1] + st.total.fingerprint) % 2**64, acc[2] + st.total.comps]
+    assert tuple(acc) == (whole["edges"], whole["fingerprint"], whole["comps"])
+    # and the device-sampler path shards identically
+    full = rhg.generate_stats(p)
+    acc = [0, 0, 0]
+    for r in range(world):
+        st = rhg.generate_stats(p, rhg.GenOptions(rank=r, world=world))
+        acc = [acc[0] + st.total.edges, (acc[1] + st.total.fingerprint) % 2**64, acc[2] + st.total.comps]
+    assert tuple(acc) == triple(full)
+
+
+def _mt_uniforms_expected(oracle, p):
+    L = oracle.layout(p.n, p.alpha, p.C, p.seed, p.chunks)
+    ua = np.empty(p.n)
+    ur = np.empty(p.n)
+    for i in range(L.count):
+        for c in range(p.chunks):
+            cnt, base = int(L.chunk_counts[i, c]), int(L.id_base[i, c])
+            if not cnt:
+                continue
+            for phase, out in ((3, ua), (4, ur)):
+                x = oracle.mt_outputs(oracle.derive_seed(p.seed, [phase, i, c]), cnt)
+                out[base:base + cnt] = (x >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    return ua, ur
+
+
+@pytest.mark.parametrize("cfg", [(20000, 16.0, 2.6, 5, 4), (200000, 64.0, 2.2, 7, 64), (3000, 8.0, 3.0, 2, 1)])
+def test_sampler_uniform_streams_bit_exact(oracle, cfg):
+    n, d, g, seed, P = cfg
+    p = rhg.ModelParams.from_avg_degree(n, rhg.alpha_from_gamma(g), d, seed, P)
+    ua, ur = rhg.sample_uniforms(p)
+    ea, er = _mt_uniforms_expected(oracle, p)
+    assert np.array_equal(ua.view(np.uint64), ea.view(np.uint64))
+    assert np.array_equal(ur.view(np.uint64), er.view(np.uint64))
+
+
+def ulp_diff(a, b):
+    ia, ib = a.view(np.int64), b.view(np.int64)
+    return np.abs(ia - ib)
+
+
+@pytest.mark.parametrize("cfg", [(20000, 16.0, 2.6, 5, 4), (1 << 20, 16.0, 3.0, 1, 8)])
+def test_sampler_points_close_and_edges_exact(oracle, cfg):
+    """Device libm (CUDA) is not glibc: attributes may differ by a few ulp,
+    amplified by acos near 1 for the half-width (d acos / dx ~ 1/hw), so the
+    sanity tolerances are: radial attributes 1e-12 relative, angles and
+    trig values 1e-6 absolute.  The edge rule on the device's points must
+    match the oracle's edge rule on the same points exactly."""
+    n, d, g, seed, P = cfg
+    alpha = rhg.alpha_from_gamma(g)
+    p = rhg.ModelParams.from_avg_degree(n, alpha, d, seed, P)
+    dev = rhg.sample_points(p)
+    ref = oracle.points(n, alpha, p.C, seed, P)
+    for f in ("r", "coth_r", "inv_sinh_r"):
+        a, b = getattr(dev, f), getattr(ref, f)
+        bad = np.abs(a - b) > 1e-12 * np.abs(b)
+        assert not bad.any(), (f, np.flatnonzero(bad)[:5])
+    for f in ("beta", "theta", "half_width", "cos_theta", "sin_theta"):
+        a, b = getattr(dev, f), getattr(ref, f)
+        d = np.abs(a - b)
+        if f == "theta":  # wrap at 2pi
+            d = np.minimum(d, rhg.two_pi - d)
+        assert not (d > 1e-6).any(), (f, np.flatnonzero(d > 1e-6)[:5])
+    # chunk structure is exact: begins sorted inside each stream, theta = beta + hw (mod 2pi)
+    th = dev.beta + dev.half_width
+    th = np.where(th >= rhg.two_pi, th - rhg.two_pi, th)
+    assert np.array_equal(th, dev.theta)
+    want = oracle.count_edges_from_points(n, alpha, p.C, seed, P, dev)
+    got = rhg.generate_stats(p)
+    assert triple(got) == (want["edges"], want["fingerprint"], want["comps"])
+
+
+def test_degrees_exact(oracle):
+    n, alpha, d, seed, P = 50000, 0.75, 16.0, 3, 8
+    p = rhg.ModelParams.from_avg_degree(n, alpha, d, seed, P)
+    pts = oracle.points(n, alpha, p.C, seed, P)
+    want = oracle.generate_stats(n, alpha, p.C, seed, P, degrees=True)
+    got = rhg.count_edges_from_points(p, pts, degrees=True)
+    assert np.array_equal(got.degrees, want["degrees"])
+    got2 = rhg.generate_stats(p, degrees=True)
+    assert int(got2.degrees.sum()) == 2 * got2.total.edges
+
+
+def test_repeatable_and_context_reuse():
+    p = rhg.ModelParams.from_avg_degree(300000, 0.8, 16.0, 9, 16)
+    a = rhg.generate_stats(p)
+    b = rhg.generate_stats(rhg.ModelParams.from_avg_degree(1000, 0.8, 16.0, 9, 2))
+    c = rhg.generate_stats(p)
+    assert triple(a) == triple(c) and a.total.edges > 0 and b.total.edges > 0
+    assert a.kernel_launches > 0 and a.device_ms > 0
