@@ -6,6 +6,8 @@
 // one D2H copy of the counters.  All device work is on the context's stream,
 // timed with CUDA events on that stream.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cstring>
 #include <new>
@@ -98,7 +100,7 @@ struct rhg_ctx {
     int          device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t  ev[4]{};
-    DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, cells, counters, degrees, longsegs, tasks;
+    DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, cells, counters, degrees, tasks, dbg, nid;
     HostPinned   staging;
 };
 
@@ -264,23 +266,27 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     e.beta = ctx->beta.as<double>(), e.hw = ctx->hw.as<double>();
     e.rec0 = ctx->rec0.as<double2>(), e.rec1 = ctx->rec1.as<double2>(), e.rec2 = ctx->rec2.as<double2>();
     e.cellstart = ctx->cells.as<std::uint64_t>();
+    ctx->nid.ensure((pl.n_ext + 2) * sizeof(unsigned long long));
+    e.nid = ctx->nid.as<unsigned long long>();
     e.ctr       = ctx->counters.as<Counters>();
     e.dmax_bits = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + align256(3 * sizeof(Counters)));
-    e.long_ctr  = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + cnt_bytes - 256);
-    e.task_ctr  = e.long_ctr + 1;
+    e.task_ctr  = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + cnt_bytes - 256);
     e.task_cap  = std::uint64_t(1) << 21; // 64 MiB of deferred dense tiles; overflow runs inline
     ctx->tasks.ensure(e.task_cap * sizeof(TileTask));
     e.tasks = ctx->tasks.as<TileTask>();
-    // deferred long lists: room for 2^20 segments (96 MiB); overflow is processed inline
-    e.long_cap = std::uint64_t(1) << 20;
-    ctx->longsegs.ensure(e.long_cap * sizeof(LongSeg));
-    e.long_segs = ctx->longsegs.as<LongSeg>();
     e.cosh_R = pl.L.cosh_R, e.chunk0_upper = chunk_upper_bound(0, pl.L.chunks);
     e.lift_part   = pl.e1 == pl.L.chunks && pl.T > 0;
     e.stream_jobs = t.sjobs, e.n_stream_jobs = int(pl.sjobs.size()), e.stream_warps = pl.swarps;
     e.glob_jobs = t.gjobs, e.n_glob_jobs = int(pl.gjobs.size()), e.glob_warps = pl.gwarps;
     e.gg_tile_begin = pl.gg_t0, e.gg_tile_end = pl.gg_t1;
     e.degrees       = degrees ? ctx->degrees.as<unsigned>() : nullptr;
+    const char* dbg_env = std::getenv("RHG_DEBUG_STATS");
+    const bool  dbg     = dbg_env && dbg_env[0] == '1';
+    if (dbg) {
+        ctx->dbg.ensure(kDbgSlots * sizeof(unsigned long long));
+        CK(cudaMemsetAsync(ctx->dbg.p, 0, kDbgSlots * sizeof(unsigned long long), ctx->stream));
+        e.dbg = ctx->dbg.as<unsigned long long>();
+    }
     launch_cell_index(e, pl.ncells, ctx->stream, launches);
     launch_edges(e, ctx->stream, launches);
     CK(cudaGetLastError());
@@ -291,6 +297,15 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     if (degrees)
         CK(cudaMemcpyAsync(degrees, ctx->degrees.p, pl.L.n * sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    if (dbg) {
+        unsigned long long h[kDbgSlots];
+        CK(cudaMemcpy(h, ctx->dbg.p, sizeof h, cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "RHG_DEBUG_STATS {\"groups\": [%llu,%llu,%llu,%llu,%llu,%llu], \"sumU\": [%llu,%llu,%llu,%llu,%llu,%llu], "
+                             "\"slots\": [%llu,%llu,%llu,%llu,%llu,%llu], \"serial_warps\": %llu, \"serial_slots\": %llu, "
+                             "\"serial_cands\": %llu, \"tasks\": %llu, \"warps\": %llu, \"cands\": %llu}\n",
+                     h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[10], h[11], h[12], h[13], h[14], h[15],
+                     h[16], h[17], h[18], h[19], h[20], h[21], h[22], h[23]);
+    }
     out->edges       = hc[0].edges + hc[1].edges + hc[2].edges;
     out->fingerprint = hc[0].fp + hc[1].fp + hc[2].fp;
     out->comps       = hc[0].comps + hc[1].comps + hc[2].comps;
@@ -372,7 +387,7 @@ void rhg_destroy(rhg_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     for (DevBuf* b: {&c->beta, &c->hw, &c->rec0, &c->rec1, &c->rec2, &c->r_out, &c->beta_raw, &c->tables, &c->cells,
-                     &c->counters, &c->degrees, &c->longsegs, &c->tasks})
+                     &c->counters, &c->degrees, &c->tasks, &c->dbg, &c->nid})
         b->release();
     if (c->staging.p) cudaFreeHost(c->staging.p);
     for (auto& e: c->ev) cudaEventDestroy(e);
@@ -405,7 +420,7 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
         out->kernel_launches = launches;
         out->device_bytes    = ctx->beta.cap + ctx->hw.cap + ctx->rec0.cap + ctx->rec1.cap + ctx->rec2.cap +
                             ctx->r_out.cap + ctx->beta_raw.cap + ctx->tables.cap + ctx->cells.cap + ctx->counters.cap +
-                            ctx->degrees.cap + ctx->longsegs.cap + ctx->tasks.cap;
+                            ctx->degrees.cap + ctx->tasks.cap + ctx->nid.cap;
         out->seconds = std::chrono::duration<double>(Clock::now() - t0).count();
     });
 }

@@ -44,24 +44,14 @@ struct PairJob {
     std::int32_t  a, j;
 };
 
-// A candidate list too long for one warp's inline pass (> kLongSeg nodes):
-// deferred to long_pairs_kernel, which splits it into kLongChunk-node chunks
-// spread evenly over the whole GPU.
-struct LongSeg {
-    double             cs, sn, coth, rci;
-    unsigned long long tkey, id, lo, hi;
-    std::uint64_t      c0, c1, chunk_base;
-    std::int32_t       j, same;
-};
-constexpr std::uint64_t kLongSeg   = 2048;
-constexpr std::uint64_t kLongChunk = 256;
-constexpr int           kCtrShift  = 40; // long counter: segments << 40 | chunks
-
-// A dense warp tile too large to run inline: 32 requests starting at p0 of
-// pair job `job` against nodes [u0, u1) of its target annulus.
+// A piece of a tile too large to run inline: 2^lgR requests starting at p0
+// of pair job `job` (kind 0 streaming, 1 global with window w) against nodes
+// [u0, u1) of the job's target annulus.
 struct TileTask {
     std::uint64_t p0, u0, u1;
-    std::int64_t  job;
+    std::int32_t  job;
+    std::int16_t  kind, lgR;
+    std::int32_t  w, pad;
 };
 
 struct Counters { // one per edge-producing kernel family

@@ -38,6 +38,7 @@ struct EdgeArgs {
     const double2*    rec1 = nullptr;
     const double2*    rec2 = nullptr;
     std::uint64_t*    cellstart = nullptr;
+    unsigned long long* nid = nullptr;       // [n_ext + 2] vertex id | halo bit (cell_index_kernel)
     unsigned long long* dmax_bits = nullptr; // per annulus, max half-width (bits)
     double            cosh_R = 1.0;
     double            chunk0_upper = 0.0; // chunk_upper_bound(0, P)
@@ -52,10 +53,8 @@ struct EdgeArgs {
     TileTask*         tasks = nullptr;
     std::uint64_t     task_cap = 0;
     unsigned long long* task_ctr = nullptr;
-    LongSeg*          long_segs = nullptr;
-    std::uint64_t     long_cap  = 0;
-    unsigned long long* long_ctr = nullptr;
     Counters*         ctr = nullptr; // [0] streaming, [1] global requests, [2] global unit
+    unsigned long long* dbg = nullptr; // optional path statistics (RHG_DEBUG_STATS=1), kDbgSlots entries
     unsigned int*     degrees = nullptr;
 };
 
@@ -63,5 +62,8 @@ void launch_cell_index(const EdgeArgs& a, std::uint64_t ncells_total, cudaStream
 void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches);
 
 constexpr int kGGTile = 128;
+// dbg layout: [0..5] groups per lgR, [6..11] sum U per lgR, [12..17] slots per lgR, [18] serial warps,
+// [19] serial slots (32*maxlen), [20] serial candidates, [21] tasks, [22] warps, [23] candidates total
+constexpr int kDbgSlots = 32;
 
 } // namespace rhgb
