@@ -1,0 +1,263 @@
+"""Benchmark: threshold-RHG edges/s on B200 (driver contract, one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+A "step" is one full stats-only generation (generator.hpp:219-291) of the
+workload: host layout, device sampler, cell index, every edge kernel, and the
+counters back on the host.  The workload at N=1 is BASELINE.json configs[1]
+(n=2^24, d=64, gamma=2.2, seed=7) at the survey's recommended chunk count
+P=64; with N>1 (torchrun, one process per GPU) the same graph is
+split into N engine shards (chunks [r*P/N, (r+1)*P/N)) — strong scaling — and
+the only collective is an all-reduce of the (edges, fingerprint, comps) counters.
+
+value = whole-graph edges / (max over ranks of the summed per-step device
+time, CUDA events on the library's stream).  e2e = the same metric through the
+public API call (host layout + table upload + kernels + counter readback),
+host wall clock per call.  --impl reference times the reference's own CPU
+generator (oracle/_ref, the unmodified reference headers compiled in place)
+on the host cores with all threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "edges/sec (device-timed, max over ranks) at 1/2/4/8 B200; % of FP64 roofline"
+UNIT = "edges/s"
+
+CONFIGS = {  # name: (n, avg degree, gamma, seed, chunks)  -- BASELINE.json configs, SURVEY §8(d) P
+    "cfg1": (1 << 20, 16.0, 3.0, 1, 8),
+    "cfg2": (1 << 24, 64.0, 2.2, 7, 64),
+    "cfg3": (1 << 26, 256.0, 3.0, 11, 512),
+    "cfg4": (1 << 28, 4.0, 3.0, 13, 4096),
+    "cfg5": (1 << 30, 16.0, 2.6, 17, 2048),
+}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def traffic_from_profile():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    try:
+        return json.load(open(p))
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_reference_run(cfg, threads=0):
+    """The reference's generate_stats on the host cores (oracle/_ref)."""
+    from oracle.refbind import Ref
+    ref = Ref()
+    n, d, g, seed, P = cfg
+    alpha = ref.alpha_from_gamma(g)
+    C = ref.radial_const_from_avg_degree(d, alpha)
+    t = time.perf_counter()
+    st = ref.generate_stats(n, alpha, C, seed, P, threads)
+    wall = time.perf_counter() - t
+    return st, wall
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_run(cfg)
+    tot_edges, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        st, wall = cpu_reference_run(cfg)
+        tot_edges += st["edges"]
+        tot_s += st["seconds"]
+    v = tot_edges / tot_s
+    n, d, g, seed, P = cfg
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded model sampler)",
+            "config": workload_config(args.config, cfg, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": f"full {args.config} graph per step (RunStats.seconds), "
+                                       f"GenOptions.workers = hardware_concurrency"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "result": {"edges": st["edges"], "fingerprint": st["fingerprint"], "comps": st["comps"]}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(name, cfg, world):
+    n, d, g, seed, P = cfg
+    return {"workload": f"{name}: threshold RHG n={n}, avg degree {d:g}, gamma {g}, seed {seed}, chunks P={P}",
+            "n": n, "avg_degree": d, "gamma": g, "seed": seed, "chunks": P, "parallelism": f"chunk-shard x{world}",
+            "l2": "inputs larger than L2: every step regenerates the full point set (~64 B/point in HBM)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_env()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1710_07565_b200 as rhg
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, d, g, seed, P = cfg
+    params = rhg.ModelParams.from_avg_degree(n, rhg.alpha_from_gamma(g), d, seed, P)
+    opts = rhg.GenOptions(device=local, rank=rank, world=world)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        rhg.generate_stats(params, opts)
+    barrier()
+    dev_ms, wall_s, launches, h2d, d2h = 0.0, 0.0, 0, 0, 0
+    edges_ms = 0.0
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            st = rhg.generate_stats(params, opts)
+            wall_s += time.perf_counter() - t
+            dev_ms += st.device_ms
+            edges_ms += st.edges_ms
+            launches += st.kernel_launches
+            h2d += st.h2d_bytes
+            d2h += st.d2h_bytes
+    barrier()
+    # whole-graph counters: wrapping u64 sums over shards (the one collective)
+    cnt = torch.tensor([st.total.edges, st.total.fingerprint - (1 << 64 if st.total.fingerprint >= 1 << 63 else 0),
+                        st.total.comps], dtype=torch.int64, device="cuda")
+    tm = torch.tensor([dev_ms, wall_s, edges_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    edges, fp, comps = int(cnt[0]), int(cnt[1]) % (1 << 64), int(cnt[2])
+    dev_ms, wall_s, edges_ms = float(tm[0]), float(tm[1]), float(tm[2])
+    value = edges * args.steps / (dev_ms * 1e-3)
+    e2e = edges * args.steps / wall_s
+    if rank == 0:
+        ops, lat, _ = rhg.fp64_peak(local)
+        # algorithmic FP64-pipe work = 8 per reference predicate test
+        # (5 DMUL + 2 DADD + 1 DSETP); the edge kernels do comps tests per step.
+        achieved = 8.0 * comps * args.steps / (edges_ms * 1e-3) / 1e12
+        peak = ops / 1e12
+        tr = traffic_from_profile()
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded model sampler)",
+                "config": workload_config(args.config, cfg, world),
+                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
+                        "d2h_bytes_per_step": d2h // args.steps},
+                "gpu_launches": launches,
+                "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                             "frac": achieved / peak,
+                             "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                             "kernel": "edge kernels (cell index + all pair kernels), CUDA events on the library stream",
+                             "peak_source": "measured live: non-FMA DMUL+DADD rate (rhg_fp64_peak)",
+                             "work": "8 FP64-pipe ops per reference predicate test x comps (SURVEY 8(d))",
+                             "dmul_latency_cycles": lat},
+                "fp64_roofline_frac_whole_step": (8.0 * comps * args.steps / (dev_ms * 1e-3)) / ops,
+                "clocks": clk.summary(),
+                "result": {"edges": edges, "fingerprint": fp, "comps": comps,
+                           "W_ops_per_edge": 8.0 * comps / max(edges, 1)}}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                stc, wall = cpu_reference_run(cfg)
+                line["cpu_baseline"] = {"value": stc["edges"] / stc["seconds"], "unit": UNIT,
+                                        "cores": os.cpu_count() or 1, "kind": "reference",
+                                        "sample": f"one full {args.config} generate_stats (oracle/_ref, all host "
+                                                  f"threads), {stc['seconds']:.2f} s",
+                                        "result": {"edges": stc["edges"], "fingerprint": stc["fingerprint"],
+                                                   "comps": stc["comps"]}}
+            except Exception as e:  # noqa: BLE001 - report, do not fail the bench
+                line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1,
+                                        "kind": "reference", "sample": f"unavailable: {e}"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

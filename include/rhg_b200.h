@@ -84,6 +84,8 @@ typedef struct {
     double seconds;    /* wall time of the whole call (RunStats.seconds)    */
     uint64_t kernel_launches; /* kernels this call launched                 */
     uint64_t device_bytes;    /* device memory held by the context          */
+    uint64_t h2d_bytes;       /* host->device bytes this call copied        */
+    uint64_t d2h_bytes;       /* device->host bytes this call copied        */
 } rhg_run_stats;
 
 /* Host point arrays in vertex-id order (n entries each; any may be NULL

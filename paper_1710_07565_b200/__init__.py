@@ -128,6 +128,8 @@ class RunStats:
     host_ms: float = 0.0
     kernel_launches: int = 0
     device_bytes: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
     degrees: Optional[np.ndarray] = None
 
     def avg_degree(self) -> float:
@@ -142,7 +144,8 @@ class RunStats:
                    total=ChunkStats(s.edges, s.comps, s.streaming_vertices, s.fingerprint), seconds=s.seconds,
                    R=s.R, annuli=s.annuli, first_streaming=s.first_streaming, global_edges=s.global_edges,
                    global_comps=s.global_comps, device_ms=s.device_ms, sample_ms=s.sample_ms, edges_ms=s.edges_ms,
-                   host_ms=s.host_ms, kernel_launches=s.kernel_launches, device_bytes=s.device_bytes)
+                   host_ms=s.host_ms, kernel_launches=s.kernel_launches, device_bytes=s.device_bytes,
+                   h2d_bytes=s.h2d_bytes, d2h_bytes=s.d2h_bytes)
 
 
 class _Context:

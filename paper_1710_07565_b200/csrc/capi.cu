@@ -209,7 +209,7 @@ struct Tables {
 };
 
 // Pack all tables into one pinned blob and send it with one copy.
-Tables upload_tables(rhg_ctx* ctx, const Plan& pl) {
+Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr) {
     const std::size_t o_ann = 0, o_jobs = align256(o_ann + pl.ann.size() * sizeof(AnnulusDev));
     const std::size_t o_sj = align256(o_jobs + pl.jobs.size() * sizeof(StreamJob));
     const std::size_t o_gj = align256(o_sj + pl.sjobs.size() * sizeof(PairJob));
@@ -222,6 +222,7 @@ Tables upload_tables(rhg_ctx* ctx, const Plan& pl) {
     std::memcpy(h + o_gj, pl.gjobs.data(), pl.gjobs.size() * sizeof(PairJob));
     ctx->tables.ensure(bytes);
     CK(cudaMemcpyAsync(ctx->tables.p, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    if (h2d) *h2d += bytes;
     char* d = ctx->tables.as<char>();
     return {reinterpret_cast<AnnulusDev*>(d + o_ann), reinterpret_cast<StreamJob*>(d + o_jobs),
             reinterpret_cast<PairJob*>(d + o_sj), reinterpret_cast<PairJob*>(d + o_gj)};
@@ -311,6 +312,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     out->comps       = hc[0].comps + hc[1].comps + hc[2].comps;
     out->global_edges = hc[2].edges;
     out->global_comps = hc[2].comps;
+    out->d2h_bytes += 3 * sizeof(Counters) + (degrees ? pl.L.n * sizeof(unsigned) : 0);
 }
 
 void fill_common(const Plan& pl, rhg_run_stats* out) {
@@ -406,7 +408,7 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
         const Plan    pl = make_plan(P, shard);
         std::uint64_t launches = 0;
         ensure_points(ctx, pl.total, false);
-        const Tables t = upload_tables(ctx, pl);
+        const Tables t = upload_tables(ctx, pl, &out->h2d_bytes);
         const double host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         launch_sampler(sampler_args(ctx, pl, t), ctx->stream, &launches);
