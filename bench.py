@@ -206,14 +206,13 @@ def main():
             d2h += st.d2h_bytes
     barrier()
     # whole-graph counters: wrapping u64 sums over shards (the one collective)
-    cnt = torch.tensor([st.total.edges, st.total.fingerprint - (1 << 64 if st.total.fingerprint >= 1 << 63 else 0),
-                        st.total.comps], dtype=torch.int64, device="cuda")
-    tm = torch.tensor([dev_ms, wall_s, edges_ms], dtype=torch.float64, device="cuda")
+    from paper_1710_07565_b200.distributed import ShardResult, reduce_shards
+    g = reduce_shards(ShardResult(st.total.edges, st.total.fingerprint, st.total.comps, dev_ms), device="cuda")
+    edges, fp, comps = g.edges, g.fingerprint, g.comps
+    tm = torch.tensor([wall_s, edges_ms], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-    edges, fp, comps = int(cnt[0]), int(cnt[1]) % (1 << 64), int(cnt[2])
-    dev_ms, wall_s, edges_ms = float(tm[0]), float(tm[1]), float(tm[2])
+    dev_ms, wall_s, edges_ms = g.max_device_ms, float(tm[0]), float(tm[1])
     value = edges * args.steps / (dev_ms * 1e-3)
     e2e = edges * args.steps / wall_s
     if rank == 0:

@@ -229,6 +229,7 @@ class Oracle(_Base):
         L.orc_generate_stats.argtypes = [u64, f64, f64, u64, u32, u32, C.POINTER(OrcStats), P_u32]
         L.orc_count_edges_from_points.argtypes = [u64, f64, f64, u64, u32, u32] + [P_f64] * 7 + [
             C.POINTER(OrcStats), P_u32]
+        L.orc_generate_stats_shard.argtypes = [u64, f64, f64, u64, u32, u32, u32, u32, C.POINTER(OrcStats)]
 
     def radial_const_from_avg_degree(self, d_bar, alpha):
         out = f64()
@@ -293,6 +294,11 @@ class Oracle(_Base):
         if degrees:
             res["degrees"] = deg
         return res
+
+    def generate_stats_shard(self, n, alpha, Cc, seed, chunks, rank, world, threads=0):
+        st = OrcStats()
+        self._check(self.L.orc_generate_stats_shard(n, alpha, Cc, seed, chunks, rank, world, threads, C.byref(st)))
+        return st.asdict()
 
     def count_edges_from_points(self, n, alpha, Cc, seed, chunks, pts: Points, threads=0, degrees=False):
         st = OrcStats()

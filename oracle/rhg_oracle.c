@@ -891,6 +891,8 @@ typedef struct {
     cstats st, gst;
     uint32_t* degrees;
     uint64_t* mat;
+    uint32_t e0, e1;         /* engines [e0, e1) */
+    uint32_t grank, gworld;  /* global-unit rows i with i % gworld == grank */
     int err;
     char errmsg[256];
 } unit_job;
@@ -899,7 +901,8 @@ typedef struct {
 static void global_unit_rows(unit_job* j) {
     const pts_t* P = j->P;
     const double cosh_R = j->L->cosh_R;
-    for (uint64_t i = j->w; i < j->g_end; i += j->W)
+    for (uint64_t i = j->w; i < j->g_end; i += j->W) {
+        if (i % j->gworld != j->grank) continue;
         for (uint64_t k = i + 1; k < j->g_end; ++k) {
             ++j->gst.comps;
             const double lhs = P->cs[i] * P->cs[k] + P->sn[i] * P->sn[k];
@@ -910,13 +913,14 @@ static void global_unit_rows(unit_job* j) {
                 deg_add(j->degrees, i, k);
             }
         }
+    }
 }
 /* generator.hpp:106-114 + sweep.hpp:265-270 */
 static void* unit_worker(void* arg) {
     unit_job* j = arg;
     const layout_t* L = j->L;
     global_unit_rows(j);
-    for (uint32_t c = j->w; c < L->chunks; c += j->W) {
+    for (uint32_t c = j->e0 + j->w; c < j->e1; c += j->W) {
         engine e;
         engine_init(&e, L, j->P, c, j->degrees);
         e.mat = j->mat;
@@ -951,7 +955,13 @@ static double now_s(void) {
 }
 
 static uint64_t* g_mat = NULL; /* diagnostics only (orc_comps_matrix) */
+static int run_units_shard(const layout_t* L, const pts_t* P, uint32_t threads, orc_stats* out, uint32_t* degrees,
+                           uint32_t rank, uint32_t world);
 static int run_units(const layout_t* L, const pts_t* P, uint32_t threads, orc_stats* out, uint32_t* degrees) {
+    return run_units_shard(L, P, threads, out, degrees, 0, 1);
+}
+static int run_units_shard(const layout_t* L, const pts_t* P, uint32_t threads, orc_stats* out, uint32_t* degrees,
+                           uint32_t rank, uint32_t world) {
     const uint64_t nG = L->first_streaming < L->count ? L->id_base[(size_t)L->first_streaming * L->chunks] : L->n;
     const uint32_t ns = L->count - L->first_streaming;
     /* generator.hpp:58-72: per-global half-widths in every streaming annulus */
@@ -965,6 +975,9 @@ static int run_units(const layout_t* L, const pts_t* P, uint32_t threads, orc_st
     for (uint32_t w = 0; w < threads; ++w) {
         jobs[w].L = L, jobs[w].P = P, jobs[w].g_end = nG, jobs[w].ghw = ghw, jobs[w].ns = ns, jobs[w].w = w,
         jobs[w].W = threads, jobs[w].degrees = degrees, jobs[w].mat = g_mat;
+        jobs[w].e0 = (uint32_t)((uint64_t)L->chunks * rank / world);
+        jobs[w].e1 = (uint32_t)((uint64_t)L->chunks * (rank + 1) / world);
+        jobs[w].grank = rank, jobs[w].gworld = world;
         pthread_create(&th[w], NULL, unit_worker, &jobs[w]);
     }
     memset(out, 0, sizeof *out);
@@ -1044,5 +1057,27 @@ int orc_comps_matrix(uint64_t n, double alpha, double C, uint64_t seed, uint32_t
     g_mat = mat;
     int rc = orc_generate_stats(n, alpha, C, seed, chunks, threads, &st, NULL);
     g_mat = NULL;
+    return rc;
+}
+
+/* One engine shard (rank of world): engines [rank*P/world, (rank+1)*P/world)
+ * and the global-unit rows i % world == rank.  Shards sum to the whole graph. */
+int orc_generate_stats_shard(uint64_t n, double alpha, double C, uint64_t seed, uint32_t chunks, uint32_t rank,
+                             uint32_t world, uint32_t threads, orc_stats* out) {
+    if (world < 1 || rank >= world) return fail(ORC_INVALID_ARGUMENT, "shard: rank must lie in [0, world)");
+    const double t0 = now_s();
+    layout_t L;
+    int rc = make_layout(&L, n, alpha, C, seed, chunks);
+    if (rc) {
+        layout_free(&L);
+        return rc;
+    }
+    double* buf = malloc(8 * n * sizeof(double));
+    pts_t P = {buf, NULL, buf + n, buf + 2 * n, buf + 3 * n, buf + 4 * n, buf + 5 * n, buf + 6 * n};
+    draw_all(&L, &P, threads);
+    rc = run_units_shard(&L, &P, threads, out, NULL, rank, world);
+    free(buf);
+    layout_free(&L);
+    out->seconds = now_s() - t0;
     return rc;
 }

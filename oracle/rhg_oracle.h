@@ -70,6 +70,11 @@ int orc_count_edges_from_points(uint64_t n, double alpha, double C, uint64_t see
                                 const double* cos_theta, const double* sin_theta, orc_stats* out,
                                 uint32_t* degrees);
 
+/* One engine shard: engines [rank*P/world, (rank+1)*P/world) and the
+ * global-unit rows i % world == rank (partial results sum to the whole). */
+int orc_generate_stats_shard(uint64_t n, double alpha, double C, uint64_t seed, uint32_t chunks, uint32_t rank,
+                             uint32_t world, uint32_t threads, orc_stats* out);
+
 /* Diagnostics: chunk-sweep tests per (request home annulus, node annulus). */
 int orc_comps_matrix(uint64_t n, double alpha, double C, uint64_t seed, uint32_t chunks, uint32_t threads,
                      uint64_t* mat);
