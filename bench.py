@@ -194,6 +194,7 @@ def main():
     barrier()
     dev_ms, wall_s, launches, h2d, d2h = 0.0, 0.0, 0, 0, 0
     edges_ms = 0.0
+    pairs_ms = 0.0
     with Clocks(local) as clk:
         for _ in range(args.steps):
             t = time.perf_counter()
@@ -201,6 +202,7 @@ def main():
             wall_s += time.perf_counter() - t
             dev_ms += st.device_ms
             edges_ms += st.edges_ms
+            pairs_ms += st.pairs_ms
             launches += st.kernel_launches
             h2d += st.h2d_bytes
             d2h += st.d2h_bytes

@@ -86,6 +86,7 @@ typedef struct {
     uint64_t device_bytes;    /* device memory held by the context          */
     uint64_t h2d_bytes;       /* host->device bytes this call copied        */
     uint64_t d2h_bytes;       /* device->host bytes this call copied        */
+    double pairs_ms;          /* the streaming pair kernel alone (dominant) */
 } rhg_run_stats;
 
 /* Host point arrays in vertex-id order (n entries each; any may be NULL

@@ -130,6 +130,7 @@ class RunStats:
     device_bytes: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    pairs_ms: float = 0.0
     degrees: Optional[np.ndarray] = None
 
     def avg_degree(self) -> float:
@@ -145,7 +146,7 @@ class RunStats:
                    R=s.R, annuli=s.annuli, first_streaming=s.first_streaming, global_edges=s.global_edges,
                    global_comps=s.global_comps, device_ms=s.device_ms, sample_ms=s.sample_ms, edges_ms=s.edges_ms,
                    host_ms=s.host_ms, kernel_launches=s.kernel_launches, device_bytes=s.device_bytes,
-                   h2d_bytes=s.h2d_bytes, d2h_bytes=s.d2h_bytes)
+                   h2d_bytes=s.h2d_bytes, d2h_bytes=s.d2h_bytes, pairs_ms=s.pairs_ms)
 
 
 class _Context:

@@ -94,13 +94,20 @@ struct HostPinned {
 
 std::size_t align256(std::size_t x) { return (x + 255) & ~std::size_t(255); }
 
+double ms_between(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+}
+
 } // namespace
 
 struct rhg_ctx {
     int          device = 0;
     cudaStream_t stream = nullptr;
-    cudaEvent_t  ev[4]{};
+    cudaEvent_t  ev[6]{};
     DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, cells, counters, degrees, tasks, dbg, nid;
+    DevBuf       lcells, perm, s_beta, s_hw, s_rec0, s_rec1, s_rec2;
     HostPinned   staging;
 };
 
@@ -114,6 +121,9 @@ struct Plan {
     std::vector<AnnulusDev> ann;
     std::vector<StreamJob>  jobs;
     std::vector<PairJob>    sjobs, gjobs;
+    std::vector<std::uint64_t> blk_prefix;  // angular-block item order (see edges.cu map_item)
+    std::vector<std::uint32_t> blk_job_off;
+    int                        nblk = 1;
     std::uint64_t           n_ext = 0, n_glob = 0, total = 0, swarps = 0, gwarps = 0, ncells = 0;
     std::uint64_t           gg_t0 = 0, gg_t1 = 0;
 };
@@ -161,6 +171,7 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
         const double top      = pl.e1 == Pc ? kTwoPi + chunk_upper_bound(0, Pc) : chunk_upper_bound(pl.e1, Pc);
         A.cell_inv_w          = double(A.ncells) / (top - A.cell_origin);
         A.cell_off            = pl.ncells;
+        A.wrap                = A.halo;
         pl.ncells += A.ncells + 1;
     }
     pl.n_ext  = run;
@@ -197,15 +208,40 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
             pl.gjobs.push_back(J);
             pl.gwarps += (pl.n_glob + 31) / 32;
         }
+    // angular blocks: ~32 MB of node data per block so one block of every annulus stays in L2
+    {
+        const std::uint64_t bytes = pl.n_ext * 72;
+        std::uint64_t       M     = bytes / (32ull << 20);
+        M                         = std::max<std::uint64_t>(1, std::min<std::uint64_t>(M, 1024));
+        pl.nblk                   = int(M);
+        const std::size_t nj      = pl.sjobs.size();
+        pl.blk_prefix.assign(M + 1, 0);
+        pl.blk_job_off.assign(M * std::max<std::size_t>(nj, 1), 0);
+        std::uint64_t acc = 0;
+        for (std::uint64_t b = 0; b < M; ++b) {
+            pl.blk_prefix[b] = acc;
+            std::uint32_t in = 0;
+            for (std::size_t k = 0; k < nj; ++k) {
+                const std::uint64_t nb = (pl.sjobs[k].req_end - pl.sjobs[k].req_off + 31) / 32;
+                pl.blk_job_off[b * nj + k] = in;
+                in += std::uint32_t((b + 1) * nb / M - b * nb / M);
+            }
+            acc += in;
+        }
+        pl.blk_prefix[M] = acc;
+        if (acc != pl.swarps) throw Invariant("plan: angular block item count mismatch");
+    }
     const std::uint64_t nT = (pl.n_glob + kGGTile - 1) / kGGTile, tiles = nT * (nT + 1) / 2;
     pl.gg_t0 = tiles * r / W, pl.gg_t1 = tiles * (r + 1) / W;
     return pl;
 }
 
 struct Tables {
-    AnnulusDev* ann;
-    StreamJob*  jobs;
-    PairJob *   sjobs, *gjobs;
+    AnnulusDev*    ann;
+    StreamJob*     jobs;
+    PairJob *      sjobs, *gjobs;
+    std::uint64_t* blk_prefix;
+    std::uint32_t* blk_job_off;
 };
 
 // Pack all tables into one pinned blob and send it with one copy.
@@ -213,19 +249,24 @@ Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr)
     const std::size_t o_ann = 0, o_jobs = align256(o_ann + pl.ann.size() * sizeof(AnnulusDev));
     const std::size_t o_sj = align256(o_jobs + pl.jobs.size() * sizeof(StreamJob));
     const std::size_t o_gj = align256(o_sj + pl.sjobs.size() * sizeof(PairJob));
-    const std::size_t bytes = align256(o_gj + pl.gjobs.size() * sizeof(PairJob)) + 256;
+    const std::size_t o_bp = align256(o_gj + pl.gjobs.size() * sizeof(PairJob));
+    const std::size_t o_bj = align256(o_bp + pl.blk_prefix.size() * sizeof(std::uint64_t));
+    const std::size_t bytes = align256(o_bj + pl.blk_job_off.size() * sizeof(std::uint32_t)) + 256;
     ctx->staging.ensure(bytes);
     char* h = static_cast<char*>(ctx->staging.p);
     std::memcpy(h + o_ann, pl.ann.data(), pl.ann.size() * sizeof(AnnulusDev));
     std::memcpy(h + o_jobs, pl.jobs.data(), pl.jobs.size() * sizeof(StreamJob));
     std::memcpy(h + o_sj, pl.sjobs.data(), pl.sjobs.size() * sizeof(PairJob));
     std::memcpy(h + o_gj, pl.gjobs.data(), pl.gjobs.size() * sizeof(PairJob));
+    std::memcpy(h + o_bp, pl.blk_prefix.data(), pl.blk_prefix.size() * sizeof(std::uint64_t));
+    std::memcpy(h + o_bj, pl.blk_job_off.data(), pl.blk_job_off.size() * sizeof(std::uint32_t));
     ctx->tables.ensure(bytes);
     CK(cudaMemcpyAsync(ctx->tables.p, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
     if (h2d) *h2d += bytes;
     char* d = ctx->tables.as<char>();
     return {reinterpret_cast<AnnulusDev*>(d + o_ann), reinterpret_cast<StreamJob*>(d + o_jobs),
-            reinterpret_cast<PairJob*>(d + o_sj), reinterpret_cast<PairJob*>(d + o_gj)};
+            reinterpret_cast<PairJob*>(d + o_sj), reinterpret_cast<PairJob*>(d + o_gj),
+            reinterpret_cast<std::uint64_t*>(d + o_bp), reinterpret_cast<std::uint32_t*>(d + o_bj)};
 }
 
 void ensure_points(rhg_ctx* ctx, std::uint64_t total, bool with_export) {
@@ -267,8 +308,22 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     e.beta = ctx->beta.as<double>(), e.hw = ctx->hw.as<double>();
     e.rec0 = ctx->rec0.as<double2>(), e.rec1 = ctx->rec1.as<double2>(), e.rec2 = ctx->rec2.as<double2>();
     e.cellstart = ctx->cells.as<std::uint64_t>();
-    ctx->nid.ensure((pl.n_ext + 2) * sizeof(unsigned long long));
-    e.nid = ctx->nid.as<unsigned long long>();
+    ctx->lcells.ensure(std::max<std::uint64_t>(pl.ncells, 1) * sizeof(std::uint64_t));
+    e.lcellstart = ctx->lcells.as<std::uint64_t>();
+    {
+        const std::size_t ne = pl.n_ext + 2;
+        ctx->perm.ensure(ne * sizeof(std::uint64_t));
+        ctx->s_beta.ensure(ne * sizeof(double));
+        ctx->s_hw.ensure(ne * sizeof(double));
+        ctx->s_rec0.ensure(ne * sizeof(double2));
+        ctx->s_rec1.ensure(ne * sizeof(double2));
+        ctx->s_rec2.ensure(ne * sizeof(double2));
+        ctx->nid.ensure(ne * sizeof(unsigned long long));
+        e.perm = ctx->perm.as<std::uint64_t>(), e.s_beta = ctx->s_beta.as<double>(), e.s_hw = ctx->s_hw.as<double>();
+        e.s_rec0 = ctx->s_rec0.as<double2>(), e.s_rec1 = ctx->s_rec1.as<double2>(), e.s_rec2 = ctx->s_rec2.as<double2>();
+        e.s_id = ctx->nid.as<unsigned long long>();
+    }
+    e.ann_rw = t.ann;
     e.ctr       = ctx->counters.as<Counters>();
     e.dmax_bits = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + align256(3 * sizeof(Counters)));
     e.task_ctr  = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + cnt_bytes - 256);
@@ -278,6 +333,8 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     e.cosh_R = pl.L.cosh_R, e.chunk0_upper = chunk_upper_bound(0, pl.L.chunks);
     e.lift_part   = pl.e1 == pl.L.chunks && pl.T > 0;
     e.stream_jobs = t.sjobs, e.n_stream_jobs = int(pl.sjobs.size()), e.stream_warps = pl.swarps;
+    e.blk_prefix = t.blk_prefix, e.blk_job_off = t.blk_job_off, e.nblk = pl.nblk;
+    e.ev_pairs0 = ctx->ev[4], e.ev_pairs1 = ctx->ev[5];
     e.glob_jobs = t.gjobs, e.n_glob_jobs = int(pl.gjobs.size()), e.glob_warps = pl.gwarps;
     e.gg_tile_begin = pl.gg_t0, e.gg_tile_end = pl.gg_t1;
     e.degrees       = degrees ? ctx->degrees.as<unsigned>() : nullptr;
@@ -312,6 +369,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     out->comps       = hc[0].comps + hc[1].comps + hc[2].comps;
     out->global_edges = hc[2].edges;
     out->global_comps = hc[2].comps;
+    out->pairs_ms     = pl.swarps ? ms_between(ctx->ev[4], ctx->ev[5]) : 0.0;
     out->d2h_bytes += 3 * sizeof(Counters) + (degrees ? pl.L.n * sizeof(unsigned) : 0);
 }
 
@@ -328,11 +386,7 @@ void fill_common(const Plan& pl, rhg_run_stats* out) {
     out->streaming_vertices = owned;
 }
 
-double ms_between(cudaEvent_t a, cudaEvent_t b) {
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, a, b));
-    return ms;
-}
+
 
 Params to_params(const rhg_params* p) {
     if (!p) throw InvalidArgument("rhg: params is null");
@@ -389,7 +443,8 @@ void rhg_destroy(rhg_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     for (DevBuf* b: {&c->beta, &c->hw, &c->rec0, &c->rec1, &c->rec2, &c->r_out, &c->beta_raw, &c->tables, &c->cells,
-                     &c->counters, &c->degrees, &c->tasks, &c->dbg, &c->nid})
+                     &c->counters, &c->degrees, &c->tasks, &c->dbg, &c->nid, &c->lcells, &c->perm, &c->s_beta,
+                     &c->s_hw, &c->s_rec0, &c->s_rec1, &c->s_rec2})
         b->release();
     if (c->staging.p) cudaFreeHost(c->staging.p);
     for (auto& e: c->ev) cudaEventDestroy(e);
@@ -422,7 +477,8 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
         out->kernel_launches = launches;
         out->device_bytes    = ctx->beta.cap + ctx->hw.cap + ctx->rec0.cap + ctx->rec1.cap + ctx->rec2.cap +
                             ctx->r_out.cap + ctx->beta_raw.cap + ctx->tables.cap + ctx->cells.cap + ctx->counters.cap +
-                            ctx->degrees.cap + ctx->tasks.cap + ctx->nid.cap;
+                            ctx->degrees.cap + ctx->tasks.cap + ctx->nid.cap + ctx->lcells.cap + ctx->perm.cap +
+                            ctx->s_beta.cap + ctx->s_hw.cap + ctx->s_rec0.cap + ctx->s_rec1.cap + ctx->s_rec2.cap;
         out->seconds = std::chrono::duration<double>(Clock::now() - t0).count();
     });
 }

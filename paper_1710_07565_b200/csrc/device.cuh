@@ -22,8 +22,9 @@ struct AnnulusDev {
     std::uint64_t off, halo, end;      // [off, halo) owned chunks, [halo, end) halo chunk
     std::int64_t  dlt0, dlt1;          // id = idx + dlt0 (idx < halo) else idx + dlt1
     double        cell_origin, cell_inv_w;
-    std::uint64_t cell_off;            // into the cell-start table
+    std::uint64_t cell_off;            // into the beta- and lambda-cell tables
     std::uint32_t ncells, pad;
+    std::uint64_t wrap;                // first sorted owned index with lambda >= 2pi (device-written; halo if none)
 };
 
 // One sorted-uniform / radius stream pair = one (annulus, chunk) point

@@ -4,23 +4,30 @@
 // (edges, fingerprint, comps) without materialising a single edge.
 //
 // The pair set is the pure-function restatement of the sweep documented in
-// DESIGN.md §3 (and SURVEY Appendix A): a request p in extended chunk t of
-// annulus a tests node q of annulus j >= a iff q's engine-frame angle lambda
-// lies in p's window W_j(p) = own [b, b+2hw) (j == a) or [lambda-h_j,
-// lambda+h_j) (j > a), q is in chunk t-1, t or t+1 of this shard's extended
-// array (halo requests only against the last owned chunk), not q == p, and for
-// j == a the request has the smaller (theta, id).  Global points request
-// clipped windows (sweep.hpp:404-432) against owned nodes.
+// a request p of annulus a tests node q of annulus j >= a iff
+// q's engine-frame angle lambda lies in p's window W_j(p) (own [b, b+2hw) for
+// j == a, [lambda-h_j, lambda+h_j) for j > a), q is reachable from p's chunk
+// (halo requests: owned nodes only), q != p, and for j == a (theta_p, id_p) <
+// (theta_q, id_q).  Global points request clipped windows (sweep.hpp:404-432)
+// against owned nodes.
 //
-//   cell_index_kernel    per-annulus cell -> first-index table over beta, the
-//                        exact max half-width (candidate superset bound) and the
-//                        node-id array (vertex id | halo bit) the tiles stage
-//   stream_pairs_kernel  streaming requests: one warp per 32 requests x target
-//                        annulus, processed as an adaptive R x C register tile
-//                        (see process_warp) or thread-serially when sparse
-//   glob_req_kernel      global requests x owned streaming nodes (same engine)
-//   tile_tasks_kernel    deferred pieces of very large tiles, load-balanced
-//   glob_pairs_kernel    global unit, 128x128 tiles of the upper triangle
+// Layout: each streaming annulus keeps two lambda-sorted blocks, the owned
+// chunks [off, halo) and the halo chunk [halo, end).  A window is then an
+// EXACT index range, and for ordinary same-annulus pairs (both owned, lambda <
+// 2pi, where lambda == theta) the (theta, id) dedup is just "node index >
+// request index" — the hot loop has no window or dedup compares at all.
+//
+//   beta_cells_kernel   beta-cell starts of the beta-ordered sampler output and
+//                       the exact per-annulus max half-width
+//   rank_kernel         exact rank of every point by (lambda, id) inside its block
+//   scatter_kernel      the lambda-sorted arrays (+ node ids)
+//   lambda_cells_kernel lambda-cell starts of the owned blocks, first wrapped index
+//   stream_pairs_kernel streaming requests: one warp per 32 requests x target
+//                       annulus; adaptive R x C register tile over TMA-staged
+//                       node batches, thread-serial when sparse
+//   glob_req_kernel     global requests x owned streaming nodes (same engine)
+//   tile_tasks_kernel   deferred pieces of very large tiles, load-balanced
+//   glob_pairs_kernel   global unit, 128x128 tiles of the upper triangle
 #include "device.cuh"
 #include "kernels.hpp"
 
@@ -28,7 +35,7 @@ namespace rhgb {
 
 namespace {
 
-constexpr unsigned kFull  = 0xffffffffu;
+constexpr unsigned kFull = 0xffffffffu;
 
 struct Acc {
     unsigned long long edges = 0, fp = 0, comps = 0;
@@ -48,6 +55,8 @@ __device__ __forceinline__ void flush(Acc& acc, Counters* c, int lane) {
     }
 }
 
+// Monotone cell index of an angle (same origin/width for the beta and the
+// lambda tables of an annulus).
 __device__ __forceinline__ std::uint32_t cellf(const AnnulusDev& A, double x) {
     const double t = fmul(fsub(x, A.cell_origin), A.cell_inv_w);
     if (!(t > 0.0)) return 0;
@@ -66,95 +75,176 @@ __device__ __forceinline__ int streaming_annulus_of(const AnnulusDev* __restrict
     return lo;
 }
 
-__global__ void cell_index_kernel(EdgeArgs A) {
-    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(kFull, v, o);
+        v                          = t > v ? t : v;
+    }
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+// Fill a cell-start table: entries (kp, k] = i, and after the last point of
+// the block (k, ncells] = end.
+__device__ __forceinline__ void cell_fill(std::uint64_t* tab, std::int64_t kp, std::uint32_t k, std::uint64_t i,
+                                          bool last, std::uint32_t ncells, std::uint64_t end) {
+    for (std::int64_t c = kp + 1; c <= std::int64_t(k); ++c) tab[c] = i;
+    if (last)
+        for (std::uint32_t c = k + 1; c <= ncells; ++c) tab[c] = end;
+}
+
+// ---------------------------------------------------------------- sort ---
+__global__ void beta_cells_kernel(EdgeArgs A) {
+    const std::uint64_t i    = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int           lane = threadIdx.x & 31;
-    // empty streaming annuli: their 1-cell table is [off, off]
-    if (i < std::uint64_t(A.count) && int(i) >= A.first_streaming) {
+    if (i < std::uint64_t(A.count) && int(i) >= A.first_streaming) { // empty blocks: [off, off]
         const AnnulusDev& E = A.ann[i];
         if (E.end == E.off)
             for (std::uint32_t k = 0; k <= E.ncells; ++k) A.cellstart[E.cell_off + k] = E.off;
+        if (E.halo == E.off)
+            for (std::uint32_t k = 0; k <= E.ncells; ++k) A.lcellstart[E.cell_off + k] = E.off;
     }
     unsigned long long hwbits = 0;
     int                j      = -1;
     if (i < A.n_ext) {
         j                   = streaming_annulus_of(A.ann, A.first_streaming, A.count, i);
         const AnnulusDev& J = A.ann[j];
-        const double      b = A.beta[i];
-        const std::uint32_t k  = cellf(J, b);
+        const std::uint32_t k  = cellf(J, A.beta[i]);
         const std::int64_t  kp = i > J.off ? std::int64_t(cellf(J, A.beta[i - 1])) : -1;
-        for (std::int64_t c = kp + 1; c <= std::int64_t(k); ++c) A.cellstart[J.cell_off + c] = i;
-        if (i + 1 == J.end)
-            for (std::uint32_t c = k + 1; c <= J.ncells; ++c) A.cellstart[J.cell_off + c] = J.end;
+        cell_fill(A.cellstart + J.cell_off, kp, k, i, i + 1 == J.end, J.ncells, J.end);
         hwbits = static_cast<unsigned long long>(__double_as_longlong(A.hw[i])); // hw >= +0
-        A.nid[i] = i < J.halo ? (i + static_cast<unsigned long long>(J.dlt0))
-                              : ((i + static_cast<unsigned long long>(J.dlt1)) | (1ull << 63));
     }
-    // warp max per annulus (lanes of one warp almost always share it)
     const int  j0   = __shfl_sync(kFull, j, 0);
     const bool same = __all_sync(kFull, j == j0);
     if (same) {
-        unsigned long long m = hwbits;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long t = __shfl_down_sync(kFull, m, o);
-            m = t > m ? t : m;
-        }
+        const unsigned long long m = warp_max_u64(hwbits);
         if (lane == 0 && j0 >= 0) atomicMax(&A.dmax_bits[j0], m);
     } else if (j >= 0) {
         atomicMax(&A.dmax_bits[j], hwbits);
     }
 }
 
+// Exact rank of point i by (lambda, beta-order index) inside its block; in the
+// owned block beta-order index order is id order, so the sorted order is
+// (lambda, id).  Only points whose beta lies in [lambda_i - dmax, lambda_i]
+// can compare either way: everything before that window is smaller
+// (lambda <= beta + dmax), everything after is larger (lambda >= beta).
+__global__ void rank_kernel(EdgeArgs A) {
+    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= A.n_ext) return;
+    const int           j  = streaming_annulus_of(A.ann, A.first_streaming, A.count, i);
+    const AnnulusDev&   J  = A.ann[j];
+    const bool          hb = i >= J.halo;
+    const std::uint64_t bs = hb ? J.halo : J.off, be = hb ? J.end : J.halo;
+    const double        li = A.rec0[i].x;
+    const double        dm = __longlong_as_double(static_cast<long long>(A.dmax_bits[j]));
+    std::uint64_t       k0 = A.cellstart[J.cell_off + cellf(J, fsub(fsub(li, dm), 1e-12))];
+    std::uint64_t       k1 = A.cellstart[J.cell_off + cellf(J, li) + 1];
+    k0 = k0 < bs ? bs : k0;
+    k1 = k1 > be ? be : k1;
+    std::uint64_t rank = k0 - bs;
+    for (std::uint64_t k = k0; k < k1; ++k) {
+        const double lk = A.rec0[k].x;
+        rank += (lk < li) || (lk == li && k < i);
+    }
+    A.perm[i] = bs + rank;
+}
+
+__global__ void scatter_kernel(EdgeArgs A) {
+    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= A.n_ext) return;
+    const int           j = streaming_annulus_of(A.ann, A.first_streaming, A.count, i);
+    const AnnulusDev&   J = A.ann[j];
+    const std::uint64_t d = A.perm[i];
+    A.s_beta[d]           = A.beta[i];
+    A.s_hw[d]             = A.hw[i];
+    A.s_rec0[d]           = A.rec0[i];
+    A.s_rec1[d]           = A.rec1[i];
+    A.s_rec2[d]           = A.rec2[i];
+    A.s_id[d]             = i + static_cast<unsigned long long>(i < J.halo ? J.dlt0 : J.dlt1);
+}
+
+// Lambda-cell starts of every owned block, and the first owned index with
+// lambda >= 2pi (wrapped points: theta = lambda - 2pi there).
+__global__ void lambda_cells_kernel(EdgeArgs A) {
+    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= A.n_ext) return;
+    const int   j = streaming_annulus_of(A.ann, A.first_streaming, A.count, i);
+    AnnulusDev& J = A.ann_rw[j];
+    if (i >= J.halo) return;
+    const double        l  = A.s_rec0[i].x;
+    const std::uint32_t k  = cellf(J, l);
+    const std::int64_t  kp = i > J.off ? std::int64_t(cellf(J, A.s_rec0[i - 1].x)) : -1;
+    cell_fill(A.lcellstart + J.cell_off, kp, k, i, i + 1 == J.halo, J.ncells, J.halo);
+    if (l >= kTwoPiD && (i == J.off || A.s_rec0[i - 1].x < kTwoPiD)) J.wrap = i;
+}
+
+// ------------------------------------------------------------ requests ---
+// First index k in the sorted owned block with lambda[k] >= x (exact).
+__device__ __forceinline__ std::uint64_t lower_bound_owned(const EdgeArgs& A, const AnnulusDev& J, double x) {
+    const std::uint32_t c = cellf(J, x);
+    std::uint64_t       k = A.lcellstart[J.cell_off + c];
+    const std::uint64_t e = A.lcellstart[J.cell_off + c + 1];
+    while (k < e && A.s_rec0[k].x < x) ++k;
+    return k;
+}
+__device__ __forceinline__ std::uint64_t lower_bound_halo(const EdgeArgs& A, const AnnulusDev& J, double x) {
+    std::uint64_t lo = J.halo, hi = J.end; // binary search (one chunk, rarely searched)
+    while (lo < hi) {
+        const std::uint64_t mid = (lo + hi) >> 1;
+        if (A.s_rec0[mid].x < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
 struct Req {
     double             cs, sn, coth, rci; // rci = fl(cosh(R) * inv_sinh_r), hoisted (sweep.hpp:532 order)
-    unsigned long long tkey, id;
+    unsigned long long id;
+    double             theta;
 };
 
-// One request against one target annulus: its window as order-preserving
-// keys, its candidate superset [c0, c1) over the beta-sorted nodes, and
-// hmask = bit 63 for halo requests (they must not test halo nodes).
+// One request against one target annulus: the simple index range handled by
+// the tile engine, the halo-block range and the "general" range of pairs that
+// need the full (theta, id) dedup (same-annulus pairs with wrapped or halo points).
 struct Lane {
-    Req                q;
-    unsigned long long lo, hi, hmask;
-    std::uint64_t      c0, c1;
+    Req           q;
+    std::uint64_t s0, s1; // simple owned range
+    std::uint64_t h0, h1; // halo-block range (simple when j != a, general when j == a)
+    std::uint64_t g0, g1; // general owned range (j == a only)
 };
 
-constexpr unsigned long long kHaloBit = 1ull << 63;
-
-// Candidate index range [c0, c1) over the beta-sorted nodes of annulus J that
-// can hold lambda in [lo, hi): lambda = fl(beta + hw) in [beta, beta + dmax].
-__device__ __forceinline__ void cand_range(const EdgeArgs& A, const AnnulusDev& J, double dmax, double lo, double hi,
-                                           std::uint64_t& c0, std::uint64_t& c1) {
-    if (!(hi > lo)) {
-        c0 = c1 = 0;
-        return;
+__device__ __forceinline__ void window_ranges(const EdgeArgs& A, const AnnulusDev& J, double lo, double hi,
+                                              bool want_halo, Lane& L) {
+    if (!(hi > lo)) return;
+    L.s0 = lower_bound_owned(A, J, lo);
+    L.s1 = lower_bound_owned(A, J, hi);
+    if (want_halo && J.end > J.halo && hi > A.s_rec0[J.halo].x && lo <= A.s_rec0[J.end - 1].x) {
+        L.h0 = lower_bound_halo(A, J, lo);
+        L.h1 = lower_bound_halo(A, J, hi);
     }
-    const double        x0 = fsub(fsub(lo, dmax), 1e-12);
-    const std::uint32_t k0 = cellf(J, x0), k1 = cellf(J, hi);
-    c0                     = A.cellstart[J.cell_off + k0];
-    c1                     = A.cellstart[J.cell_off + k1 + 1];
 }
 
-__device__ __forceinline__ double dmax_of(const EdgeArgs& A, int j) {
-    return __longlong_as_double(static_cast<long long>(A.dmax_bits[j]));
-}
-
-// Streaming request p of annulus Jb.a against annulus Jb.j (sweep.hpp:455-461, 478-479).
+// Streaming request at sorted index p of annulus Jb.a against annulus Jb.j
+// (sweep.hpp:455-461, 478-479).
 __device__ __forceinline__ void setup_stream(const EdgeArgs& A, const PairJob& Jb, std::uint64_t p, Lane& L) {
     L = Lane{};
     if (p >= Jb.req_end) return;
     const AnnulusDev& Aa = A.ann[Jb.a];
     const AnnulusDev& Aj = A.ann[Jb.j];
-    const double  b  = A.beta[p];
-    const double  hw = A.hw[p];
-    const double2 r0 = A.rec0[p], r1 = A.rec1[p], r2 = A.rec2[p];
+    const double      b  = A.s_beta[p];
+    const double      hw = A.s_hw[p];
+    const double2     r0 = A.s_rec0[p], r1 = A.s_rec1[p], r2 = A.s_rec2[p];
     L.q.cs = r1.x, L.q.sn = r1.y, L.q.coth = r2.x, L.q.rci = fmul(A.cosh_R, r2.y);
-    L.q.tkey        = nonneg_key(r0.y);
+    L.q.id          = A.s_id[p];
+    L.q.theta       = r0.y;
     const bool halo = p >= Aa.halo;
-    L.q.id          = p + static_cast<unsigned long long>(halo ? Aa.dlt1 : Aa.dlt0);
-    L.hmask         = halo ? kHaloBit : 0ull;
-    double lo, hi;
+    double     lo, hi;
     if (Jb.j == Jb.a) { // own window [b, b + 2hw)
         lo = b;
         hi = fadd(b, fmul(2.0, hw));
@@ -163,10 +253,20 @@ __device__ __forceinline__ void setup_stream(const EdgeArgs& A, const PairJob& J
         lo             = fsub(r0.x, h);
         hi             = fadd(r0.x, h);
     }
-    L.lo = nonneg_key(lo), L.hi = nonneg_key(hi);
-    cand_range(A, Aj, dmax_of(A, Jb.j), lo, hi, L.c0, L.c1);
-    if (halo && L.c1 > Aj.halo) L.c1 = Aj.halo; // no Foreign x Foreign
-    if (L.c1 < L.c0) L.c1 = L.c0;
+    window_ranges(A, Aj, lo, hi, !halo, L); // halo requests: owned nodes only (no Foreign x Foreign)
+    if (Jb.j == Jb.a) {
+        if (!halo && p < Aa.wrap) { // theta == lambda and index order == (lambda, id) order
+            const std::uint64_t w = Aj.wrap;
+            L.g0 = L.s0 > w ? L.s0 : w, L.g1 = L.s1; // wrapped nodes: general
+            L.s1 = L.s1 < w ? L.s1 : w;
+            L.s0 = L.s0 > p + 1 ? L.s0 : p + 1;      // dedup == index order, self excluded
+        } else {
+            L.g0 = L.s0, L.g1 = L.s1, L.s0 = L.s1 = 0; // all general
+        }
+    }
+    if (L.s1 < L.s0) L.s1 = L.s0;
+    if (L.g1 < L.g0) L.g1 = L.g0;
+    if (L.h1 < L.h0) L.h1 = L.h0;
 }
 
 // Global request g against streaming annulus Jb.j, window number w (0..3):
@@ -210,36 +310,37 @@ __device__ __forceinline__ void setup_global(const EdgeArgs& A, const PairJob& J
     if (w >= nw) return;
     L.q.cs = r1.x, L.q.sn = r1.y, L.q.coth = r2.x, L.q.rci = fmul(A.cosh_R, r2.y);
     L.q.id = g - A.n_ext;
-    L.lo = nonneg_key(lo), L.hi = nonneg_key(hi);
-    cand_range(A, Aj, dmax_of(A, Jb.j), lo, hi, L.c0, L.c1);
-    if (L.c1 > Aj.halo) L.c1 = Aj.halo;
-    if (L.c1 < L.c0) L.c1 = L.c0;
+    window_ranges(A, Aj, lo, hi, false, L);
+    if (L.s1 < L.s0) L.s1 = L.s0;
 }
 
-// The exact test of one (request, node) pair: window membership, the
-// Foreign x Foreign / self / same-annulus dedup filters (sweep.hpp:515-527),
-// then the predicate in the reference's rounding order:
+// The reference predicate (sweep.hpp:531-533), in its rounding order:
 //   lhs = fl(fl(c_r c_n) + fl(s_r s_n)),  rhs = fl(fl(k_r k_n) - fl(fl(coshR i_r) i_n)),  edge iff lhs > rhs.
-template <bool DEG, bool SAME>
-__device__ __forceinline__ void test_pair(const EdgeArgs& A, const Lane& L, double2 n0, double2 n1, double2 n2,
-                                          unsigned long long nidf, Acc& acc) {
-    const unsigned long long lam = static_cast<unsigned long long>(__double_as_longlong(n0.x));
-    const unsigned long long nid = nidf & ~kHaloBit;
-    bool in = lam >= L.lo && lam < L.hi && !(nidf & L.hmask);
-    if (SAME) {
-        const unsigned long long tk = nonneg_key(n0.y);
-        in = in && nid != L.q.id && !(L.q.tkey > tk || (L.q.tkey == tk && L.q.id > nid));
-    }
-    const double lhs = fadd(fmul(L.q.cs, n1.x), fmul(L.q.sn, n1.y));
-    const double rhs = fsub(fmul(L.q.coth, n2.x), fmul(L.q.rci, n2.y));
+template <bool DEG>
+__device__ __forceinline__ void predicate(const EdgeArgs& A, const Req& q, bool in, double2 n1, double2 n2,
+                                          unsigned long long nid, Acc& acc) {
+    const double lhs = fadd(fmul(q.cs, n1.x), fmul(q.sn, n1.y));
+    const double rhs = fsub(fmul(q.coth, n2.x), fmul(q.rci, n2.y));
+    const bool   e   = in & (lhs > rhs);
     acc.comps += in;
-    if (in && lhs > rhs) {
-        ++acc.edges;
-        acc.fp += L.q.id + nid;
-        if (DEG) {
-            atomicAdd(&A.degrees[L.q.id], 1u);
-            atomicAdd(&A.degrees[nid], 1u);
-        }
+    acc.edges += e;
+    acc.fp += e ? q.id + nid : 0ull;
+    if (DEG && e) {
+        atomicAdd(&A.degrees[q.id], 1u);
+        atomicAdd(&A.degrees[nid], 1u);
+    }
+}
+
+// Same-annulus pairs that need the full dedup (sweep.hpp:517-526): not self,
+// and (theta_p, id_p) < (theta_q, id_q).  Rare; thread-serial.
+template <bool DEG>
+__device__ __forceinline__ void general_range(const EdgeArgs& A, const Req& q, std::uint64_t k0, std::uint64_t k1,
+                                              Acc& acc) {
+    for (std::uint64_t k = k0; k < k1; ++k) {
+        const unsigned long long nid = A.s_id[k];
+        const double             tq  = A.s_rec0[k].y;
+        const bool in = nid != q.id && (q.theta < tq || (q.theta == tq && q.id < nid));
+        predicate<DEG>(A, q, in, A.s_rec1[k], A.s_rec2[k], nid, acc);
     }
 }
 
@@ -252,11 +353,17 @@ constexpr int kBatch  = 64;
 constexpr int kStages = 3;
 
 struct Stage {
-    double2            r0[kBatch], r1[kBatch], r2[kBatch];
-    unsigned long long nid[kBatch + 2]; // copied from an even index: node t is nid[t + (base & 1)]
+    double2            r1[kBatch], r2[kBatch];
+    unsigned long long id[kBatch + 2]; // copied from an even index: node t is id[t + (base & 1)]
+};
+// A tile row as the tile loop needs it (staged once per warp in shared memory).
+struct RowSm {
+    double             cs, sn, coth, rci;
+    unsigned long long id, r0, r1, pad; // simple range [r0, r1)
 };
 struct WarpSmem {
     Stage              st[kStages];
+    RowSm              rows[32];
     unsigned long long bar[kStages];
     int                meta_g[kStages];
     int                meta_cnt[kStages];
@@ -301,40 +408,23 @@ __device__ __forceinline__ void warp_smem_init(WarpSmem* ws, int lane) {
     __syncwarp();
 }
 
-// Lane 0 queues one batch [base, base+cnt) of annulus-array nodes into stage
-// s.  The 8-byte node ids are copied from the even index below base (bulk
-// copies need 16 B alignment and size); the 16-byte records need nothing.
+// Lane 0 queues one batch [base, base+cnt) of sorted nodes into stage s.  The
+// 8-byte ids are copied from the even index below base (bulk copies need 16 B
+// alignment and size); the 16-byte records need nothing.
 __device__ __forceinline__ void issue_batch(const EdgeArgs& A, WarpSmem* ws, int s, int g, std::uint64_t base,
                                             int cnt) {
-    const std::uint32_t b16  = std::uint32_t(cnt) * 16u;
-    const std::uint64_t nb   = base & ~1ull;
-    const std::uint32_t bid  = std::uint32_t(((base + cnt + 1) & ~1ull) - nb) * 8u;
+    const std::uint32_t b16 = std::uint32_t(cnt) * 16u;
+    const std::uint64_t nb  = base & ~1ull;
+    const std::uint32_t bid = std::uint32_t(((base + cnt + 1) & ~1ull) - nb) * 8u;
     ws->meta_g[s] = g, ws->meta_cnt[s] = cnt, ws->meta_base[s] = base;
-    mbar_expect_tx(&ws->bar[s], 3 * b16 + bid);
-    bulk_g2s(ws->st[s].r0, A.rec0 + base, b16, &ws->bar[s]);
-    bulk_g2s(ws->st[s].r1, A.rec1 + base, b16, &ws->bar[s]);
-    bulk_g2s(ws->st[s].r2, A.rec2 + base, b16, &ws->bar[s]);
-    bulk_g2s(ws->st[s].nid, A.nid + nb, bid, &ws->bar[s]);
+    mbar_expect_tx(&ws->bar[s], 2 * b16 + bid);
+    bulk_g2s(ws->st[s].r1, A.s_rec1 + base, b16, &ws->bar[s]);
+    bulk_g2s(ws->st[s].r2, A.s_rec2 + base, b16, &ws->bar[s]);
+    bulk_g2s(ws->st[s].id, A.s_id + nb, bid, &ws->bar[s]);
 }
 
-__device__ __forceinline__ Lane shfl_lane(const Lane& L, int src) {
-    Lane o;
-    o.q.cs   = __shfl_sync(kFull, L.q.cs, src);
-    o.q.sn   = __shfl_sync(kFull, L.q.sn, src);
-    o.q.coth = __shfl_sync(kFull, L.q.coth, src);
-    o.q.rci  = __shfl_sync(kFull, L.q.rci, src);
-    o.q.tkey = __shfl_sync(kFull, L.q.tkey, src);
-    o.q.id   = __shfl_sync(kFull, L.q.id, src);
-    o.lo     = __shfl_sync(kFull, L.lo, src);
-    o.hi     = __shfl_sync(kFull, L.hi, src);
-    o.hmask  = __shfl_sync(kFull, L.hmask, src);
-    o.c0     = __shfl_sync(kFull, L.c0, src);
-    o.c1     = __shfl_sync(kFull, L.c1, src);
-    return o;
-}
-
-// Batch cursor over the groups' unions: group g spans [ga_g, gb_g);
-// unions live in lanes g*R (ga, gb); empty groups (gb <= ga) are skipped.
+// Batch cursor over the groups' unions: group g spans [ga_g, gb_g); unions
+// live in lanes g*R; empty groups (gb <= ga) are skipped.
 struct Cursor {
     int           g;
     std::uint64_t base, end;
@@ -352,19 +442,18 @@ __device__ __forceinline__ bool cursor_group(Cursor& c, int R, int C, std::uint6
 
 // R x C register tile, TMA-pipelined: the warp's C groups of R requests (one
 // per lane row, replicated over C = 32/R columns) against the unions of their
-// candidate ranges; lane (r, c) tests nodes c, c+C, ... of every batch against
-// request r of the current group.  Equivalent to testing each request's own
-// [c0, c1): nodes outside it cannot lie in its window.
-template <bool DEG, bool SAME, int R>
-__device__ __forceinline__ void tile_run(const EdgeArgs& A, const Lane& L, std::uint64_t ga, std::uint64_t gb,
-                                         Acc& acc, int lane, WarpSmem* ws, std::uint32_t& phase) {
+// simple ranges; lane (r, c) tests nodes c, c+C, ... of every batch against
+// request r of the current group.  Exact: a node is tested iff its index lies
+// in the row's range.
+template <bool DEG, int R>
+__device__ __forceinline__ void tile_run(const EdgeArgs& A, std::uint64_t ga, std::uint64_t gb, Acc& acc, int lane,
+                                         WarpSmem* ws, std::uint32_t& phase) {
     constexpr int C   = 32 / R;
     const int     col = lane % C, row = lane / C;
     Cursor        prod{0, 0, 0};
-    bool          more = cursor_group(prod, R, C, ga, gb);
+    bool          more    = cursor_group(prod, R, C, ga, gb);
     int           s_issue = 0, inflight = 0;
-    // prologue: fill the ring
-    while (more && inflight < kStages) {
+    while (more && inflight < kStages) { // prologue: fill the ring
         const int cnt = prod.end - prod.base < kBatch ? int(prod.end - prod.base) : kBatch;
         if (lane == 0) issue_batch(A, ws, s_issue, prod.g, prod.base, cnt);
         prod.base += kBatch;
@@ -375,26 +464,34 @@ __device__ __forceinline__ void tile_run(const EdgeArgs& A, const Lane& L, std::
         s_issue = s_issue + 1 == kStages ? 0 : s_issue + 1;
         ++inflight;
     }
-    int  s = 0, cur_g = -1;
-    Lane Lr;
+    int           s = 0, cur_g = -1;
+    Req           q{};
+    std::uint64_t r0 = 0, r1 = 0;
     while (inflight) {
         mbar_wait(&ws->bar[s], (phase >> s) & 1u);
         phase ^= 1u << s;
-        const int g = ws->meta_g[s], cnt = ws->meta_cnt[s], no = int(ws->meta_base[s] & 1);
+        const int           g = ws->meta_g[s], cnt = ws->meta_cnt[s];
+        const std::uint64_t base = ws->meta_base[s];
+        const int           no   = int(base & 1);
         if (g != cur_g) {
-            cur_g = g;
-            Lr    = shfl_lane(L, g * R + row);
+            cur_g            = g;
+            const RowSm& src = ws->rows[g * R + row];
+            q.cs = src.cs, q.sn = src.sn, q.coth = src.coth, q.rci = src.rci, q.id = src.id;
+            r0 = src.r0, r1 = src.r1;
         }
-        const Stage& S = ws->st[s];
+        // the row's range relative to this batch, clamped to [0, 64]: int compares
+        const int    lo = r0 > base ? int(r0 - base < 64 ? r0 - base : 64) : 0;
+        const int    hi = r1 > base ? int(r1 - base < 64 ? r1 - base : 64) : 0;
+        const Stage& S  = ws->st[s];
         if (cnt == kBatch) {
 #pragma unroll 4
             for (int i = 0; i < kBatch / C; ++i) {
                 const int t = col + C * i;
-                test_pair<DEG, SAME>(A, Lr, S.r0[t], S.r1[t], S.r2[t], S.nid[t + no], acc);
+                predicate<DEG>(A, q, (t >= lo) & (t < hi), S.r1[t], S.r2[t], S.id[t + no], acc);
             }
         } else {
             for (int t = col; t < cnt; t += C)
-                test_pair<DEG, SAME>(A, Lr, S.r0[t], S.r1[t], S.r2[t], S.nid[t + no], acc);
+                predicate<DEG>(A, q, (t >= lo) & (t < hi), S.r1[t], S.r2[t], S.id[t + no], acc);
         }
         __syncwarp();
         --inflight;
@@ -413,48 +510,41 @@ __device__ __forceinline__ void tile_run(const EdgeArgs& A, const Lane& L, std::
     __syncwarp();
 }
 
-template <bool DEG, bool SAME>
-__device__ __forceinline__ void tile_dispatch(int lgR, const EdgeArgs& A, const Lane& L, std::uint64_t ga,
-                                              std::uint64_t gb, Acc& acc, int lane, WarpSmem* ws,
-                                              std::uint32_t& phase) {
+template <bool DEG>
+__device__ __forceinline__ void tile_dispatch(int lgR, const EdgeArgs& A, const Req& q, std::uint64_t c0,
+                                              std::uint64_t c1, std::uint64_t ga, std::uint64_t gb, Acc& acc,
+                                              int lane, WarpSmem* ws, std::uint32_t& phase) {
+    __syncwarp();
+    RowSm& me = ws->rows[lane];
+    me.cs = q.cs, me.sn = q.sn, me.coth = q.coth, me.rci = q.rci, me.id = q.id, me.r0 = c0, me.r1 = c1;
+    __syncwarp();
     switch (lgR) {
-    case 0: tile_run<DEG, SAME, 1>(A, L, ga, gb, acc, lane, ws, phase); break;
-    case 1: tile_run<DEG, SAME, 2>(A, L, ga, gb, acc, lane, ws, phase); break;
-    case 2: tile_run<DEG, SAME, 4>(A, L, ga, gb, acc, lane, ws, phase); break;
-    case 3: tile_run<DEG, SAME, 8>(A, L, ga, gb, acc, lane, ws, phase); break;
-    case 4: tile_run<DEG, SAME, 16>(A, L, ga, gb, acc, lane, ws, phase); break;
-    default: tile_run<DEG, SAME, 32>(A, L, ga, gb, acc, lane, ws, phase); break;
+    case 0: tile_run<DEG, 1>(A, ga, gb, acc, lane, ws, phase); break;
+    case 1: tile_run<DEG, 2>(A, ga, gb, acc, lane, ws, phase); break;
+    case 2: tile_run<DEG, 4>(A, ga, gb, acc, lane, ws, phase); break;
+    case 3: tile_run<DEG, 8>(A, ga, gb, acc, lane, ws, phase); break;
+    case 4: tile_run<DEG, 16>(A, ga, gb, acc, lane, ws, phase); break;
+    default: tile_run<DEG, 32>(A, ga, gb, acc, lane, ws, phase); break;
     }
-}
-
-__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-    return v;
 }
 
 constexpr std::uint64_t kTilePiece = 4096;   // node range of one deferred tile task
 constexpr std::uint64_t kDeferCost = 150000; // defer a warp's big groups above this estimated cost
 
-// One warp = 32 requests (one per lane) x one target annulus.  Picks, from
-// the lanes' candidate ranges, the cheapest of: thread-serial (each lane its
-// own list; sparse warps) or an R x C tile for R in {1..32} (cost model in
-// issue cycles: ~22 per 32 pair slots, ~12 per staged batch, ~40 per group).
+// One warp = 32 requests (one per lane) with one simple index range each.
+// Picks, from the ranges, the cheapest of: thread-serial (each lane its own
+// list; sparse warps) or an R x C tile for R in {1..32} (cost model in issue
+// cycles: ~18 per 32 pair slots, ~10 per staged batch, ~40 per group).
 // Groups of very expensive warps are cut into tile tasks (balanced later).
-template <bool DEG, bool SAME>
-__device__ __forceinline__ void process_warp(const EdgeArgs& A, const AnnulusDev& J, const Lane& L, int kind, int job,
-                                             std::uint64_t p0, int w, Acc& acc, int lane, WarpSmem* ws,
-                                             std::uint32_t& phase) {
-    const std::uint64_t len = L.c1 - L.c0;
-    std::uint64_t       mx  = len;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const std::uint64_t t = __shfl_xor_sync(kFull, mx, o);
-        mx                    = t > mx ? t : mx;
-    }
+template <bool DEG>
+__device__ __forceinline__ void process_range(const EdgeArgs& A, const Req& q, std::uint64_t c0, std::uint64_t c1,
+                                              int kind, int job, std::uint64_t p0, int pass, Acc& acc, int lane,
+                                              WarpSmem* ws, std::uint32_t& phase) {
+    const std::uint64_t len = c1 > c0 ? c1 - c0 : 0;
+    const std::uint64_t mx  = warp_max_u64(len);
     if (mx == 0) return;
-    std::uint64_t gmin = len ? L.c0 : ~0ull, gmax = len ? L.c1 : 0ull;
-    std::uint64_t best = mx * 48 + 16; // thread-serial: per-lane loop, latency-exposed loads
+    std::uint64_t gmin = len ? c0 : ~0ull, gmax = len ? c1 : 0ull;
+    std::uint64_t best = mx * 36 + 16; // thread-serial: per-lane loop, latency-exposed loads
     int           lgR  = -1;
     std::uint64_t ga = 0, gb = 0; // this lane's group union for the chosen R (valid in group leaders)
 #pragma unroll
@@ -467,7 +557,7 @@ __device__ __forceinline__ void process_warp(const EdgeArgs& A, const AnnulusDev
         }
         const bool          leader = (lane & ((1 << k) - 1)) == 0;
         const std::uint64_t U      = gmax > gmin ? gmax - gmin : 0;
-        const std::uint64_t mine   = leader && U ? (U << k) * 22 / 32 + ((U + kBatch - 1) / kBatch) * 12 + 40 : 0;
+        const std::uint64_t mine   = leader && U ? (U << k) * 18 / 32 + ((U + kBatch - 1) / kBatch) * 10 + 40 : 0;
         const std::uint64_t cost   = warp_sum_u64(mine);
         if (cost < best) best = cost, lgR = k, ga = gmin, gb = gmax;
     }
@@ -477,8 +567,7 @@ __device__ __forceinline__ void process_warp(const EdgeArgs& A, const AnnulusDev
         if (lgR < 0 && lane == 0) atomicAdd(&A.dbg[18], 1ull), atomicAdd(&A.dbg[19], 32ull * mx), atomicAdd(&A.dbg[20], tl);
     }
     if (lgR < 0) { // sparse: every lane walks its own few candidates
-        for (std::uint64_t k = L.c0; k < L.c1; ++k)
-            test_pair<DEG, SAME>(A, L, A.rec0[k], A.rec1[k], A.rec2[k], A.nid[k], acc);
+        for (std::uint64_t k = c0; k < c1; ++k) predicate<DEG>(A, q, true, A.s_rec1[k], A.s_rec2[k], A.s_id[k], acc);
         return;
     }
     const int  R      = 1 << lgR;
@@ -490,9 +579,9 @@ __device__ __forceinline__ void process_warp(const EdgeArgs& A, const AnnulusDev
         atomicAdd(&A.dbg[12 + lgR], static_cast<unsigned long long>((gb - ga) << lgR));
     }
     if (best > kDeferCost && A.task_cap) { // cut big groups into balanced tile tasks
-        const std::uint64_t npc = leader && gb - ga > kTilePiece ? (gb - (ga & ~1ull) + kTilePiece - 1) / kTilePiece : 0;
-        // warp-wide reservation
-        std::uint64_t incl = npc;
+        const std::uint64_t a0   = ga & ~1ull;
+        const std::uint64_t npc  = leader && gb - ga > kTilePiece ? (gb - a0 + kTilePiece - 1) / kTilePiece : 0;
+        std::uint64_t       incl = npc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const std::uint64_t t = __shfl_up_sync(kFull, incl, o);
@@ -509,28 +598,17 @@ __device__ __forceinline__ void process_warp(const EdgeArgs& A, const AnnulusDev
                     if (A.dbg) atomicAdd(&A.dbg[21], static_cast<unsigned long long>(total));
                 }
                 const std::uint64_t first = t0 + incl - npc;
-                const std::uint64_t a0    = ga & ~1ull; // even piece starts: the TMA base rounding stays inside a piece
-                for (std::uint64_t i = 0; i < npc; ++i) {
+                for (std::uint64_t i = 0; i < npc; ++i) { // even piece starts (TMA id copies)
                     TileTask& T = A.tasks[first + i];
                     T.p0 = p0 + std::uint64_t(lane), T.u0 = i ? a0 + i * kTilePiece : ga;
                     T.u1 = a0 + (i + 1) * kTilePiece < gb ? a0 + (i + 1) * kTilePiece : gb;
-                    T.job = job, T.kind = std::int16_t(kind), T.lgR = std::int16_t(lgR), T.w = w;
+                    T.job = job, T.kind = std::int16_t(kind), T.lgR = std::int16_t(lgR), T.w = pass;
                 }
                 if (npc) gb = ga; // handed off
             }
         }
     }
-    tile_dispatch<DEG, SAME>(lgR, A, L, ga, gb, acc, lane, ws, phase);
-}
-
-__device__ __forceinline__ int find_pair_job(const PairJob* __restrict__ jobs, int n, std::uint64_t gw) {
-    int lo = 0, hi = n - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (jobs[mid].warp_begin <= gw) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
+    tile_dispatch<DEG>(lgR, A, q, c0, c1, ga, gb, acc, lane, ws, phase);
 }
 
 __device__ __forceinline__ WarpSmem* my_warp_smem() {
@@ -538,23 +616,54 @@ __device__ __forceinline__ WarpSmem* my_warp_smem() {
     return reinterpret_cast<WarpSmem*>(dyn_smem) + (threadIdx.x >> 5);
 }
 
+// Work item t -> (pair job, batch of 32 requests).  Items are ordered by
+// angular block first (block b holds batches [floor(b nb/M), floor((b+1) nb/M))
+// of every job), so the warps in flight all work on one narrow angular band.
+__device__ __forceinline__ void map_item(const EdgeArgs& A, std::uint64_t t, int& job, std::uint64_t& batch) {
+    int lo = 0, hi = A.nblk - 1; // last block with prefix <= t
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (A.blk_prefix[mid] <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    const int            b     = lo;
+    const std::uint32_t  local = std::uint32_t(t - A.blk_prefix[b]);
+    const std::uint32_t* off   = A.blk_job_off + std::size_t(b) * A.n_stream_jobs;
+    int                  k0 = 0, k1 = A.n_stream_jobs - 1; // last job with off <= local
+    while (k0 < k1) {
+        const int mid = (k0 + k1 + 1) >> 1;
+        if (off[mid] <= local) k0 = mid;
+        else k1 = mid - 1;
+    }
+    job                    = k0;
+    const PairJob&      J  = A.stream_jobs[job];
+    const std::uint64_t nb = (J.req_end - J.req_off + 31) / 32;
+    batch                  = std::uint64_t(b) * nb / std::uint64_t(A.nblk) + (local - off[k0]);
+}
+
 template <bool DEG>
 __global__ void __launch_bounds__(256, 2) stream_pairs_kernel(EdgeArgs A) {
     const int           lane = threadIdx.x & 31;
-    const std::uint64_t gw   = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (gw >= A.stream_warps) return;
+    const std::uint64_t t    = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (t >= A.stream_warps) return;
     WarpSmem* ws = my_warp_smem();
     warp_smem_init(ws, lane);
-    std::uint32_t       phase = 0;
-    const int           job = find_pair_job(A.stream_jobs, A.n_stream_jobs, gw);
-    const PairJob       Jb  = A.stream_jobs[job];
-    const std::uint64_t p0  = Jb.req_off + (gw - Jb.warp_begin) * 32;
+    std::uint32_t phase = 0;
+    Acc           acc;
+    int           job;
+    std::uint64_t batch;
+    map_item(A, t, job, batch);
+    const PairJob       Jb = A.stream_jobs[job];
+    const std::uint64_t p0 = Jb.req_off + batch * 32;
     Lane                L;
     setup_stream(A, Jb, p0 + lane, L);
-    Acc acc;
-    const AnnulusDev& J = A.ann[Jb.j];
-    if (Jb.j == Jb.a) process_warp<DEG, true>(A, J, L, 0, job, p0, 0, acc, lane, ws, phase);
-    else process_warp<DEG, false>(A, J, L, 0, job, p0, 0, acc, lane, ws, phase);
+    process_range<DEG>(A, L.q, L.s0, L.s1, 0, job, p0, 0, acc, lane, ws, phase);
+    if (Jb.j != Jb.a) {
+        process_range<DEG>(A, L.q, L.h0, L.h1, 0, job, p0, 1, acc, lane, ws, phase);
+    } else { // same-annulus pairs with wrapped or halo points: full dedup
+        general_range<DEG>(A, L.q, L.g0, L.g1, acc);
+        general_range<DEG>(A, L.q, L.h0, L.h1, acc);
+    }
     flush(acc, &A.ctr[0], lane);
 }
 
@@ -565,23 +674,29 @@ __global__ void __launch_bounds__(256, 2) glob_req_kernel(EdgeArgs A) {
     if (gw >= A.glob_warps) return;
     WarpSmem* ws = my_warp_smem();
     warp_smem_init(ws, lane);
-    std::uint32_t       phase = 0;
-    const int           job = find_pair_job(A.glob_jobs, A.n_glob_jobs, gw);
+    std::uint32_t phase = 0;
+    int           lo = 0, hi = A.n_glob_jobs - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (A.glob_jobs[mid].warp_begin <= gw) lo = mid;
+        else hi = mid - 1;
+    }
+    const int           job = lo;
     const PairJob       Jb  = A.glob_jobs[job];
     const std::uint64_t g0  = Jb.req_off + (gw - Jb.warp_begin) * 32;
-    const AnnulusDev&   J   = A.ann[Jb.j];
     Acc                 acc;
 #pragma unroll 1
     for (int w = 0; w < 4; ++w) {
         Lane L;
         setup_global(A, Jb, g0 + lane, w, L);
-        process_warp<DEG, false>(A, J, L, 1, job, g0, w, acc, lane, ws, phase);
+        process_range<DEG>(A, L.q, L.s0, L.s1, 1, job, g0, w, acc, lane, ws, phase);
     }
     flush(acc, &A.ctr[1], lane);
 }
 
 // Deferred tile pieces: the R requests of one group x kTilePiece nodes
-// (KIND 0 streaming requests, 1 global requests).
+// (KIND 0 streaming requests with T.w = pass 0 owned / 1 halo block, KIND 1
+// global requests with T.w = window).
 template <bool DEG, int KIND>
 __global__ void __launch_bounds__(256, 2) tile_tasks_kernel(EdgeArgs A) {
     const int           lane  = threadIdx.x & 31;
@@ -599,14 +714,12 @@ __global__ void __launch_bounds__(256, 2) tile_tasks_kernel(EdgeArgs A) {
         const std::uint64_t ga = lane == 0 ? T.u0 : 0, gb = lane == 0 ? T.u1 : 0;
         Lane                L;
         if (KIND == 0) {
-            const PairJob Jb = A.stream_jobs[T.job];
-            setup_stream(A, Jb, p, L);
-            if (Jb.j == Jb.a) tile_dispatch<DEG, true>(T.lgR, A, L, ga, gb, acc, lane, ws, phase);
-            else tile_dispatch<DEG, false>(T.lgR, A, L, ga, gb, acc, lane, ws, phase);
+            setup_stream(A, A.stream_jobs[T.job], p, L);
+            if (T.w == 0) tile_dispatch<DEG>(T.lgR, A, L.q, L.s0, L.s1, ga, gb, acc, lane, ws, phase);
+            else tile_dispatch<DEG>(T.lgR, A, L.q, L.h0, L.h1, ga, gb, acc, lane, ws, phase);
         } else {
-            const PairJob Jb = A.glob_jobs[T.job];
-            setup_global(A, Jb, p, T.w, L);
-            tile_dispatch<DEG, false>(T.lgR, A, L, ga, gb, acc, lane, ws, phase);
+            setup_global(A, A.glob_jobs[T.job], p, T.w, L);
+            tile_dispatch<DEG>(T.lgR, A, L.q, L.s0, L.s1, ga, gb, acc, lane, ws, phase);
         }
     }
     flush(acc, &A.ctr[KIND], lane);
@@ -623,8 +736,8 @@ __global__ void __launch_bounds__(kGGTile) glob_pairs_kernel(EdgeArgs A, std::ui
     auto start = [nT](std::uint64_t r) { return r * nT - r * (r - 1) / 2; };
     while (I > 0 && start(I) > t) --I;
     while (start(I + 1) <= t) ++I;
-    const std::uint64_t J = I + (t - start(I));
-    const std::uint64_t nG = A.n_glob;
+    const std::uint64_t J   = I + (t - start(I));
+    const std::uint64_t nG  = A.n_glob;
     const std::uint64_t col = J * kGGTile + threadIdx.x;
     if (col < nG) {
         s1[threadIdx.x] = A.rec1[A.n_ext + col];
@@ -634,25 +747,14 @@ __global__ void __launch_bounds__(kGGTile) glob_pairs_kernel(EdgeArgs A, std::ui
     const std::uint64_t i = I * kGGTile + threadIdx.x;
     Acc                 acc;
     if (i < nG) {
+        Req           q{};
         const double2 r1 = A.rec1[A.n_ext + i], r2 = A.rec2[A.n_ext + i];
-        const double  rci = fmul(A.cosh_R, r2.y);
-        std::uint64_t k0  = J * kGGTile;
+        q.cs = r1.x, q.sn = r1.y, q.coth = r2.x, q.rci = fmul(A.cosh_R, r2.y), q.id = i;
+        std::uint64_t k0 = J * kGGTile;
         if (k0 <= i) k0 = i + 1;
         const std::uint64_t k1 = (J + 1) * kGGTile < nG ? (J + 1) * kGGTile : nG;
-        for (std::uint64_t k = k0; k < k1; ++k) {
-            const double2 n1  = s1[k - J * kGGTile], n2 = s2[k - J * kGGTile];
-            const double  lhs = fadd(fmul(r1.x, n1.x), fmul(r1.y, n1.y));
-            const double  rhs = fsub(fmul(r2.x, n2.x), fmul(rci, n2.y));
-            ++acc.comps;
-            if (lhs > rhs) {
-                ++acc.edges;
-                acc.fp += i + k;
-                if (DEG) {
-                    atomicAdd(&A.degrees[i], 1u);
-                    atomicAdd(&A.degrees[k], 1u);
-                }
-            }
-        }
+        for (std::uint64_t k = k0; k < k1; ++k)
+            predicate<DEG>(A, q, true, s1[k - J * kGGTile], s2[k - J * kGGTile], k, acc);
     }
     flush(acc, &A.ctr[2], threadIdx.x & 31);
 }
@@ -660,14 +762,22 @@ __global__ void __launch_bounds__(kGGTile) glob_pairs_kernel(EdgeArgs A, std::ui
 } // namespace
 
 void launch_cell_index(const EdgeArgs& a, std::uint64_t, cudaStream_t st, std::uint64_t* launches) {
-    const std::uint64_t n = a.n_ext > std::uint64_t(a.count) ? a.n_ext : std::uint64_t(a.count);
     if (a.first_streaming >= a.count) return;
-    cell_index_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a);
+    const std::uint64_t n  = a.n_ext > std::uint64_t(a.count) ? a.n_ext : std::uint64_t(a.count);
+    const unsigned      gb = unsigned((n + 255) / 256);
+    beta_cells_kernel<<<gb, 256, 0, st>>>(a);
     ++*launches;
+    if (a.n_ext) {
+        const unsigned g = unsigned((a.n_ext + 255) / 256);
+        rank_kernel<<<g, 256, 0, st>>>(a);
+        scatter_kernel<<<g, 256, 0, st>>>(a);
+        lambda_cells_kernel<<<g, 256, 0, st>>>(a);
+        *launches += 3;
+    }
 }
 
 void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches) {
-    const bool deg = a.degrees != nullptr;
+    const bool  deg   = a.degrees != nullptr;
     static bool attrs = false;
     if (!attrs) { // > 48 KiB of dynamic shared memory per block
         cudaFuncSetAttribute(stream_pairs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
@@ -680,10 +790,12 @@ void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches) {
         cudaFuncSetAttribute(tile_tasks_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
         attrs = true;
     }
-    if (a.stream_warps) {
+    if (a.stream_warps) { // one warp per item, items in angular-block order
         const unsigned blocks = unsigned((a.stream_warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+        if (a.ev_pairs0) cudaEventRecord(a.ev_pairs0, st);
         if (deg) stream_pairs_kernel<true><<<blocks, 32 * kWarpsPerBlock, kTileSmem, st>>>(a);
         else stream_pairs_kernel<false><<<blocks, 32 * kWarpsPerBlock, kTileSmem, st>>>(a);
+        if (a.ev_pairs1) cudaEventRecord(a.ev_pairs1, st);
         ++*launches;
     }
     if (a.glob_warps) {

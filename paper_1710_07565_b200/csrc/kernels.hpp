@@ -29,6 +29,7 @@ void launch_mt_uniforms(const SamplerArgs& a, cudaStream_t st, std::uint64_t* la
 
 struct EdgeArgs {
     const AnnulusDev* ann = nullptr;
+    AnnulusDev*       ann_rw = nullptr; // same table (lambda_cells_kernel writes `wrap`)
     int               count = 0, first_streaming = 0;
     std::uint64_t     n_ext = 0;   // streaming extended points; global points follow
     std::uint64_t     n_glob = 0;  // global points (ids 0..n_glob-1)
@@ -37,15 +38,27 @@ struct EdgeArgs {
     const double2*    rec0 = nullptr;
     const double2*    rec1 = nullptr;
     const double2*    rec2 = nullptr;
-    std::uint64_t*    cellstart = nullptr;
-    unsigned long long* nid = nullptr;       // [n_ext + 2] vertex id | halo bit (cell_index_kernel)
+    std::uint64_t*    cellstart = nullptr;  // beta cells (sampler order)
+    std::uint64_t*    lcellstart = nullptr; // lambda cells (sorted owned blocks)
+    std::uint64_t*    perm = nullptr;       // sampler index -> sorted index
+    // lambda-sorted copies (per annulus: owned block, halo block)
+    double*           s_beta = nullptr;
+    double*           s_hw   = nullptr;
+    double2*          s_rec0 = nullptr;
+    double2*          s_rec1 = nullptr;
+    double2*          s_rec2 = nullptr;
+    unsigned long long* s_id = nullptr;     // [n_ext + 2] vertex ids
     unsigned long long* dmax_bits = nullptr; // per annulus, max half-width (bits)
     double            cosh_R = 1.0;
     double            chunk0_upper = 0.0; // chunk_upper_bound(0, P)
     int               lift_part = 0;      // shard owns engine P-1 (halo = lifted chunk 0)
     const PairJob*    stream_jobs = nullptr;
     int               n_stream_jobs = 0;
-    std::uint64_t     stream_warps = 0;
+    std::uint64_t     stream_warps = 0;      // work items (batches of 32 requests x target annulus)
+    const std::uint64_t* blk_prefix = nullptr; // [nblk + 1] items before angular block b
+    const std::uint32_t* blk_job_off = nullptr; // [nblk * n_stream_jobs] item offset of job k inside block b
+    int               nblk = 1;
+    cudaEvent_t       ev_pairs0 = nullptr, ev_pairs1 = nullptr; // optional: time the streaming pair kernel
     const PairJob*    glob_jobs = nullptr;
     int               n_glob_jobs = 0;
     std::uint64_t     glob_warps = 0;
