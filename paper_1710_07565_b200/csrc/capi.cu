@@ -192,13 +192,11 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
     for (std::uint32_t a = L.first_streaming; a < L.count; ++a) {
         const std::uint64_t na = pl.ann[a].end - pl.ann[a].off;
         if (!na) continue;
-        for (std::uint32_t j = a; j < L.count; ++j) {
-            if (pl.ann[j].end == pl.ann[j].off) continue;
-            PairJob J{};
-            J.warp_begin = pl.swarps, J.req_off = pl.ann[a].off, J.req_end = pl.ann[a].end, J.a = int(a), J.j = int(j);
-            pl.sjobs.push_back(J);
-            pl.swarps += (na + 31) / 32;
-        }
+        // one item = 32 requests of annulus a against every target annulus j >= a
+        PairJob J{};
+        J.warp_begin = pl.swarps, J.req_off = pl.ann[a].off, J.req_end = pl.ann[a].end, J.a = int(a), J.j = -1;
+        pl.sjobs.push_back(J);
+        pl.swarps += (na + 31) / 32;
     }
     if (pl.n_glob)
         for (std::uint32_t s = L.first_streaming; s < L.count; ++s) {

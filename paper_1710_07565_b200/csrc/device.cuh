@@ -38,7 +38,8 @@ struct StreamJob {
 };
 
 // Work list of the pair kernels: requests of annulus `a` (or the global
-// points, a = -1) against nodes of annulus `j`, in batches of 32 requests.
+// points, a = -1) against nodes of annulus `j` (streaming jobs: j = -1, every
+// target annulus >= a), in batches of 32 requests.
 struct PairJob {
     std::uint64_t warp_begin;   // prefix over jobs
     std::uint64_t req_off, req_end;
@@ -52,7 +53,7 @@ struct TileTask {
     std::uint64_t p0, u0, u1;
     std::int32_t  job;
     std::int16_t  kind, lgR;
-    std::int32_t  w, pad;
+    std::int32_t  w, j; // w: pass (streaming) or window (global); j: target annulus
 };
 
 struct Counters { // one per edge-producing kernel family

@@ -24,7 +24,7 @@
 //   lambda_cells_kernel lambda-cell starts of the owned blocks, first wrapped index
 //   stream_pairs_kernel streaming requests: one warp per 32 requests x target
 //                       annulus; adaptive R x C register tile over TMA-staged
-//                       node batches, thread-serial when sparse
+//                       node batches, a flattened pair list when sparse
 //   glob_req_kernel     global requests x owned streaming nodes (same engine)
 //   tile_tasks_kernel   deferred pieces of very large tiles, load-balanced
 //   glob_pairs_kernel   global unit, 128x128 tiles of the upper triangle
@@ -230,13 +230,13 @@ __device__ __forceinline__ void window_ranges(const EdgeArgs& A, const AnnulusDe
     }
 }
 
-// Streaming request at sorted index p of annulus Jb.a against annulus Jb.j
+// Streaming request at sorted index p of annulus a against annulus j
 // (sweep.hpp:455-461, 478-479).
-__device__ __forceinline__ void setup_stream(const EdgeArgs& A, const PairJob& Jb, std::uint64_t p, Lane& L) {
+__device__ __forceinline__ void setup_stream(const EdgeArgs& A, const PairJob& Jb, int j, std::uint64_t p, Lane& L) {
     L = Lane{};
     if (p >= Jb.req_end) return;
     const AnnulusDev& Aa = A.ann[Jb.a];
-    const AnnulusDev& Aj = A.ann[Jb.j];
+    const AnnulusDev& Aj = A.ann[j];
     const double      b  = A.s_beta[p];
     const double      hw = A.s_hw[p];
     const double2     r0 = A.s_rec0[p], r1 = A.s_rec1[p], r2 = A.s_rec2[p];
@@ -245,7 +245,7 @@ __device__ __forceinline__ void setup_stream(const EdgeArgs& A, const PairJob& J
     L.q.theta       = r0.y;
     const bool halo = p >= Aa.halo;
     double     lo, hi;
-    if (Jb.j == Jb.a) { // own window [b, b + 2hw)
+    if (j == Jb.a) { // own window [b, b + 2hw)
         lo = b;
         hi = fadd(b, fmul(2.0, hw));
     } else { // propagated window [lambda - h_j, lambda + h_j)
@@ -254,7 +254,7 @@ __device__ __forceinline__ void setup_stream(const EdgeArgs& A, const PairJob& J
         hi             = fadd(r0.x, h);
     }
     window_ranges(A, Aj, lo, hi, !halo, L); // halo requests: owned nodes only (no Foreign x Foreign)
-    if (Jb.j == Jb.a) {
+    if (j == Jb.a) {
         if (!halo && p < Aa.wrap) { // theta == lambda and index order == (lambda, id) order
             const std::uint64_t w = Aj.wrap;
             L.g0 = L.s0 > w ? L.s0 : w, L.g1 = L.s1; // wrapped nodes: general
@@ -331,6 +331,31 @@ __device__ __forceinline__ void predicate(const EdgeArgs& A, const Req& q, bool 
     }
 }
 
+// Tile-loop variant: per-row 32-bit counters; the fingerprint is folded as
+// E * id_p + sum(node ids) when the row changes (RowAcc::fold).
+struct RowAcc {
+    std::uint32_t      comps = 0, edges = 0;
+    unsigned long long nsum  = 0;
+    __device__ __forceinline__ void fold(Acc& acc, unsigned long long id) {
+        acc.comps += comps, acc.edges += edges, acc.fp += edges * id + nsum;
+        comps = edges = 0, nsum = 0;
+    }
+};
+template <bool DEG>
+__device__ __forceinline__ void predicate_row(const EdgeArgs& A, const Req& q, bool in, double2 n1, double2 n2,
+                                              unsigned long long nid, RowAcc& ra) {
+    const double lhs = fadd(fmul(q.cs, n1.x), fmul(q.sn, n1.y));
+    const double rhs = fsub(fmul(q.coth, n2.x), fmul(q.rci, n2.y));
+    const bool   e   = in & (lhs > rhs);
+    ra.comps += in;
+    ra.edges += e;
+    ra.nsum += e ? nid : 0ull;
+    if (DEG && e) {
+        atomicAdd(&A.degrees[q.id], 1u);
+        atomicAdd(&A.degrees[nid], 1u);
+    }
+}
+
 // Same-annulus pairs that need the full dedup (sweep.hpp:517-526): not self,
 // and (theta_p, id_p) < (theta_q, id_q).  Rare; thread-serial.
 template <bool DEG>
@@ -349,8 +374,8 @@ __device__ __forceinline__ void general_range(const EdgeArgs& A, const Req& q, s
 // by TMA bulk copies (cp.async.bulk, completion on an mbarrier), SoA so that
 // lanes reading consecutive nodes are conflict-free and a whole-warp read of
 // one node is a broadcast.
-constexpr int kBatch  = 64;
-constexpr int kStages = 3;
+constexpr int kBatch  = 128;
+constexpr int kStages = 2;
 
 struct Stage {
     double2            r1[kBatch], r2[kBatch];
@@ -467,6 +492,7 @@ __device__ __forceinline__ void tile_run(const EdgeArgs& A, std::uint64_t ga, st
     int           s = 0, cur_g = -1;
     Req           q{};
     std::uint64_t r0 = 0, r1 = 0;
+    RowAcc        ra;
     while (inflight) {
         mbar_wait(&ws->bar[s], (phase >> s) & 1u);
         phase ^= 1u << s;
@@ -474,24 +500,25 @@ __device__ __forceinline__ void tile_run(const EdgeArgs& A, std::uint64_t ga, st
         const std::uint64_t base = ws->meta_base[s];
         const int           no   = int(base & 1);
         if (g != cur_g) {
+            ra.fold(acc, q.id);
             cur_g            = g;
             const RowSm& src = ws->rows[g * R + row];
             q.cs = src.cs, q.sn = src.sn, q.coth = src.coth, q.rci = src.rci, q.id = src.id;
             r0 = src.r0, r1 = src.r1;
         }
-        // the row's range relative to this batch, clamped to [0, 64]: int compares
-        const int    lo = r0 > base ? int(r0 - base < 64 ? r0 - base : 64) : 0;
-        const int    hi = r1 > base ? int(r1 - base < 64 ? r1 - base : 64) : 0;
+        // the row's range relative to this batch, clamped to [0, kBatch]: int compares
+        const int    lo = r0 > base ? int(r0 - base < kBatch ? r0 - base : kBatch) : 0;
+        const int    hi = r1 > base ? int(r1 - base < kBatch ? r1 - base : kBatch) : 0;
         const Stage& S  = ws->st[s];
         if (cnt == kBatch) {
 #pragma unroll 4
             for (int i = 0; i < kBatch / C; ++i) {
                 const int t = col + C * i;
-                predicate<DEG>(A, q, (t >= lo) & (t < hi), S.r1[t], S.r2[t], S.id[t + no], acc);
+                predicate_row<DEG>(A, q, (t >= lo) & (t < hi), S.r1[t], S.r2[t], S.id[t + no], ra);
             }
         } else {
             for (int t = col; t < cnt; t += C)
-                predicate<DEG>(A, q, (t >= lo) & (t < hi), S.r1[t], S.r2[t], S.id[t + no], acc);
+                predicate_row<DEG>(A, q, (t >= lo) & (t < hi), S.r1[t], S.r2[t], S.id[t + no], ra);
         }
         __syncwarp();
         --inflight;
@@ -507,6 +534,7 @@ __device__ __forceinline__ void tile_run(const EdgeArgs& A, std::uint64_t ga, st
         }
         s = s + 1 == kStages ? 0 : s + 1;
     }
+    ra.fold(acc, q.id);
     __syncwarp();
 }
 
@@ -528,23 +556,57 @@ __device__ __forceinline__ void tile_dispatch(int lgR, const EdgeArgs& A, const 
     }
 }
 
+// Flattened pairs: the warp's (request, candidate) pairs numbered 0..T-1 in
+// lane order and processed 32 per round, one pair per lane — no divergence,
+// independent loads.  The owner of pair t is the last lane whose exclusive
+// prefix is <= t (5-step shuffle search).  For sparse and medium warps.
+template <bool DEG>
+__device__ __forceinline__ void flat_run(const EdgeArgs& A, const Req& q, std::uint64_t c0, std::uint32_t len,
+                                         std::uint32_t excl, std::uint32_t total, Acc& acc, int lane,
+                                         WarpSmem* ws) {
+    __syncwarp();
+    RowSm& me = ws->rows[lane];
+    me.cs = q.cs, me.sn = q.sn, me.coth = q.coth, me.rci = q.rci, me.id = q.id, me.r0 = c0 - excl;
+    __syncwarp();
+    for (std::uint32_t B = 0; B < total; B += 32) {
+        const std::uint32_t t = B + std::uint32_t(lane);
+        int                 o = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const std::uint32_t v = __shfl_sync(kFull, excl, o + step);
+            if (v <= t) o += step;
+        }
+        if (t < total) {
+            const RowSm&        r = ws->rows[o];
+            const std::uint64_t k = r.r0 + t; // = c0_o + (t - excl_o)
+            Req                 rq;
+            rq.cs = r.cs, rq.sn = r.sn, rq.coth = r.coth, rq.rci = r.rci, rq.id = r.id;
+            predicate<DEG>(A, rq, true, A.s_rec1[k], A.s_rec2[k], A.s_id[k], acc);
+        }
+    }
+    __syncwarp();
+}
+
 constexpr std::uint64_t kTilePiece = 4096;   // node range of one deferred tile task
 constexpr std::uint64_t kDeferCost = 150000; // defer a warp's big groups above this estimated cost
 
+constexpr std::uint32_t kFlatMax = 1u << 16; // flattened path only below this many pairs per warp
+
 // One warp = 32 requests (one per lane) with one simple index range each.
-// Picks, from the ranges, the cheapest of: thread-serial (each lane its own
-// list; sparse warps) or an R x C tile for R in {1..32} (cost model in issue
-// cycles: ~18 per 32 pair slots, ~10 per staged batch, ~40 per group).
-// Groups of very expensive warps are cut into tile tasks (balanced later).
+// Picks, from the ranges, the cheapest of: the flattened pair list (sparse and
+// medium warps) or an R x C tile for R in {1..32} (cost model in issue
+// cycles: ~20 per 32 pair slots, ~10 per staged batch, ~40 per group; ~40
+// per flattened round).  Groups of very expensive warps are cut into tile
+// tasks (balanced later).
 template <bool DEG>
 __device__ __forceinline__ void process_range(const EdgeArgs& A, const Req& q, std::uint64_t c0, std::uint64_t c1,
-                                              int kind, int job, std::uint64_t p0, int pass, Acc& acc, int lane,
-                                              WarpSmem* ws, std::uint32_t& phase) {
-    const std::uint64_t len = c1 > c0 ? c1 - c0 : 0;
-    const std::uint64_t mx  = warp_max_u64(len);
-    if (mx == 0) return;
+                                              int kind, int job, int j, std::uint64_t p0, int pass, Acc& acc,
+                                              int lane, WarpSmem* ws, std::uint32_t& phase) {
+    const std::uint64_t len   = c1 > c0 ? c1 - c0 : 0;
+    const std::uint64_t total = warp_sum_u64(len);
+    if (total == 0) return;
     std::uint64_t gmin = len ? c0 : ~0ull, gmax = len ? c1 : 0ull;
-    std::uint64_t best = mx * 36 + 16; // thread-serial: per-lane loop, latency-exposed loads
+    std::uint64_t best = total < kFlatMax ? (total + 31) / 32 * 40 + 60 : ~0ull;
     int           lgR  = -1;
     std::uint64_t ga = 0, gb = 0; // this lane's group union for the chosen R (valid in group leaders)
 #pragma unroll
@@ -557,17 +619,22 @@ __device__ __forceinline__ void process_range(const EdgeArgs& A, const Req& q, s
         }
         const bool          leader = (lane & ((1 << k) - 1)) == 0;
         const std::uint64_t U      = gmax > gmin ? gmax - gmin : 0;
-        const std::uint64_t mine   = leader && U ? (U << k) * 18 / 32 + ((U + kBatch - 1) / kBatch) * 10 + 40 : 0;
+        const std::uint64_t mine   = leader && U ? (U << k) * 20 / 32 + ((U + kBatch - 1) / kBatch) * 10 + 40 : 0;
         const std::uint64_t cost   = warp_sum_u64(mine);
         if (cost < best) best = cost, lgR = k, ga = gmin, gb = gmax;
     }
-    if (A.dbg) {
-        const unsigned long long tl = warp_sum_u64(len);
-        if (lane == 0) atomicAdd(&A.dbg[22], 1ull), atomicAdd(&A.dbg[23], tl);
-        if (lgR < 0 && lane == 0) atomicAdd(&A.dbg[18], 1ull), atomicAdd(&A.dbg[19], 32ull * mx), atomicAdd(&A.dbg[20], tl);
+    if (A.dbg && lane == 0) {
+        atomicAdd(&A.dbg[22], 1ull), atomicAdd(&A.dbg[23], total);
+        if (lgR < 0) atomicAdd(&A.dbg[18], 1ull), atomicAdd(&A.dbg[19], (total + 31) / 32 * 32), atomicAdd(&A.dbg[20], total);
     }
-    if (lgR < 0) { // sparse: every lane walks its own few candidates
-        for (std::uint64_t k = c0; k < c1; ++k) predicate<DEG>(A, q, true, A.s_rec1[k], A.s_rec2[k], A.s_id[k], acc);
+    if (lgR < 0) {
+        std::uint32_t incl = std::uint32_t(len);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const std::uint32_t t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += t;
+        }
+        flat_run<DEG>(A, q, c0, std::uint32_t(len), incl - std::uint32_t(len), std::uint32_t(total), acc, lane, ws);
         return;
     }
     const int  R      = 1 << lgR;
@@ -602,7 +669,7 @@ __device__ __forceinline__ void process_range(const EdgeArgs& A, const Req& q, s
                     TileTask& T = A.tasks[first + i];
                     T.p0 = p0 + std::uint64_t(lane), T.u0 = i ? a0 + i * kTilePiece : ga;
                     T.u1 = a0 + (i + 1) * kTilePiece < gb ? a0 + (i + 1) * kTilePiece : gb;
-                    T.job = job, T.kind = std::int16_t(kind), T.lgR = std::int16_t(lgR), T.w = pass;
+                    T.job = job, T.kind = std::int16_t(kind), T.lgR = std::int16_t(lgR), T.w = pass, T.j = j;
                 }
                 if (npc) gb = ga; // handed off
             }
@@ -655,14 +722,18 @@ __global__ void __launch_bounds__(256, 2) stream_pairs_kernel(EdgeArgs A) {
     map_item(A, t, job, batch);
     const PairJob       Jb = A.stream_jobs[job];
     const std::uint64_t p0 = Jb.req_off + batch * 32;
-    Lane                L;
-    setup_stream(A, Jb, p0 + lane, L);
-    process_range<DEG>(A, L.q, L.s0, L.s1, 0, job, p0, 0, acc, lane, ws, phase);
-    if (Jb.j != Jb.a) {
-        process_range<DEG>(A, L.q, L.h0, L.h1, 0, job, p0, 1, acc, lane, ws, phase);
-    } else { // same-annulus pairs with wrapped or halo points: full dedup
-        general_range<DEG>(A, L.q, L.g0, L.g1, acc);
-        general_range<DEG>(A, L.q, L.h0, L.h1, acc);
+#pragma unroll 1
+    for (int j = Jb.a; j < A.count; ++j) { // every target annulus of these 32 requests
+        if (A.ann[j].end == A.ann[j].off) continue;
+        Lane L;
+        setup_stream(A, Jb, j, p0 + lane, L);
+        process_range<DEG>(A, L.q, L.s0, L.s1, 0, job, j, p0, 0, acc, lane, ws, phase);
+        if (j != Jb.a) {
+            process_range<DEG>(A, L.q, L.h0, L.h1, 0, job, j, p0, 1, acc, lane, ws, phase);
+        } else { // same-annulus pairs with wrapped or halo points: full dedup
+            general_range<DEG>(A, L.q, L.g0, L.g1, acc);
+            general_range<DEG>(A, L.q, L.h0, L.h1, acc);
+        }
     }
     flush(acc, &A.ctr[0], lane);
 }
@@ -689,7 +760,7 @@ __global__ void __launch_bounds__(256, 2) glob_req_kernel(EdgeArgs A) {
     for (int w = 0; w < 4; ++w) {
         Lane L;
         setup_global(A, Jb, g0 + lane, w, L);
-        process_range<DEG>(A, L.q, L.s0, L.s1, 1, job, g0, w, acc, lane, ws, phase);
+        process_range<DEG>(A, L.q, L.s0, L.s1, 1, job, Jb.j, g0, w, acc, lane, ws, phase);
     }
     flush(acc, &A.ctr[1], lane);
 }
@@ -714,7 +785,7 @@ __global__ void __launch_bounds__(256, 2) tile_tasks_kernel(EdgeArgs A) {
         const std::uint64_t ga = lane == 0 ? T.u0 : 0, gb = lane == 0 ? T.u1 : 0;
         Lane                L;
         if (KIND == 0) {
-            setup_stream(A, A.stream_jobs[T.job], p, L);
+            setup_stream(A, A.stream_jobs[T.job], T.j, p, L);
             if (T.w == 0) tile_dispatch<DEG>(T.lgR, A, L.q, L.s0, L.s1, ga, gb, acc, lane, ws, phase);
             else tile_dispatch<DEG>(T.lgR, A, L.q, L.h0, L.h1, ga, gb, acc, lane, ws, phase);
         } else {
