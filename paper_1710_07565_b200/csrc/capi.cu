@@ -107,7 +107,7 @@ struct rhg_ctx {
     cudaStream_t stream = nullptr;
     cudaEvent_t  ev[6]{};
     DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, cells, counters, degrees, tasks, dbg, nid;
-    DevBuf       lcells, perm, s_beta, s_hw, s_rec0, s_rec1, s_rec2;
+    DevBuf       lcells, perm, s_beta, s_hw, s_rec0, s_rec1, s_rec2, gsort;
     HostPinned   staging;
 };
 
@@ -121,6 +121,7 @@ struct Plan {
     std::vector<AnnulusDev> ann;
     std::vector<StreamJob>  jobs;
     std::vector<PairJob>    sjobs, gjobs;
+    std::vector<std::uint64_t> gseg;        // global-point annulus offsets (segments of the theta sort)
     std::vector<std::uint64_t> blk_prefix;  // angular-block item order (see edges.cu map_item)
     std::vector<std::uint32_t> blk_job_off;
     int                        nblk = 1;
@@ -188,6 +189,8 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
             pl.jobs.push_back(J);
         }
     pl.total = pl.n_ext + pl.n_glob;
+    for (std::uint32_t i = 0; i < L.first_streaming; ++i) pl.gseg.push_back(L.chunk_id_base(i, 0));
+    pl.gseg.push_back(pl.n_glob);
     // pair work lists
     for (std::uint32_t a = L.first_streaming; a < L.count; ++a) {
         const std::uint64_t na = pl.ann[a].end - pl.ann[a].off;
@@ -240,6 +243,7 @@ struct Tables {
     PairJob *      sjobs, *gjobs;
     std::uint64_t* blk_prefix;
     std::uint32_t* blk_job_off;
+    std::uint64_t* gseg;
 };
 
 // Pack all tables into one pinned blob and send it with one copy.
@@ -249,7 +253,8 @@ Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr)
     const std::size_t o_gj = align256(o_sj + pl.sjobs.size() * sizeof(PairJob));
     const std::size_t o_bp = align256(o_gj + pl.gjobs.size() * sizeof(PairJob));
     const std::size_t o_bj = align256(o_bp + pl.blk_prefix.size() * sizeof(std::uint64_t));
-    const std::size_t bytes = align256(o_bj + pl.blk_job_off.size() * sizeof(std::uint32_t)) + 256;
+    const std::size_t o_gs = align256(o_bj + pl.blk_job_off.size() * sizeof(std::uint32_t));
+    const std::size_t bytes = align256(o_gs + pl.gseg.size() * sizeof(std::uint64_t)) + 256;
     ctx->staging.ensure(bytes);
     char* h = static_cast<char*>(ctx->staging.p);
     std::memcpy(h + o_ann, pl.ann.data(), pl.ann.size() * sizeof(AnnulusDev));
@@ -258,13 +263,15 @@ Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr)
     std::memcpy(h + o_gj, pl.gjobs.data(), pl.gjobs.size() * sizeof(PairJob));
     std::memcpy(h + o_bp, pl.blk_prefix.data(), pl.blk_prefix.size() * sizeof(std::uint64_t));
     std::memcpy(h + o_bj, pl.blk_job_off.data(), pl.blk_job_off.size() * sizeof(std::uint32_t));
+    std::memcpy(h + o_gs, pl.gseg.data(), pl.gseg.size() * sizeof(std::uint64_t));
     ctx->tables.ensure(bytes);
     CK(cudaMemcpyAsync(ctx->tables.p, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
     if (h2d) *h2d += bytes;
     char* d = ctx->tables.as<char>();
     return {reinterpret_cast<AnnulusDev*>(d + o_ann), reinterpret_cast<StreamJob*>(d + o_jobs),
             reinterpret_cast<PairJob*>(d + o_sj), reinterpret_cast<PairJob*>(d + o_gj),
-            reinterpret_cast<std::uint64_t*>(d + o_bp), reinterpret_cast<std::uint32_t*>(d + o_bj)};
+            reinterpret_cast<std::uint64_t*>(d + o_bp), reinterpret_cast<std::uint32_t*>(d + o_bj),
+            reinterpret_cast<std::uint64_t*>(d + o_gs)};
 }
 
 void ensure_points(rhg_ctx* ctx, std::uint64_t total, bool with_export) {
@@ -344,6 +351,13 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         e.dbg = ctx->dbg.as<unsigned long long>();
     }
     launch_cell_index(e, pl.ncells, ctx->stream, launches);
+    if (pl.n_glob && pl.gwarps) { // global requests in (annulus, theta) order
+        std::size_t need = 0;
+        launch_sort_globals(e, t.gseg, int(pl.gseg.size() - 1), nullptr, 0, &need, ctx->stream, launches);
+        ctx->gsort.ensure(need);
+        launch_sort_globals(e, t.gseg, int(pl.gseg.size() - 1), ctx->gsort.p, ctx->gsort.cap, &need, ctx->stream,
+                            launches);
+    }
     launch_edges(e, ctx->stream, launches);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[2], ctx->stream));
@@ -442,7 +456,7 @@ void rhg_destroy(rhg_ctx* c) {
     cudaStreamSynchronize(c->stream);
     for (DevBuf* b: {&c->beta, &c->hw, &c->rec0, &c->rec1, &c->rec2, &c->r_out, &c->beta_raw, &c->tables, &c->cells,
                      &c->counters, &c->degrees, &c->tasks, &c->dbg, &c->nid, &c->lcells, &c->perm, &c->s_beta,
-                     &c->s_hw, &c->s_rec0, &c->s_rec1, &c->s_rec2})
+                     &c->s_hw, &c->s_rec0, &c->s_rec1, &c->s_rec2, &c->gsort})
         b->release();
     if (c->staging.p) cudaFreeHost(c->staging.p);
     for (auto& e: c->ev) cudaEventDestroy(e);

@@ -28,6 +28,8 @@
 //   glob_req_kernel     global requests x owned streaming nodes (same engine)
 //   tile_tasks_kernel   deferred pieces of very large tiles, load-balanced
 //   glob_pairs_kernel   global unit, 128x128 tiles of the upper triangle
+#include <cub/cub.cuh>
+
 #include "device.cuh"
 #include "kernels.hpp"
 
@@ -272,10 +274,12 @@ __device__ __forceinline__ void setup_stream(const EdgeArgs& A, const PairJob& J
 // Global request g against streaming annulus Jb.j, window number w (0..3):
 // split_wraparound pieces (sweep.hpp:41-58) and, when this shard owns engine
 // P-1, their chunk-0 parts lifted by 2pi (sweep.hpp:404-432).  Owned nodes only.
-__device__ __forceinline__ void setup_global(const EdgeArgs& A, const PairJob& Jb, std::uint64_t g, int w, Lane& L) {
+__device__ __forceinline__ void setup_global(const EdgeArgs& A, const PairJob& Jb, std::uint64_t gs, int w, Lane& L) {
     L = Lane{};
-    if (g >= Jb.req_end) return;
-    const AnnulusDev& Aj = A.ann[Jb.j];
+    if (gs >= Jb.req_end) return;
+    // requests run in (annulus, theta) order so that neighbouring lanes share nodes
+    const std::uint64_t g  = A.gperm ? A.n_ext + A.gperm[gs - A.n_ext] : gs;
+    const AnnulusDev&   Aj = A.ann[Jb.j];
     const double2     r0 = A.rec0[g], r1 = A.rec1[g], r2 = A.rec2[g];
     const double      th = r0.y;
     const double      h  = half_width_in(Aj, r2.x, r2.y); // generator.hpp:67
@@ -796,6 +800,17 @@ __global__ void __launch_bounds__(256, 2) tile_tasks_kernel(EdgeArgs A) {
     flush(acc, &A.ctr[KIND], lane);
 }
 
+// Sort keys of the global points: theta quantised to 32 bits (any order is
+// exact; this one makes neighbouring requests' windows overlap).
+__global__ void glob_keys_kernel(EdgeArgs A, std::uint32_t* keys, std::uint32_t* vals) {
+    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= A.n_glob) return;
+    const double th = A.rec0[A.n_ext + i].y; // [0, 2pi)
+    const double q  = th * (4294967296.0 / kTwoPiD);
+    keys[i]         = q >= 4294967295.0 ? 0xffffffffu : std::uint32_t(q);
+    vals[i]         = std::uint32_t(i);
+}
+
 // generator.hpp:84-102: all pairs i < k of the global points, request = i.
 template <bool DEG>
 __global__ void __launch_bounds__(kGGTile) glob_pairs_kernel(EdgeArgs A, std::uint64_t nT) {
@@ -845,6 +860,31 @@ void launch_cell_index(const EdgeArgs& a, std::uint64_t, cudaStream_t st, std::u
         lambda_cells_kernel<<<g, 256, 0, st>>>(a);
         *launches += 3;
     }
+}
+
+void launch_sort_globals(EdgeArgs& a, const std::uint64_t* seg_off_dev, int nseg, void* scratch,
+                         std::size_t scratch_bytes, std::size_t* need, cudaStream_t st, std::uint64_t* launches) {
+    // scratch: keys_in | keys_out | vals_in | perm(out) | cub temp
+    const std::size_t n   = a.n_glob;
+    const std::size_t al  = (n * 4 + 255) & ~std::size_t(255);
+    std::size_t       tmp = 0;
+    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, static_cast<const std::uint32_t*>(nullptr),
+                                             static_cast<std::uint32_t*>(nullptr),
+                                             static_cast<const std::uint32_t*>(nullptr),
+                                             static_cast<std::uint32_t*>(nullptr), int(n), nseg, seg_off_dev,
+                                             seg_off_dev + 1, 0, 32, st);
+    *need = 4 * al + tmp + 256;
+    if (!scratch || scratch_bytes < *need || n == 0) return;
+    char*          p    = static_cast<char*>(scratch);
+    std::uint32_t* kin  = reinterpret_cast<std::uint32_t*>(p);
+    std::uint32_t* kout = reinterpret_cast<std::uint32_t*>(p + al);
+    std::uint32_t* vin  = reinterpret_cast<std::uint32_t*>(p + 2 * al);
+    std::uint32_t* perm = reinterpret_cast<std::uint32_t*>(p + 3 * al);
+    glob_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kin, vin);
+    cub::DeviceSegmentedRadixSort::SortPairs(p + 4 * al, tmp, kin, kout, vin, perm, int(n), nseg, seg_off_dev,
+                                             seg_off_dev + 1, 0, 32, st);
+    a.gperm = perm;
+    *launches += 2;
 }
 
 void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches) {

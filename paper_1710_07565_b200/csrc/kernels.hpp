@@ -48,6 +48,7 @@ struct EdgeArgs {
     double2*          s_rec1 = nullptr;
     double2*          s_rec2 = nullptr;
     unsigned long long* s_id = nullptr;     // [n_ext + 2] vertex ids
+    const std::uint32_t* gperm = nullptr;  // global requests in (annulus, theta) order (null: id order)
     unsigned long long* dmax_bits = nullptr; // per annulus, max half-width (bits)
     double            cosh_R = 1.0;
     double            chunk0_upper = 0.0; // chunk_upper_bound(0, P)
@@ -73,6 +74,10 @@ struct EdgeArgs {
 
 void launch_cell_index(const EdgeArgs& a, std::uint64_t ncells_total, cudaStream_t st, std::uint64_t* launches);
 void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches);
+// Sorts the global points by (annulus, theta) into a.gperm (scratch layout
+// internal); with scratch == nullptr only reports the bytes needed in *need.
+void launch_sort_globals(EdgeArgs& a, const std::uint64_t* seg_off_dev, int nseg, void* scratch,
+                         std::size_t scratch_bytes, std::size_t* need, cudaStream_t st, std::uint64_t* launches);
 
 constexpr int kGGTile = 128;
 // dbg layout: [0..5] groups per lgR, [6..11] sum U per lgR, [12..17] slots per lgR, [18] serial warps,
