@@ -224,8 +224,24 @@ struct Lane {
 __device__ __forceinline__ void window_ranges(const EdgeArgs& A, const AnnulusDev& J, double lo, double hi,
                                               bool want_halo, Lane& L) {
     if (!(hi > lo)) return;
-    L.s0 = lower_bound_owned(A, J, lo);
-    L.s1 = lower_bound_owned(A, J, hi);
+    { // both lower bounds interleaved: independent loads in flight together
+        const std::uint32_t ca = cellf(J, lo), cb = cellf(J, hi);
+        std::uint64_t       ka = A.lcellstart[J.cell_off + ca], kb = A.lcellstart[J.cell_off + cb];
+        const std::uint64_t ea = A.lcellstart[J.cell_off + ca + 1], eb = A.lcellstart[J.cell_off + cb + 1];
+        bool                ma = ka < ea, mb = kb < eb;
+        while (ma || mb) {
+            const double xa = ma ? A.s_rec0[ka].x : 0.0, xb = mb ? A.s_rec0[kb].x : 0.0;
+            if (ma) {
+                if (xa < lo) ma = ++ka < ea;
+                else ma = false;
+            }
+            if (mb) {
+                if (xb < hi) mb = ++kb < eb;
+                else mb = false;
+            }
+        }
+        L.s0 = ka, L.s1 = kb;
+    }
     if (want_halo && J.end > J.halo && hi > A.s_rec0[J.halo].x && lo <= A.s_rec0[J.end - 1].x) {
         L.h0 = lower_bound_halo(A, J, lo);
         L.h1 = lower_bound_halo(A, J, hi);
@@ -572,20 +588,38 @@ __device__ __forceinline__ void flat_run(const EdgeArgs& A, const Req& q, std::u
     RowSm& me = ws->rows[lane];
     me.cs = q.cs, me.sn = q.sn, me.coth = q.coth, me.rci = q.rci, me.id = q.id, me.r0 = c0 - excl;
     __syncwarp();
-    for (std::uint32_t B = 0; B < total; B += 32) {
-        const std::uint32_t t = B + std::uint32_t(lane);
-        int                 o = 0;
+    constexpr int kU = 4; // rounds per iteration: 3*kU independent loads in flight per lane
+    for (std::uint32_t B = 0; B < total; B += 32 * kU) {
+        std::uint64_t k[kU];
+        int           own[kU];
+        bool          ok[kU];
 #pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-            const std::uint32_t v = __shfl_sync(kFull, excl, o + step);
-            if (v <= t) o += step;
+        for (int u = 0; u < kU; ++u) {
+            const std::uint32_t t = B + 32u * u + std::uint32_t(lane);
+            int                 o = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const std::uint32_t v = __shfl_sync(kFull, excl, o + step);
+                if (v <= t) o += step;
+            }
+            own[u] = o;
+            ok[u]  = t < total;
+            k[u]   = ok[u] ? ws->rows[o].r0 + t : 0; // = c0_o + (t - excl_o)
         }
-        if (t < total) {
-            const RowSm&        r = ws->rows[o];
-            const std::uint64_t k = r.r0 + t; // = c0_o + (t - excl_o)
-            Req                 rq;
+        double2            n1[kU], n2[kU];
+        unsigned long long nid[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            n1[u]  = A.s_rec1[k[u]];
+            n2[u]  = A.s_rec2[k[u]];
+            nid[u] = A.s_id[k[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const RowSm& r = ws->rows[own[u]];
+            Req          rq;
             rq.cs = r.cs, rq.sn = r.sn, rq.coth = r.coth, rq.rci = r.rci, rq.id = r.id;
-            predicate<DEG>(A, rq, true, A.s_rec1[k], A.s_rec2[k], A.s_id[k], acc);
+            predicate<DEG>(A, rq, ok[u], n1[u], n2[u], nid[u], acc);
         }
     }
     __syncwarp();
@@ -606,13 +640,15 @@ template <bool DEG>
 __device__ __forceinline__ void process_range(const EdgeArgs& A, const Req& q, std::uint64_t c0, std::uint64_t c1,
                                               int kind, int job, int j, std::uint64_t p0, int pass, Acc& acc,
                                               int lane, WarpSmem* ws, std::uint32_t& phase) {
-    const std::uint64_t len   = c1 > c0 ? c1 - c0 : 0;
-    const std::uint64_t total = warp_sum_u64(len);
-    if (total == 0) return;
-    std::uint64_t gmin = len ? c0 : ~0ull, gmax = len ? c1 : 0ull;
-    std::uint64_t best = total < kFlatMax ? (total + 31) / 32 * 40 + 60 : ~0ull;
-    int           lgR  = -1;
-    std::uint64_t ga = 0, gb = 0; // this lane's group union for the chosen R (valid in group leaders)
+    const std::uint64_t len  = c1 > c0 ? c1 - c0 : 0;
+    const std::uint32_t lenS = len < (1u << 26) ? std::uint32_t(len) : (1u << 26); // saturated: sums fit 32 bits
+    const std::uint32_t tot  = __reduce_add_sync(kFull, lenS);
+    if (tot == 0) return;
+    const std::uint64_t total = tot;
+    std::uint64_t       gmin = len ? c0 : ~0ull, gmax = len ? c1 : 0ull;
+    std::uint32_t       best = tot < kFlatMax ? (tot + 31) / 32 * 40 + 60 : 0xffffffffu;
+    int                 lgR  = -1;
+    std::uint64_t       ga = 0, gb = 0; // this lane's group union for the chosen R (valid in group leaders)
 #pragma unroll
     for (int k = 0; k <= 5; ++k) {
         if (k > 0) {
@@ -623,8 +659,9 @@ __device__ __forceinline__ void process_range(const EdgeArgs& A, const Req& q, s
         }
         const bool          leader = (lane & ((1 << k) - 1)) == 0;
         const std::uint64_t U      = gmax > gmin ? gmax - gmin : 0;
-        const std::uint64_t mine   = leader && U ? (U << k) * 20 / 32 + ((U + kBatch - 1) / kBatch) * 10 + 40 : 0;
-        const std::uint64_t cost   = warp_sum_u64(mine);
+        const std::uint64_t U1     = U < (1ull << 20) ? U : (1ull << 20); // saturate (cost only ranks options)
+        const std::uint32_t mine   = leader && U ? std::uint32_t((U1 << k) * 20 / 32 + ((U1 + kBatch - 1) / kBatch) * 10 + 40) : 0;
+        const std::uint32_t cost   = __reduce_add_sync(kFull, mine);
         if (cost < best) best = cost, lgR = k, ga = gmin, gb = gmax;
     }
     if (A.dbg && lane == 0) {
@@ -638,7 +675,7 @@ __device__ __forceinline__ void process_range(const EdgeArgs& A, const Req& q, s
             const std::uint32_t t = __shfl_up_sync(kFull, incl, o);
             if (lane >= o) incl += t;
         }
-        flat_run<DEG>(A, q, c0, std::uint32_t(len), incl - std::uint32_t(len), std::uint32_t(total), acc, lane, ws);
+        flat_run<DEG>(A, q, c0, std::uint32_t(len), incl - std::uint32_t(len), tot, acc, lane, ws);
         return;
     }
     const int  R      = 1 << lgR;
