@@ -104,8 +104,9 @@ double ms_between(cudaEvent_t a, cudaEvent_t b) {
 
 struct rhg_ctx {
     int          device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr, side = nullptr;
     cudaEvent_t  ev[6]{};
+    cudaEvent_t  fork = nullptr, join = nullptr; // timing-free events for the side stream
     DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, cells, counters, degrees, tasks, dbg, nid;
     DevBuf       lcells, perm, s_beta, s_hw, s_rec0, s_rec1, s_rec2, gsort;
     HostPinned   staging;
@@ -122,6 +123,7 @@ struct Plan {
     std::vector<StreamJob>  jobs;
     std::vector<PairJob>    sjobs, gjobs;
     std::vector<std::uint64_t> gseg;        // global-point annulus offsets (segments of the theta sort)
+    std::vector<std::uint32_t> ann_blk;     // 256-point blocks per streaming annulus (prefix, count + 1)
     std::vector<std::uint64_t> blk_prefix;  // angular-block item order (see edges.cu map_item)
     std::vector<std::uint32_t> blk_job_off;
     int                        nblk = 1;
@@ -177,6 +179,9 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
     }
     pl.n_ext  = run;
     pl.n_glob = L.global_vertices();
+    pl.ann_blk.assign(L.count + 1, 0);
+    for (std::uint32_t i = 0; i < L.count; ++i)
+        pl.ann_blk[i + 1] = pl.ann_blk[i] + std::uint32_t((pl.ann[i].end - pl.ann[i].off + 255) / 256);
     for (std::uint32_t i = 0; i < L.first_streaming; ++i)
         for (std::uint32_t c = 0; c < Pc; ++c) {
             const std::uint64_t cnt = L.chunk_count(i, c);
@@ -244,6 +249,7 @@ struct Tables {
     std::uint64_t* blk_prefix;
     std::uint32_t* blk_job_off;
     std::uint64_t* gseg;
+    std::uint32_t* ann_blk;
 };
 
 // Pack all tables into one pinned blob and send it with one copy.
@@ -254,7 +260,8 @@ Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr)
     const std::size_t o_bp = align256(o_gj + pl.gjobs.size() * sizeof(PairJob));
     const std::size_t o_bj = align256(o_bp + pl.blk_prefix.size() * sizeof(std::uint64_t));
     const std::size_t o_gs = align256(o_bj + pl.blk_job_off.size() * sizeof(std::uint32_t));
-    const std::size_t bytes = align256(o_gs + pl.gseg.size() * sizeof(std::uint64_t)) + 256;
+    const std::size_t o_ab = align256(o_gs + pl.gseg.size() * sizeof(std::uint64_t));
+    const std::size_t bytes = align256(o_ab + pl.ann_blk.size() * sizeof(std::uint32_t)) + 256;
     ctx->staging.ensure(bytes);
     char* h = static_cast<char*>(ctx->staging.p);
     std::memcpy(h + o_ann, pl.ann.data(), pl.ann.size() * sizeof(AnnulusDev));
@@ -264,6 +271,7 @@ Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr)
     std::memcpy(h + o_bp, pl.blk_prefix.data(), pl.blk_prefix.size() * sizeof(std::uint64_t));
     std::memcpy(h + o_bj, pl.blk_job_off.data(), pl.blk_job_off.size() * sizeof(std::uint32_t));
     std::memcpy(h + o_gs, pl.gseg.data(), pl.gseg.size() * sizeof(std::uint64_t));
+    std::memcpy(h + o_ab, pl.ann_blk.data(), pl.ann_blk.size() * sizeof(std::uint32_t));
     ctx->tables.ensure(bytes);
     CK(cudaMemcpyAsync(ctx->tables.p, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
     if (h2d) *h2d += bytes;
@@ -271,7 +279,7 @@ Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr)
     return {reinterpret_cast<AnnulusDev*>(d + o_ann), reinterpret_cast<StreamJob*>(d + o_jobs),
             reinterpret_cast<PairJob*>(d + o_sj), reinterpret_cast<PairJob*>(d + o_gj),
             reinterpret_cast<std::uint64_t*>(d + o_bp), reinterpret_cast<std::uint32_t*>(d + o_bj),
-            reinterpret_cast<std::uint64_t*>(d + o_gs)};
+            reinterpret_cast<std::uint64_t*>(d + o_gs), reinterpret_cast<std::uint32_t*>(d + o_ab)};
 }
 
 void ensure_points(rhg_ctx* ctx, std::uint64_t total, bool with_export) {
@@ -292,6 +300,7 @@ SamplerArgs sampler_args(rhg_ctx* ctx, const Plan& pl, const Tables& t) {
     s.jobs = t.jobs, s.njobs = int(pl.jobs.size()), s.ann = t.ann, s.alpha = pl.L.alpha, s.total = pl.total;
     s.beta = ctx->beta.as<double>(), s.hw = ctx->hw.as<double>();
     s.rec0 = ctx->rec0.as<double2>(), s.rec1 = ctx->rec1.as<double2>(), s.rec2 = ctx->rec2.as<double2>();
+    s.side = ctx->side, s.ev_fork = ctx->fork, s.ev_join = ctx->join;
     return s;
 }
 
@@ -350,7 +359,8 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         CK(cudaMemsetAsync(ctx->dbg.p, 0, kDbgSlots * sizeof(unsigned long long), ctx->stream));
         e.dbg = ctx->dbg.as<unsigned long long>();
     }
-    launch_cell_index(e, pl.ncells, ctx->stream, launches);
+    e.ann_blk = t.ann_blk;
+    launch_cell_index(e, pl.ann_blk[pl.L.count], ctx->stream, launches);
     if (pl.n_glob && pl.gwarps) { // global requests in (annulus, theta) order
         std::size_t need = 0;
         launch_sort_globals(e, t.gseg, int(pl.gseg.size() - 1), nullptr, 0, &need, ctx->stream, launches);
@@ -445,7 +455,10 @@ int rhg_create(int device, rhg_ctx** out) {
         auto* c   = new rhg_ctx;
         c->device = device;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
         for (auto& e: c->ev) CK(cudaEventCreate(&e));
+        CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         *out = c;
     });
 }
@@ -454,12 +467,16 @@ void rhg_destroy(rhg_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(c->side);
     for (DevBuf* b: {&c->beta, &c->hw, &c->rec0, &c->rec1, &c->rec2, &c->r_out, &c->beta_raw, &c->tables, &c->cells,
                      &c->counters, &c->degrees, &c->tasks, &c->dbg, &c->nid, &c->lcells, &c->perm, &c->s_beta,
                      &c->s_hw, &c->s_rec0, &c->s_rec1, &c->s_rec2, &c->gsort})
         b->release();
     if (c->staging.p) cudaFreeHost(c->staging.p);
     for (auto& e: c->ev) cudaEventDestroy(e);
+    cudaEventDestroy(c->fork);
+    cudaEventDestroy(c->join);
+    cudaStreamDestroy(c->side);
     cudaStreamDestroy(c->stream);
     delete c;
 }

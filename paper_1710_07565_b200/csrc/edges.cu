@@ -77,6 +77,21 @@ __device__ __forceinline__ int streaming_annulus_of(const AnnulusDev* __restrict
     return lo;
 }
 
+// Sort-phase kernels run ceil(n_j / 256) blocks per streaming annulus j
+// (prefix table A.ann_blk), so every block knows its annulus without a search
+// per thread.  Returns the annulus of this block and sets i (maybe >= end).
+__device__ __forceinline__ int block_annulus(const EdgeArgs& A, std::uint64_t& i) {
+    const std::uint32_t b  = blockIdx.x;
+    int                 lo = A.first_streaming, hi = A.count - 1; // last annulus with ann_blk <= b
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (A.ann_blk[mid] <= b) lo = mid;
+        else hi = mid - 1;
+    }
+    i = A.ann[lo].off + std::uint64_t(b - A.ann_blk[lo]) * 256u + threadIdx.x;
+    return lo;
+}
+
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -91,43 +106,40 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
     return v;
 }
 
-// Fill a cell-start table: entries (kp, k] = i, and after the last point of
-// the block (k, ncells] = end.
-__device__ __forceinline__ void cell_fill(std::uint64_t* tab, std::int64_t kp, std::uint32_t k, std::uint64_t i,
-                                          bool last, std::uint32_t ncells, std::uint64_t end) {
+// Fill a cell-start table: entries (kp, k] = i.  The tail after the last
+// point, (k_last, ncells] = end, is filled in parallel by cell_tail_kernel.
+__device__ __forceinline__ void cell_fill(std::uint64_t* tab, std::int64_t kp, std::uint32_t k, std::uint64_t i) {
     for (std::int64_t c = kp + 1; c <= std::int64_t(k); ++c) tab[c] = i;
-    if (last)
-        for (std::uint32_t c = k + 1; c <= ncells; ++c) tab[c] = end;
 }
 
 // ---------------------------------------------------------------- sort ---
-__global__ void beta_cells_kernel(EdgeArgs A) {
-    const std::uint64_t i    = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int           lane = threadIdx.x & 31;
-    if (i < std::uint64_t(A.count) && int(i) >= A.first_streaming) { // empty blocks: [off, off]
-        const AnnulusDev& E = A.ann[i];
+__global__ void __launch_bounds__(256) beta_cells_kernel(EdgeArgs A) {
+    const int lane = threadIdx.x & 31;
+    if (blockIdx.x == 0 && int(threadIdx.x) < A.count && int(threadIdx.x) >= A.first_streaming) {
+        const AnnulusDev& E = A.ann[threadIdx.x]; // empty blocks: [off, off]
         if (E.end == E.off)
             for (std::uint32_t k = 0; k <= E.ncells; ++k) A.cellstart[E.cell_off + k] = E.off;
         if (E.halo == E.off)
             for (std::uint32_t k = 0; k <= E.ncells; ++k) A.lcellstart[E.cell_off + k] = E.off;
     }
-    unsigned long long hwbits = 0;
-    int                j      = -1;
-    if (i < A.n_ext) {
-        j                   = streaming_annulus_of(A.ann, A.first_streaming, A.count, i);
-        const AnnulusDev& J = A.ann[j];
+    std::uint64_t       i;
+    const int           j = block_annulus(A, i);
+    const AnnulusDev&   J = A.ann[j];
+    unsigned long long  hwbits = 0;
+    if (i < J.end) {
         const std::uint32_t k  = cellf(J, A.beta[i]);
         const std::int64_t  kp = i > J.off ? std::int64_t(cellf(J, A.beta[i - 1])) : -1;
-        cell_fill(A.cellstart + J.cell_off, kp, k, i, i + 1 == J.end, J.ncells, J.end);
+        cell_fill(A.cellstart + J.cell_off, kp, k, i);
         hwbits = static_cast<unsigned long long>(__double_as_longlong(A.hw[i])); // hw >= +0
     }
-    const int  j0   = __shfl_sync(kFull, j, 0);
-    const bool same = __all_sync(kFull, j == j0);
-    if (same) {
-        const unsigned long long m = warp_max_u64(hwbits);
-        if (lane == 0 && j0 >= 0) atomicMax(&A.dmax_bits[j0], m);
-    } else if (j >= 0) {
-        atomicMax(&A.dmax_bits[j], hwbits);
+    __shared__ unsigned long long wmax[8]; // one atomic per block (all its points share the annulus)
+    const unsigned long long m = warp_max_u64(hwbits);
+    if (lane == 0) wmax[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long b = 0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) b = wmax[w] > b ? wmax[w] : b;
+        if (b) atomicMax(&A.dmax_bits[j], b);
     }
 }
 
@@ -136,11 +148,11 @@ __global__ void beta_cells_kernel(EdgeArgs A) {
 // (lambda, id).  Only points whose beta lies in [lambda_i - dmax, lambda_i]
 // can compare either way: everything before that window is smaller
 // (lambda <= beta + dmax), everything after is larger (lambda >= beta).
-__global__ void rank_kernel(EdgeArgs A) {
-    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= A.n_ext) return;
-    const int           j  = streaming_annulus_of(A.ann, A.first_streaming, A.count, i);
-    const AnnulusDev&   J  = A.ann[j];
+__global__ void __launch_bounds__(256) rank_kernel(EdgeArgs A) {
+    std::uint64_t       i;
+    const int           j = block_annulus(A, i);
+    const AnnulusDev&   J = A.ann[j];
+    if (i >= J.end) return;
     const bool          hb = i >= J.halo;
     const std::uint64_t bs = hb ? J.halo : J.off, be = hb ? J.end : J.halo;
     const double        li = A.rec0[i].x;
@@ -157,11 +169,11 @@ __global__ void rank_kernel(EdgeArgs A) {
     A.perm[i] = bs + rank;
 }
 
-__global__ void scatter_kernel(EdgeArgs A) {
-    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= A.n_ext) return;
-    const int           j = streaming_annulus_of(A.ann, A.first_streaming, A.count, i);
+__global__ void __launch_bounds__(256) scatter_kernel(EdgeArgs A) {
+    std::uint64_t       i;
+    const int           j = block_annulus(A, i);
     const AnnulusDev&   J = A.ann[j];
+    if (i >= J.end) return;
     const std::uint64_t d = A.perm[i];
     A.s_beta[d]           = A.beta[i];
     A.s_hw[d]             = A.hw[i];
@@ -173,17 +185,30 @@ __global__ void scatter_kernel(EdgeArgs A) {
 
 // Lambda-cell starts of every owned block, and the first owned index with
 // lambda >= 2pi (wrapped points: theta = lambda - 2pi there).
-__global__ void lambda_cells_kernel(EdgeArgs A) {
-    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= A.n_ext) return;
-    const int   j = streaming_annulus_of(A.ann, A.first_streaming, A.count, i);
-    AnnulusDev& J = A.ann_rw[j];
+__global__ void __launch_bounds__(256) lambda_cells_kernel(EdgeArgs A) {
+    std::uint64_t i;
+    const int     j = block_annulus(A, i);
+    AnnulusDev&   J = A.ann_rw[j];
     if (i >= J.halo) return;
     const double        l  = A.s_rec0[i].x;
     const std::uint32_t k  = cellf(J, l);
     const std::int64_t  kp = i > J.off ? std::int64_t(cellf(J, A.s_rec0[i - 1].x)) : -1;
-    cell_fill(A.lcellstart + J.cell_off, kp, k, i, i + 1 == J.halo, J.ncells, J.halo);
+    cell_fill(A.lcellstart + J.cell_off, kp, k, i);
     if (l >= kTwoPiD && (i == J.off || A.s_rec0[i - 1].x < kTwoPiD)) J.wrap = i;
+}
+
+// Tails of both cell tables: cells after the last point of a block hold the
+// block end (beta table: whole annulus array; lambda table: owned block).
+__global__ void cell_tail_kernel(EdgeArgs A, int lambda) {
+    const int         j  = A.first_streaming + int(blockIdx.y);
+    const AnnulusDev& J  = A.ann[j];
+    const std::uint64_t e = lambda ? J.halo : J.end;
+    if (e == J.off) return; // empty: initialised by beta_cells_kernel
+    const double        last = lambda ? A.s_rec0[e - 1].x : A.beta[e - 1];
+    const std::uint32_t k0   = cellf(J, last) + 1;
+    std::uint64_t*      tab  = (lambda ? A.lcellstart : A.cellstart) + J.cell_off;
+    for (std::uint32_t c = k0 + blockIdx.x * blockDim.x + threadIdx.x; c <= J.ncells; c += gridDim.x * blockDim.x)
+        tab[c] = e;
 }
 
 // ------------------------------------------------------------ requests ---
@@ -884,18 +909,19 @@ __global__ void __launch_bounds__(kGGTile) glob_pairs_kernel(EdgeArgs A, std::ui
 
 } // namespace
 
-void launch_cell_index(const EdgeArgs& a, std::uint64_t, cudaStream_t st, std::uint64_t* launches) {
+void launch_cell_index(const EdgeArgs& a, std::uint64_t nblocks, cudaStream_t st, std::uint64_t* launches) {
     if (a.first_streaming >= a.count) return;
-    const std::uint64_t n  = a.n_ext > std::uint64_t(a.count) ? a.n_ext : std::uint64_t(a.count);
-    const unsigned      gb = unsigned((n + 255) / 256);
-    beta_cells_kernel<<<gb, 256, 0, st>>>(a);
-    ++*launches;
-    if (a.n_ext) {
-        const unsigned g = unsigned((a.n_ext + 255) / 256);
+    const unsigned g = unsigned(nblocks ? nblocks : 1); // >= 1: block 0 also initialises empty annuli
+    const dim3     tails(64, unsigned(a.count - a.first_streaming));
+    beta_cells_kernel<<<g, 256, 0, st>>>(a);
+    cell_tail_kernel<<<tails, 256, 0, st>>>(a, 0);
+    *launches += 2;
+    if (nblocks) {
         rank_kernel<<<g, 256, 0, st>>>(a);
         scatter_kernel<<<g, 256, 0, st>>>(a);
         lambda_cells_kernel<<<g, 256, 0, st>>>(a);
-        *launches += 3;
+        cell_tail_kernel<<<tails, 256, 0, st>>>(a, 1);
+        *launches += 4;
     }
 }
 

@@ -21,6 +21,8 @@ struct SamplerArgs {
     double2*          rec2  = nullptr; // (coth r, 1/sinh r)
     double*           r_out = nullptr;             // optional: radius
     double*           beta_unlifted_out = nullptr; // optional: raw beta
+    cudaStream_t      side = nullptr;                // optional second stream (fork/join with events)
+    cudaEvent_t       ev_fork = nullptr, ev_join = nullptr;
 };
 
 void launch_sampler(const SamplerArgs& a, cudaStream_t st, std::uint64_t* launches);
@@ -49,6 +51,7 @@ struct EdgeArgs {
     double2*          s_rec2 = nullptr;
     unsigned long long* s_id = nullptr;     // [n_ext + 2] vertex ids
     const std::uint32_t* gperm = nullptr;  // global requests in (annulus, theta) order (null: id order)
+    const std::uint32_t* ann_blk = nullptr; // [count + 1] prefix of 256-point blocks per streaming annulus
     unsigned long long* dmax_bits = nullptr; // per annulus, max half-width (bits)
     double            cosh_R = 1.0;
     double            chunk0_upper = 0.0; // chunk_upper_bound(0, P)
@@ -72,7 +75,7 @@ struct EdgeArgs {
     unsigned int*     degrees = nullptr;
 };
 
-void launch_cell_index(const EdgeArgs& a, std::uint64_t ncells_total, cudaStream_t st, std::uint64_t* launches);
+void launch_cell_index(const EdgeArgs& a, std::uint64_t nblocks, cudaStream_t st, std::uint64_t* launches);
 void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches);
 // Sorts the global points by (annulus, theta) into a.gperm (scratch layout
 // internal); with scratch == nullptr only reports the bytes needed in *need.

@@ -5,10 +5,11 @@
 //                           seeded by derive_seed(seed,{3|4,i,c}) (rng.hpp:41-69),
 //                           312-word twist done warp-parallel in shared memory,
 //                           output (x >> 11) * 2^-53 written coalesced.
-//   S2 point_radial_kernel  per point: x_k = pow(U_k, 1/remaining) for the
-//                           sorted stream (rng.hpp:221), and the radius-only
-//                           attributes r, coth r, 1/sinh r, half-width
-//                           (partition.hpp:64-70, sweep.hpp:121-134).
+//   S2 point_pow_kernel     per point: x_k = pow(U_k, 1/remaining) for the
+//                           sorted stream (rng.hpp:221);
+//      point_radial_kernel  per point, on a side stream beside S2/S3: the
+//                           radius-only attributes r, coth r, 1/sinh r,
+//                           half-width (partition.hpp:64-70, sweep.hpp:121-134).
 //   S3 sorted_chain_kernel  one thread per angle stream: the serial product
 //                           chain cur *= x_k, beta = a + w (1 - cur), clamp
 //                           (rng.hpp:218-229) — the only serial dependency.
@@ -72,15 +73,16 @@ __device__ __forceinline__ void mt_twist_warp(std::uint64_t* mt, int lane) {
 
 constexpr int kMtWarps = 4;
 
+// which: 0 = both streams of every job, 1 = angle streams only, 2 = radius streams only
 __global__ void __launch_bounds__(32 * kMtWarps) mt_uniforms_kernel(const StreamJob* __restrict__ jobs, int njobs,
                                                                      double* __restrict__ u_ang,
-                                                                     double* __restrict__ u_rad) {
+                                                                     double* __restrict__ u_rad, int which) {
     __shared__ std::uint64_t state[kMtWarps][kMtN];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gw   = blockIdx.x * kMtWarps + warp;
-    if (gw >= 2 * njobs) return;
-    const StreamJob& J   = jobs[gw >> 1];
-    const bool       ang = (gw & 1) == 0;
+    if (gw >= (which ? 1 : 2) * njobs) return;
+    const StreamJob& J   = jobs[which ? gw : gw >> 1];
+    const bool       ang = which ? which == 1 : (gw & 1) == 0;
     double*          out = (ang ? u_ang : u_rad) + J.out_off;
     std::uint64_t*   mt  = state[warp];
     if (J.count == 0) return;
@@ -112,23 +114,28 @@ __device__ __forceinline__ int find_job(const StreamJob* __restrict__ jobs, int 
     return lo;
 }
 
-__global__ void point_radial_kernel(const StreamJob* __restrict__ jobs, int njobs, const AnnulusDev* __restrict__ ann,
-                                    double alpha, std::uint64_t total, double* __restrict__ u_ang,
-                                    double* __restrict__ hw_out, double2* __restrict__ rec2, double* __restrict__ r_out) {
+// rng.hpp:221: cur_max *= pow(U, 1.0 / remaining), remaining = count - k
+__global__ void point_pow_kernel(const StreamJob* __restrict__ jobs, int njobs, std::uint64_t total,
+                                 double* __restrict__ u_ang) {
     const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= total) return;
-    const StreamJob& J = jobs[find_job(jobs, njobs, i)];
-    const std::uint64_t k = i - J.out_off;
-    // rng.hpp:221: cur_max *= pow(U, 1.0 / remaining), remaining = count - k
-    const double rem = double(J.count - k);
-    u_ang[i]         = pow(u_ang[i], __ddiv_rn(1.0, rem));
-    // partition.hpp:64-70 radius_from_uniform
+    const StreamJob&    J   = jobs[find_job(jobs, njobs, i)];
+    const double        rem = double(J.count - (i - J.out_off));
+    u_ang[i]                = pow(u_ang[i], __ddiv_rn(1.0, rem));
+}
+
+// partition.hpp:64-70 radius_from_uniform, then sweep.hpp:125-134.
+__global__ void point_radial_kernel(const StreamJob* __restrict__ jobs, int njobs, const AnnulusDev* __restrict__ ann,
+                                    double alpha, std::uint64_t total, double* __restrict__ hw_out,
+                                    double2* __restrict__ rec2, double* __restrict__ r_out) {
+    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const StreamJob&  J = jobs[find_job(jobs, njobs, i)];
     const AnnulusDev& A = ann[J.annulus];
     const double      u = hw_out[i];
     const double      c = fadd(A.cal, fmul(u, fsub(A.cau, A.cal)));
     double            r = __ddiv_rn(acosh(c < 1.0 ? 1.0 : c), alpha);
     r                   = r > 1e-12 ? r : 1e-12;
-    // sweep.hpp:125-134
     const double ex   = exp(r);
     const double mex  = __ddiv_rn(1.0, ex);
     const double sh   = fmul(0.5, fsub(ex, mex));
@@ -233,23 +240,36 @@ __global__ void frames_from_points_kernel(const StreamJob* __restrict__ jobs, in
 
 } // namespace
 
+// Two streams: the angle side (MT -> pow -> serial chain) is latency-bound
+// and occupies few SMs, so the radius side (MT -> radial attributes) runs
+// beside it; the angular kernel joins both.
 void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
     if (S.total == 0 || S.njobs == 0) return;
-    const int mt_blocks = (2 * S.njobs + kMtWarps - 1) / kMtWarps;
-    mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw);
-    const unsigned pblocks = unsigned((S.total + 255) / 256);
-    point_radial_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.beta, S.hw, S.rec2,
-                                                 S.r_out);
+    const int      mt_blocks = (S.njobs + kMtWarps - 1) / kMtWarps;
+    const unsigned pblocks   = unsigned((S.total + 255) / 256);
+    cudaStream_t   side      = S.side ? S.side : st;
+    if (S.side) {
+        cudaEventRecord(S.ev_fork, st);
+        cudaStreamWaitEvent(side, S.ev_fork, 0);
+    }
+    mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, side>>>(S.jobs, S.njobs, S.beta, S.hw, 2);
+    point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
+    mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 1);
+    point_pow_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.total, S.beta);
     sorted_chain_kernel<<<(S.njobs + 3) / 4, 128, 0, st>>>(S.jobs, S.njobs, S.beta);
+    if (S.side) {
+        cudaEventRecord(S.ev_join, side);
+        cudaStreamWaitEvent(st, S.ev_join, 0);
+    }
     point_angular_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.total, S.beta, S.hw, S.rec0, S.rec1,
                                                   S.beta_unlifted_out);
-    *launches += 4;
+    *launches += 6;
 }
 
 void launch_mt_uniforms(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
     if (S.total == 0 || S.njobs == 0) return;
     const int mt_blocks = (2 * S.njobs + kMtWarps - 1) / kMtWarps;
-    mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw);
+    mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 0);
     *launches += 1;
 }
 
