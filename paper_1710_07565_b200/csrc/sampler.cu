@@ -10,7 +10,7 @@
 //      point_radial_kernel  per point, on a side stream beside S2/S3: the
 //                           radius-only attributes r, coth r, 1/sinh r,
 //                           half-width (partition.hpp:64-70, sweep.hpp:121-134).
-//   S3 sorted_chain_kernel  one thread per angle stream: the serial product
+//   S3 sorted_chain_kernel  one warp per angle stream: the serial product
 //                           chain cur *= x_k, beta = a + w (1 - cur), clamp
 //                           (rng.hpp:218-229) — the only serial dependency.
 //   S4 point_angular_kernel per point: theta = beta + hw (mod 2pi), cos, sin,
@@ -242,7 +242,7 @@ __global__ void frames_from_points_kernel(const StreamJob* __restrict__ jobs, in
 
 // Two streams: the angle side (MT -> pow -> serial chain) is latency-bound
 // and occupies few SMs, so the radius side (MT -> radial attributes) runs
-// beside it; the angular kernel joins both.
+// beside it on a second stream; the angular kernel joins both.
 void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
     if (S.total == 0 || S.njobs == 0) return;
     const int      mt_blocks = (S.njobs + kMtWarps - 1) / kMtWarps;
