@@ -2,7 +2,10 @@
 #include "layout.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <exception>
+#include <thread>
 
 namespace rhgb {
 
@@ -225,8 +228,33 @@ Layout make_layout(const Params& p) {
         L.counts[L.count - 1] = remaining;
     }
     L.chunk_counts.assign(std::size_t(L.count) * p.chunks, 0);
-    for (std::uint32_t i = 0; i < L.count; ++i)
-        split_chunk_range(p.seed, i, L.counts[i], 0, p.chunks, 1, L.chunk_counts.data() + std::size_t(i) * p.chunks);
+    // per-annulus binomial trees are independent (seeded by their own paths):
+    // spread them over host threads when there is enough work
+    {
+        const unsigned hw      = std::max(1u, std::thread::hardware_concurrency());
+        const unsigned threads = p.chunks >= 256 ? std::min<unsigned>(hw, std::min<unsigned>(L.count, 16)) : 1;
+        std::atomic<std::uint32_t> next{0};
+        std::exception_ptr         err;
+        std::atomic<bool>          failed{false};
+        auto work = [&] {
+            try {
+                for (std::uint32_t i = next++; i < L.count && !failed; i = next++)
+                    split_chunk_range(p.seed, i, L.counts[i], 0, p.chunks, 1,
+                                      L.chunk_counts.data() + std::size_t(i) * p.chunks);
+            } catch (...) {
+                if (!failed.exchange(true)) err = std::current_exception();
+            }
+        };
+        if (threads <= 1) {
+            work();
+        } else {
+            std::vector<std::thread> pool;
+            for (unsigned t = 1; t < threads; ++t) pool.emplace_back(work);
+            work();
+            for (auto& t: pool) t.join();
+        }
+        if (err) std::rethrow_exception(err);
+    }
 
     // classify, partition.hpp:195-217
     L.classes.assign(L.count, 1);
