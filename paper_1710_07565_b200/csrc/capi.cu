@@ -6,6 +6,7 @@
 // one D2H copy of the counters.  All device work is on the context's stream,
 // timed with CUDA events on that stream.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <chrono>
@@ -107,8 +108,8 @@ struct rhg_ctx {
     cudaStream_t stream = nullptr, side = nullptr;
     cudaEvent_t  ev[6]{};
     cudaEvent_t  fork = nullptr, join = nullptr; // timing-free events for the side stream
-    DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, cells, counters, degrees, tasks, dbg, nid;
-    DevBuf       lcells, perm, s_beta, s_hw, s_rec0, s_rec1, s_rec2, gsort;
+    DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, cells, counters, degrees, dbg, nid;
+    DevBuf       lcells, perm, s_beta, s_hw, s_lt, s_rec1, s_rec2, gsort, gbuf;
     HostPinned   staging;
 };
 
@@ -121,15 +122,49 @@ struct Plan {
     std::uint32_t           e0 = 0, e1 = 0, T = 0;
     std::vector<AnnulusDev> ann;
     std::vector<StreamJob>  jobs;
-    std::vector<PairJob>    sjobs, gjobs;
+    std::vector<std::uint64_t> gt_prefix;   // dense-engine warps (512-node owned strips) before annulus j
     std::vector<std::uint64_t> gseg;        // global-point annulus offsets (segments of the theta sort)
+    std::vector<unsigned long long> dense_mask; // [count] bit j: (a, j) runs on the dense engine
+    std::vector<std::uint64_t> req_off;     // [count] unified dense-request index of annulus a's first request
+    std::uint64_t              n_req = 0;
     std::vector<std::uint32_t> ann_blk;     // 256-point blocks per streaming annulus (prefix, count + 1)
-    std::vector<std::uint64_t> blk_prefix;  // angular-block item order (see edges.cu map_item)
-    std::vector<std::uint32_t> blk_job_off;
-    int                        nblk = 1;
-    std::uint64_t           n_ext = 0, n_glob = 0, total = 0, swarps = 0, gwarps = 0, ncells = 0;
+    std::vector<unsigned long long> src_mask; // [count] bit a: (a, j) runs on the slab join
+    std::vector<double>        hbound;      // [count * count] half-width bound of a's requests in j
+    std::vector<std::uint64_t> slab_prefix; // [count + 1] slabs (1024 owned nodes) before annulus j
+    std::vector<unsigned long long> slab_tab; // [n_slabs] (j << 32) | slab index, angle-interleaved
+    std::vector<std::uint64_t> tail_prefix; // [count + 1] tail threads before annulus a
+    std::vector<double>        tail_lam;    // [count] owned requests with lambda >= this are tail requests
+    std::uint64_t           n_ext = 0, n_glob = 0, total = 0, gtwarps = 0, ncells = 0, n_slabs = 0, n_tail = 0;
     std::uint64_t           gg_t0 = 0, gg_t1 = 0;
 };
+
+// Expected number of annulus-j nodes in the window of an annulus-a request
+// at a's median radius (density ~ sinh(alpha r)); same-annulus windows count
+// half (dedup).  Only chooses the engine for (a, j); never affects results.
+constexpr double kDenseMin = 32.0;
+double expected_window_nodes(const Layout& L, std::uint32_t a, std::uint32_t j) {
+    const double r    = std::acosh(0.5 * (L.cosh_alpha_lower[a] + L.cosh_alpha_upper[a])) / L.alpha;
+    const double ex   = std::exp(r), mex = 1.0 / ex, sh = 0.5 * (ex - mex);
+    const double coth = 0.5 * (ex + mex) / sh, inv = 1.0 / sh;
+    double       h    = kPi;
+    if (L.lower[j] > 0.0) {
+        const double arg = coth * L.coth_lower[j] - L.coshR_inv_sinh_lower[j] * inv;
+        h                = arg <= -1.0 ? kPi : arg >= 1.0 ? 0.0 : std::acos(arg);
+    }
+    return double(L.counts[j]) * 2.0 * h / kTwoPi * (a == j ? 0.5 : 1.0);
+}
+
+// Upper bound on the window half-width of any annulus-a request in annulus j
+// (own window: the own half-width): the half-width at a's lower radius, where
+// it is largest, plus a margin for libm differences.  Only sizes candidate
+// searches (supersets); never affects results.
+double half_width_bound(const Layout& L, std::uint32_t a, std::uint32_t j) {
+    if (!(L.lower[a] > 0.0) || !(L.lower[j] > 0.0)) return kPi;
+    const double inv = 1.0 / std::sinh(L.lower[a]);
+    const double arg = L.coth_lower[a] * L.coth_lower[j] - L.coshR_inv_sinh_lower[j] * inv;
+    const double h   = arg <= -1.0 ? kPi : arg >= 1.0 ? 0.0 : std::acos(arg);
+    return std::min(kPi, h * (1.0 + 1e-6) + 1e-9);
+}
 
 Plan make_plan(const Params& P, const rhg_shard* shard) {
     Plan pl;
@@ -196,90 +231,132 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
     pl.total = pl.n_ext + pl.n_glob;
     for (std::uint32_t i = 0; i < L.first_streaming; ++i) pl.gseg.push_back(L.chunk_id_base(i, 0));
     pl.gseg.push_back(pl.n_glob);
-    // pair work lists
+    // (annulus, target) pairs whose windows hold >= kDenseMin nodes on average run on the dense
+    // engine (node tiles x streamed requests); the rest on the streaming kernel
+    pl.dense_mask.assign(L.count, 0ull);
+    pl.req_off.assign(L.count, 0);
+    pl.n_req = pl.n_glob;
     for (std::uint32_t a = L.first_streaming; a < L.count; ++a) {
-        const std::uint64_t na = pl.ann[a].end - pl.ann[a].off;
-        if (!na) continue;
-        // one item = 32 requests of annulus a against every target annulus j >= a
-        PairJob J{};
-        J.warp_begin = pl.swarps, J.req_off = pl.ann[a].off, J.req_end = pl.ann[a].end, J.a = int(a), J.j = -1;
-        pl.sjobs.push_back(J);
-        pl.swarps += (na + 31) / 32;
+        for (std::uint32_t j = a; j < L.count && j < 64; ++j)
+            if (expected_window_nodes(L, a, j) >= kDenseMin) pl.dense_mask[a] |= 1ull << j;
+        pl.req_off[a] = pl.n_req;
+        if (pl.dense_mask[a]) pl.n_req += pl.ann[a].end - pl.ann[a].off;
     }
-    if (pl.n_glob)
-        for (std::uint32_t s = L.first_streaming; s < L.count; ++s) {
-            if (pl.ann[s].halo == pl.ann[s].off) continue;
-            PairJob J{};
-            J.warp_begin = pl.gwarps, J.req_off = pl.n_ext, J.req_end = pl.n_ext + pl.n_glob, J.a = -1, J.j = int(s);
-            pl.gjobs.push_back(J);
-            pl.gwarps += (pl.n_glob + 31) / 32;
+    // slab join for the sparse pairs: slabs of every target annulus with sparse sources, the
+    // half-width bounds that find a slab's requests, and the tail (wrap / halo) requests
+    const std::uint32_t K = L.count;
+    pl.src_mask.assign(K, 0ull);
+    pl.hbound.assign(std::size_t(K) * K, 0.0);
+    pl.slab_prefix.assign(K + 1, 0);
+    pl.tail_prefix.assign(K + 1, 0);
+    pl.tail_lam.assign(K, 0.0);
+    for (std::uint32_t a = L.first_streaming; a < K; ++a)
+        for (std::uint32_t j = a; j < K; ++j) {
+            pl.hbound[std::size_t(a) * K + j] = half_width_bound(L, a, j);
+            if (!((pl.dense_mask[a] >> j) & 1ull) && pl.ann[a].end > pl.ann[a].off) pl.src_mask[j] |= 1ull << a;
         }
-    // angular blocks: ~32 MB of node data per block so one block of every annulus stays in L2
-    {
-        const std::uint64_t bytes = pl.n_ext * 72;
-        std::uint64_t       M     = bytes / (32ull << 20);
-        M                         = std::max<std::uint64_t>(1, std::min<std::uint64_t>(M, 1024));
-        pl.nblk                   = int(M);
-        const std::size_t nj      = pl.sjobs.size();
-        pl.blk_prefix.assign(M + 1, 0);
-        pl.blk_job_off.assign(M * std::max<std::size_t>(nj, 1), 0);
-        std::uint64_t acc = 0;
-        for (std::uint64_t b = 0; b < M; ++b) {
-            pl.blk_prefix[b] = acc;
-            std::uint32_t in = 0;
-            for (std::size_t k = 0; k < nj; ++k) {
-                const std::uint64_t nb = (pl.sjobs[k].req_end - pl.sjobs[k].req_off + 31) / 32;
-                pl.blk_job_off[b * nj + k] = in;
-                in += std::uint32_t((b + 1) * nb / M - b * nb / M);
+    for (std::uint32_t j = 0; j < K; ++j) {
+        const std::uint64_t own = pl.src_mask[j] ? pl.ann[j].halo - pl.ann[j].off : 0;
+        pl.slab_prefix[j + 1]   = pl.slab_prefix[j] + (own + 1023) / 1024;
+    }
+    pl.n_slabs = pl.slab_prefix[K];
+    { // slabs in angular order across targets: requests are re-read from L2 by the next target's slab
+        std::vector<std::pair<double, unsigned long long>> order;
+        order.reserve(pl.n_slabs);
+        for (std::uint32_t j = 0; j < K; ++j) {
+            const std::uint64_t ns = pl.slab_prefix[j + 1] - pl.slab_prefix[j];
+            for (std::uint64_t i = 0; i < ns; ++i)
+                order.push_back({(double(i) + 0.5) / double(ns), (static_cast<unsigned long long>(j) << 32) | i});
+        }
+        std::stable_sort(order.begin(), order.end(),
+                         [](const auto& x, const auto& y) { return x.first < y.first; });
+        pl.slab_tab.resize(order.size());
+        for (std::size_t i = 0; i < order.size(); ++i) pl.slab_tab[i] = order[i].second;
+    }
+    const double Bnd = chunk_lower_bound(pl.e1, Pc); // halo nodes and wrapped points have lambda >= Bnd
+    for (std::uint32_t a = 0; a < K; ++a) {
+        std::uint64_t n = 0;
+        if (a >= L.first_streaming && pl.T) {
+            double hm = 0.0;
+            bool   any = false;
+            for (std::uint32_t j = a; j < K; ++j)
+                if (!((pl.dense_mask[a] >> j) & 1ull)) any = true, hm = std::max(hm, pl.hbound[std::size_t(a) * K + j]);
+            if (any) {
+                pl.tail_lam[a]  = Bnd - hm - 1e-9;
+                const double hw = pl.hbound[std::size_t(a) * K + a];
+                std::uint64_t owned_tail = 0; // points of the owned chunks that can reach lambda >= tail_lam
+                for (std::uint32_t t = 0; t < pl.T; ++t) {
+                    const std::uint32_t c = pl.e0 + t;
+                    if (chunk_upper_bound(c, Pc) + hw + 1e-9 >= pl.tail_lam[a]) owned_tail += L.chunk_count(a, c);
+                }
+                n = owned_tail + (pl.ann[a].end - pl.ann[a].halo);
             }
-            acc += in;
         }
-        pl.blk_prefix[M] = acc;
-        if (acc != pl.swarps) throw Invariant("plan: angular block item count mismatch");
+        pl.tail_prefix[a + 1] = pl.tail_prefix[a] + n;
     }
+    pl.n_tail = pl.tail_prefix[K];
+    // dense engine: one warp per strip of 512 owned nodes of every streaming annulus
+    pl.gt_prefix.assign(L.count + 1, 0);
+    for (std::uint32_t j = 0; j < L.count; ++j) {
+        const std::uint64_t own = j >= L.first_streaming && pl.n_req ? pl.ann[j].halo - pl.ann[j].off : 0;
+        pl.gt_prefix[j + 1]     = pl.gt_prefix[j] + (own + 511) / 512; // strips of 4 x 128 nodes
+    }
+    pl.gtwarps = pl.gt_prefix[L.count];
+    if (pl.n_ext >= (std::uint64_t(1) << 32) || pl.n_req >= (std::uint64_t(1) << 31) || L.n >= (std::uint64_t(1) << 32))
+        throw InvalidArgument("rhg: more than 2^32 points (per device) are not supported");
     const std::uint64_t nT = (pl.n_glob + kGGTile - 1) / kGGTile, tiles = nT * (nT + 1) / 2;
     pl.gg_t0 = tiles * r / W, pl.gg_t1 = tiles * (r + 1) / W;
     return pl;
 }
 
 struct Tables {
-    AnnulusDev*    ann;
-    StreamJob*     jobs;
-    PairJob *      sjobs, *gjobs;
-    std::uint64_t* blk_prefix;
-    std::uint32_t* blk_job_off;
-    std::uint64_t* gseg;
-    std::uint32_t* ann_blk;
+    AnnulusDev*         ann;
+    unsigned long long* dense_mask;
+    std::uint64_t*      req_off;
+    StreamJob*          jobs;
+    std::uint64_t*      gt_prefix;
+    std::uint64_t*      gseg;
+    std::uint32_t*      ann_blk;
+    unsigned long long* src_mask;
+    double*             hbound;
+    unsigned long long* slab_tab;
+    std::uint64_t*      tail_prefix;
+    double*             tail_lam;
 };
 
 // Pack all tables into one pinned blob and send it with one copy.
 Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr) {
-    const std::size_t o_ann = 0, o_jobs = align256(o_ann + pl.ann.size() * sizeof(AnnulusDev));
-    const std::size_t o_sj = align256(o_jobs + pl.jobs.size() * sizeof(StreamJob));
-    const std::size_t o_gj = align256(o_sj + pl.sjobs.size() * sizeof(PairJob));
-    const std::size_t o_bp = align256(o_gj + pl.gjobs.size() * sizeof(PairJob));
-    const std::size_t o_bj = align256(o_bp + pl.blk_prefix.size() * sizeof(std::uint64_t));
-    const std::size_t o_gs = align256(o_bj + pl.blk_job_off.size() * sizeof(std::uint32_t));
-    const std::size_t o_ab = align256(o_gs + pl.gseg.size() * sizeof(std::uint64_t));
-    const std::size_t bytes = align256(o_ab + pl.ann_blk.size() * sizeof(std::uint32_t)) + 256;
+    struct Part {
+        const void* src;
+        std::size_t bytes, off;
+    };
+    std::vector<Part> parts;
+    std::size_t       bytes = 0;
+    auto add = [&](const auto& v) {
+        parts.push_back({v.data(), v.size() * sizeof(v[0]), bytes});
+        bytes = align256(bytes + v.size() * sizeof(v[0]));
+        return parts.size() - 1;
+    };
+    const std::size_t i_ann = add(pl.ann), i_dm = add(pl.dense_mask), i_ro = add(pl.req_off), i_jobs = add(pl.jobs);
+    const std::size_t i_gt = add(pl.gt_prefix), i_gs = add(pl.gseg), i_ab = add(pl.ann_blk), i_sm = add(pl.src_mask);
+    const std::size_t i_hb = add(pl.hbound), i_sp = add(pl.slab_tab), i_tp = add(pl.tail_prefix);
+    const std::size_t i_tl = add(pl.tail_lam);
+    bytes += 256;
     ctx->staging.ensure(bytes);
     char* h = static_cast<char*>(ctx->staging.p);
-    std::memcpy(h + o_ann, pl.ann.data(), pl.ann.size() * sizeof(AnnulusDev));
-    std::memcpy(h + o_jobs, pl.jobs.data(), pl.jobs.size() * sizeof(StreamJob));
-    std::memcpy(h + o_sj, pl.sjobs.data(), pl.sjobs.size() * sizeof(PairJob));
-    std::memcpy(h + o_gj, pl.gjobs.data(), pl.gjobs.size() * sizeof(PairJob));
-    std::memcpy(h + o_bp, pl.blk_prefix.data(), pl.blk_prefix.size() * sizeof(std::uint64_t));
-    std::memcpy(h + o_bj, pl.blk_job_off.data(), pl.blk_job_off.size() * sizeof(std::uint32_t));
-    std::memcpy(h + o_gs, pl.gseg.data(), pl.gseg.size() * sizeof(std::uint64_t));
-    std::memcpy(h + o_ab, pl.ann_blk.data(), pl.ann_blk.size() * sizeof(std::uint32_t));
+    for (const Part& q: parts)
+        if (q.bytes) std::memcpy(h + q.off, q.src, q.bytes);
     ctx->tables.ensure(bytes);
     CK(cudaMemcpyAsync(ctx->tables.p, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
     if (h2d) *h2d += bytes;
-    char* d = ctx->tables.as<char>();
-    return {reinterpret_cast<AnnulusDev*>(d + o_ann), reinterpret_cast<StreamJob*>(d + o_jobs),
-            reinterpret_cast<PairJob*>(d + o_sj), reinterpret_cast<PairJob*>(d + o_gj),
-            reinterpret_cast<std::uint64_t*>(d + o_bp), reinterpret_cast<std::uint32_t*>(d + o_bj),
-            reinterpret_cast<std::uint64_t*>(d + o_gs), reinterpret_cast<std::uint32_t*>(d + o_ab)};
+    char* d  = ctx->tables.as<char>();
+    auto  at = [&](std::size_t i) { return static_cast<void*>(d + parts[i].off); };
+    return {static_cast<AnnulusDev*>(at(i_ann)),        static_cast<unsigned long long*>(at(i_dm)),
+            static_cast<std::uint64_t*>(at(i_ro)),      static_cast<StreamJob*>(at(i_jobs)),
+            static_cast<std::uint64_t*>(at(i_gt)),      static_cast<std::uint64_t*>(at(i_gs)),
+            static_cast<std::uint32_t*>(at(i_ab)),      static_cast<unsigned long long*>(at(i_sm)),
+            static_cast<double*>(at(i_hb)),             static_cast<unsigned long long*>(at(i_sp)),
+            static_cast<std::uint64_t*>(at(i_tp)),      static_cast<double*>(at(i_tl))};
 }
 
 void ensure_points(rhg_ctx* ctx, std::uint64_t total, bool with_export) {
@@ -307,8 +384,12 @@ SamplerArgs sampler_args(rhg_ctx* ctx, const Plan& pl, const Tables& t) {
 // Cell index + every edge kernel + counters back to the host.
 void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out, std::uint32_t* degrees,
                std::uint64_t* launches) {
-    const std::size_t cnt_bytes = align256(3 * sizeof(Counters)) + align256(pl.L.count * sizeof(unsigned long long)) +
-                                  256;
+    const std::uint32_t K         = pl.L.count;
+    const std::size_t   o_dmax    = align256(3 * sizeof(Counters));
+    const std::size_t   o_hmax    = o_dmax + align256(K * sizeof(unsigned long long));
+    const std::size_t   o_cseg    = o_hmax + align256(std::size_t(kMaxCls) * K * sizeof(unsigned long long));
+    const std::size_t   o_slots   = o_cseg + align256((kMaxCls + 1) * sizeof(std::uint32_t));
+    const std::size_t   cnt_bytes = o_slots + 3 * kSlots * sizeof(SlotCounter) + 256;
     ctx->counters.ensure(cnt_bytes);
     CK(cudaMemsetAsync(ctx->counters.p, 0, cnt_bytes, ctx->stream));
     ctx->cells.ensure(std::max<std::uint64_t>(pl.ncells, 1) * sizeof(std::uint64_t));
@@ -317,7 +398,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         CK(cudaMemsetAsync(ctx->degrees.p, 0, pl.L.n * sizeof(unsigned), ctx->stream));
     }
     EdgeArgs e;
-    e.ann = t.ann, e.count = int(pl.L.count), e.first_streaming = int(pl.L.first_streaming);
+    e.ann = t.ann, e.count = int(K), e.first_streaming = int(pl.L.first_streaming);
     e.n_ext = pl.n_ext, e.n_glob = pl.n_glob;
     e.beta = ctx->beta.as<double>(), e.hw = ctx->hw.as<double>();
     e.rec0 = ctx->rec0.as<double2>(), e.rec1 = ctx->rec1.as<double2>(), e.rec2 = ctx->rec2.as<double2>();
@@ -329,29 +410,45 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         ctx->perm.ensure(ne * sizeof(std::uint64_t));
         ctx->s_beta.ensure(ne * sizeof(double));
         ctx->s_hw.ensure(ne * sizeof(double));
-        ctx->s_rec0.ensure(ne * sizeof(double2));
+        ctx->s_lt.ensure(2 * ne * sizeof(double));
         ctx->s_rec1.ensure(ne * sizeof(double2));
         ctx->s_rec2.ensure(ne * sizeof(double2));
         ctx->nid.ensure(ne * sizeof(unsigned long long));
         e.perm = ctx->perm.as<std::uint64_t>(), e.s_beta = ctx->s_beta.as<double>(), e.s_hw = ctx->s_hw.as<double>();
-        e.s_rec0 = ctx->s_rec0.as<double2>(), e.s_rec1 = ctx->s_rec1.as<double2>(), e.s_rec2 = ctx->s_rec2.as<double2>();
+        e.s_lam = ctx->s_lt.as<double>(), e.s_theta = ctx->s_lt.as<double>() + ne;
+        e.s_rec1 = ctx->s_rec1.as<double2>(), e.s_rec2 = ctx->s_rec2.as<double2>();
         e.s_id = ctx->nid.as<unsigned long long>();
+    }
+    {   // global requests: theta-sorted records and window-piece rows
+        const std::size_t nG  = std::max<std::uint64_t>(pl.n_req, 1);
+        const std::size_t nst = pl.L.count - pl.L.first_streaming;
+        const std::size_t o_th = align256(2 * nG * sizeof(double2));
+        const std::size_t o_id = o_th + align256(nG * sizeof(double));
+        const std::size_t o_rw = o_id + align256(nG * sizeof(std::uint32_t));
+        ctx->gbuf.ensure(o_rw + align256(std::max<std::size_t>(nst, 1) * nG * 8 * sizeof(std::uint32_t)));
+        char* g     = ctx->gbuf.as<char>();
+        e.g_rec     = reinterpret_cast<double2*>(g);
+        e.g_theta   = reinterpret_cast<double*>(g + o_th);
+        e.g_id      = reinterpret_cast<std::uint32_t*>(g + o_id);
+        e.g_rows    = reinterpret_cast<std::uint32_t*>(g + o_rw);
+        e.hmax_bits = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + o_hmax);
+        e.cseg      = reinterpret_cast<std::uint32_t*>(ctx->counters.as<char>() + o_cseg);
+        e.n_cls     = reinterpret_cast<int*>(ctx->counters.as<char>() + cnt_bytes - 256);
+        e.gt_prefix = t.gt_prefix, e.glob_tile_warps = pl.gtwarps;
+        e.n_req = pl.n_req, e.req_off = t.req_off, e.dense_mask = t.dense_mask;
     }
     e.ann_rw = t.ann;
     e.ctr       = ctx->counters.as<Counters>();
-    e.dmax_bits = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + align256(3 * sizeof(Counters)));
-    e.task_ctr  = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + cnt_bytes - 256);
-    e.task_cap  = std::uint64_t(1) << 21; // 64 MiB of deferred dense tiles; overflow runs inline
-    ctx->tasks.ensure(e.task_cap * sizeof(TileTask));
-    e.tasks = ctx->tasks.as<TileTask>();
+    e.slots     = reinterpret_cast<SlotCounter*>(ctx->counters.as<char>() + o_slots);
+    e.dmax_bits = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + o_dmax);
     e.cosh_R = pl.L.cosh_R, e.chunk0_upper = chunk_upper_bound(0, pl.L.chunks);
     e.lift_part   = pl.e1 == pl.L.chunks && pl.T > 0;
-    e.stream_jobs = t.sjobs, e.n_stream_jobs = int(pl.sjobs.size()), e.stream_warps = pl.swarps;
-    e.blk_prefix = t.blk_prefix, e.blk_job_off = t.blk_job_off, e.nblk = pl.nblk;
+    e.slab_tab = t.slab_tab, e.n_slabs = pl.n_slabs, e.src_mask = t.src_mask, e.hbound = t.hbound;
+    e.tail_prefix = t.tail_prefix, e.tail_lam = t.tail_lam, e.n_tail = pl.n_tail;
     e.ev_pairs0 = ctx->ev[4], e.ev_pairs1 = ctx->ev[5];
-    e.glob_jobs = t.gjobs, e.n_glob_jobs = int(pl.gjobs.size()), e.glob_warps = pl.gwarps;
     e.gg_tile_begin = pl.gg_t0, e.gg_tile_end = pl.gg_t1;
     e.degrees       = degrees ? ctx->degrees.as<unsigned>() : nullptr;
+    if (const char* ab = std::getenv("RHG_ABLATE")) e.ablate = std::atoi(ab);
     const char* dbg_env = std::getenv("RHG_DEBUG_STATS");
     const bool  dbg     = dbg_env && dbg_env[0] == '1';
     if (dbg) {
@@ -361,12 +458,11 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     }
     e.ann_blk = t.ann_blk;
     launch_cell_index(e, pl.ann_blk[pl.L.count], ctx->stream, launches);
-    if (pl.n_glob && pl.gwarps) { // global requests in (annulus, theta) order
+    if (pl.n_req && pl.L.first_streaming < pl.L.count) { // dense-engine requests in (source, class, angle) order
         std::size_t need = 0;
-        launch_sort_globals(e, t.gseg, int(pl.gseg.size() - 1), nullptr, 0, &need, ctx->stream, launches);
+        launch_sort_globals(e, nullptr, 0, &need, ctx->stream, launches);
         ctx->gsort.ensure(need);
-        launch_sort_globals(e, t.gseg, int(pl.gseg.size() - 1), ctx->gsort.p, ctx->gsort.cap, &need, ctx->stream,
-                            launches);
+        launch_sort_globals(e, ctx->gsort.p, ctx->gsort.cap, &need, ctx->stream, launches);
     }
     launch_edges(e, ctx->stream, launches);
     CK(cudaGetLastError());
@@ -374,24 +470,26 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     ctx->staging.ensure(4096);
     auto* hc = static_cast<Counters*>(ctx->staging.p);
     CK(cudaMemcpyAsync(hc, ctx->counters.p, 3 * sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+    int* h_ncls = reinterpret_cast<int*>(hc + 3);
+    *h_ncls     = 0;
+    if (e.n_cls) CK(cudaMemcpyAsync(h_ncls, e.n_cls, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     if (degrees)
         CK(cudaMemcpyAsync(degrees, ctx->degrees.p, pl.L.n * sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    if (*h_ncls > kMaxCls) throw Invariant("dense engine: too many request segments");
     if (dbg) {
         unsigned long long h[kDbgSlots];
         CK(cudaMemcpy(h, ctx->dbg.p, sizeof h, cudaMemcpyDeviceToHost));
-        std::fprintf(stderr, "RHG_DEBUG_STATS {\"groups\": [%llu,%llu,%llu,%llu,%llu,%llu], \"sumU\": [%llu,%llu,%llu,%llu,%llu,%llu], "
-                             "\"slots\": [%llu,%llu,%llu,%llu,%llu,%llu], \"serial_warps\": %llu, \"serial_slots\": %llu, "
-                             "\"serial_cands\": %llu, \"tasks\": %llu, \"warps\": %llu, \"cands\": %llu}\n",
-                     h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[10], h[11], h[12], h[13], h[14], h[15],
-                     h[16], h[17], h[18], h[19], h[20], h[21], h[22], h[23]);
+        std::fprintf(stderr, "RHG_DEBUG_STATS [");
+        for (int i = 0; i < kDbgSlots; ++i) std::fprintf(stderr, "%s%llu", i ? "," : "", h[i]);
+        std::fprintf(stderr, "]\n");
     }
     out->edges       = hc[0].edges + hc[1].edges + hc[2].edges;
     out->fingerprint = hc[0].fp + hc[1].fp + hc[2].fp;
     out->comps       = hc[0].comps + hc[1].comps + hc[2].comps;
     out->global_edges = hc[2].edges;
     out->global_comps = hc[2].comps;
-    out->pairs_ms     = pl.swarps ? ms_between(ctx->ev[4], ctx->ev[5]) : 0.0;
+    out->pairs_ms     = pl.n_slabs ? ms_between(ctx->ev[4], ctx->ev[5]) : 0.0;
     out->d2h_bytes += 3 * sizeof(Counters) + (degrees ? pl.L.n * sizeof(unsigned) : 0);
 }
 
@@ -469,8 +567,8 @@ void rhg_destroy(rhg_ctx* c) {
     cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->side);
     for (DevBuf* b: {&c->beta, &c->hw, &c->rec0, &c->rec1, &c->rec2, &c->r_out, &c->beta_raw, &c->tables, &c->cells,
-                     &c->counters, &c->degrees, &c->tasks, &c->dbg, &c->nid, &c->lcells, &c->perm, &c->s_beta,
-                     &c->s_hw, &c->s_rec0, &c->s_rec1, &c->s_rec2, &c->gsort})
+                     &c->counters, &c->degrees, &c->dbg, &c->nid, &c->lcells, &c->perm, &c->s_beta,
+                     &c->s_hw, &c->s_lt, &c->s_rec1, &c->s_rec2, &c->gsort, &c->gbuf})
         b->release();
     if (c->staging.p) cudaFreeHost(c->staging.p);
     for (auto& e: c->ev) cudaEventDestroy(e);
@@ -506,8 +604,8 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
         out->kernel_launches = launches;
         out->device_bytes    = ctx->beta.cap + ctx->hw.cap + ctx->rec0.cap + ctx->rec1.cap + ctx->rec2.cap +
                             ctx->r_out.cap + ctx->beta_raw.cap + ctx->tables.cap + ctx->cells.cap + ctx->counters.cap +
-                            ctx->degrees.cap + ctx->tasks.cap + ctx->nid.cap + ctx->lcells.cap + ctx->perm.cap +
-                            ctx->s_beta.cap + ctx->s_hw.cap + ctx->s_rec0.cap + ctx->s_rec1.cap + ctx->s_rec2.cap;
+                            ctx->degrees.cap + ctx->nid.cap + ctx->lcells.cap + ctx->perm.cap + ctx->s_beta.cap +
+                            ctx->s_hw.cap + ctx->s_lt.cap + ctx->s_rec1.cap + ctx->s_rec2.cap + ctx->gbuf.cap;
         out->seconds = std::chrono::duration<double>(Clock::now() - t0).count();
     });
 }

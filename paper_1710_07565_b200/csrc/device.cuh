@@ -37,28 +37,13 @@ struct StreamJob {
     std::uint32_t chunk, pad;
 };
 
-// Work list of the pair kernels: requests of annulus `a` (or the global
-// points, a = -1) against nodes of annulus `j` (streaming jobs: j = -1, every
-// target annulus >= a), in batches of 32 requests.
-struct PairJob {
-    std::uint64_t warp_begin;   // prefix over jobs
-    std::uint64_t req_off, req_end;
-    std::int32_t  a, j;
-};
-
-// A piece of a tile too large to run inline: 2^lgR requests starting at p0
-// of pair job `job` (kind 0 streaming, 1 global with window w) against nodes
-// [u0, u1) of the job's target annulus.
-struct TileTask {
-    std::uint64_t p0, u0, u1;
-    std::int32_t  job;
-    std::int16_t  kind, lgR;
-    std::int32_t  w, j; // w: pass (streaming) or window (global); j: target annulus
-};
-
 struct Counters { // one per edge-producing kernel family
     unsigned long long edges, fp, comps;
 };
+struct SlotCounter { // one of kSlots partial counters of a family (32 B apart)
+    unsigned long long edges, fp, comps, pad;
+};
+constexpr int kSlots = 4096;
 
 __device__ __forceinline__ double fmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double fadd(double a, double b) { return __dadd_rn(a, b); }

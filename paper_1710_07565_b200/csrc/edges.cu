@@ -15,18 +15,24 @@
 // chunks [off, halo) and the halo chunk [halo, end).  A window is then an
 // EXACT index range, and for ordinary same-annulus pairs (both owned, lambda <
 // 2pi, where lambda == theta) the (theta, id) dedup is just "node index >
-// request index" — the hot loop has no window or dedup compares at all.
+// request index" — the hot loops have no window or dedup compares at all.
 //
 //   beta_cells_kernel   beta-cell starts of the beta-ordered sampler output and
 //                       the exact per-annulus max half-width
 //   rank_kernel         exact rank of every point by (lambda, id) inside its block
 //   scatter_kernel      the lambda-sorted arrays (+ node ids)
 //   lambda_cells_kernel lambda-cell starts of the owned blocks, first wrapped index
-//   stream_pairs_kernel streaming requests: one warp per 32 requests x target
-//                       annulus; adaptive R x C register tile over TMA-staged
-//                       node batches, a flattened pair list when sparse
-//   glob_req_kernel     global requests x owned streaming nodes (same engine)
-//   tile_tasks_kernel   deferred pieces of very large tiles, load-balanced
+//   stream_kernel       streaming requests (sparse engine): one warp = 32
+//                       consecutive requests x every target annulus; the warp's
+//                       window union is staged in shared memory and searched
+//                       per lane; short ranges run as one flattened pair list,
+//                       long ranges cooperatively (32 lanes per request)
+//   glob_rows_kernel    global requests: exact clipped window pieces per
+//                       (request, target annulus) as index ranges, comps,
+//                       per-(global annulus, target) max half-width
+//   glob_tiles_kernel   global requests (dense engine): one warp = 128 owned
+//                       nodes held in registers x every global request whose
+//                       window can reach them (theta-sorted candidate ranges)
 //   glob_pairs_kernel   global unit, 128x128 tiles of the upper triangle
 #include <cub/cub.cuh>
 
@@ -43,7 +49,10 @@ struct Acc {
     unsigned long long edges = 0, fp = 0, comps = 0;
 };
 
-__device__ __forceinline__ void flush(Acc& acc, Counters* c, int lane) {
+// Warp-reduce the lane accumulators and add them to one of kSlots spread
+// counter slots of family f (same-address atomics from every warp would
+// serialise in L2); reduce_counters_kernel folds the slots at the end.
+__device__ __forceinline__ void flush(Acc& acc, const EdgeArgs& A, int f, int lane) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         acc.edges += __shfl_down_sync(kFull, acc.edges, o);
@@ -51,9 +60,11 @@ __device__ __forceinline__ void flush(Acc& acc, Counters* c, int lane) {
         acc.comps += __shfl_down_sync(kFull, acc.comps, o);
     }
     if (lane == 0 && (acc.comps | acc.edges)) {
-        atomicAdd(&c->edges, acc.edges);
-        atomicAdd(&c->fp, acc.fp);
-        atomicAdd(&c->comps, acc.comps);
+        const unsigned w    = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        SlotCounter&   slot = A.slots[f * kSlots + (w & (kSlots - 1))];
+        atomicAdd(&slot.edges, acc.edges);
+        atomicAdd(&slot.fp, acc.fp);
+        atomicAdd(&slot.comps, acc.comps);
     }
 }
 
@@ -64,17 +75,6 @@ __device__ __forceinline__ std::uint32_t cellf(const AnnulusDev& A, double x) {
     if (!(t > 0.0)) return 0;
     if (t >= double(A.ncells)) return A.ncells - 1;
     return std::uint32_t(t);
-}
-
-__device__ __forceinline__ int streaming_annulus_of(const AnnulusDev* __restrict__ ann, int fs, int count,
-                                                    std::uint64_t i) {
-    int lo = fs, hi = count - 1; // last streaming annulus with off <= i
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (ann[mid].off <= i) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
 }
 
 // Sort-phase kernels run ceil(n_j / 256) blocks per streaming annulus j
@@ -98,11 +98,6 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
         const unsigned long long t = __shfl_xor_sync(kFull, v, o);
         v                          = t > v ? t : v;
     }
-    return v;
-}
-__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
     return v;
 }
 
@@ -174,13 +169,15 @@ __global__ void __launch_bounds__(256) scatter_kernel(EdgeArgs A) {
     const int           j = block_annulus(A, i);
     const AnnulusDev&   J = A.ann[j];
     if (i >= J.end) return;
-    const std::uint64_t d = A.perm[i];
-    A.s_beta[d]           = A.beta[i];
-    A.s_hw[d]             = A.hw[i];
-    A.s_rec0[d]           = A.rec0[i];
-    A.s_rec1[d]           = A.rec1[i];
-    A.s_rec2[d]           = A.rec2[i];
-    A.s_id[d]             = i + static_cast<unsigned long long>(i < J.halo ? J.dlt0 : J.dlt1);
+    const std::uint64_t d  = A.perm[i];
+    const double2       r0 = A.rec0[i];
+    A.s_beta[d]            = A.beta[i];
+    A.s_hw[d]              = A.hw[i];
+    A.s_lam[d]             = r0.x;
+    A.s_theta[d]           = r0.y;
+    A.s_rec1[d]            = A.rec1[i];
+    A.s_rec2[d]            = A.rec2[i];
+    A.s_id[d]              = i + static_cast<unsigned long long>(i < J.halo ? J.dlt0 : J.dlt1);
 }
 
 // Lambda-cell starts of every owned block, and the first owned index with
@@ -190,687 +187,746 @@ __global__ void __launch_bounds__(256) lambda_cells_kernel(EdgeArgs A) {
     const int     j = block_annulus(A, i);
     AnnulusDev&   J = A.ann_rw[j];
     if (i >= J.halo) return;
-    const double        l  = A.s_rec0[i].x;
+    const double        l  = A.s_lam[i];
     const std::uint32_t k  = cellf(J, l);
-    const std::int64_t  kp = i > J.off ? std::int64_t(cellf(J, A.s_rec0[i - 1].x)) : -1;
+    const std::int64_t  kp = i > J.off ? std::int64_t(cellf(J, A.s_lam[i - 1])) : -1;
     cell_fill(A.lcellstart + J.cell_off, kp, k, i);
-    if (l >= kTwoPiD && (i == J.off || A.s_rec0[i - 1].x < kTwoPiD)) J.wrap = i;
+    if (l >= kTwoPiD && (i == J.off || A.s_lam[i - 1] < kTwoPiD)) J.wrap = i;
 }
 
 // Tails of both cell tables: cells after the last point of a block hold the
 // block end (beta table: whole annulus array; lambda table: owned block).
 __global__ void cell_tail_kernel(EdgeArgs A, int lambda) {
-    const int         j  = A.first_streaming + int(blockIdx.y);
-    const AnnulusDev& J  = A.ann[j];
+    const int           j = A.first_streaming + int(blockIdx.y);
+    const AnnulusDev&   J = A.ann[j];
     const std::uint64_t e = lambda ? J.halo : J.end;
     if (e == J.off) return; // empty: initialised by beta_cells_kernel
-    const double        last = lambda ? A.s_rec0[e - 1].x : A.beta[e - 1];
+    const double        last = lambda ? A.s_lam[e - 1] : A.beta[e - 1];
     const std::uint32_t k0   = cellf(J, last) + 1;
     std::uint64_t*      tab  = (lambda ? A.lcellstart : A.cellstart) + J.cell_off;
     for (std::uint32_t c = k0 + blockIdx.x * blockDim.x + threadIdx.x; c <= J.ncells; c += gridDim.x * blockDim.x)
         tab[c] = e;
 }
 
-// ------------------------------------------------------------ requests ---
-// First index k in the sorted owned block with lambda[k] >= x (exact).
+// ------------------------------------------------------- window search ---
+// Advance k over the nodes of [k, e) with lambda < x, four independent loads
+// at a time (cells hold ~2 nodes, so one step almost always suffices).
+__device__ __forceinline__ std::uint64_t scan_lt(const double* __restrict__ lam, std::uint64_t k, std::uint64_t e,
+                                                 double x) {
+    while (k < e) {
+        const std::uint64_t n = e - k;
+        const double        x0 = lam[k];
+        const double        x1 = n > 1 ? lam[k + 1] : x;
+        const double        x2 = n > 2 ? lam[k + 2] : x;
+        const double        x3 = n > 3 ? lam[k + 3] : x;
+        const unsigned      c  = unsigned(x0 < x) + unsigned(x1 < x) + unsigned(x2 < x) + unsigned(x3 < x);
+        k += c;
+        if (c < 4) break;
+    }
+    return k;
+}
+// First index k in the sorted owned block with lambda[k] >= x (exact): the
+// lambda cell of x bounds it from both sides (cellf is monotone).
 __device__ __forceinline__ std::uint64_t lower_bound_owned(const EdgeArgs& A, const AnnulusDev& J, double x) {
     const std::uint32_t c = cellf(J, x);
-    std::uint64_t       k = A.lcellstart[J.cell_off + c];
-    const std::uint64_t e = A.lcellstart[J.cell_off + c + 1];
-    while (k < e && A.s_rec0[k].x < x) ++k;
-    return k;
+    return scan_lt(A.s_lam, A.lcellstart[J.cell_off + c], A.lcellstart[J.cell_off + c + 1], x);
+}
+// Both bounds of [lo, hi): the four cell-table loads are issued together.
+__device__ __forceinline__ void owned_range(const EdgeArgs& A, const AnnulusDev& J, double lo, double hi,
+                                            std::uint64_t& s0, std::uint64_t& s1) {
+    const std::uint32_t ca = cellf(J, lo), cb = cellf(J, hi);
+    const std::uint64_t ka = A.lcellstart[J.cell_off + ca], kb = A.lcellstart[J.cell_off + cb];
+    const std::uint64_t ea = A.lcellstart[J.cell_off + ca + 1], eb = A.lcellstart[J.cell_off + cb + 1];
+    s0 = scan_lt(A.s_lam, ka, ea, lo);
+    s1 = scan_lt(A.s_lam, kb, eb, hi);
 }
 __device__ __forceinline__ std::uint64_t lower_bound_halo(const EdgeArgs& A, const AnnulusDev& J, double x) {
     std::uint64_t lo = J.halo, hi = J.end; // binary search (one chunk, rarely searched)
     while (lo < hi) {
         const std::uint64_t mid = (lo + hi) >> 1;
-        if (A.s_rec0[mid].x < x) lo = mid + 1;
+        if (A.s_lam[mid] < x) lo = mid + 1;
         else hi = mid;
     }
     return lo;
 }
 
-struct Req {
-    double             cs, sn, coth, rci; // rci = fl(cosh(R) * inv_sinh_r), hoisted (sweep.hpp:532 order)
-    unsigned long long id;
-    double             theta;
-};
-
-// One request against one target annulus: the simple index range handled by
-// the tile engine, the halo-block range and the "general" range of pairs that
-// need the full (theta, id) dedup (same-annulus pairs with wrapped or halo points).
-struct Lane {
-    Req           q;
-    std::uint64_t s0, s1; // simple owned range
-    std::uint64_t h0, h1; // halo-block range (simple when j != a, general when j == a)
-    std::uint64_t g0, g1; // general owned range (j == a only)
-};
-
-__device__ __forceinline__ void window_ranges(const EdgeArgs& A, const AnnulusDev& J, double lo, double hi,
-                                              bool want_halo, Lane& L) {
-    if (!(hi > lo)) return;
-    { // both lower bounds interleaved: independent loads in flight together
-        const std::uint32_t ca = cellf(J, lo), cb = cellf(J, hi);
-        std::uint64_t       ka = A.lcellstart[J.cell_off + ca], kb = A.lcellstart[J.cell_off + cb];
-        const std::uint64_t ea = A.lcellstart[J.cell_off + ca + 1], eb = A.lcellstart[J.cell_off + cb + 1];
-        bool                ma = ka < ea, mb = kb < eb;
-        while (ma || mb) {
-            const double xa = ma ? A.s_rec0[ka].x : 0.0, xb = mb ? A.s_rec0[kb].x : 0.0;
-            if (ma) {
-                if (xa < lo) ma = ++ka < ea;
-                else ma = false;
-            }
-            if (mb) {
-                if (xb < hi) mb = ++kb < eb;
-                else mb = false;
-            }
-        }
-        L.s0 = ka, L.s1 = kb;
-    }
-    if (want_halo && J.end > J.halo && hi > A.s_rec0[J.halo].x && lo <= A.s_rec0[J.end - 1].x) {
-        L.h0 = lower_bound_halo(A, J, lo);
-        L.h1 = lower_bound_halo(A, J, hi);
-    }
-}
-
-// Streaming request at sorted index p of annulus a against annulus j
-// (sweep.hpp:455-461, 478-479).
-__device__ __forceinline__ void setup_stream(const EdgeArgs& A, const PairJob& Jb, int j, std::uint64_t p, Lane& L) {
-    L = Lane{};
-    if (p >= Jb.req_end) return;
-    const AnnulusDev& Aa = A.ann[Jb.a];
-    const AnnulusDev& Aj = A.ann[j];
-    const double      b  = A.s_beta[p];
-    const double      hw = A.s_hw[p];
-    const double2     r0 = A.s_rec0[p], r1 = A.s_rec1[p], r2 = A.s_rec2[p];
-    L.q.cs = r1.x, L.q.sn = r1.y, L.q.coth = r2.x, L.q.rci = fmul(A.cosh_R, r2.y);
-    L.q.id          = A.s_id[p];
-    L.q.theta       = r0.y;
-    const bool halo = p >= Aa.halo;
-    double     lo, hi;
-    if (j == Jb.a) { // own window [b, b + 2hw)
-        lo = b;
-        hi = fadd(b, fmul(2.0, hw));
-    } else { // propagated window [lambda - h_j, lambda + h_j)
-        const double h = half_width_in(Aj, r2.x, r2.y);
-        lo             = fsub(r0.x, h);
-        hi             = fadd(r0.x, h);
-    }
-    window_ranges(A, Aj, lo, hi, !halo, L); // halo requests: owned nodes only (no Foreign x Foreign)
-    if (j == Jb.a) {
-        if (!halo && p < Aa.wrap) { // theta == lambda and index order == (lambda, id) order
-            const std::uint64_t w = Aj.wrap;
-            L.g0 = L.s0 > w ? L.s0 : w, L.g1 = L.s1; // wrapped nodes: general
-            L.s1 = L.s1 < w ? L.s1 : w;
-            L.s0 = L.s0 > p + 1 ? L.s0 : p + 1;      // dedup == index order, self excluded
-        } else {
-            L.g0 = L.s0, L.g1 = L.s1, L.s0 = L.s1 = 0; // all general
-        }
-    }
-    if (L.s1 < L.s0) L.s1 = L.s0;
-    if (L.g1 < L.g0) L.g1 = L.g0;
-    if (L.h1 < L.h0) L.h1 = L.h0;
-}
-
-// Global request g against streaming annulus Jb.j, window number w (0..3):
-// split_wraparound pieces (sweep.hpp:41-58) and, when this shard owns engine
-// P-1, their chunk-0 parts lifted by 2pi (sweep.hpp:404-432).  Owned nodes only.
-__device__ __forceinline__ void setup_global(const EdgeArgs& A, const PairJob& Jb, std::uint64_t gs, int w, Lane& L) {
-    L = Lane{};
-    if (gs >= Jb.req_end) return;
-    // requests run in (annulus, theta) order so that neighbouring lanes share nodes
-    const std::uint64_t g  = A.gperm ? A.n_ext + A.gperm[gs - A.n_ext] : gs;
-    const AnnulusDev&   Aj = A.ann[Jb.j];
-    const double2     r0 = A.rec0[g], r1 = A.rec1[g], r2 = A.rec2[g];
-    const double      th = r0.y;
-    const double      h  = half_width_in(Aj, r2.x, r2.y); // generator.hpp:67
-    const double      a = fsub(th, h), b = fadd(th, h);
-    double            pa[2], pb[2];
-    int               np = 1;
-    if (fsub(b, a) >= kTwoPiD) {
-        pa[0] = 0.0, pb[0] = kTwoPiD;
-    } else if (a < 0.0) {
-        pa[0] = fadd(a, kTwoPiD), pb[0] = kTwoPiD, pa[1] = 0.0, pb[1] = b, np = 2;
-    } else if (b > kTwoPiD) {
-        pa[0] = a, pb[0] = kTwoPiD, pa[1] = 0.0, pb[1] = fsub(b, kTwoPiD), np = 2;
-    } else {
-        pa[0] = a, pb[0] = b;
-    }
-    double lo = 0.0, hi = 0.0;
-    int    nw = 0;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        if (k >= np) break;
-        if (nw == w) lo = pa[k], hi = pb[k];
-        ++nw;
-        if (A.lift_part) {
-            const double l2 = pa[k] < 0.0 ? 0.0 : pa[k];                      // max(begin, w0 = 0)
-            const double h2 = A.chunk0_upper < pb[k] ? A.chunk0_upper : pb[k]; // min(end, w1)
-            if (l2 < h2) {
-                if (nw == w) lo = fadd(l2, kTwoPiD), hi = fadd(h2, kTwoPiD);
-                ++nw;
-            }
-        }
-    }
-    if (w >= nw) return;
-    L.q.cs = r1.x, L.q.sn = r1.y, L.q.coth = r2.x, L.q.rci = fmul(A.cosh_R, r2.y);
-    L.q.id = g - A.n_ext;
-    window_ranges(A, Aj, lo, hi, false, L);
-    if (L.s1 < L.s0) L.s1 = L.s0;
-}
-
 // The reference predicate (sweep.hpp:531-533), in its rounding order:
 //   lhs = fl(fl(c_r c_n) + fl(s_r s_n)),  rhs = fl(fl(k_r k_n) - fl(fl(coshR i_r) i_n)),  edge iff lhs > rhs.
+// rci = fl(coshR * i_r) is hoisted per request.
+__device__ __forceinline__ bool edge_test(double cs, double sn, double coth, double rci, double2 n1, double2 n2) {
+    const double lhs = fadd(fmul(cs, n1.x), fmul(sn, n1.y));
+    const double rhs = fsub(fmul(coth, n2.x), fmul(rci, n2.y));
+    return lhs > rhs;
+}
+
 template <bool DEG>
-__device__ __forceinline__ void predicate(const EdgeArgs& A, const Req& q, bool in, double2 n1, double2 n2,
-                                          unsigned long long nid, Acc& acc) {
-    const double lhs = fadd(fmul(q.cs, n1.x), fmul(q.sn, n1.y));
-    const double rhs = fsub(fmul(q.coth, n2.x), fmul(q.rci, n2.y));
-    const bool   e   = in & (lhs > rhs);
-    acc.comps += in;
+__device__ __forceinline__ void count_edge(const EdgeArgs& A, bool e, unsigned long long id_r,
+                                           unsigned long long id_n, Acc& acc) {
     acc.edges += e;
-    acc.fp += e ? q.id + nid : 0ull;
+    acc.fp += e ? id_r + id_n : 0ull;
     if (DEG && e) {
-        atomicAdd(&A.degrees[q.id], 1u);
-        atomicAdd(&A.degrees[nid], 1u);
+        atomicAdd(&A.degrees[id_r], 1u);
+        atomicAdd(&A.degrees[id_n], 1u);
     }
 }
 
-// Tile-loop variant: per-row 32-bit counters; the fingerprint is folded as
-// E * id_p + sum(node ids) when the row changes (RowAcc::fold).
-struct RowAcc {
-    std::uint32_t      comps = 0, edges = 0;
-    unsigned long long nsum  = 0;
-    __device__ __forceinline__ void fold(Acc& acc, unsigned long long id) {
-        acc.comps += comps, acc.edges += edges, acc.fp += edges * id + nsum;
-        comps = edges = 0, nsum = 0;
-    }
+// ------------------------------------------------ streaming (sparse) ---
+
+struct SRow { // one request as the cooperative loop reads it (broadcast from shared memory)
+    double             cs, sn, coth, rci;
+    unsigned long long id, pad;
 };
-template <bool DEG>
-__device__ __forceinline__ void predicate_row(const EdgeArgs& A, const Req& q, bool in, double2 n1, double2 n2,
-                                              unsigned long long nid, RowAcc& ra) {
-    const double lhs = fadd(fmul(q.cs, n1.x), fmul(q.sn, n1.y));
-    const double rhs = fsub(fmul(q.coth, n2.x), fmul(q.rci, n2.y));
-    const bool   e   = in & (lhs > rhs);
-    ra.comps += in;
-    ra.edges += e;
-    ra.nsum += e ? nid : 0ull;
-    if (DEG && e) {
-        atomicAdd(&A.degrees[q.id], 1u);
-        atomicAdd(&A.degrees[nid], 1u);
-    }
-}
 
-// Same-annulus pairs that need the full dedup (sweep.hpp:517-526): not self,
-// and (theta_p, id_p) < (theta_q, id_q).  Rare; thread-serial.
+// Thread-serial pairs (rare): halo-block ranges and same-annulus pairs that
+// need the full (theta, id) dedup (sweep.hpp:517-526).
 template <bool DEG>
-__device__ __forceinline__ void general_range(const EdgeArgs& A, const Req& q, std::uint64_t k0, std::uint64_t k1,
-                                              Acc& acc) {
+__device__ __forceinline__ void serial_range(const EdgeArgs& A, const SRow& q, double theta, bool dedup,
+                                             std::uint64_t k0, std::uint64_t k1, Acc& acc) {
     for (std::uint64_t k = k0; k < k1; ++k) {
         const unsigned long long nid = A.s_id[k];
-        const double             tq  = A.s_rec0[k].y;
-        const bool in = nid != q.id && (q.theta < tq || (q.theta == tq && q.id < nid));
-        predicate<DEG>(A, q, in, A.s_rec1[k], A.s_rec2[k], nid, acc);
+        bool                     in  = true;
+        if (dedup) {
+            const double tq = A.s_theta[k];
+            in              = nid != q.id && (theta < tq || (theta == tq && q.id < nid));
+        }
+        if (!in) continue;
+        if (A.dbg) atomicAdd(&A.dbg[5], 1ull);
+        acc.comps += 1;
+        count_edge<DEG>(A, edge_test(q.cs, q.sn, q.coth, q.rci, A.s_rec1[k], A.s_rec2[k]), q.id, nid, acc);
     }
 }
 
-// ---------------------------------------------------------------- tiles ---
-// Per-warp shared memory: a kStages-deep ring of kBatch-node batches filled
-// by TMA bulk copies (cp.async.bulk, completion on an mbarrier), SoA so that
-// lanes reading consecutive nodes are conflict-free and a whole-warp read of
-// one node is a broadcast.
-constexpr int kBatch  = 128;
-constexpr int kStages = 2;
+// ---------------------------------------------------------- slab join ---
+// Sparse (annulus a, target j) pairs.  CTA = one slab of kSlab consecutive
+// nodes of j's owned block, staged in shared memory once (coalesced).  For
+// every sparse source annulus a <= j the requests whose window can reach the
+// slab (lambda within hbound(a, j) of it: a contiguous run of a's sorted
+// owned block, from a's lambda-cell table) are streamed through the warps,
+// 32 at a time; each lane finds its exact node range in the slab by binary
+// search over the staged lambdas and tests it lane-serially from shared
+// memory.  Every pair belongs to exactly one slab (its node's), so comps add.
+// Own annulus (j == a): requests and nodes below the wrap index only, nodes
+// after the request (index order == (theta, id) dedup order); everything
+// else - halo requests, halo nodes, wrapped points - runs in tail_kernel.
+constexpr int kSlab        = 1024;
+constexpr int kSlabThreads = 256;
 
-struct Stage {
-    double2            r1[kBatch], r2[kBatch];
-    unsigned long long id[kBatch + 2]; // copied from an even index: node t is id[t + (base & 1)]
+constexpr int kListCap     = 1024; // flattened pairs per list batch (one byte each: the owning lane)
+
+struct SlabWarp {
+    SRow          rows[32];       // the warp's current requests (pad = local node of pair 0)
+    unsigned char list[kListCap]; // flattened pair t -> owning lane
 };
-// A tile row as the tile loop needs it (staged once per warp in shared memory).
-struct RowSm {
-    double             cs, sn, coth, rci;
-    unsigned long long id, r0, r1, pad; // simple range [r0, r1)
+struct SlabSmem {
+    double             lam[kSlab];
+    double2            r1[kSlab], r2[kSlab];
+    unsigned long long id[kSlab];
+    std::uint16_t      bstart[kSlab + 1]; // bucket b: first local node with bucket(lambda) >= b
+    SlabWarp           w[kSlabThreads / 32];
 };
-struct WarpSmem {
-    Stage              st[kStages];
-    RowSm              rows[32];
-    unsigned long long bar[kStages];
-    int                meta_g[kStages];
-    int                meta_cnt[kStages];
-    std::uint64_t      meta_base[kStages];
-};
-constexpr int kWarpsPerBlock = 8;
-constexpr int kTileSmem      = kWarpsPerBlock * int(sizeof(WarpSmem));
 
-__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
-    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+// Bucket of an angle inside the slab: monotone in x (fsub, fmul, clamp), so
+// lower_bound(x) lies in [bstart[b], bstart[b + 1]] for b = bucket(x).
+__device__ __forceinline__ std::uint32_t slab_bucket(double x, double org, double inv_w) {
+    const double t = fmul(fsub(x, org), inv_w);
+    if (!(t > 0.0)) return 0;
+    if (t >= double(kSlab - 1)) return kSlab - 1;
+    return std::uint32_t(t);
 }
-__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, std::uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32_t bytes, unsigned long long* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, std::uint32_t parity) {
-    std::uint32_t done = 0;
-    while (!done) {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-                     : "=r"(done)
-                     : "r"(smem_u32(bar)), "r"(parity)
-                     : "memory");
-    }
-}
-
-__device__ __forceinline__ void warp_smem_init(WarpSmem* ws, int lane) {
-    if (lane == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&ws->bar[s]);
-        fence_mbar_init();
-    }
-    __syncwarp();
-}
-
-// Lane 0 queues one batch [base, base+cnt) of sorted nodes into stage s.  The
-// 8-byte ids are copied from the even index below base (bulk copies need 16 B
-// alignment and size); the 16-byte records need nothing.
-__device__ __forceinline__ void issue_batch(const EdgeArgs& A, WarpSmem* ws, int s, int g, std::uint64_t base,
-                                            int cnt) {
-    const std::uint32_t b16 = std::uint32_t(cnt) * 16u;
-    const std::uint64_t nb  = base & ~1ull;
-    const std::uint32_t bid = std::uint32_t(((base + cnt + 1) & ~1ull) - nb) * 8u;
-    ws->meta_g[s] = g, ws->meta_cnt[s] = cnt, ws->meta_base[s] = base;
-    mbar_expect_tx(&ws->bar[s], 2 * b16 + bid);
-    bulk_g2s(ws->st[s].r1, A.s_rec1 + base, b16, &ws->bar[s]);
-    bulk_g2s(ws->st[s].r2, A.s_rec2 + base, b16, &ws->bar[s]);
-    bulk_g2s(ws->st[s].id, A.s_id + nb, bid, &ws->bar[s]);
-}
-
-// Batch cursor over the groups' unions: group g spans [ga_g, gb_g); unions
-// live in lanes g*R; empty groups (gb <= ga) are skipped.
-struct Cursor {
-    int           g;
-    std::uint64_t base, end;
-};
-__device__ __forceinline__ bool cursor_group(Cursor& c, int R, int C, std::uint64_t ga, std::uint64_t gb) {
-    for (; c.g < C; ++c.g) {
-        const std::uint64_t a = __shfl_sync(kFull, ga, c.g * R), b = __shfl_sync(kFull, gb, c.g * R);
-        if (b > a) {
-            c.base = a, c.end = b;
-            return true;
-        }
-    }
-    return false;
-}
-
-// R x C register tile, TMA-pipelined: the warp's C groups of R requests (one
-// per lane row, replicated over C = 32/R columns) against the unions of their
-// simple ranges; lane (r, c) tests nodes c, c+C, ... of every batch against
-// request r of the current group.  Exact: a node is tested iff its index lies
-// in the row's range.
-template <bool DEG, int R>
-__device__ __forceinline__ void tile_run(const EdgeArgs& A, std::uint64_t ga, std::uint64_t gb, Acc& acc, int lane,
-                                         WarpSmem* ws, std::uint32_t& phase) {
-    constexpr int C   = 32 / R;
-    const int     col = lane % C, row = lane / C;
-    Cursor        prod{0, 0, 0};
-    bool          more    = cursor_group(prod, R, C, ga, gb);
-    int           s_issue = 0, inflight = 0;
-    while (more && inflight < kStages) { // prologue: fill the ring
-        const int cnt = prod.end - prod.base < kBatch ? int(prod.end - prod.base) : kBatch;
-        if (lane == 0) issue_batch(A, ws, s_issue, prod.g, prod.base, cnt);
-        prod.base += kBatch;
-        if (prod.base >= prod.end) {
-            ++prod.g;
-            more = cursor_group(prod, R, C, ga, gb);
-        }
-        s_issue = s_issue + 1 == kStages ? 0 : s_issue + 1;
-        ++inflight;
-    }
-    int           s = 0, cur_g = -1;
-    Req           q{};
-    std::uint64_t r0 = 0, r1 = 0;
-    RowAcc        ra;
-    while (inflight) {
-        mbar_wait(&ws->bar[s], (phase >> s) & 1u);
-        phase ^= 1u << s;
-        const int           g = ws->meta_g[s], cnt = ws->meta_cnt[s];
-        const std::uint64_t base = ws->meta_base[s];
-        const int           no   = int(base & 1);
-        if (g != cur_g) {
-            ra.fold(acc, q.id);
-            cur_g            = g;
-            const RowSm& src = ws->rows[g * R + row];
-            q.cs = src.cs, q.sn = src.sn, q.coth = src.coth, q.rci = src.rci, q.id = src.id;
-            r0 = src.r0, r1 = src.r1;
-        }
-        // the row's range relative to this batch, clamped to [0, kBatch]: int compares
-        const int    lo = r0 > base ? int(r0 - base < kBatch ? r0 - base : kBatch) : 0;
-        const int    hi = r1 > base ? int(r1 - base < kBatch ? r1 - base : kBatch) : 0;
-        const Stage& S  = ws->st[s];
-        if (cnt == kBatch) {
-#pragma unroll 4
-            for (int i = 0; i < kBatch / C; ++i) {
-                const int t = col + C * i;
-                predicate_row<DEG>(A, q, (t >= lo) & (t < hi), S.r1[t], S.r2[t], S.id[t + no], ra);
-            }
-        } else {
-            for (int t = col; t < cnt; t += C)
-                predicate_row<DEG>(A, q, (t >= lo) & (t < hi), S.r1[t], S.r2[t], S.id[t + no], ra);
-        }
-        __syncwarp();
-        --inflight;
-        if (more) { // refill this stage
-            const int c2 = prod.end - prod.base < kBatch ? int(prod.end - prod.base) : kBatch;
-            if (lane == 0) issue_batch(A, ws, s, prod.g, prod.base, c2);
-            prod.base += kBatch;
-            if (prod.base >= prod.end) {
-                ++prod.g;
-                more = cursor_group(prod, R, C, ga, gb);
-            }
-            ++inflight;
-        }
-        s = s + 1 == kStages ? 0 : s + 1;
-    }
-    ra.fold(acc, q.id);
-    __syncwarp();
+__device__ __forceinline__ std::uint32_t slab_lb(const SlabSmem& S, double x, double org, double inv_w) {
+    const std::uint32_t b = slab_bucket(x, org, inv_w);
+    std::uint32_t       k = S.bstart[b];
+    const std::uint32_t e = S.bstart[b + 1];
+    while (k < e && S.lam[k] < x) ++k;
+    return k;
 }
 
 template <bool DEG>
-__device__ __forceinline__ void tile_dispatch(int lgR, const EdgeArgs& A, const Req& q, std::uint64_t c0,
-                                              std::uint64_t c1, std::uint64_t ga, std::uint64_t gb, Acc& acc,
-                                              int lane, WarpSmem* ws, std::uint32_t& phase) {
-    __syncwarp();
-    RowSm& me = ws->rows[lane];
-    me.cs = q.cs, me.sn = q.sn, me.coth = q.coth, me.rci = q.rci, me.id = q.id, me.r0 = c0, me.r1 = c1;
-    __syncwarp();
-    switch (lgR) {
-    case 0: tile_run<DEG, 1>(A, ga, gb, acc, lane, ws, phase); break;
-    case 1: tile_run<DEG, 2>(A, ga, gb, acc, lane, ws, phase); break;
-    case 2: tile_run<DEG, 4>(A, ga, gb, acc, lane, ws, phase); break;
-    case 3: tile_run<DEG, 8>(A, ga, gb, acc, lane, ws, phase); break;
-    case 4: tile_run<DEG, 16>(A, ga, gb, acc, lane, ws, phase); break;
-    default: tile_run<DEG, 32>(A, ga, gb, acc, lane, ws, phase); break;
+__global__ void __launch_bounds__(kSlabThreads, 3) slab_kernel(EdgeArgs A) {
+    extern __shared__ __align__(16) unsigned char slab_raw[];
+    SlabSmem&                S    = *reinterpret_cast<SlabSmem*>(slab_raw);
+    const int                lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned long long sl   = A.slab_tab[blockIdx.x]; // (j << 32) | slab index in j (angle-interleaved order)
+    const int                j    = int(sl >> 32);
+    const AnnulusDev&        Aj   = A.ann[j];
+    const std::uint64_t      N0   = Aj.off + (sl & 0xffffffffull) * kSlab;
+    const std::uint32_t      m    = std::uint32_t(Aj.halo - N0 < std::uint64_t(kSlab) ? Aj.halo - N0 : kSlab);
+    for (std::uint32_t i = threadIdx.x; i < m; i += kSlabThreads) {
+        S.lam[i] = A.s_lam[N0 + i];
+        S.r1[i]  = A.s_rec1[N0 + i];
+        S.r2[i]  = A.s_rec2[N0 + i];
+        S.id[i]  = A.s_id[N0 + i];
     }
-}
-
-// Flattened pairs: the warp's (request, candidate) pairs numbered 0..T-1 in
-// lane order and processed 32 per round, one pair per lane — no divergence,
-// independent loads.  The owner of pair t is the last lane whose exclusive
-// prefix is <= t (5-step shuffle search).  For sparse and medium warps.
-template <bool DEG>
-__device__ __forceinline__ void flat_run(const EdgeArgs& A, const Req& q, std::uint64_t c0, std::uint32_t len,
-                                         std::uint32_t excl, std::uint32_t total, Acc& acc, int lane,
-                                         WarpSmem* ws) {
-    __syncwarp();
-    RowSm& me = ws->rows[lane];
-    me.cs = q.cs, me.sn = q.sn, me.coth = q.coth, me.rci = q.rci, me.id = q.id, me.r0 = c0 - excl;
-    __syncwarp();
-    constexpr int kU = 4; // rounds per iteration: 3*kU independent loads in flight per lane
-    for (std::uint32_t B = 0; B < total; B += 32 * kU) {
-        std::uint64_t k[kU];
-        int           own[kU];
-        bool          ok[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const std::uint32_t t = B + 32u * u + std::uint32_t(lane);
-            int                 o = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const std::uint32_t v = __shfl_sync(kFull, excl, o + step);
-                if (v <= t) o += step;
+    __syncthreads();
+    const double lam_first = S.lam[0], lam_last = S.lam[m - 1];
+    const double inv_w     = lam_last > lam_first ? double(kSlab - 1) / (lam_last - lam_first) : 0.0;
+    for (std::uint32_t i = threadIdx.x; i < m; i += kSlabThreads) { // bucket starts (cell_fill pattern)
+        const std::uint32_t b  = slab_bucket(S.lam[i], lam_first, inv_w);
+        const std::int32_t  bp = i ? std::int32_t(slab_bucket(S.lam[i - 1], lam_first, inv_w)) : -1;
+        for (std::int32_t c = bp + 1; c <= std::int32_t(b); ++c) S.bstart[c] = std::uint16_t(i);
+        if (i == m - 1)
+            for (std::uint32_t c = b + 1; c <= kSlab; ++c) S.bstart[c] = std::uint16_t(m);
+    }
+    __syncthreads();
+    const unsigned long long srcs = (A.ablate & 1) ? 0ull : A.src_mask[j]; // ablate: timing experiments only
+    Acc                      acc;
+    for (int a = A.first_streaming; a <= j; ++a) {
+        if (!((srcs >> a) & 1ull)) continue;
+        const AnnulusDev& Aa = A.ann[a];
+        const double      hb = A.hbound[a * A.count + j];
+        const bool        own = a == j;
+        // requests with lambda in [first - hb, last + hb]: a superset from a's cell table
+        std::uint64_t R0 = A.lcellstart[Aa.cell_off + cellf(Aa, lam_first - hb)];
+        std::uint64_t R1 = A.lcellstart[Aa.cell_off + cellf(Aa, lam_last + hb) + 1];
+        if (own && R1 > Aa.wrap) R1 = Aa.wrap; // own annulus: unwrapped requests only
+        const std::uint32_t wl = own ? std::uint32_t(Aa.wrap > N0 ? (Aa.wrap - N0 < m ? Aa.wrap - N0 : m) : 0) : m;
+        for (std::uint64_t g = R0 + std::uint64_t(warp) * 32; g < R1; g += kSlabThreads) {
+            const std::uint64_t p     = g + std::uint64_t(lane);
+            const bool          valid = p < R1;
+            const std::uint64_t pc    = valid ? p : g;
+            const double2       r2 = A.s_rec2[pc];
+            double              lo, hi;
+            if (own) {
+                const double b = A.s_beta[pc], hw = A.s_hw[pc];
+                lo = b, hi = fadd(b, fmul(2.0, hw));
+            } else {
+                const double lam = A.s_lam[pc];
+                const double h   = half_width_in(Aj, r2.x, r2.y);
+                lo = fsub(lam, h), hi = fadd(lam, h);
             }
-            own[u] = o;
-            ok[u]  = t < total;
-            k[u]   = ok[u] ? ws->rows[o].r0 + t : 0; // = c0_o + (t - excl_o)
-        }
-        double2            n1[kU], n2[kU];
-        unsigned long long nid[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            n1[u]  = A.s_rec1[k[u]];
-            n2[u]  = A.s_rec2[k[u]];
-            nid[u] = A.s_id[k[u]];
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const RowSm& r = ws->rows[own[u]];
-            Req          rq;
-            rq.cs = r.cs, rq.sn = r.sn, rq.coth = r.coth, rq.rci = r.rci, rq.id = r.id;
-            predicate<DEG>(A, rq, ok[u], n1[u], n2[u], nid[u], acc);
-        }
-    }
-    __syncwarp();
-}
-
-constexpr std::uint64_t kTilePiece = 4096;   // node range of one deferred tile task
-constexpr std::uint64_t kDeferCost = 150000; // defer a warp's big groups above this estimated cost
-
-constexpr std::uint32_t kFlatMax = 1u << 16; // flattened path only below this many pairs per warp
-
-// One warp = 32 requests (one per lane) with one simple index range each.
-// Picks, from the ranges, the cheapest of: the flattened pair list (sparse and
-// medium warps) or an R x C tile for R in {1..32} (cost model in issue
-// cycles: ~20 per 32 pair slots, ~10 per staged batch, ~40 per group; ~40
-// per flattened round).  Groups of very expensive warps are cut into tile
-// tasks (balanced later).
-template <bool DEG>
-__device__ __forceinline__ void process_range(const EdgeArgs& A, const Req& q, std::uint64_t c0, std::uint64_t c1,
-                                              int kind, int job, int j, std::uint64_t p0, int pass, Acc& acc,
-                                              int lane, WarpSmem* ws, std::uint32_t& phase) {
-    const std::uint64_t len  = c1 > c0 ? c1 - c0 : 0;
-    const std::uint32_t lenS = len < (1u << 26) ? std::uint32_t(len) : (1u << 26); // saturated: sums fit 32 bits
-    const std::uint32_t tot  = __reduce_add_sync(kFull, lenS);
-    if (tot == 0) return;
-    const std::uint64_t total = tot;
-    std::uint64_t       gmin = len ? c0 : ~0ull, gmax = len ? c1 : 0ull;
-    std::uint32_t       best = tot < kFlatMax ? (tot + 31) / 32 * 40 + 60 : 0xffffffffu;
-    int                 lgR  = -1;
-    std::uint64_t       ga = 0, gb = 0; // this lane's group union for the chosen R (valid in group leaders)
-#pragma unroll
-    for (int k = 0; k <= 5; ++k) {
-        if (k > 0) {
-            const std::uint64_t a = __shfl_xor_sync(kFull, gmin, 1 << (k - 1));
-            const std::uint64_t b = __shfl_xor_sync(kFull, gmax, 1 << (k - 1));
-            gmin                  = a < gmin ? a : gmin;
-            gmax                  = b > gmax ? b : gmax;
-        }
-        const bool          leader = (lane & ((1 << k) - 1)) == 0;
-        const std::uint64_t U      = gmax > gmin ? gmax - gmin : 0;
-        const std::uint64_t U1     = U < (1ull << 20) ? U : (1ull << 20); // saturate (cost only ranks options)
-        const std::uint32_t mine   = leader && U ? std::uint32_t((U1 << k) * 20 / 32 + ((U1 + kBatch - 1) / kBatch) * 10 + 40) : 0;
-        const std::uint32_t cost   = __reduce_add_sync(kFull, mine);
-        if (cost < best) best = cost, lgR = k, ga = gmin, gb = gmax;
-    }
-    if (A.dbg && lane == 0) {
-        atomicAdd(&A.dbg[22], 1ull), atomicAdd(&A.dbg[23], total);
-        if (lgR < 0) atomicAdd(&A.dbg[18], 1ull), atomicAdd(&A.dbg[19], (total + 31) / 32 * 32), atomicAdd(&A.dbg[20], total);
-    }
-    if (lgR < 0) {
-        std::uint32_t incl = std::uint32_t(len);
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const std::uint32_t t = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += t;
-        }
-        flat_run<DEG>(A, q, c0, std::uint32_t(len), incl - std::uint32_t(len), tot, acc, lane, ws);
-        return;
-    }
-    const int  R      = 1 << lgR;
-    const bool leader = (lane & (R - 1)) == 0;
-    if (!leader) ga = gb = 0;
-    if (A.dbg && leader && gb > ga) {
-        atomicAdd(&A.dbg[lgR], 1ull);
-        atomicAdd(&A.dbg[6 + lgR], static_cast<unsigned long long>(gb - ga));
-        atomicAdd(&A.dbg[12 + lgR], static_cast<unsigned long long>((gb - ga) << lgR));
-    }
-    if (best > kDeferCost && A.task_cap) { // cut big groups into balanced tile tasks
-        const std::uint64_t a0   = ga & ~1ull;
-        const std::uint64_t npc  = leader && gb - ga > kTilePiece ? (gb - a0 + kTilePiece - 1) / kTilePiece : 0;
-        std::uint64_t       incl = npc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const std::uint64_t t = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += t;
-        }
-        const std::uint64_t total = __shfl_sync(kFull, incl, 31);
-        if (total) {
-            unsigned long long t0 = 0;
-            if (lane == 0) t0 = atomicAdd(A.task_ctr, static_cast<unsigned long long>(total));
-            t0 = __shfl_sync(kFull, t0, 0);
-            if (t0 + total <= A.task_cap) {
-                if (lane == 0) {
-                    atomicMax(A.task_ctr + 1, static_cast<unsigned long long>(t0 + total)); // valid prefix
-                    if (A.dbg) atomicAdd(&A.dbg[21], static_cast<unsigned long long>(total));
+            std::uint32_t l0 = 0, l1 = 0;
+            if (valid && hi > lo && hi > lam_first && lo <= lam_last) {
+                l0 = slab_lb(S, lo, lam_first, inv_w), l1 = slab_lb(S, hi, lam_first, inv_w);
+                if (own) {
+                    if (p + 1 > N0 && l0 < std::uint32_t(p + 1 - N0)) l0 = std::uint32_t(p + 1 - N0 < m ? p + 1 - N0 : m);
+                    if (l1 > wl) l1 = wl;
                 }
-                const std::uint64_t first = t0 + incl - npc;
-                for (std::uint64_t i = 0; i < npc; ++i) { // even piece starts (TMA id copies)
-                    TileTask& T = A.tasks[first + i];
-                    T.p0 = p0 + std::uint64_t(lane), T.u0 = i ? a0 + i * kTilePiece : ga;
-                    T.u1 = a0 + (i + 1) * kTilePiece < gb ? a0 + (i + 1) * kTilePiece : gb;
-                    T.job = job, T.kind = std::int16_t(kind), T.lgR = std::int16_t(lgR), T.w = pass, T.j = j;
+            }
+            // flattened pair list over the warp: pair t belongs to the lane whose prefix covers it
+            const std::uint32_t len  = l1 > l0 ? l1 - l0 : 0u;
+            std::uint32_t       incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const std::uint32_t x = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += x;
+            }
+            const std::uint32_t T = __shfl_sync(kFull, incl, 31);
+            if (T == 0 || (A.ablate & 2)) { acc.comps += len; continue; }
+            const std::uint32_t excl = incl - len;
+            acc.comps += len;
+            SlabWarp& W = S.w[warp];
+            __syncwarp();
+            {
+                const double2 r1 = A.s_rec1[pc];
+                SRow          q;
+                q.cs = r1.x, q.sn = r1.y, q.coth = r2.x, q.rci = fmul(A.cosh_R, r2.y), q.id = A.s_id[pc];
+                q.pad     = std::uint32_t(l0 - excl); // local node of pair t: pad + t (mod 2^32)
+                W.rows[lane] = q;
+            }
+            for (std::uint32_t B0 = 0; B0 < T; B0 += kListCap) {
+                const std::uint32_t B1 = T - B0 < std::uint32_t(kListCap) ? T : B0 + kListCap;
+                const std::uint32_t w0 = excl > B0 ? excl : B0, w1 = incl < B1 ? incl : B1;
+                for (std::uint32_t t = w0; t < w1; ++t) W.list[t - B0] = static_cast<unsigned char>(lane);
+                __syncwarp();
+                for (std::uint32_t t = B0 + std::uint32_t(lane); t < B1; t += 64) { // two pairs per lane in flight
+                    const std::uint32_t tb = t + 32;
+                    const bool          vb = tb < B1;
+                    const SRow&         qa = W.rows[W.list[t - B0]];
+                    const SRow&         qb = W.rows[W.list[(vb ? tb : t) - B0]];
+                    const std::uint32_t ka = std::uint32_t(qa.pad) + t, kb = std::uint32_t(qb.pad) + (vb ? tb : t);
+                    const bool ea = edge_test(qa.cs, qa.sn, qa.coth, qa.rci, S.r1[ka], S.r2[ka]);
+                    const bool eb = vb && edge_test(qb.cs, qb.sn, qb.coth, qb.rci, S.r1[kb], S.r2[kb]);
+                    count_edge<DEG>(A, ea, qa.id, S.id[ka], acc);
+                    count_edge<DEG>(A, eb, qb.id, S.id[kb], acc);
                 }
-                if (npc) gb = ga; // handed off
+                __syncwarp();
             }
         }
     }
-    tile_dispatch<DEG>(lgR, A, q, c0, c1, ga, gb, acc, lane, ws, phase);
+    flush(acc, A, 0, lane);
 }
 
-__device__ __forceinline__ WarpSmem* my_warp_smem() {
-    extern __shared__ __align__(128) unsigned char dyn_smem[];
-    return reinterpret_cast<WarpSmem*>(dyn_smem) + (threadIdx.x >> 5);
-}
-
-// Work item t -> (pair job, batch of 32 requests).  Items are ordered by
-// angular block first (block b holds batches [floor(b nb/M), floor((b+1) nb/M))
-// of every job), so the warps in flight all work on one narrow angular band.
-__device__ __forceinline__ void map_item(const EdgeArgs& A, std::uint64_t t, int& job, std::uint64_t& batch) {
-    int lo = 0, hi = A.nblk - 1; // last block with prefix <= t
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (A.blk_prefix[mid] <= t) lo = mid;
-        else hi = mid - 1;
-    }
-    const int            b     = lo;
-    const std::uint32_t  local = std::uint32_t(t - A.blk_prefix[b]);
-    const std::uint32_t* off   = A.blk_job_off + std::size_t(b) * A.n_stream_jobs;
-    int                  k0 = 0, k1 = A.n_stream_jobs - 1; // last job with off <= local
-    while (k0 < k1) {
-        const int mid = (k0 + k1 + 1) >> 1;
-        if (off[mid] <= local) k0 = mid;
-        else k1 = mid - 1;
-    }
-    job                    = k0;
-    const PairJob&      J  = A.stream_jobs[job];
-    const std::uint64_t nb = (J.req_end - J.req_off + 31) / 32;
-    batch                  = std::uint64_t(b) * nb / std::uint64_t(A.nblk) + (local - off[k0]);
-}
-
+// Pairs the slab join leaves out: halo requests (Foreign replica) x owned
+// nodes, owned requests x halo nodes, and own-annulus pairs with a wrapped
+// request or node (full (theta, id) dedup, sweep.hpp:517-526).  Only the
+// requests near the end of the owned block (lambda >= tail_lam(a)) and the
+// halo requests can have such pairs; thread = one of them, all its sparse targets.
 template <bool DEG>
-__global__ void __launch_bounds__(256, 2) stream_pairs_kernel(EdgeArgs A) {
-    const int           lane = threadIdx.x & 31;
-    const std::uint64_t t    = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (t >= A.stream_warps) return;
-    WarpSmem* ws = my_warp_smem();
-    warp_smem_init(ws, lane);
-    std::uint32_t phase = 0;
-    Acc           acc;
-    int           job;
-    std::uint64_t batch;
-    map_item(A, t, job, batch);
-    const PairJob       Jb = A.stream_jobs[job];
-    const std::uint64_t p0 = Jb.req_off + batch * 32;
-#pragma unroll 1
-    for (int j = Jb.a; j < A.count; ++j) { // every target annulus of these 32 requests
-        if (A.ann[j].end == A.ann[j].off) continue;
-        Lane L;
-        setup_stream(A, Jb, j, p0 + lane, L);
-        process_range<DEG>(A, L.q, L.s0, L.s1, 0, job, j, p0, 0, acc, lane, ws, phase);
-        if (j != Jb.a) {
-            process_range<DEG>(A, L.q, L.h0, L.h1, 0, job, j, p0, 1, acc, lane, ws, phase);
-        } else { // same-annulus pairs with wrapped or halo points: full dedup
-            general_range<DEG>(A, L.q, L.g0, L.g1, acc);
-            general_range<DEG>(A, L.q, L.h0, L.h1, acc);
-        }
-    }
-    flush(acc, &A.ctr[0], lane);
-}
-
-template <bool DEG>
-__global__ void __launch_bounds__(256, 2) glob_req_kernel(EdgeArgs A) {
-    const int           lane = threadIdx.x & 31;
-    const std::uint64_t gw   = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (gw >= A.glob_warps) return;
-    WarpSmem* ws = my_warp_smem();
-    warp_smem_init(ws, lane);
-    std::uint32_t phase = 0;
-    int           lo = 0, hi = A.n_glob_jobs - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (A.glob_jobs[mid].warp_begin <= gw) lo = mid;
-        else hi = mid - 1;
-    }
-    const int           job = lo;
-    const PairJob       Jb  = A.glob_jobs[job];
-    const std::uint64_t g0  = Jb.req_off + (gw - Jb.warp_begin) * 32;
+__global__ void __launch_bounds__(256) tail_kernel(EdgeArgs A) {
+    const std::uint64_t t  = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     Acc                 acc;
-#pragma unroll 1
-    for (int w = 0; w < 4; ++w) {
-        Lane L;
-        setup_global(A, Jb, g0 + lane, w, L);
-        process_range<DEG>(A, L.q, L.s0, L.s1, 1, job, Jb.j, g0, w, acc, lane, ws, phase);
-    }
-    flush(acc, &A.ctr[1], lane);
-}
-
-// Deferred tile pieces: the R requests of one group x kTilePiece nodes
-// (KIND 0 streaming requests with T.w = pass 0 owned / 1 halo block, KIND 1
-// global requests with T.w = window).
-template <bool DEG, int KIND>
-__global__ void __launch_bounds__(256, 2) tile_tasks_kernel(EdgeArgs A) {
-    const int           lane  = threadIdx.x & 31;
-    const std::uint64_t ntask = A.task_ctr[1]; // reservations that fit (later ones ran inline)
-    const std::uint64_t nw    = (std::uint64_t(gridDim.x) * blockDim.x) >> 5;
-    WarpSmem*           ws    = my_warp_smem();
-    warp_smem_init(ws, lane);
-    std::uint32_t phase = 0;
-    Acc           acc;
-    for (std::uint64_t t = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; t < ntask; t += nw) {
-        const TileTask T = A.tasks[t];
-        if (T.kind != KIND) continue;
-        // lanes 0..R-1 hold the group's requests; lane 0 leads the single group
-        const std::uint64_t p  = lane < (1 << T.lgR) ? T.p0 + std::uint64_t(lane) : ~0ull;
-        const std::uint64_t ga = lane == 0 ? T.u0 : 0, gb = lane == 0 ? T.u1 : 0;
-        Lane                L;
-        if (KIND == 0) {
-            setup_stream(A, A.stream_jobs[T.job], T.j, p, L);
-            if (T.w == 0) tile_dispatch<DEG>(T.lgR, A, L.q, L.s0, L.s1, ga, gb, acc, lane, ws, phase);
-            else tile_dispatch<DEG>(T.lgR, A, L.q, L.h0, L.h1, ga, gb, acc, lane, ws, phase);
-        } else {
-            setup_global(A, A.glob_jobs[T.job], p, T.w, L);
-            tile_dispatch<DEG>(T.lgR, A, L.q, L.s0, L.s1, ga, gb, acc, lane, ws, phase);
+    if (t < A.tail_prefix[A.count]) {
+        int a = A.first_streaming, ha = A.count - 1; // last annulus with tail_prefix <= t
+        while (a < ha) {
+            const int mid = (a + ha + 1) >> 1;
+            if (A.tail_prefix[mid] <= t) a = mid;
+            else ha = mid - 1;
+        }
+        const AnnulusDev&   Aa = A.ann[a];
+        const std::uint64_t n  = A.tail_prefix[a + 1] - A.tail_prefix[a];
+        const std::uint64_t p  = Aa.end - n + (t - A.tail_prefix[a]); // [halo - owned tail, end)
+        const bool          halo_req = p >= Aa.halo;
+        const double        lam = A.s_lam[p];
+        if (halo_req || lam >= A.tail_lam[a]) {
+            const double2 r1 = A.s_rec1[p], r2 = A.s_rec2[p];
+            SRow          q;
+            q.cs = r1.x, q.sn = r1.y, q.coth = r2.x, q.rci = fmul(A.cosh_R, r2.y), q.id = A.s_id[p], q.pad = 0;
+            const double             theta = A.s_theta[p];
+            const unsigned long long srcm  = ~A.dense_mask[a];
+            for (int j = a; j < A.count; ++j) {
+                const AnnulusDev& Aj = A.ann[j];
+                if (Aj.end == Aj.off || !((srcm >> j) & 1ull)) continue;
+                const bool own = j == a;
+                double     lo, hi;
+                if (own) {
+                    const double b = A.s_beta[p], hw = A.s_hw[p];
+                    lo = b, hi = fadd(b, fmul(2.0, hw));
+                } else {
+                    const double h = half_width_in(Aj, r2.x, r2.y);
+                    lo = fsub(lam, h), hi = fadd(lam, h);
+                }
+                if (!(hi > lo)) continue;
+                if (Aj.halo > Aj.off) {
+                    std::uint64_t g0 = 0, g1 = 0;
+                    if (halo_req) {
+                        owned_range(A, Aj, lo, hi, g0, g1);
+                    } else if (own) {
+                        if (p >= Aa.wrap) owned_range(A, Aj, lo, hi, g0, g1);
+                        else g0 = Aj.wrap, g1 = lower_bound_owned(A, Aj, hi); // wrapped nodes
+                    }
+                    if (g1 > g0) serial_range<DEG>(A, q, theta, own, g0, g1, acc);
+                }
+                if (!halo_req && Aj.end > Aj.halo && hi > A.s_lam[Aj.halo] && lo <= A.s_lam[Aj.end - 1]) {
+                    const std::uint64_t h0 = lower_bound_halo(A, Aj, lo), h1 = lower_bound_halo(A, Aj, hi);
+                    if (h1 > h0) serial_range<DEG>(A, q, theta, own, h0, h1, acc);
+                }
+            }
         }
     }
-    flush(acc, &A.ctr[KIND], lane);
+    flush(acc, A, 0, threadIdx.x & 31);
 }
 
-// Sort keys of the global points: theta quantised to 32 bits (any order is
-// exact; this one makes neighbouring requests' windows overlap).
-__global__ void glob_keys_kernel(EdgeArgs A, std::uint32_t* keys, std::uint32_t* vals) {
-    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= A.n_glob) return;
-    const double th = A.rec0[A.n_ext + i].y; // [0, 2pi)
-    const double q  = th * (4294967296.0 / kTwoPiD);
-    keys[i]         = q >= 4294967295.0 ? 0xffffffffu : std::uint32_t(q);
-    vals[i]         = std::uint32_t(i);
+// --------------------------------------------------------- dense engine ---
+// Requests with wide windows: every global point and the streaming requests
+// of the (annulus, target) pairs whose windows hold >= ~32 nodes on average
+// (host-chosen, A.dense_mask).  Unified request u: u < n_glob is global point
+// u; otherwise annulus a's sorted request p = ann[a].off + (u - req_off[a]).
+
+__device__ __forceinline__ int req_annulus(const EdgeArgs& A, std::uint64_t u) {
+    int lo = A.first_streaming, hi = A.count - 1; // last annulus with req_off <= u
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (A.req_off[mid] <= u) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Sort keys: (source, radial class, theta or lambda quantised to 32 bits).
+// Source 0 = global points, a - first_streaming + 1 = streaming annulus a;
+// the class is the binary exponent of 1/sinh r halved, so the half-widths of
+// one segment differ by at most ~2x and a segment's angle-sorted run is a
+// tight candidate list for the node tiles (any order is exact: the rows carry
+// exact index ranges).
+__global__ void req_keys_kernel(EdgeArgs A, unsigned long long* keys, std::uint32_t* vals) {
+    const std::uint64_t u = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (u >= A.n_req) return;
+    double   th, inv;
+    unsigned src = 0;
+    if (u < A.n_glob) {
+        th = A.rec0[A.n_ext + u].y, inv = A.rec2[A.n_ext + u].y;
+    } else {
+        const int           a = req_annulus(A, u);
+        const std::uint64_t p = A.ann[a].off + (u - A.req_off[a]);
+        th = A.s_lam[p], inv = A.s_rec2[p].y;
+        while (th >= kTwoPiD) th -= kTwoPiD;
+        src = unsigned(a - A.first_streaming + 1);
+    }
+    const unsigned      cls = unsigned(static_cast<unsigned long long>(__double_as_longlong(inv)) >> 53) & 0x3ffu;
+    const double        q   = th * (4294967296.0 / kTwoPiD);
+    const std::uint32_t tq  = q >= 4294967295.0 ? 0xffffffffu : std::uint32_t(q);
+    keys[u]                 = (static_cast<unsigned long long>(src) << 42) | (static_cast<unsigned long long>(cls) << 32) | tq;
+    vals[u]                 = std::uint32_t(u);
+}
+
+// Start positions of the non-empty (source, class) segments in the sorted
+// keys, compacted: cseg[0..n_cls] and n_cls.  One block; thread c scans the
+// segment ids c, c + 1024, ...
+__global__ void __launch_bounds__(1024) req_segments_kernel(EdgeArgs A, const unsigned long long* keys) {
+    __shared__ int wsum[32];
+    __shared__ int base;
+    const int      lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    auto           lb   = [&](unsigned long long seg) {
+        std::uint64_t lo = 0, hi = A.n_req;
+        while (lo < hi) {
+            const std::uint64_t mid = (lo + hi) >> 1;
+            if ((keys[mid] >> 32) < seg) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    const unsigned nseg = unsigned(A.count - A.first_streaming + 1) << 10;
+    for (unsigned c0 = 0; c0 < nseg; c0 += 1024) {
+        const unsigned      c  = c0 + threadIdx.x;
+        const std::uint64_t s0 = c < nseg ? lb(c) : 0, s1 = c < nseg ? lb(c + 1) : 0;
+        const bool          ne = s1 > s0;
+        const unsigned      m  = __ballot_sync(kFull, ne);
+        if (lane == 0) wsum[w] = __popc(m);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int k = 0; k < 32; ++k) {
+            before += k < w ? wsum[k] : 0;
+            total += wsum[k];
+        }
+        const int idx = base + before + __popc(m & ((1u << lane) - 1));
+        if (ne && idx < kMaxCls) A.cseg[idx] = std::uint32_t(s0);
+        __syncthreads();
+        if (threadIdx.x == 0) base += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const int n = base < kMaxCls ? base : kMaxCls; // overflow is checked on the host via n_cls
+        A.cseg[n]   = std::uint32_t(A.n_req);
+        *A.n_cls    = base;
+    }
+}
+
+// Row (sorted request s, target annulus j): the exact index ranges ("pieces")
+// of j's owned block the request tests there.  Global requests: the
+// split_wraparound pieces of [theta - h, theta + h) (sweep.hpp:41-58) and,
+// when this shard owns engine P-1, their chunk-0 parts lifted by 2pi
+// (sweep.hpp:404-432).  Streaming requests (dense targets only): [s0, s1) of
+// the window (own window: (p, lower_bound(hi)) in index order); the rare
+// pairs that need the full (theta, id) dedup or live in the halo block run
+// right here, thread-serially.  Also writes the sorted request records and
+// the per-(segment, target) max half-width.
+template <bool DEG>
+__global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
+    const std::uint64_t nR  = A.n_req;
+    const int           nst = A.count - A.first_streaming;
+    const std::uint64_t idx = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool          ok  = idx < nR * std::uint64_t(nst);
+    Acc                 acc;
+    int                 hkey  = -1;
+    unsigned long long  hbits = 0;
+    if (ok) {
+        const int           jt = int(idx / nR);
+        const std::uint64_t s  = idx - std::uint64_t(jt) * nR;
+        const int           j  = A.first_streaming + jt;
+        const std::uint32_t u  = A.gperm[s];
+        const AnnulusDev&   Aj = A.ann[j];
+        std::uint32_t       pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        double              h     = -1.0; // half-width that bounds the pieces around the key angle
+        if (u < A.n_glob) {
+            const std::uint64_t g  = A.n_ext + u;
+            const double2       r0 = A.rec0[g], r1 = A.rec1[g], r2 = A.rec2[g];
+            const double        th = r0.y;
+            if (jt == 0) {
+                A.g_rec[2 * s]     = r1;
+                A.g_rec[2 * s + 1] = make_double2(r2.x, fmul(A.cosh_R, r2.y));
+                A.g_theta[s]       = th;
+                A.g_id[s]          = u;
+            }
+            if (Aj.halo > Aj.off) {
+                h              = half_width_in(Aj, r2.x, r2.y); // generator.hpp:67
+                const double a = fsub(th, h), b = fadd(th, h);
+                double       pa[2], pb[2];
+                int          np = 1;
+                if (fsub(b, a) >= kTwoPiD) {
+                    pa[0] = 0.0, pb[0] = kTwoPiD;
+                } else if (a < 0.0) {
+                    pa[0] = fadd(a, kTwoPiD), pb[0] = kTwoPiD, pa[1] = 0.0, pb[1] = b, np = 2;
+                } else if (b > kTwoPiD) {
+                    pa[0] = a, pb[0] = kTwoPiD, pa[1] = 0.0, pb[1] = fsub(b, kTwoPiD), np = 2;
+                } else {
+                    pa[0] = a, pb[0] = b;
+                }
+                int nw = 0;
+                for (int k = 0; k < np; ++k) {
+                    double lo[2] = {pa[k], 0.0}, hi[2] = {pb[k], 0.0};
+                    int    nl    = 1;
+                    if (A.lift_part) {
+                        const double l2 = pa[k] < 0.0 ? 0.0 : pa[k];                      // max(begin, w0 = 0)
+                        const double h2 = A.chunk0_upper < pb[k] ? A.chunk0_upper : pb[k]; // min(end, w1)
+                        if (l2 < h2) lo[1] = fadd(l2, kTwoPiD), hi[1] = fadd(h2, kTwoPiD), nl = 2;
+                    }
+                    for (int v = 0; v < nl; ++v) {
+                        if (hi[v] > lo[v]) {
+                            std::uint64_t s0, s1;
+                            owned_range(A, Aj, lo[v], hi[v], s0, s1);
+                            if (s1 > s0) {
+                                pc[2 * nw] = std::uint32_t(s0), pc[2 * nw + 1] = std::uint32_t(s1);
+                                acc.comps += s1 - s0;
+                                ++nw;
+                            }
+                        }
+                    }
+                }
+            }
+        } else {
+            const int           a  = req_annulus(A, u);
+            const AnnulusDev&   Aa = A.ann[a];
+            const std::uint64_t p  = Aa.off + (u - A.req_off[a]);
+            const double2       r1 = A.s_rec1[p], r2 = A.s_rec2[p];
+            SRow                q;
+            q.cs = r1.x, q.sn = r1.y, q.coth = r2.x, q.rci = fmul(A.cosh_R, r2.y), q.id = A.s_id[p], q.pad = 0;
+            if (jt == 0) {
+                double th = A.s_lam[p];
+                while (th >= kTwoPiD) th -= kTwoPiD;
+                A.g_rec[2 * s]     = r1;
+                A.g_rec[2 * s + 1] = make_double2(q.coth, q.rci);
+                A.g_theta[s]       = th;
+                A.g_id[s]          = std::uint32_t(q.id);
+            }
+            if (j >= a && ((A.dense_mask[a] >> j) & 1ull)) {
+                const bool halo_req  = p >= Aa.halo;
+                const bool same_simp = !halo_req && p < Aa.wrap;
+                double     lo, hi;
+                if (j == a) {
+                    const double b = A.s_beta[p], hw = A.s_hw[p];
+                    lo = b, hi = fadd(b, fmul(2.0, hw)), h = hw;
+                } else {
+                    const double lam = A.s_lam[p];
+                    h                = half_width_in(Aj, r2.x, r2.y);
+                    lo = fsub(lam, h), hi = fadd(lam, h);
+                }
+                if (hi > lo) {
+                    std::uint64_t g0 = 0, g1 = 0;
+                    if (Aj.halo > Aj.off) {
+                        std::uint64_t s0, s1;
+                        if (j == a && same_simp) {
+                            const std::uint64_t w = Aj.wrap, ub = lower_bound_owned(A, Aj, hi);
+                            s0 = p + 1, s1 = ub < w ? ub : w;
+                            g0 = w, g1 = ub;
+                        } else {
+                            owned_range(A, Aj, lo, hi, s0, s1);
+                            if (j == a) g0 = s0, g1 = s1, s1 = s0;
+                        }
+                        if (s1 > s0) {
+                            pc[0] = std::uint32_t(s0), pc[1] = std::uint32_t(s1);
+                            acc.comps += s1 - s0;
+                        }
+                    }
+                    const double theta = A.s_theta[p];
+                    if (g1 > g0) serial_range<DEG>(A, q, theta, true, g0, g1, acc);
+                    if (!halo_req && Aj.end > Aj.halo && hi > A.s_lam[Aj.halo] && lo <= A.s_lam[Aj.end - 1]) {
+                        const std::uint64_t h0 = lower_bound_halo(A, Aj, lo), h1 = lower_bound_halo(A, Aj, hi);
+                        if (h1 > h0) serial_range<DEG>(A, q, theta, j == a, h0, h1, acc);
+                    }
+                }
+            }
+        }
+        if (h >= 0.0 && pc[1] > pc[0]) {
+            int c0 = 0, c1 = (*A.n_cls < kMaxCls ? *A.n_cls : kMaxCls) - 1; // segment of s
+            while (c0 < c1) {
+                const int mid = (c0 + c1 + 1) >> 1;
+                if (A.cseg[mid] <= s) c0 = mid;
+                else c1 = mid - 1;
+            }
+            hkey  = c0 * A.count + j;
+            hbits = static_cast<unsigned long long>(__double_as_longlong(h));
+        }
+        uint4* row = reinterpret_cast<uint4*>(A.g_rows + (std::uint64_t(jt) * nR + s) * 8);
+        row[0]     = make_uint4(pc[0], pc[1], pc[2], pc[3]);
+        row[1]     = make_uint4(pc[4], pc[5], pc[6], pc[7]);
+    }
+    // per-(segment, target) max half-width: one atomic per group of lanes sharing the key
+    {   // the high word bounds the value from above (non-negative doubles order like their bits)
+        const unsigned grp = __match_any_sync(kFull, hkey);
+        const unsigned mx  = __reduce_max_sync(grp, unsigned(hbits >> 32));
+        if (hkey >= 0 && int(threadIdx.x & 31) == __ffs(grp) - 1 && hbits)
+            atomicMax(&A.hmax_bits[hkey], (static_cast<unsigned long long>(mx) << 32) | 0xffffffffull);
+    }
+    flush(acc, A, 1, threadIdx.x & 31);
+}
+
+constexpr int kTN    = 128; // owned nodes per dense-engine tile (4 per lane, in registers)
+constexpr int kQ     = kTN / 32;
+constexpr int kStrip = 4;   // tiles per warp sharing one candidate search
+
+struct GEnt { // one (request, piece) intersecting the current tile, compacted
+    double        cs, sn, coth, rci;
+    std::uint32_t id, lohi; // piece clipped to the tile: local [lo, hi) packed lo | hi << 16
+};
+struct GWarp {
+    GEnt          e[128];   // up to 4 pieces per candidate, 32 candidates per chunk
+    std::uint32_t rng[128]; // candidate ranges (lo, hi) of sorted positions, two per segment
+};
+
+// angle of the sorted requests of one segment: first position in [lo, hi)
+// with angle >= x.
+__device__ __forceinline__ std::uint32_t gtheta_lb(const double* th, std::uint32_t lo, std::uint32_t hi, double x) {
+    while (lo < hi) {
+        const std::uint32_t mid = (lo + hi) >> 1;
+        if (th[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// One warp = a strip of kStrip consecutive 128-node tiles of annulus j's
+// owned block.  The candidate requests of the strip (per segment: angle
+// within hmax(segment, j) of the strip, circularly) are found once; per tile
+// the nodes sit in registers, each chunk of 32 candidates is clipped to the
+// tile and compacted into (request, piece) entries in shared memory, and the
+// warp sweeps the entries (32-node slices outside an entry are skipped).
+template <bool DEG>
+__global__ void __launch_bounds__(256, 2) glob_tiles_kernel(EdgeArgs A) {
+    __shared__ GWarp    smem[8];
+    const int           lane = threadIdx.x & 31;
+    const std::uint64_t w    = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= A.gt_prefix[A.count]) return;
+    GWarp* ws = &smem[threadIdx.x >> 5];
+    int    j  = A.first_streaming, hj = A.count - 1; // last annulus with gt_prefix <= w
+    while (j < hj) {
+        const int mid = (j + hj + 1) >> 1;
+        if (A.gt_prefix[mid] <= w) j = mid;
+        else hj = mid - 1;
+    }
+    const AnnulusDev&   Aj   = A.ann[j];
+    const std::uint32_t sb0  = std::uint32_t(Aj.off + (w - A.gt_prefix[j]) * (kTN * kStrip));
+    const std::uint32_t sb1  = std::uint32_t(sb0 + kTN * kStrip < Aj.halo ? sb0 + kTN * kStrip : Aj.halo);
+    const std::uint64_t gjb  = std::uint64_t(j - A.first_streaming) * A.n_req;
+    const int           ncls = *A.n_cls < kMaxCls ? *A.n_cls : kMaxCls;
+    const double        lam_lo = A.s_lam[sb0], lam_hi = A.s_lam[sb1 - 1];
+    Acc                 acc;
+    unsigned long long  rsum = 0; // sum of request ids over the warp's edges (uniform; lane 0 reports it)
+    for (int a0 = 0; a0 < ncls; a0 += 32) {
+        // candidate ranges of sorted positions: lane = segment a0 + lane
+        {
+            const int     a  = a0 + lane;
+            std::uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+            if (a < ncls) {
+                const std::uint32_t      sa = A.cseg[a], sb = A.cseg[a + 1];
+                const unsigned long long hb = A.hmax_bits[a * A.count + j];
+                if (sb > sa && hb) {
+                    const double hmax = __longlong_as_double(static_cast<long long>(hb));
+                    // margin: the angles are sorted by a 32-bit quantised key (2pi/2^32 = 1.5e-9)
+                    const double L = (lam_hi - lam_lo) + 2.0 * hmax + 2e-7;
+                    if (L >= kTwoPiD) {
+                        r0 = sa, r1 = sb;
+                    } else {
+                        double st = lam_lo - hmax - 1e-7;
+                        while (st < 0.0) st += kTwoPiD;
+                        while (st >= kTwoPiD) st -= kTwoPiD;
+                        const double en = st + L;
+                        r0              = gtheta_lb(A.g_theta, sa, sb, st);
+                        if (en <= kTwoPiD) {
+                            r1 = gtheta_lb(A.g_theta, sa, sb, en);
+                        } else {
+                            r1 = sb;
+                            r2 = sa, r3 = gtheta_lb(A.g_theta, sa, sb, en - kTwoPiD);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            ws->rng[4 * lane] = r0, ws->rng[4 * lane + 1] = r1, ws->rng[4 * lane + 2] = r2, ws->rng[4 * lane + 3] = r3;
+            __syncwarp();
+        }
+        const int nrng = 2 * (ncls - a0 < 32 ? ncls - a0 : 32);
+        for (std::uint32_t t0 = sb0; t0 < sb1; t0 += kTN) {
+            const std::uint32_t t1 = t0 + kTN < sb1 ? t0 + kTN : sb1;
+            double2             n1[kQ], n2[kQ];
+            std::uint32_t       ecnt[kQ];
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) {
+                const std::uint32_t k = t0 + std::uint32_t(lane + 32 * q);
+                const std::uint32_t kc = k < t1 ? k : t0;
+                n1[q] = A.s_rec1[kc], n2[q] = A.s_rec2[kc];
+                ecnt[q] = 0;
+            }
+            for (int r = 0; r < nrng; ++r) {
+                const std::uint32_t lo = ws->rng[2 * r], hi = ws->rng[2 * r + 1];
+                for (std::uint32_t c0 = lo; c0 < hi; c0 += 32) {
+                    // stage: lane = candidate c0 + lane; its pieces clipped to [t0, t1)
+                    std::uint32_t pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    const std::uint32_t s = c0 + std::uint32_t(lane);
+                    if (s < hi) {
+                        const uint4* row = reinterpret_cast<const uint4*>(A.g_rows + (gjb + s) * 8);
+                        const uint4  pa = row[0], pb = row[1];
+                        pc[0] = pa.x, pc[1] = pa.y, pc[2] = pa.z, pc[3] = pa.w;
+                        pc[4] = pb.x, pc[5] = pb.y, pc[6] = pb.z, pc[7] = pb.w;
+                    }
+                    std::uint32_t ne = 0, lh[4];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) { // pieces are disjoint and packed
+                        const std::uint32_t ps = pc[2 * v], pe = pc[2 * v + 1];
+                        lh[v] = 0;
+                        if (pe > ps && pe > t0 && ps < t1) {
+                            const std::uint32_t l = ps > t0 ? ps - t0 : 0u, h = (pe < t1 ? pe : t1) - t0;
+                            lh[v] = l | (h << 16);
+                            ++ne;
+                        }
+                    }
+                    std::uint32_t incl = ne;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const std::uint32_t x = __shfl_up_sync(kFull, incl, o);
+                        if (lane >= o) incl += x;
+                    }
+                    const std::uint32_t tot = __shfl_sync(kFull, incl, 31);
+                    if (tot == 0) continue;
+                    __syncwarp();
+                    if (ne) {
+                        const double2 a1 = A.g_rec[2 * s], a2 = A.g_rec[2 * s + 1];
+                        const std::uint32_t id = A.g_id[s];
+                        std::uint32_t pos = incl - ne;
+#pragma unroll
+                        for (int v = 0; v < 4; ++v)
+                            if (lh[v]) {
+                                GEnt& E = ws->e[pos++];
+                                E.cs = a1.x, E.sn = a1.y, E.coth = a2.x, E.rci = a2.y, E.id = id, E.lohi = lh[v];
+                            }
+                    }
+                    __syncwarp();
+                    if (A.dbg && lane == 0) atomicAdd(&A.dbg[8], 32ull), atomicAdd(&A.dbg[9], static_cast<unsigned long long>(tot));
+                    for (std::uint32_t c = 0; c < tot; ++c) {
+                        const GEnt&         E  = ws->e[c];
+                        const double        cs = E.cs, sn = E.sn, coth = E.coth, rci = E.rci;
+                        const std::uint32_t el = E.lohi & 0xffffu, eh = E.lohi >> 16;
+                        std::uint32_t       ce = 0; // this lane's edges with request E
+                        if (el == 0 && eh == kTN) { // the piece covers the whole tile
+#pragma unroll
+                            for (int q = 0; q < kQ; ++q) {
+                                const bool e = edge_test(cs, sn, coth, rci, n1[q], n2[q]);
+                                ecnt[q] += e, ce += e;
+                                if (DEG && e) {
+                                    atomicAdd(&A.degrees[E.id], 1u);
+                                    atomicAdd(&A.degrees[A.s_id[t0 + std::uint32_t(lane + 32 * q)]], 1u);
+                                }
+                            }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < kQ; ++q) {
+                                if (eh <= std::uint32_t(32 * q) || el >= std::uint32_t(32 * q + 32)) continue; // slice untouched
+                                const std::uint32_t kl = std::uint32_t(lane + 32 * q);
+                                const bool e = kl >= el && kl < eh && edge_test(cs, sn, coth, rci, n1[q], n2[q]);
+                                ecnt[q] += e, ce += e;
+                                if (DEG && e) {
+                                    atomicAdd(&A.degrees[E.id], 1u);
+                                    atomicAdd(&A.degrees[A.s_id[t0 + kl]], 1u);
+                                }
+                            }
+                        }
+                        rsum += static_cast<unsigned long long>(__reduce_add_sync(kFull, ce)) * E.id;
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) {
+                const std::uint32_t k = t0 + std::uint32_t(lane + 32 * q);
+                if (ecnt[q]) {
+                    acc.edges += ecnt[q];
+                    acc.fp += static_cast<unsigned long long>(ecnt[q]) * A.s_id[k];
+                }
+            }
+        }
+    }
+    if (lane == 0) acc.fp += rsum;
+    flush(acc, A, 1, lane);
 }
 
 // generator.hpp:84-102: all pairs i < k of the global points, request = i.
@@ -895,16 +951,41 @@ __global__ void __launch_bounds__(kGGTile) glob_pairs_kernel(EdgeArgs A, std::ui
     const std::uint64_t i = I * kGGTile + threadIdx.x;
     Acc                 acc;
     if (i < nG) {
-        Req           q{};
         const double2 r1 = A.rec1[A.n_ext + i], r2 = A.rec2[A.n_ext + i];
-        q.cs = r1.x, q.sn = r1.y, q.coth = r2.x, q.rci = fmul(A.cosh_R, r2.y), q.id = i;
+        const double  cs = r1.x, sn = r1.y, coth = r2.x, rci = fmul(A.cosh_R, r2.y);
         std::uint64_t k0 = J * kGGTile;
         if (k0 <= i) k0 = i + 1;
         const std::uint64_t k1 = (J + 1) * kGGTile < nG ? (J + 1) * kGGTile : nG;
+        acc.comps              = k1 > k0 ? k1 - k0 : 0;
         for (std::uint64_t k = k0; k < k1; ++k)
-            predicate<DEG>(A, q, true, s1[k - J * kGGTile], s2[k - J * kGGTile], k, acc);
+            count_edge<DEG>(A, edge_test(cs, sn, coth, rci, s1[k - J * kGGTile], s2[k - J * kGGTile]), i, k, acc);
     }
-    flush(acc, &A.ctr[2], threadIdx.x & 31);
+    flush(acc, A, 2, threadIdx.x & 31);
+}
+
+// Fold the counter slots of the three families into A.ctr.
+__global__ void __launch_bounds__(1024) reduce_counters_kernel(EdgeArgs A) {
+    const int          f = blockIdx.x;
+    unsigned long long e = 0, fp = 0, c = 0;
+    for (int i = threadIdx.x; i < kSlots; i += blockDim.x) {
+        const SlotCounter& s = A.slots[f * kSlots + i];
+        e += s.edges, fp += s.fp, c += s.comps;
+    }
+    __shared__ unsigned long long red[3][32];
+    const int                     lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        e += __shfl_down_sync(kFull, e, o);
+        fp += __shfl_down_sync(kFull, fp, o);
+        c += __shfl_down_sync(kFull, c, o);
+    }
+    if (lane == 0) red[0][w] = e, red[1][w] = fp, red[2][w] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Counters out{0, 0, 0};
+        for (int k = 0; k < int(blockDim.x >> 5); ++k) out.edges += red[0][k], out.fp += red[1][k], out.comps += red[2][k];
+        A.ctr[f] = out;
+    }
 }
 
 } // namespace
@@ -925,68 +1006,63 @@ void launch_cell_index(const EdgeArgs& a, std::uint64_t nblocks, cudaStream_t st
     }
 }
 
-void launch_sort_globals(EdgeArgs& a, const std::uint64_t* seg_off_dev, int nseg, void* scratch,
-                         std::size_t scratch_bytes, std::size_t* need, cudaStream_t st, std::uint64_t* launches) {
+void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, std::size_t* need, cudaStream_t st,
+                         std::uint64_t* launches) {
     // scratch: keys_in | keys_out | vals_in | perm(out) | cub temp
-    const std::size_t n   = a.n_glob;
-    const std::size_t al  = (n * 4 + 255) & ~std::size_t(255);
+    const std::size_t n   = a.n_req;
+    const std::size_t a8  = (n * 8 + 255) & ~std::size_t(255);
+    const std::size_t a4  = (n * 4 + 255) & ~std::size_t(255);
     std::size_t       tmp = 0;
-    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, static_cast<const std::uint32_t*>(nullptr),
-                                             static_cast<std::uint32_t*>(nullptr),
-                                             static_cast<const std::uint32_t*>(nullptr),
-                                             static_cast<std::uint32_t*>(nullptr), int(n), nseg, seg_off_dev,
-                                             seg_off_dev + 1, 0, 32, st);
-    *need = 4 * al + tmp + 256;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, static_cast<const unsigned long long*>(nullptr),
+                                    static_cast<unsigned long long*>(nullptr),
+                                    static_cast<const std::uint32_t*>(nullptr), static_cast<std::uint32_t*>(nullptr),
+                                    int(n), 0, 48, st);
+    *need = 2 * a8 + 2 * a4 + tmp + 256;
     if (!scratch || scratch_bytes < *need || n == 0) return;
-    char*          p    = static_cast<char*>(scratch);
-    std::uint32_t* kin  = reinterpret_cast<std::uint32_t*>(p);
-    std::uint32_t* kout = reinterpret_cast<std::uint32_t*>(p + al);
-    std::uint32_t* vin  = reinterpret_cast<std::uint32_t*>(p + 2 * al);
-    std::uint32_t* perm = reinterpret_cast<std::uint32_t*>(p + 3 * al);
-    glob_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kin, vin);
-    cub::DeviceSegmentedRadixSort::SortPairs(p + 4 * al, tmp, kin, kout, vin, perm, int(n), nseg, seg_off_dev,
-                                             seg_off_dev + 1, 0, 32, st);
+    char*               p    = static_cast<char*>(scratch);
+    unsigned long long* kin  = reinterpret_cast<unsigned long long*>(p);
+    unsigned long long* kout = reinterpret_cast<unsigned long long*>(p + a8);
+    std::uint32_t*      vin  = reinterpret_cast<std::uint32_t*>(p + 2 * a8);
+    std::uint32_t*      perm = reinterpret_cast<std::uint32_t*>(p + 2 * a8 + a4);
+    req_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kin, vin);
+    cub::DeviceRadixSort::SortPairs(p + 2 * a8 + 2 * a4, tmp, kin, kout, vin, perm, int(n), 0, 48, st);
+    req_segments_kernel<<<1, 1024, 0, st>>>(a, kout);
     a.gperm = perm;
-    *launches += 2;
+    *launches += 3;
 }
 
 void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches) {
-    const bool  deg   = a.degrees != nullptr;
-    static bool attrs = false;
-    if (!attrs) { // > 48 KiB of dynamic shared memory per block
-        cudaFuncSetAttribute(stream_pairs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
-        cudaFuncSetAttribute(stream_pairs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
-        cudaFuncSetAttribute(glob_req_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
-        cudaFuncSetAttribute(glob_req_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
-        cudaFuncSetAttribute(tile_tasks_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
-        cudaFuncSetAttribute(tile_tasks_kernel<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
-        cudaFuncSetAttribute(tile_tasks_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
-        cudaFuncSetAttribute(tile_tasks_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
-        attrs = true;
-    }
-    if (a.stream_warps) { // one warp per item, items in angular-block order
-        const unsigned blocks = unsigned((a.stream_warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    const bool deg = a.degrees != nullptr;
+    if (a.n_slabs) { // sparse pairs: slab join + tail
+        const int smem = int(sizeof(SlabSmem));
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(slab_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(slab_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            attr = true;
+        }
         if (a.ev_pairs0) cudaEventRecord(a.ev_pairs0, st);
-        if (deg) stream_pairs_kernel<true><<<blocks, 32 * kWarpsPerBlock, kTileSmem, st>>>(a);
-        else stream_pairs_kernel<false><<<blocks, 32 * kWarpsPerBlock, kTileSmem, st>>>(a);
+        if (deg) slab_kernel<true><<<unsigned(a.n_slabs), kSlabThreads, smem, st>>>(a);
+        else slab_kernel<false><<<unsigned(a.n_slabs), kSlabThreads, smem, st>>>(a);
         if (a.ev_pairs1) cudaEventRecord(a.ev_pairs1, st);
         ++*launches;
     }
-    if (a.glob_warps) {
-        const unsigned blocks = unsigned((a.glob_warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
-        if (deg) glob_req_kernel<true><<<blocks, 32 * kWarpsPerBlock, kTileSmem, st>>>(a);
-        else glob_req_kernel<false><<<blocks, 32 * kWarpsPerBlock, kTileSmem, st>>>(a);
+    if (a.n_tail) {
+        if (deg) tail_kernel<true><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
+        else tail_kernel<false><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
         ++*launches;
     }
-    if (a.stream_warps && a.task_cap) {
-        if (deg) tile_tasks_kernel<true, 0><<<148 * 2, 32 * kWarpsPerBlock, kTileSmem, st>>>(a);
-        else tile_tasks_kernel<false, 0><<<148 * 2, 32 * kWarpsPerBlock, kTileSmem, st>>>(a);
+    if (a.n_req && a.first_streaming < a.count) {
+        const std::uint64_t rows = a.n_req * std::uint64_t(a.count - a.first_streaming);
+        if (deg) req_rows_kernel<true><<<unsigned((rows + 255) / 256), 256, 0, st>>>(a);
+        else req_rows_kernel<false><<<unsigned((rows + 255) / 256), 256, 0, st>>>(a);
         ++*launches;
-    }
-    if (a.glob_warps && a.task_cap) {
-        if (deg) tile_tasks_kernel<true, 1><<<148 * 2, 32 * kWarpsPerBlock, kTileSmem, st>>>(a);
-        else tile_tasks_kernel<false, 1><<<148 * 2, 32 * kWarpsPerBlock, kTileSmem, st>>>(a);
-        ++*launches;
+        if (a.glob_tile_warps) {
+            const unsigned blocks = unsigned((a.glob_tile_warps + 7) / 8);
+            if (deg) glob_tiles_kernel<true><<<blocks, 256, 0, st>>>(a);
+            else glob_tiles_kernel<false><<<blocks, 256, 0, st>>>(a);
+            ++*launches;
+        }
     }
     if (a.gg_tile_end > a.gg_tile_begin) {
         const std::uint64_t nT     = (a.n_glob + kGGTile - 1) / kGGTile;
@@ -995,6 +1071,8 @@ void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches) {
         else glob_pairs_kernel<false><<<blocks, kGGTile, 0, st>>>(a, nT);
         ++*launches;
     }
+    reduce_counters_kernel<<<3, 1024, 0, st>>>(a);
+    ++*launches;
 }
 
 } // namespace rhgb

@@ -46,31 +46,44 @@ struct EdgeArgs {
     // lambda-sorted copies (per annulus: owned block, halo block)
     double*           s_beta = nullptr;
     double*           s_hw   = nullptr;
-    double2*          s_rec0 = nullptr;
+    double*           s_lam   = nullptr; // lambda (engine-frame centre)
+    double*           s_theta = nullptr; // raw theta (same-annulus dedup)
     double2*          s_rec1 = nullptr;
     double2*          s_rec2 = nullptr;
     unsigned long long* s_id = nullptr;     // [n_ext + 2] vertex ids
     const std::uint32_t* gperm = nullptr;  // global requests in (annulus, theta) order (null: id order)
+    std::uint32_t*    cseg = nullptr;      // [kMaxCls + 1] sorted-position starts of the non-empty segments
+    int*              n_cls = nullptr;     // number of non-empty (source, class) segments (device-written)
+    // dense engine: unified requests u (global points, then the streaming requests of annuli with
+    // dense targets), sorted by (source, radial class, angle) into positions s
+    std::uint64_t     n_req = 0;
+    const std::uint64_t* req_off = nullptr;      // [count] first unified index of streaming annulus a
+    const unsigned long long* dense_mask = nullptr; // [count] bit j: (a, j) runs on the dense engine
+    double2*          g_rec = nullptr;     // [2 n_req] sorted requests: (cos, sin), (coth, coshR/sinh)
+    double*           g_theta = nullptr;   // [n_req] key angle (theta, or lambda mod 2pi), sorted per segment
+    std::uint32_t*    g_id = nullptr;      // [n_req] vertex id
+    std::uint32_t*    g_rows = nullptr;    // [streaming annuli][n_req][8] window pieces (s0, s1) as owned indices
+    unsigned long long* hmax_bits = nullptr; // [kMaxCls * count] max half-width per (radial class, target) (bits)
+    const std::uint64_t* gt_prefix = nullptr; // [count + 1] dense-engine warps (128-node owned tiles) before annulus j
+    std::uint64_t     glob_tile_warps = 0;
     const std::uint32_t* ann_blk = nullptr; // [count + 1] prefix of 256-point blocks per streaming annulus
     unsigned long long* dmax_bits = nullptr; // per annulus, max half-width (bits)
     double            cosh_R = 1.0;
     double            chunk0_upper = 0.0; // chunk_upper_bound(0, P)
     int               lift_part = 0;      // shard owns engine P-1 (halo = lifted chunk 0)
-    const PairJob*    stream_jobs = nullptr;
-    int               n_stream_jobs = 0;
-    std::uint64_t     stream_warps = 0;      // work items (batches of 32 requests x target annulus)
-    const std::uint64_t* blk_prefix = nullptr; // [nblk + 1] items before angular block b
-    const std::uint32_t* blk_job_off = nullptr; // [nblk * n_stream_jobs] item offset of job k inside block b
-    int               nblk = 1;
+    // slab join (sparse pairs): slabs of 1024 owned nodes of every target annulus with sparse sources
+    const unsigned long long* slab_tab = nullptr; // [n_slabs] (j << 32) | slab index in j, angle-interleaved order
+    std::uint64_t     n_slabs = 0;
+    const unsigned long long* src_mask = nullptr; // [count] bit a: (a, j) is sparse (slab join)
+    const double*     hbound = nullptr;           // [count * count] bound on the half-width of a's requests in j
+    const std::uint64_t* tail_prefix = nullptr;   // [count + 1] tail requests (owned tail + halo block) before annulus a
+    const double*     tail_lam = nullptr;         // [count] owned requests with lambda >= tail_lam[a] are tail requests
+    std::uint64_t     n_tail = 0;
     cudaEvent_t       ev_pairs0 = nullptr, ev_pairs1 = nullptr; // optional: time the streaming pair kernel
-    const PairJob*    glob_jobs = nullptr;
-    int               n_glob_jobs = 0;
-    std::uint64_t     glob_warps = 0;
     std::uint64_t     gg_tile_begin = 0, gg_tile_end = 0; // this shard's global-unit tiles
-    TileTask*         tasks = nullptr;
-    std::uint64_t     task_cap = 0;
-    unsigned long long* task_ctr = nullptr;
-    Counters*         ctr = nullptr; // [0] streaming, [1] global requests, [2] global unit
+    Counters*         ctr = nullptr; // [0] streaming kernel, [1] dense engine, [2] global unit
+    SlotCounter*      slots = nullptr; // [3 * kSlots] partial counters (folded into ctr at the end)
+    int               ablate = 0;       // RHG_ABLATE bit flags: skip kernel phases (timing experiments; results invalid)
     unsigned long long* dbg = nullptr; // optional path statistics (RHG_DEBUG_STATS=1), kDbgSlots entries
     unsigned int*     degrees = nullptr;
 };
@@ -79,12 +92,14 @@ void launch_cell_index(const EdgeArgs& a, std::uint64_t nblocks, cudaStream_t st
 void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches);
 // Sorts the global points by (annulus, theta) into a.gperm (scratch layout
 // internal); with scratch == nullptr only reports the bytes needed in *need.
-void launch_sort_globals(EdgeArgs& a, const std::uint64_t* seg_off_dev, int nseg, void* scratch,
-                         std::size_t scratch_bytes, std::size_t* need, cudaStream_t st, std::uint64_t* launches);
+void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, std::size_t* need, cudaStream_t st,
+                         std::uint64_t* launches);
 
 constexpr int kGGTile = 128;
-// dbg layout: [0..5] groups per lgR, [6..11] sum U per lgR, [12..17] slots per lgR, [18] serial warps,
-// [19] serial slots (32*maxlen), [20] serial candidates, [21] tasks, [22] warps, [23] candidates total
+constexpr int kMaxCls = 1024; // (source, radial class) segments of the dense-engine requests
+// dbg layout (RHG_DEBUG_STATS=1): [0] stream (warp, target) steps, [1] staged unions, [2] per-lane
+// searches, [3] long rows, [4] flattened pairs, [5] serial pairs, [8] dense candidates loaded,
+// [9] dense (request, tile) pieces evaluated, [10] dense warps
 constexpr int kDbgSlots = 32;
 
 } // namespace rhgb

@@ -1,11 +1,12 @@
 """Per-source-line stall samples / executed instructions from an ncu source
-page exported with --print-source cuda,sass --csv."""
+page exported with --print-source cuda,sass --csv.  Usage: src_hot.py CSV [N] [sort=s|i]"""
 import csv
 import sys
 from collections import defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+by = sys.argv[3] if len(sys.argv) > 3 else "s"
 cur, hdr, agg, src = None, None, defaultdict(lambda: [0.0, 0.0]), {}
 for r in rows:
     if not r:
@@ -30,5 +31,6 @@ for r in rows:
 tn = sum(v[0] for v in agg.values()) or 1
 te = sum(v[1] for v in agg.values()) or 1
 print(f"samples {tn:.0f} inst {te:.3e}")
-for k, (n, e) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:N]:
-    print(f"{k[0]:12s}:{k[1]:<5d} s {100*n/tn:5.1f}% i {100*e/te:5.1f}%  {src[k].strip()[:85]}")
+idx = 0 if by == "s" else 1
+for k, (n, e) in sorted(agg.items(), key=lambda kv: -kv[1][idx])[:N]:
+    print(f"{k[0]:12s}:{k[1]:<5d} s {100*n/tn:5.1f}% i {100*e/te:5.1f}%  {(src.get(k) or '').strip()[:85]}")
