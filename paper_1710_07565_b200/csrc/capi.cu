@@ -257,7 +257,7 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
         }
     for (std::uint32_t j = 0; j < K; ++j) {
         const std::uint64_t own = pl.src_mask[j] ? pl.ann[j].halo - pl.ann[j].off : 0;
-        pl.slab_prefix[j + 1]   = pl.slab_prefix[j] + (own + 1023) / 1024;
+        pl.slab_prefix[j + 1]   = pl.slab_prefix[j] + (own + kSlabNodes - 1) / kSlabNodes;
     }
     pl.n_slabs = pl.slab_prefix[K];
     { // slabs in angular order across targets: requests are re-read from L2 by the next target's slab
@@ -458,13 +458,16 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     }
     e.ann_blk = t.ann_blk;
     launch_cell_index(e, pl.ann_blk[pl.L.count], ctx->stream, launches);
+    // dense chain on the side stream, concurrent with the sparse pairs
+    CK(cudaEventRecord(ctx->fork, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
     if (pl.n_req && pl.L.first_streaming < pl.L.count) { // dense-engine requests in (source, class, angle) order
         std::size_t need = 0;
-        launch_sort_globals(e, nullptr, 0, &need, ctx->stream, launches);
+        launch_sort_globals(e, nullptr, 0, &need, ctx->side, launches);
         ctx->gsort.ensure(need);
-        launch_sort_globals(e, ctx->gsort.p, ctx->gsort.cap, &need, ctx->stream, launches);
+        launch_sort_globals(e, ctx->gsort.p, ctx->gsort.cap, &need, ctx->side, launches);
     }
-    launch_edges(e, ctx->stream, launches);
+    launch_edges(e, ctx->stream, ctx->side, ctx->join, launches);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[2], ctx->stream));
     ctx->staging.ensure(4096);

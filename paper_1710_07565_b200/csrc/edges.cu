@@ -308,14 +308,13 @@ __device__ __forceinline__ void serial_range(const EdgeArgs& A, const SRow& q, d
 // Own annulus (j == a): requests and nodes below the wrap index only, nodes
 // after the request (index order == (theta, id) dedup order); everything
 // else - halo requests, halo nodes, wrapped points - runs in tail_kernel.
-constexpr int kSlab        = 1024;
+constexpr int kSlab        = kSlabNodes;
 constexpr int kSlabThreads = 256;
 
-constexpr int kListCap     = 1024; // flattened pairs per list batch (one byte each: the owning lane)
 
 struct SlabWarp {
-    SRow          rows[32];       // the warp's current requests (pad = local node of pair 0)
-    unsigned char list[kListCap]; // flattened pair t -> owning lane
+    SRow          rows[32]; // the warp's current requests (pad = local node of pair 0)
+    std::uint32_t incl[32]; // inclusive prefix of the lanes' pair counts
 };
 struct SlabSmem {
     double             lam[kSlab];
@@ -342,7 +341,7 @@ __device__ __forceinline__ std::uint32_t slab_lb(const SlabSmem& S, double x, do
 }
 
 template <bool DEG>
-__global__ void __launch_bounds__(kSlabThreads, 3) slab_kernel(EdgeArgs A) {
+__global__ void __launch_bounds__(kSlabThreads, 4) slab_kernel(EdgeArgs A) {
     extern __shared__ __align__(16) unsigned char slab_raw[];
     SlabSmem&                S    = *reinterpret_cast<SlabSmem*>(slab_raw);
     const int                lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -368,21 +367,53 @@ __global__ void __launch_bounds__(kSlabThreads, 3) slab_kernel(EdgeArgs A) {
             for (std::uint32_t c = b + 1; c <= kSlab; ++c) S.bstart[c] = std::uint16_t(m);
     }
     __syncthreads();
-    const unsigned long long srcs = (A.ablate & 1) ? 0ull : A.src_mask[j]; // ablate: timing experiments only
-    Acc                      acc;
-    for (int a = A.first_streaming; a <= j; ++a) {
-        if (!((srcs >> a) & 1ull)) continue;
-        const AnnulusDev& Aa = A.ann[a];
-        const double      hb = A.hbound[a * A.count + j];
-        const bool        own = a == j;
-        // requests with lambda in [first - hb, last + hb]: a superset from a's cell table
-        std::uint64_t R0 = A.lcellstart[Aa.cell_off + cellf(Aa, lam_first - hb)];
-        std::uint64_t R1 = A.lcellstart[Aa.cell_off + cellf(Aa, lam_last + hb) + 1];
-        if (own && R1 > Aa.wrap) R1 = Aa.wrap; // own annulus: unwrapped requests only
-        const std::uint32_t wl = own ? std::uint32_t(Aa.wrap > N0 ? (Aa.wrap - N0 < m ? Aa.wrap - N0 : m) : 0) : m;
-        for (std::uint64_t g = R0 + std::uint64_t(warp) * 32; g < R1; g += kSlabThreads) {
+    // request runs of every sparse source annulus a <= j (lambda within
+    // hbound(a, j) of the slab: a superset from a's cell table), numbered as
+    // one CTA-wide list of 32-request groups shared by all warps
+    __shared__ std::uint64_t run_r0[64];
+    __shared__ std::uint32_t run_g[65]; // group prefix over the sources
+    if (warp == 0) {
+        const unsigned long long srcs = (A.ablate & 1) ? 0ull : A.src_mask[j]; // ablate: timing experiments only
+        for (int a0 = 0; a0 < 64; a0 += 32) {
+            const int     a  = a0 + lane;
+            std::uint64_t r0 = 0, r1 = 0;
+            if (a <= j && ((srcs >> a) & 1ull)) {
+                const AnnulusDev& Aa = A.ann[a];
+                const double      hb = A.hbound[a * A.count + j];
+                r0 = A.lcellstart[Aa.cell_off + cellf(Aa, lam_first - hb)];
+                r1 = A.lcellstart[Aa.cell_off + cellf(Aa, lam_last + hb) + 1];
+                if (a == j && r1 > Aa.wrap) r1 = Aa.wrap; // own annulus: unwrapped requests only
+                if (r1 < r0) r1 = r0;
+            }
+            const std::uint32_t ng   = std::uint32_t((r1 - r0 + 31) / 32);
+            std::uint32_t       incl = ng;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const std::uint32_t x = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += x;
+            }
+            const std::uint32_t base = a0 ? run_g[a0] : 0u;
+            run_r0[a]                = r0;
+            run_g[a + 1]             = base + incl;
+            if (a == 0) run_g[0] = 0;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    const std::uint32_t ngroups = run_g[64];
+    Acc                 acc;
+    int a = 0; // source of group gi: last a with run_g[a] <= gi (gi only grows)
+    for (std::uint32_t gi = warp; gi < ngroups; gi += kSlabThreads / 32) {
+        while (run_g[a + 1] <= gi) ++a;
+        {
+            const AnnulusDev&   Aa = A.ann[a];
+            const bool          own = a == j;
+            const std::uint64_t g   = run_r0[a] + std::uint64_t(gi - run_g[a]) * 32;
+            const std::uint64_t R1  = run_r0[a] + std::uint64_t(run_g[a + 1] - run_g[a]) * 32; // group end bound
+            const std::uint64_t Rend = own ? (Aa.wrap < Aa.halo ? Aa.wrap : Aa.halo) : Aa.halo;
+            const std::uint32_t wl = own ? std::uint32_t(Aa.wrap > N0 ? (Aa.wrap - N0 < m ? Aa.wrap - N0 : m) : 0) : m;
             const std::uint64_t p     = g + std::uint64_t(lane);
-            const bool          valid = p < R1;
+            const bool          valid = p < R1 && p < Rend;
             const std::uint64_t pc    = valid ? p : g;
             const double2       r2 = A.s_rec2[pc];
             double              lo, hi;
@@ -420,27 +451,37 @@ __global__ void __launch_bounds__(kSlabThreads, 3) slab_kernel(EdgeArgs A) {
                 const double2 r1 = A.s_rec1[pc];
                 SRow          q;
                 q.cs = r1.x, q.sn = r1.y, q.coth = r2.x, q.rci = fmul(A.cosh_R, r2.y), q.id = A.s_id[pc];
-                q.pad     = std::uint32_t(l0 - excl); // local node of pair t: pad + t (mod 2^32)
+                q.pad        = std::uint32_t(l0 - excl); // local node of pair t: pad + t (mod 2^32)
                 W.rows[lane] = q;
+                W.incl[lane] = incl;
             }
-            for (std::uint32_t B0 = 0; B0 < T; B0 += kListCap) {
-                const std::uint32_t B1 = T - B0 < std::uint32_t(kListCap) ? T : B0 + kListCap;
-                const std::uint32_t w0 = excl > B0 ? excl : B0, w1 = incl < B1 ? incl : B1;
-                for (std::uint32_t t = w0; t < w1; ++t) W.list[t - B0] = static_cast<unsigned char>(lane);
-                __syncwarp();
-                for (std::uint32_t t = B0 + std::uint32_t(lane); t < B1; t += 64) { // two pairs per lane in flight
-                    const std::uint32_t tb = t + 32;
-                    const bool          vb = tb < B1;
-                    const SRow&         qa = W.rows[W.list[t - B0]];
-                    const SRow&         qb = W.rows[W.list[(vb ? tb : t) - B0]];
-                    const std::uint32_t ka = std::uint32_t(qa.pad) + t, kb = std::uint32_t(qb.pad) + (vb ? tb : t);
-                    const bool ea = edge_test(qa.cs, qa.sn, qa.coth, qa.rci, S.r1[ka], S.r2[ka]);
-                    const bool eb = vb && edge_test(qb.cs, qb.sn, qb.coth, qb.rci, S.r1[kb], S.r2[kb]);
-                    count_edge<DEG>(A, ea, qa.id, S.id[ka], acc);
-                    count_edge<DEG>(A, eb, qb.id, S.id[kb], acc);
+            __syncwarp();
+            // lane L runs the contiguous pairs [L c, (L + 1) c) of the warp's sequence: its
+            // request stays in registers until the owner changes (rarely), only node records
+            // come from shared memory
+            const std::uint32_t c  = (T + 31) >> 5;
+            std::uint32_t       t  = std::uint32_t(lane) * c;
+            const std::uint32_t te = t + c < T ? t + c : T;
+            if (t < te) {
+                int o = 0, ho = 31; // first lane whose inclusive prefix exceeds t
+                while (o < ho) {
+                    const int mid = (o + ho) >> 1;
+                    if (W.incl[mid] > t) ho = mid;
+                    else o = mid + 1;
                 }
-                __syncwarp();
+                SRow          q   = W.rows[o];
+                std::uint32_t end = W.incl[o];
+                for (; t < te; ++t) {
+                    if (t >= end) { // next non-empty owner
+                        do ++o;
+                        while (W.incl[o] <= t);
+                        q = W.rows[o], end = W.incl[o];
+                    }
+                    const std::uint32_t k = std::uint32_t(q.pad) + t;
+                    count_edge<DEG>(A, edge_test(q.cs, q.sn, q.coth, q.rci, S.r1[k], S.r2[k]), q.id, S.id[k], acc);
+                }
             }
+            __syncwarp();
         }
     }
     flush(acc, A, 0, lane);
@@ -1031,10 +1072,14 @@ void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, 
     *launches += 3;
 }
 
-void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches) {
+// Sparse pairs (slab join + tail) on st; the dense chain (rows, node tiles,
+// global unit) on side, concurrently (both are latency-bound at modest
+// occupancy); side joins st before the counters are folded.  The dense
+// requests must already be sorted on side (launch_sort_globals).
+void launch_edges(const EdgeArgs& a, cudaStream_t st, cudaStream_t side, cudaEvent_t join, std::uint64_t* launches) {
     const bool deg = a.degrees != nullptr;
-    if (a.n_slabs) { // sparse pairs: slab join + tail
-        const int smem = int(sizeof(SlabSmem));
+    if (a.n_slabs) {
+        const int   smem = int(sizeof(SlabSmem));
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(slab_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1054,22 +1099,26 @@ void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches) {
     }
     if (a.n_req && a.first_streaming < a.count) {
         const std::uint64_t rows = a.n_req * std::uint64_t(a.count - a.first_streaming);
-        if (deg) req_rows_kernel<true><<<unsigned((rows + 255) / 256), 256, 0, st>>>(a);
-        else req_rows_kernel<false><<<unsigned((rows + 255) / 256), 256, 0, st>>>(a);
+        if (deg) req_rows_kernel<true><<<unsigned((rows + 255) / 256), 256, 0, side>>>(a);
+        else req_rows_kernel<false><<<unsigned((rows + 255) / 256), 256, 0, side>>>(a);
         ++*launches;
         if (a.glob_tile_warps) {
             const unsigned blocks = unsigned((a.glob_tile_warps + 7) / 8);
-            if (deg) glob_tiles_kernel<true><<<blocks, 256, 0, st>>>(a);
-            else glob_tiles_kernel<false><<<blocks, 256, 0, st>>>(a);
+            if (deg) glob_tiles_kernel<true><<<blocks, 256, 0, side>>>(a);
+            else glob_tiles_kernel<false><<<blocks, 256, 0, side>>>(a);
             ++*launches;
         }
     }
     if (a.gg_tile_end > a.gg_tile_begin) {
         const std::uint64_t nT     = (a.n_glob + kGGTile - 1) / kGGTile;
         const unsigned      blocks = unsigned(a.gg_tile_end - a.gg_tile_begin);
-        if (deg) glob_pairs_kernel<true><<<blocks, kGGTile, 0, st>>>(a, nT);
-        else glob_pairs_kernel<false><<<blocks, kGGTile, 0, st>>>(a, nT);
+        if (deg) glob_pairs_kernel<true><<<blocks, kGGTile, 0, side>>>(a, nT);
+        else glob_pairs_kernel<false><<<blocks, kGGTile, 0, side>>>(a, nT);
         ++*launches;
+    }
+    if (side != st) {
+        cudaEventRecord(join, side);
+        cudaStreamWaitEvent(st, join, 0);
     }
     reduce_counters_kernel<<<3, 1024, 0, st>>>(a);
     ++*launches;

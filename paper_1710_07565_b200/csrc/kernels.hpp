@@ -89,13 +89,14 @@ struct EdgeArgs {
 };
 
 void launch_cell_index(const EdgeArgs& a, std::uint64_t nblocks, cudaStream_t st, std::uint64_t* launches);
-void launch_edges(const EdgeArgs& a, cudaStream_t st, std::uint64_t* launches);
+void launch_edges(const EdgeArgs& a, cudaStream_t st, cudaStream_t side, cudaEvent_t join, std::uint64_t* launches);
 // Sorts the global points by (annulus, theta) into a.gperm (scratch layout
 // internal); with scratch == nullptr only reports the bytes needed in *need.
 void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, std::size_t* need, cudaStream_t st,
                          std::uint64_t* launches);
 
 constexpr int kGGTile = 128;
+constexpr int kSlabNodes = 512; // owned nodes per slab of the slab join (edges.cu)
 constexpr int kMaxCls = 1024; // (source, radial class) segments of the dense-engine requests
 // dbg layout (RHG_DEBUG_STATS=1): [0] stream (warp, target) steps, [1] staged unions, [2] per-lane
 // searches, [3] long rows, [4] flattened pairs, [5] serial pairs, [8] dense candidates loaded,
