@@ -299,7 +299,7 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
     pl.gt_prefix.assign(L.count + 1, 0);
     for (std::uint32_t j = 0; j < L.count; ++j) {
         const std::uint64_t own = j >= L.first_streaming && pl.n_req ? pl.ann[j].halo - pl.ann[j].off : 0;
-        pl.gt_prefix[j + 1]     = pl.gt_prefix[j] + (own + 511) / 512; // strips of 4 x 128 nodes
+        pl.gt_prefix[j + 1]     = pl.gt_prefix[j] + (own + 127) / 128; // one 128-node tile per warp
     }
     pl.gtwarps = pl.gt_prefix[L.count];
     if (pl.n_ext >= (std::uint64_t(1) << 32) || pl.n_req >= (std::uint64_t(1) << 31) || L.n >= (std::uint64_t(1) << 32))
@@ -388,7 +388,9 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     const std::size_t   o_dmax    = align256(3 * sizeof(Counters));
     const std::size_t   o_hmax    = o_dmax + align256(K * sizeof(unsigned long long));
     const std::size_t   o_cseg    = o_hmax + align256(std::size_t(kMaxCls) * K * sizeof(unsigned long long));
-    const std::size_t   o_slots   = o_cseg + align256((kMaxCls + 1) * sizeof(std::uint32_t));
+    const std::size_t   o_bkoff   = o_cseg + align256((kMaxCls + 1) * sizeof(std::uint32_t));
+    const std::size_t   o_bksh    = o_bkoff + align256((kMaxCls + 1) * sizeof(std::uint32_t));
+    const std::size_t   o_slots   = o_bksh + align256(kMaxCls * sizeof(std::uint32_t));
     const std::size_t   cnt_bytes = o_slots + 3 * kSlots * sizeof(SlotCounter) + 256;
     ctx->counters.ensure(cnt_bytes);
     CK(cudaMemsetAsync(ctx->counters.p, 0, cnt_bytes, ctx->stream));
@@ -425,15 +427,19 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         const std::size_t o_th = align256(2 * nG * sizeof(double2));
         const std::size_t o_id = o_th + align256(nG * sizeof(double));
         const std::size_t o_rw = o_id + align256(nG * sizeof(std::uint32_t));
-        ctx->gbuf.ensure(o_rw + align256(std::max<std::size_t>(nst, 1) * nG * 8 * sizeof(std::uint32_t)));
+        const std::size_t o_bk = o_rw + align256(std::max<std::size_t>(nst, 1) * nG * 8 * sizeof(std::uint32_t));
+        ctx->gbuf.ensure(o_bk + align256((2 * nG + 65 * std::size_t(kMaxCls)) * sizeof(std::uint32_t)));
         char* g     = ctx->gbuf.as<char>();
         e.g_rec     = reinterpret_cast<double2*>(g);
         e.g_theta   = reinterpret_cast<double*>(g + o_th);
         e.g_id      = reinterpret_cast<std::uint32_t*>(g + o_id);
         e.g_rows    = reinterpret_cast<std::uint32_t*>(g + o_rw);
+        e.gbk       = reinterpret_cast<std::uint32_t*>(g + o_bk);
         e.hmax_bits = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + o_hmax);
         e.cseg      = reinterpret_cast<std::uint32_t*>(ctx->counters.as<char>() + o_cseg);
         e.n_cls     = reinterpret_cast<int*>(ctx->counters.as<char>() + cnt_bytes - 256);
+        e.bk_off    = reinterpret_cast<std::uint32_t*>(ctx->counters.as<char>() + o_bkoff);
+        e.bk_shift  = reinterpret_cast<std::uint32_t*>(ctx->counters.as<char>() + o_bksh);
         e.gt_prefix = t.gt_prefix, e.glob_tile_warps = pl.gtwarps;
         e.n_req = pl.n_req, e.req_off = t.req_off, e.dense_mask = t.dense_mask;
     }

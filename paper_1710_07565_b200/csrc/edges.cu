@@ -631,6 +631,41 @@ __global__ void __launch_bounds__(1024) req_segments_kernel(EdgeArgs A, const un
         const int n = base < kMaxCls ? base : kMaxCls; // overflow is checked on the host via n_cls
         A.cseg[n]   = std::uint32_t(A.n_req);
         *A.n_cls    = base;
+        // angle-bucket tables: segment c gets 2^k >= max(64, size) buckets over [0, 2pi)
+        std::uint32_t off = 0;
+        for (int c = 0; c < n; ++c) {
+            const std::uint32_t sz = A.cseg[c + 1] - A.cseg[c];
+            int                 lg = 6;
+            while ((1u << lg) < sz && lg < 24) ++lg;
+            A.bk_off[c]   = off;
+            A.bk_shift[c] = std::uint32_t(32 - lg);
+            off += (1u << lg) + 1;
+        }
+        A.bk_off[n] = off;
+    }
+}
+
+// Bucket starts of every segment: gbk[bk_off[c] + b] = first sorted position
+// of segment c whose quantised angle falls in bucket >= b (cell_fill pattern;
+// the angles are the low 32 bits of the sort keys).
+__global__ void req_buckets_kernel(EdgeArgs A, const unsigned long long* keys) {
+    const std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= A.n_req) return;
+    const int ncls = *A.n_cls < kMaxCls ? *A.n_cls : kMaxCls;
+    int       c = 0, hc = ncls - 1; // segment of s
+    while (c < hc) {
+        const int mid = (c + hc + 1) >> 1;
+        if (A.cseg[mid] <= s) c = mid;
+        else hc = mid - 1;
+    }
+    const std::uint32_t sh  = A.bk_shift[c];
+    std::uint32_t*      tab = A.gbk + A.bk_off[c];
+    const std::int64_t  b   = std::int64_t(std::uint32_t(keys[s]) >> sh);
+    const std::int64_t  bp  = s > A.cseg[c] ? std::int64_t(std::uint32_t(keys[s - 1]) >> sh) : -1;
+    for (std::int64_t k = bp + 1; k <= b; ++k) tab[k] = std::uint32_t(s);
+    if (s + 1 == A.cseg[c + 1]) { // last of the segment: the tail buckets hold the segment end
+        const std::int64_t nb = std::int64_t(1) << (32 - sh);
+        for (std::int64_t k = b + 1; k <= nb; ++k) tab[k] = std::uint32_t(s + 1);
     }
 }
 
@@ -785,7 +820,7 @@ __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
 
 constexpr int kTN    = 128; // owned nodes per dense-engine tile (4 per lane, in registers)
 constexpr int kQ     = kTN / 32;
-constexpr int kStrip = 4;   // tiles per warp sharing one candidate search
+constexpr int kStrip = 1;   // tiles per warp sharing one candidate search
 
 struct GEnt { // one (request, piece) intersecting the current tile, compacted
     double        cs, sn, coth, rci;
@@ -793,7 +828,8 @@ struct GEnt { // one (request, piece) intersecting the current tile, compacted
 };
 struct GWarp {
     GEnt          e[128];   // up to 4 pieces per candidate, 32 candidates per chunk
-    std::uint32_t rng[128]; // candidate ranges (lo, hi) of sorted positions, two per segment
+    std::uint32_t rng[64];  // candidate range starts (sorted positions), two per segment of a pass
+    std::uint32_t pre[65];  // exclusive prefix of the range lengths (pre[64] = total)
 };
 
 // angle of the sorted requests of one segment: first position in [lo, hi)
@@ -852,22 +888,39 @@ __global__ void __launch_bounds__(256, 2) glob_tiles_kernel(EdgeArgs A) {
                         double st = lam_lo - hmax - 1e-7;
                         while (st < 0.0) st += kTwoPiD;
                         while (st >= kTwoPiD) st -= kTwoPiD;
-                        const double en = st + L;
-                        r0              = gtheta_lb(A.g_theta, sa, sb, st);
+                        const double         en  = st + L;
+                        const std::uint32_t  sh  = A.bk_shift[a];
+                        const std::uint32_t* tab = A.gbk + A.bk_off[a];
+                        // bucket of an angle in [0, 2pi]: quantised like the sort key (superset ranges)
+                        auto bkt = [sh](double x) {
+                            const double q = x * (4294967296.0 / kTwoPiD);
+                            return (q >= 4294967295.0 ? 0xffffffffu : std::uint32_t(q > 0.0 ? q : 0.0)) >> sh;
+                        };
+                        r0 = tab[bkt(st)];
                         if (en <= kTwoPiD) {
-                            r1 = gtheta_lb(A.g_theta, sa, sb, en);
+                            r1 = tab[bkt(en) + 1];
                         } else {
                             r1 = sb;
-                            r2 = sa, r3 = gtheta_lb(A.g_theta, sa, sb, en - kTwoPiD);
+                            r2 = sa, r3 = tab[bkt(en - kTwoPiD) + 1];
                         }
                     }
                 }
             }
+            // the ranges of this pass as one list: candidate t lies in range r with pre[r] <= t < pre[r + 1]
+            const std::uint32_t la = r1 - r0, lb = r3 - r2;
+            std::uint32_t       incl = la + lb;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const std::uint32_t x = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += x;
+            }
             __syncwarp();
-            ws->rng[4 * lane] = r0, ws->rng[4 * lane + 1] = r1, ws->rng[4 * lane + 2] = r2, ws->rng[4 * lane + 3] = r3;
+            ws->rng[2 * lane] = r0, ws->rng[2 * lane + 1] = r2;
+            ws->pre[2 * lane] = incl - la - lb, ws->pre[2 * lane + 1] = incl - lb;
+            if (lane == 31) ws->pre[64] = incl;
             __syncwarp();
         }
-        const int nrng = 2 * (ncls - a0 < 32 ? ncls - a0 : 32);
+        const std::uint32_t C = ws->pre[64];
         for (std::uint32_t t0 = sb0; t0 < sb1; t0 += kTN) {
             const std::uint32_t t1 = t0 + kTN < sb1 ? t0 + kTN : sb1;
             double2             n1[kQ], n2[kQ];
@@ -879,13 +932,20 @@ __global__ void __launch_bounds__(256, 2) glob_tiles_kernel(EdgeArgs A) {
                 n1[q] = A.s_rec1[kc], n2[q] = A.s_rec2[kc];
                 ecnt[q] = 0;
             }
-            for (int r = 0; r < nrng; ++r) {
-                const std::uint32_t lo = ws->rng[2 * r], hi = ws->rng[2 * r + 1];
-                for (std::uint32_t c0 = lo; c0 < hi; c0 += 32) {
-                    // stage: lane = candidate c0 + lane; its pieces clipped to [t0, t1)
-                    std::uint32_t pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                    const std::uint32_t s = c0 + std::uint32_t(lane);
-                    if (s < hi) {
+            {
+                for (std::uint32_t c0 = 0; c0 < C; c0 += 32) {
+                    // stage: lane = candidate c0 + lane of the list; its pieces clipped to [t0, t1)
+                    std::uint32_t       pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    const std::uint32_t tc    = c0 + std::uint32_t(lane);
+                    std::uint32_t       s     = 0;
+                    if (tc < C) {
+                        int r = 0;
+#pragma unroll
+                        for (int step = 32; step > 0; step >>= 1)
+                            if (ws->pre[r + step] <= tc) r += step;
+                        s = ws->rng[r] + (tc - ws->pre[r]);
+                    }
+                    if (tc < C) {
                         const uint4* row = reinterpret_cast<const uint4*>(A.g_rows + (gjb + s) * 8);
                         const uint4  pa = row[0], pb = row[1];
                         pc[0] = pa.x, pc[1] = pa.y, pc[2] = pa.z, pc[3] = pa.w;
@@ -1068,8 +1128,9 @@ void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, 
     req_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kin, vin);
     cub::DeviceRadixSort::SortPairs(p + 2 * a8 + 2 * a4, tmp, kin, kout, vin, perm, int(n), 0, 48, st);
     req_segments_kernel<<<1, 1024, 0, st>>>(a, kout);
+    req_buckets_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kout);
     a.gperm = perm;
-    *launches += 3;
+    *launches += 4;
 }
 
 // Sparse pairs (slab join + tail) on st; the dense chain (rows, node tiles,

@@ -54,6 +54,9 @@ struct EdgeArgs {
     const std::uint32_t* gperm = nullptr;  // global requests in (annulus, theta) order (null: id order)
     std::uint32_t*    cseg = nullptr;      // [kMaxCls + 1] sorted-position starts of the non-empty segments
     int*              n_cls = nullptr;     // number of non-empty (source, class) segments (device-written)
+    std::uint32_t*    bk_off = nullptr;    // [kMaxCls + 1] segment c's angle-bucket table at gbk + bk_off[c]
+    std::uint32_t*    bk_shift = nullptr;  // [kMaxCls] 32 - log2(buckets of segment c)
+    std::uint32_t*    gbk = nullptr;       // bucket starts (sorted positions), <= 2 n_req + 65 kMaxCls entries
     // dense engine: unified requests u (global points, then the streaming requests of annuli with
     // dense targets), sorted by (source, radial class, angle) into positions s
     std::uint64_t     n_req = 0;

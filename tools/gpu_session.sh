@@ -1,1 +1,1 @@
-timeout 120 python tools/run_once.py cfg2 1 > /dev/null 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:"slab_kernel" -c 1 -o gpurun_out/slab3 python tools/run_once.py cfg2 1 > gpurun_out/ncu.log 2>&1; echo "ncu rc=$?"
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench.log | cut -c1-330
