@@ -428,16 +428,28 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         const std::size_t o_id = o_th + align256(nG * sizeof(double));
         const std::size_t o_rw = o_id + align256(nG * sizeof(std::uint32_t));
         const std::size_t o_bk = o_rw + align256(std::max<std::size_t>(nst, 1) * nG * 8 * sizeof(std::uint32_t));
-        ctx->gbuf.ensure(o_bk + align256((2 * nG + 65 * std::size_t(kMaxCls)) * sizeof(std::uint32_t)));
+        const std::size_t o_iv = o_bk + align256((2 * nG + 65 * std::size_t(kMaxCls)) * sizeof(std::uint32_t));
+        const std::size_t o_u  = o_iv + align256(nG * sizeof(double));
+        const std::size_t o_ax = o_u + align256(nG * sizeof(std::uint32_t));
+        const std::size_t o_sf = o_ax + align256(nG * sizeof(double4));
+        const std::size_t o_df = o_sf + align256((std::size_t(nst + 1) << 10) * sizeof(std::uint32_t));
+        e.defer_cap            = std::max<std::size_t>(1 << 16, 2 * nG); // a few per halo/wrapped request
+        ctx->gbuf.ensure(o_df + align256(e.defer_cap * sizeof(uint4)));
+        e.deferred = reinterpret_cast<uint4*>(ctx->gbuf.as<char>() + o_df);
         char* g     = ctx->gbuf.as<char>();
         e.g_rec     = reinterpret_cast<double2*>(g);
         e.g_theta   = reinterpret_cast<double*>(g + o_th);
         e.g_id      = reinterpret_cast<std::uint32_t*>(g + o_id);
         e.g_rows    = reinterpret_cast<std::uint32_t*>(g + o_rw);
         e.gbk       = reinterpret_cast<std::uint32_t*>(g + o_bk);
+        e.g_inv     = reinterpret_cast<double*>(g + o_iv);
+        e.g_u       = reinterpret_cast<std::uint32_t*>(g + o_u);
+        e.g_aux     = reinterpret_cast<double4*>(g + o_ax);
+        e.seg_first = reinterpret_cast<std::uint32_t*>(g + o_sf);
         e.hmax_bits = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + o_hmax);
         e.cseg      = reinterpret_cast<std::uint32_t*>(ctx->counters.as<char>() + o_cseg);
         e.n_cls     = reinterpret_cast<int*>(ctx->counters.as<char>() + cnt_bytes - 256);
+        e.defer_ctr = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + cnt_bytes - 192);
         e.bk_off    = reinterpret_cast<std::uint32_t*>(ctx->counters.as<char>() + o_bkoff);
         e.bk_shift  = reinterpret_cast<std::uint32_t*>(ctx->counters.as<char>() + o_bksh);
         e.gt_prefix = t.gt_prefix, e.glob_tile_warps = pl.gtwarps;
@@ -480,12 +492,15 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     auto* hc = static_cast<Counters*>(ctx->staging.p);
     CK(cudaMemcpyAsync(hc, ctx->counters.p, 3 * sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
     int* h_ncls = reinterpret_cast<int*>(hc + 3);
-    *h_ncls     = 0;
+    auto* h_drop = reinterpret_cast<unsigned long long*>(hc + 4);
+    *h_ncls = 0, *h_drop = 0;
     if (e.n_cls) CK(cudaMemcpyAsync(h_ncls, e.n_cls, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    if (e.defer_ctr) CK(cudaMemcpyAsync(h_drop, e.defer_ctr + 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
     if (degrees)
         CK(cudaMemcpyAsync(degrees, ctx->degrees.p, pl.L.n * sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (*h_ncls > kMaxCls) throw Invariant("dense engine: too many request segments");
+    if (*h_drop) throw Invariant("dense engine: deferred-range list overflow");
     if (dbg) {
         unsigned long long h[kDbgSlots];
         CK(cudaMemcpy(h, ctx->dbg.p, sizeof h, cudaMemcpyDeviceToHost));

@@ -282,17 +282,25 @@ struct SRow { // one request as the cooperative loop reads it (broadcast from sh
 template <bool DEG>
 __device__ __forceinline__ void serial_range(const EdgeArgs& A, const SRow& q, double theta, bool dedup,
                                              std::uint64_t k0, std::uint64_t k1, Acc& acc) {
-    for (std::uint64_t k = k0; k < k1; ++k) {
-        const unsigned long long nid = A.s_id[k];
-        bool                     in  = true;
-        if (dedup) {
-            const double tq = A.s_theta[k];
-            in              = nid != q.id && (theta < tq || (theta == tq && q.id < nid));
+    for (std::uint64_t k = k0; k < k1; k += 4) { // four independent nodes in flight
+        double2            n1[4], n2[4];
+        unsigned long long nid[4];
+        double             tq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const std::uint64_t kk = k + u < k1 ? k + u : k;
+            n1[u] = A.s_rec1[kk], n2[u] = A.s_rec2[kk], nid[u] = A.s_id[kk];
+            tq[u] = dedup ? A.s_theta[kk] : 0.0;
         }
-        if (!in) continue;
-        if (A.dbg) atomicAdd(&A.dbg[5], 1ull);
-        acc.comps += 1;
-        count_edge<DEG>(A, edge_test(q.cs, q.sn, q.coth, q.rci, A.s_rec1[k], A.s_rec2[k]), q.id, nid, acc);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            bool in = k + u < k1;
+            if (dedup) in = in && nid[u] != q.id && (theta < tq[u] || (theta == tq[u] && q.id < nid[u]));
+            if (!in) continue;
+            if (A.dbg) atomicAdd(&A.dbg[5], 1ull);
+            acc.comps += 1;
+            count_edge<DEG>(A, edge_test(q.cs, q.sn, q.coth, q.rci, n1[u], n2[u]), q.id, nid[u], acc);
+        }
     }
 }
 
@@ -591,46 +599,47 @@ __global__ void req_keys_kernel(EdgeArgs A, unsigned long long* keys, std::uint3
 }
 
 // Start positions of the non-empty (source, class) segments in the sorted
-// keys, compacted: cseg[0..n_cls] and n_cls.  One block; thread c scans the
-// segment ids c, c + 1024, ...
-__global__ void __launch_bounds__(1024) req_segments_kernel(EdgeArgs A, const unsigned long long* keys) {
+// keys: every segment's first position marks seg_first[segment id]
+// (req_marks_kernel), then one block compacts the table in id order into
+// cseg[0..n_cls] and lays out the angle-bucket tables.
+__global__ void req_marks_kernel(EdgeArgs A, const unsigned long long* keys) {
+    const std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= A.n_req) return;
+    const unsigned long long seg = keys[s] >> 32;
+    if (s == 0 || (keys[s - 1] >> 32) != seg) A.seg_first[seg] = std::uint32_t(s);
+}
+__global__ void __launch_bounds__(1024) req_segments_kernel(EdgeArgs A) {
     __shared__ int wsum[32];
-    __shared__ int base;
     const int      lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    auto           lb   = [&](unsigned long long seg) {
-        std::uint64_t lo = 0, hi = A.n_req;
-        while (lo < hi) {
-            const std::uint64_t mid = (lo + hi) >> 1;
-            if ((keys[mid] >> 32) < seg) lo = mid + 1;
-            else hi = mid;
-        }
-        return lo;
-    };
-    if (threadIdx.x == 0) base = 0;
-    __syncthreads();
     const unsigned nseg = unsigned(A.count - A.first_streaming + 1) << 10;
-    for (unsigned c0 = 0; c0 < nseg; c0 += 1024) {
-        const unsigned      c  = c0 + threadIdx.x;
-        const std::uint64_t s0 = c < nseg ? lb(c) : 0, s1 = c < nseg ? lb(c + 1) : 0;
-        const bool          ne = s1 > s0;
-        const unsigned      m  = __ballot_sync(kFull, ne);
-        if (lane == 0) wsum[w] = __popc(m);
-        __syncthreads();
-        int before = 0, total = 0;
-        for (int k = 0; k < 32; ++k) {
-            before += k < w ? wsum[k] : 0;
-            total += wsum[k];
-        }
-        const int idx = base + before + __popc(m & ((1u << lane) - 1));
-        if (ne && idx < kMaxCls) A.cseg[idx] = std::uint32_t(s0);
-        __syncthreads();
-        if (threadIdx.x == 0) base += total;
-        __syncthreads();
+    const unsigned per  = (nseg + 1023) / 1024; // thread t compacts ids [t per, (t + 1) per)
+    const unsigned i0   = threadIdx.x * per, i1 = i0 + per < nseg ? i0 + per : nseg;
+    int            mine = 0;
+    for (unsigned i = i0; i < i1; ++i) mine += A.seg_first[i] != 0xffffffffu;
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += x;
     }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int k = 0; k < 32; ++k) {
+        before += k < w ? wsum[k] : 0;
+        total += wsum[k];
+    }
+    int idx = before + incl - mine;
+    for (unsigned i = i0; i < i1; ++i)
+        if (A.seg_first[i] != 0xffffffffu) {
+            if (idx < kMaxCls) A.cseg[idx] = A.seg_first[i];
+            ++idx;
+        }
+    __syncthreads();
     if (threadIdx.x == 0) {
-        const int n = base < kMaxCls ? base : kMaxCls; // overflow is checked on the host via n_cls
+        const int n = total < kMaxCls ? total : kMaxCls; // overflow is checked on the host via n_cls
         A.cseg[n]   = std::uint32_t(A.n_req);
-        *A.n_cls    = base;
+        *A.n_cls    = total;
         // angle-bucket tables: segment c gets 2^k >= max(64, size) buckets over [0, 2pi)
         std::uint32_t off = 0;
         for (int c = 0; c < n; ++c) {
@@ -669,6 +678,80 @@ __global__ void req_buckets_kernel(EdgeArgs A, const unsigned long long* keys) {
     }
 }
 
+// Sorted copies of the dense-engine requests (one gather pass, so the rows
+// and tile kernels read them coalesced): (cos, sin), (coth, coshR / sinh),
+// 1 / sinh, key angle, id, unified index, and (lambda or theta, beta, hw, theta).
+__global__ void req_gather_kernel(EdgeArgs A) {
+    const std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= A.n_req) return;
+    const std::uint32_t u = A.gperm[s];
+    double2             r1, r2;
+    double4             ax;
+    double              key;
+    unsigned long long  id;
+    if (u < A.n_glob) {
+        const std::uint64_t g = A.n_ext + u;
+        r1 = A.rec1[g], r2 = A.rec2[g];
+        const double th = A.rec0[g].y;
+        ax = make_double4(th, 0.0, 0.0, th), key = th, id = u;
+    } else {
+        const int           a = req_annulus(A, u);
+        const std::uint64_t p = A.ann[a].off + (u - A.req_off[a]);
+        r1 = A.s_rec1[p], r2 = A.s_rec2[p];
+        const double lam = A.s_lam[p];
+        ax  = make_double4(lam, A.s_beta[p], A.s_hw[p], A.s_theta[p]);
+        key = lam;
+        while (key >= kTwoPiD) key -= kTwoPiD;
+        id = A.s_id[p];
+    }
+    A.g_rec[2 * s]     = r1;
+    A.g_rec[2 * s + 1] = make_double2(r2.x, fmul(A.cosh_R, r2.y));
+    A.g_inv[s]         = r2.y;
+    A.g_theta[s]       = key;
+    A.g_id[s]          = std::uint32_t(id);
+    A.g_u[s]           = u;
+    A.g_aux[s]         = ax;
+}
+
+// Deferred node ranges of a sorted dense request s (dedup: same-annulus pair
+// rule of sweep.hpp:517-526).  Full list: the range is dropped and counted in
+// defer_ctr[1] (the host rejects the run; cap is sized to make that unreachable).
+__device__ __forceinline__ void defer_range(const EdgeArgs& A, std::uint32_t s, std::uint64_t k0, std::uint64_t k1,
+                                            bool dedup) {
+    const unsigned long long i = atomicAdd(&A.defer_ctr[0], 1ull);
+    if (i < A.defer_cap) A.deferred[i] = make_uint4(s, std::uint32_t(k0), std::uint32_t(k1), dedup ? 1u : 0u);
+    else atomicAdd(&A.defer_ctr[1], 1ull);
+}
+
+// One warp per deferred range: lanes stride its nodes.
+template <bool DEG>
+__global__ void __launch_bounds__(256) deferred_kernel(EdgeArgs A) {
+    const int                lane = threadIdx.x & 31;
+    const unsigned long long n    = A.defer_ctr[0] < A.defer_cap ? A.defer_ctr[0] : A.defer_cap;
+    const unsigned long long nw   = (unsigned long long)(gridDim.x) * (blockDim.x >> 5);
+    Acc                      acc;
+    for (unsigned long long i = (unsigned long long)(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
+         i += nw) {
+        const uint4   E  = A.deferred[i];
+        const double2 q1 = A.g_rec[2 * E.x], q2 = A.g_rec[2 * E.x + 1];
+        SRow          q;
+        q.cs = q1.x, q.sn = q1.y, q.coth = q2.x, q.rci = q2.y, q.id = A.g_id[E.x], q.pad = 0;
+        const double theta = A.g_aux[E.x].w;
+        for (std::uint64_t k = E.y + std::uint64_t(lane); k < E.z; k += 32) {
+            const unsigned long long nid = A.s_id[k];
+            bool                     in  = true;
+            if (E.w) {
+                const double tq = A.s_theta[k];
+                in              = nid != q.id && (theta < tq || (theta == tq && q.id < nid));
+            }
+            if (!in) continue;
+            acc.comps += 1;
+            count_edge<DEG>(A, edge_test(q.cs, q.sn, q.coth, q.rci, A.s_rec1[k], A.s_rec2[k]), q.id, nid, acc);
+        }
+    }
+    flush(acc, A, 1, lane);
+}
+
 // Row (sorted request s, target annulus j): the exact index ranges ("pieces")
 // of j's owned block the request tests there.  Global requests: the
 // split_wraparound pieces of [theta - h, theta + h) (sweep.hpp:41-58) and,
@@ -691,22 +774,17 @@ __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
         const int           jt = int(idx / nR);
         const std::uint64_t s  = idx - std::uint64_t(jt) * nR;
         const int           j  = A.first_streaming + jt;
-        const std::uint32_t u  = A.gperm[s];
+        const std::uint32_t u  = A.g_u[s];
         const AnnulusDev&   Aj = A.ann[j];
         std::uint32_t       pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         double              h     = -1.0; // half-width that bounds the pieces around the key angle
+        const double2       q2 = A.g_rec[2 * s + 1];  // (coth, coshR / sinh)
+        const double        inv = A.g_inv[s];
+        const double4       ax  = A.g_aux[s];         // global: (theta, 0, 0, theta); streaming: (lambda, beta, hw, theta)
         if (u < A.n_glob) {
-            const std::uint64_t g  = A.n_ext + u;
-            const double2       r0 = A.rec0[g], r1 = A.rec1[g], r2 = A.rec2[g];
-            const double        th = r0.y;
-            if (jt == 0) {
-                A.g_rec[2 * s]     = r1;
-                A.g_rec[2 * s + 1] = make_double2(r2.x, fmul(A.cosh_R, r2.y));
-                A.g_theta[s]       = th;
-                A.g_id[s]          = u;
-            }
+            const double th = ax.x;
             if (Aj.halo > Aj.off) {
-                h              = half_width_in(Aj, r2.x, r2.y); // generator.hpp:67
+                h              = half_width_in(Aj, q2.x, inv); // generator.hpp:67
                 const double a = fsub(th, h), b = fadd(th, h);
                 double       pa[2], pb[2];
                 int          np = 1;
@@ -742,31 +820,18 @@ __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
                 }
             }
         } else {
-            const int           a  = req_annulus(A, u);
-            const AnnulusDev&   Aa = A.ann[a];
-            const std::uint64_t p  = Aa.off + (u - A.req_off[a]);
-            const double2       r1 = A.s_rec1[p], r2 = A.s_rec2[p];
-            SRow                q;
-            q.cs = r1.x, q.sn = r1.y, q.coth = r2.x, q.rci = fmul(A.cosh_R, r2.y), q.id = A.s_id[p], q.pad = 0;
-            if (jt == 0) {
-                double th = A.s_lam[p];
-                while (th >= kTwoPiD) th -= kTwoPiD;
-                A.g_rec[2 * s]     = r1;
-                A.g_rec[2 * s + 1] = make_double2(q.coth, q.rci);
-                A.g_theta[s]       = th;
-                A.g_id[s]          = std::uint32_t(q.id);
-            }
+            const int a = req_annulus(A, u);
             if (j >= a && ((A.dense_mask[a] >> j) & 1ull)) {
-                const bool halo_req  = p >= Aa.halo;
-                const bool same_simp = !halo_req && p < Aa.wrap;
-                double     lo, hi;
+                const AnnulusDev&   Aa = A.ann[a];
+                const std::uint64_t p  = Aa.off + (u - A.req_off[a]);
+                const bool          halo_req  = p >= Aa.halo;
+                const bool          same_simp = !halo_req && p < Aa.wrap;
+                double              lo, hi;
                 if (j == a) {
-                    const double b = A.s_beta[p], hw = A.s_hw[p];
-                    lo = b, hi = fadd(b, fmul(2.0, hw)), h = hw;
+                    lo = ax.y, hi = fadd(ax.y, fmul(2.0, ax.z)), h = ax.z;
                 } else {
-                    const double lam = A.s_lam[p];
-                    h                = half_width_in(Aj, r2.x, r2.y);
-                    lo = fsub(lam, h), hi = fadd(lam, h);
+                    h  = half_width_in(Aj, q2.x, inv);
+                    lo = fsub(ax.x, h), hi = fadd(ax.x, h);
                 }
                 if (hi > lo) {
                     std::uint64_t g0 = 0, g1 = 0;
@@ -785,11 +850,14 @@ __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
                             acc.comps += s1 - s0;
                         }
                     }
-                    const double theta = A.s_theta[p];
-                    if (g1 > g0) serial_range<DEG>(A, q, theta, true, g0, g1, acc);
-                    if (!halo_req && Aj.end > Aj.halo && hi > A.s_lam[Aj.halo] && lo <= A.s_lam[Aj.end - 1]) {
+                    const bool halo_nodes =
+                        !halo_req && Aj.end > Aj.halo && hi > A.s_lam[Aj.halo] && lo <= A.s_lam[Aj.end - 1];
+                    // rare pairs needing the full dedup or in the halo block: deferred to
+                    // deferred_kernel (one warp per range) so no thread runs them serially
+                    if (g1 > g0) defer_range(A, std::uint32_t(s), g0, g1, true);
+                    if (halo_nodes) {
                         const std::uint64_t h0 = lower_bound_halo(A, Aj, lo), h1 = lower_bound_halo(A, Aj, hi);
-                        if (h1 > h0) serial_range<DEG>(A, q, theta, j == a, h0, h1, acc);
+                        if (h1 > h0) defer_range(A, std::uint32_t(s), h0, h1, j == a);
                     }
                 }
             }
@@ -1127,10 +1195,14 @@ void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, 
     std::uint32_t*      perm = reinterpret_cast<std::uint32_t*>(p + 2 * a8 + a4);
     req_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kin, vin);
     cub::DeviceRadixSort::SortPairs(p + 2 * a8 + 2 * a4, tmp, kin, kout, vin, perm, int(n), 0, 48, st);
-    req_segments_kernel<<<1, 1024, 0, st>>>(a, kout);
+    cudaMemsetAsync(a.seg_first, 0xff, (std::size_t(a.count - a.first_streaming + 1) << 10) * sizeof(std::uint32_t),
+                    st);
+    req_marks_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kout);
+    req_segments_kernel<<<1, 1024, 0, st>>>(a);
     req_buckets_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kout);
     a.gperm = perm;
-    *launches += 4;
+    req_gather_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a);
+    *launches += 6;
 }
 
 // Sparse pairs (slab join + tail) on st; the dense chain (rows, node tiles,
@@ -1169,6 +1241,9 @@ void launch_edges(const EdgeArgs& a, cudaStream_t st, cudaStream_t side, cudaEve
             else glob_tiles_kernel<false><<<blocks, 256, 0, side>>>(a);
             ++*launches;
         }
+        if (deg) deferred_kernel<true><<<148 * 4, 256, 0, side>>>(a);
+        else deferred_kernel<false><<<148 * 4, 256, 0, side>>>(a);
+        ++*launches;
     }
     if (a.gg_tile_end > a.gg_tile_begin) {
         const std::uint64_t nT     = (a.n_glob + kGGTile - 1) / kGGTile;

@@ -65,6 +65,13 @@ struct EdgeArgs {
     double2*          g_rec = nullptr;     // [2 n_req] sorted requests: (cos, sin), (coth, coshR/sinh)
     double*           g_theta = nullptr;   // [n_req] key angle (theta, or lambda mod 2pi), sorted per segment
     std::uint32_t*    g_id = nullptr;      // [n_req] vertex id
+    double*           g_inv = nullptr;     // [n_req] 1 / sinh r
+    std::uint32_t*    g_u = nullptr;       // [n_req] unified request index
+    double4*          g_aux = nullptr;     // [n_req] (lambda or theta, beta, hw, theta)
+    uint4*            deferred = nullptr;  // [defer_cap] (sorted request, k0, k1, dedup) ranges of deferred_kernel
+    unsigned long long* defer_ctr = nullptr; // [0] ranges reserved, [1] ranges dropped (must stay 0)
+    std::uint64_t     defer_cap = 0;
+    std::uint32_t*    seg_first = nullptr; // [(count - first_streaming + 1) << 10] first sorted position per segment id
     std::uint32_t*    g_rows = nullptr;    // [streaming annuli][n_req][8] window pieces (s0, s1) as owned indices
     unsigned long long* hmax_bits = nullptr; // [kMaxCls * count] max half-width per (radial class, target) (bits)
     const std::uint64_t* gt_prefix = nullptr; // [count + 1] dense-engine warps (128-node owned tiles) before annulus j
