@@ -383,7 +383,7 @@ SamplerArgs sampler_args(rhg_ctx* ctx, const Plan& pl, const Tables& t) {
 
 // Cell index + every edge kernel + counters back to the host.
 void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out, std::uint32_t* degrees,
-               std::uint64_t* launches) {
+               bool gen, std::uint64_t* launches) {
     const std::uint32_t K         = pl.L.count;
     const std::size_t   o_dmax    = align256(3 * sizeof(Counters));
     const std::size_t   o_hmax    = o_dmax + align256(K * sizeof(unsigned long long));
@@ -475,7 +475,8 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         e.dbg = ctx->dbg.as<unsigned long long>();
     }
     e.ann_blk = t.ann_blk;
-    launch_cell_index(e, pl.ann_blk[pl.L.count], ctx->stream, launches);
+    e.gen = gen ? 1 : 0;
+    launch_cell_index(e, pl.ann_blk[pl.L.count], gen, ctx->stream, launches);
     // dense chain on the side stream, concurrent with the sparse pairs
     CK(cudaEventRecord(ctx->fork, ctx->stream));
     CK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
@@ -617,9 +618,11 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
         const Tables t = upload_tables(ctx, pl, &out->h2d_bytes);
         const double host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-        launch_sampler(sampler_args(ctx, pl, t), ctx->stream, &launches);
+        SamplerArgs sa  = sampler_args(ctx, pl, t);
+        sa.angular_from = pl.n_ext; // streaming frames are built while scattering (sort phase)
+        launch_sampler(sa, ctx->stream, &launches);
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
-        run_edges(ctx, pl, t, out, degrees, &launches);
+        run_edges(ctx, pl, t, out, degrees, true, &launches);
         fill_common(pl, out);
         out->sample_ms       = ms_between(ctx->ev[0], ctx->ev[1]);
         out->edges_ms        = ms_between(ctx->ev[1], ctx->ev[2]);
@@ -735,7 +738,7 @@ int rhg_count_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rh
         CK(cudaEventRecord(ctx->ev[0], st));
         launch_frames_from_points(sampler_args(ctx, pl, t), st, &launches);
         CK(cudaEventRecord(ctx->ev[1], st));
-        run_edges(ctx, pl, t, out, degrees, &launches);
+        run_edges(ctx, pl, t, out, degrees, false, &launches);
         fill_common(pl, out);
         out->sample_ms       = ms_between(ctx->ev[0], ctx->ev[1]);
         out->edges_ms        = ms_between(ctx->ev[1], ctx->ev[2]);

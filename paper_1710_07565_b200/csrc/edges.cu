@@ -108,6 +108,20 @@ __device__ __forceinline__ void cell_fill(std::uint64_t* tab, std::int64_t kp, s
 }
 
 // ---------------------------------------------------------------- sort ---
+// Engine-frame begin of point i of annulus block J (generate mode: the beta
+// array holds the unlifted beta; the halo block of the shard owning engine
+// P-1 is chunk 0 lifted by 2pi, sweep.hpp:252, 466-467).
+template <bool GEN>
+__device__ __forceinline__ double frame_beta(const EdgeArgs& A, const AnnulusDev& J, std::uint64_t i) {
+    const double b = A.beta[i];
+    return GEN && A.lift_part && i >= J.halo ? fadd(b, kTwoPiD) : b;
+}
+template <bool GEN>
+__device__ __forceinline__ double frame_lambda(const EdgeArgs& A, const AnnulusDev& J, std::uint64_t i) {
+    return GEN ? fadd(frame_beta<true>(A, J, i), A.hw[i]) : A.rec0[i].x;
+}
+
+template <bool GEN>
 __global__ void __launch_bounds__(256) beta_cells_kernel(EdgeArgs A) {
     const int lane = threadIdx.x & 31;
     if (blockIdx.x == 0 && int(threadIdx.x) < A.count && int(threadIdx.x) >= A.first_streaming) {
@@ -122,8 +136,8 @@ __global__ void __launch_bounds__(256) beta_cells_kernel(EdgeArgs A) {
     const AnnulusDev&   J = A.ann[j];
     unsigned long long  hwbits = 0;
     if (i < J.end) {
-        const std::uint32_t k  = cellf(J, A.beta[i]);
-        const std::int64_t  kp = i > J.off ? std::int64_t(cellf(J, A.beta[i - 1])) : -1;
+        const std::uint32_t k  = cellf(J, frame_beta<GEN>(A, J, i));
+        const std::int64_t  kp = i > J.off ? std::int64_t(cellf(J, frame_beta<GEN>(A, J, i - 1))) : -1;
         cell_fill(A.cellstart + J.cell_off, kp, k, i);
         hwbits = static_cast<unsigned long long>(__double_as_longlong(A.hw[i])); // hw >= +0
     }
@@ -143,6 +157,7 @@ __global__ void __launch_bounds__(256) beta_cells_kernel(EdgeArgs A) {
 // (lambda, id).  Only points whose beta lies in [lambda_i - dmax, lambda_i]
 // can compare either way: everything before that window is smaller
 // (lambda <= beta + dmax), everything after is larger (lambda >= beta).
+template <bool GEN>
 __global__ void __launch_bounds__(256) rank_kernel(EdgeArgs A) {
     std::uint64_t       i;
     const int           j = block_annulus(A, i);
@@ -150,7 +165,7 @@ __global__ void __launch_bounds__(256) rank_kernel(EdgeArgs A) {
     if (i >= J.end) return;
     const bool          hb = i >= J.halo;
     const std::uint64_t bs = hb ? J.halo : J.off, be = hb ? J.end : J.halo;
-    const double        li = A.rec0[i].x;
+    const double        li = frame_lambda<GEN>(A, J, i);
     const double        dm = __longlong_as_double(static_cast<long long>(A.dmax_bits[j]));
     std::uint64_t       k0 = A.cellstart[J.cell_off + cellf(J, fsub(fsub(li, dm), 1e-12))];
     std::uint64_t       k1 = A.cellstart[J.cell_off + cellf(J, li) + 1];
@@ -158,7 +173,7 @@ __global__ void __launch_bounds__(256) rank_kernel(EdgeArgs A) {
     k1 = k1 > be ? be : k1;
     std::uint64_t rank = k0 - bs;
     for (std::uint64_t k = k0; k < k1; ++k) {
-        const double lk = A.rec0[k].x;
+        const double lk = frame_lambda<GEN>(A, J, k);
         rank += (lk < li) || (lk == li && k < i);
     }
     A.perm[i] = bs + rank;
@@ -178,6 +193,30 @@ __global__ void __launch_bounds__(256) scatter_kernel(EdgeArgs A) {
     A.s_rec1[d]            = A.rec1[i];
     A.s_rec2[d]            = A.rec2[i];
     A.s_id[d]              = i + static_cast<unsigned long long>(i < J.halo ? J.dlt0 : J.dlt1);
+}
+
+// Generate mode: the sampler's angular step (sweep.hpp:135-139, 478-480:
+// theta = beta + hw mod 2pi, cos, sin, engine-frame begin/centre) fused with
+// the scatter, so the frames go straight to their sorted positions.
+__global__ void __launch_bounds__(256) angular_scatter_kernel(EdgeArgs A) {
+    std::uint64_t       i;
+    const int           j = block_annulus(A, i);
+    const AnnulusDev&   J = A.ann[j];
+    if (i >= J.end) return;
+    const std::uint64_t d  = A.perm[i];
+    const double        b0 = A.beta[i], h = A.hw[i];
+    double              th = fadd(b0, h);
+    if (th >= kTwoPiD) th = fsub(th, kTwoPiD);
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    const double bf = A.lift_part && i >= J.halo ? fadd(b0, kTwoPiD) : b0;
+    A.s_beta[d]     = bf;
+    A.s_hw[d]       = h;
+    A.s_lam[d]      = fadd(bf, h);
+    A.s_theta[d]    = th;
+    A.s_rec1[d]     = make_double2(cs, sn);
+    A.s_rec2[d]     = A.rec2[i];
+    A.s_id[d]       = i + static_cast<unsigned long long>(i < J.halo ? J.dlt0 : J.dlt1);
 }
 
 // Lambda-cell starts of every owned block, and the first owned index with
@@ -201,7 +240,7 @@ __global__ void cell_tail_kernel(EdgeArgs A, int lambda) {
     const AnnulusDev&   J = A.ann[j];
     const std::uint64_t e = lambda ? J.halo : J.end;
     if (e == J.off) return; // empty: initialised by beta_cells_kernel
-    const double        last = lambda ? A.s_lam[e - 1] : A.beta[e - 1];
+    const double        last = lambda ? A.s_lam[e - 1] : (A.gen ? frame_beta<true>(A, J, e - 1) : A.beta[e - 1]);
     const std::uint32_t k0   = cellf(J, last) + 1;
     std::uint64_t*      tab  = (lambda ? A.lcellstart : A.cellstart) + J.cell_off;
     for (std::uint32_t c = k0 + blockIdx.x * blockDim.x + threadIdx.x; c <= J.ncells; c += gridDim.x * blockDim.x)
@@ -1159,16 +1198,22 @@ __global__ void __launch_bounds__(1024) reduce_counters_kernel(EdgeArgs A) {
 
 } // namespace
 
-void launch_cell_index(const EdgeArgs& a, std::uint64_t nblocks, cudaStream_t st, std::uint64_t* launches) {
+void launch_cell_index(const EdgeArgs& a, std::uint64_t nblocks, bool gen, cudaStream_t st, std::uint64_t* launches) {
     if (a.first_streaming >= a.count) return;
     const unsigned g = unsigned(nblocks ? nblocks : 1); // >= 1: block 0 also initialises empty annuli
     const dim3     tails(64, unsigned(a.count - a.first_streaming));
-    beta_cells_kernel<<<g, 256, 0, st>>>(a);
+    if (gen) beta_cells_kernel<true><<<g, 256, 0, st>>>(a);
+    else beta_cells_kernel<false><<<g, 256, 0, st>>>(a);
     cell_tail_kernel<<<tails, 256, 0, st>>>(a, 0);
     *launches += 2;
     if (nblocks) {
-        rank_kernel<<<g, 256, 0, st>>>(a);
-        scatter_kernel<<<g, 256, 0, st>>>(a);
+        if (gen) {
+            rank_kernel<true><<<g, 256, 0, st>>>(a);
+            angular_scatter_kernel<<<g, 256, 0, st>>>(a);
+        } else {
+            rank_kernel<false><<<g, 256, 0, st>>>(a);
+            scatter_kernel<<<g, 256, 0, st>>>(a);
+        }
         lambda_cells_kernel<<<g, 256, 0, st>>>(a);
         cell_tail_kernel<<<tails, 256, 0, st>>>(a, 1);
         *launches += 4;

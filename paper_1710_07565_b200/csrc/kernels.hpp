@@ -21,6 +21,7 @@ struct SamplerArgs {
     double2*          rec2  = nullptr; // (coth r, 1/sinh r)
     double*           r_out = nullptr;             // optional: radius
     double*           beta_unlifted_out = nullptr; // optional: raw beta
+    std::uint64_t     angular_from = 0; // point_angular_kernel runs on [angular_from, total) (generate mode: n_ext)
     cudaStream_t      side = nullptr;                // optional second stream (fork/join with events)
     cudaEvent_t       ev_fork = nullptr, ev_join = nullptr;
 };
@@ -81,6 +82,7 @@ struct EdgeArgs {
     double            cosh_R = 1.0;
     double            chunk0_upper = 0.0; // chunk_upper_bound(0, P)
     int               lift_part = 0;      // shard owns engine P-1 (halo = lifted chunk 0)
+    int               gen = 0;            // generate mode (see launch_cell_index)
     // slab join (sparse pairs): slabs of 1024 owned nodes of every target annulus with sparse sources
     const unsigned long long* slab_tab = nullptr; // [n_slabs] (j << 32) | slab index in j, angle-interleaved order
     std::uint64_t     n_slabs = 0;
@@ -98,7 +100,9 @@ struct EdgeArgs {
     unsigned int*     degrees = nullptr;
 };
 
-void launch_cell_index(const EdgeArgs& a, std::uint64_t nblocks, cudaStream_t st, std::uint64_t* launches);
+// gen: the beta array holds the sampler's unlifted beta and no frames yet (rank from beta + hw, the
+// frames are computed while scattering); otherwise frames_from_points already built beta/rec0/rec1.
+void launch_cell_index(const EdgeArgs& a, std::uint64_t nblocks, bool gen, cudaStream_t st, std::uint64_t* launches);
 void launch_edges(const EdgeArgs& a, cudaStream_t st, cudaStream_t side, cudaEvent_t join, std::uint64_t* launches);
 // Sorts the global points by (annulus, theta) into a.gperm (scratch layout
 // internal); with scratch == nullptr only reports the bytes needed in *need.

@@ -204,11 +204,11 @@ __global__ void __launch_bounds__(128) sorted_chain_kernel(const StreamJob* __re
 }
 
 // sweep.hpp:135-139 + 478-480: node angle, trig, engine-frame begin/centre.
-__global__ void point_angular_kernel(const StreamJob* __restrict__ jobs, int njobs, std::uint64_t total,
-                                     double* __restrict__ beta, const double* __restrict__ hw,
+__global__ void point_angular_kernel(const StreamJob* __restrict__ jobs, int njobs, std::uint64_t first,
+                                     std::uint64_t total, double* __restrict__ beta, const double* __restrict__ hw,
                                      double2* __restrict__ rec0, double2* __restrict__ rec1,
                                      double* __restrict__ theta_out) {
-    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const std::uint64_t i = first + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= total) return;
     const StreamJob& J  = jobs[find_job(jobs, njobs, i)];
     const double     b0 = beta[i];
@@ -261,8 +261,11 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
         cudaEventRecord(S.ev_join, side);
         cudaStreamWaitEvent(st, S.ev_join, 0);
     }
-    point_angular_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.total, S.beta, S.hw, S.rec0, S.rec1,
-                                                  S.beta_unlifted_out);
+    // generate mode: streaming points get their frames in the sort phase (edges.cu angular_scatter_kernel)
+    const std::uint64_t first = S.angular_from;
+    if (S.total > first)
+        point_angular_kernel<<<unsigned((S.total - first + 255) / 256), 256, 0, st>>>(
+            S.jobs, S.njobs, first, S.total, S.beta, S.hw, S.rec0, S.rec1, S.beta_unlifted_out);
     *launches += 6;
 }
 
