@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define RHG_ABI_VERSION 1
+#define RHG_ABI_VERSION 2
 
 enum {
     RHG_OK = 0,
@@ -86,7 +86,9 @@ typedef struct {
     uint64_t device_bytes;    /* device memory held by the context          */
     uint64_t h2d_bytes;       /* host->device bytes this call copied        */
     uint64_t d2h_bytes;       /* device->host bytes this call copied        */
-    double pairs_ms;          /* the streaming pair kernel alone (dominant) */
+    double pairs_ms;          /* the sparse engine (slab join + tail kernels, dominant) */
+    uint64_t stream_comps;    /* predicate tests of the sparse engine (slab join + tail) */
+    uint64_t dense_comps;     /* predicate tests of the dense engine (global + wide-window requests) */
 } rhg_run_stats;
 
 /* Host point arrays in vertex-id order (n entries each; any may be NULL

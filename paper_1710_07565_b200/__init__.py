@@ -131,6 +131,8 @@ class RunStats:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     pairs_ms: float = 0.0
+    stream_comps: int = 0
+    dense_comps: int = 0
     degrees: Optional[np.ndarray] = None
 
     def avg_degree(self) -> float:
@@ -146,7 +148,8 @@ class RunStats:
                    R=s.R, annuli=s.annuli, first_streaming=s.first_streaming, global_edges=s.global_edges,
                    global_comps=s.global_comps, device_ms=s.device_ms, sample_ms=s.sample_ms, edges_ms=s.edges_ms,
                    host_ms=s.host_ms, kernel_launches=s.kernel_launches, device_bytes=s.device_bytes,
-                   h2d_bytes=s.h2d_bytes, d2h_bytes=s.d2h_bytes, pairs_ms=s.pairs_ms)
+                   h2d_bytes=s.h2d_bytes, d2h_bytes=s.d2h_bytes, pairs_ms=s.pairs_ms,
+                   stream_comps=s.stream_comps, dense_comps=s.dense_comps)
 
 
 class _Context:

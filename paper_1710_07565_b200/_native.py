@@ -30,7 +30,8 @@ class rhg_run_stats(C.Structure):
                 ("R", C.c_double), ("r_G", C.c_double), ("cosh_R", C.c_double), ("device_ms", C.c_double),
                 ("sample_ms", C.c_double), ("edges_ms", C.c_double), ("host_ms", C.c_double),
                 ("seconds", C.c_double), ("kernel_launches", C.c_uint64), ("device_bytes", C.c_uint64),
-                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("pairs_ms", C.c_double)]
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("pairs_ms", C.c_double),
+                ("stream_comps", C.c_uint64), ("dense_comps", C.c_uint64)]
 
 
 P_f64 = C.POINTER(C.c_double)

@@ -514,6 +514,8 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     out->comps       = hc[0].comps + hc[1].comps + hc[2].comps;
     out->global_edges = hc[2].edges;
     out->global_comps = hc[2].comps;
+    out->stream_comps = hc[0].comps;
+    out->dense_comps  = hc[1].comps;
     out->pairs_ms     = pl.n_slabs ? ms_between(ctx->ev[4], ctx->ev[5]) : 0.0;
     out->d2h_bytes += 3 * sizeof(Counters) + (degrees ? pl.L.n * sizeof(unsigned) : 0);
 }

@@ -1267,7 +1267,6 @@ void launch_edges(const EdgeArgs& a, cudaStream_t st, cudaStream_t side, cudaEve
         if (a.ev_pairs0) cudaEventRecord(a.ev_pairs0, st);
         if (deg) slab_kernel<true><<<unsigned(a.n_slabs), kSlabThreads, smem, st>>>(a);
         else slab_kernel<false><<<unsigned(a.n_slabs), kSlabThreads, smem, st>>>(a);
-        if (a.ev_pairs1) cudaEventRecord(a.ev_pairs1, st);
         ++*launches;
     }
     if (a.n_tail) {
@@ -1275,6 +1274,7 @@ void launch_edges(const EdgeArgs& a, cudaStream_t st, cudaStream_t side, cudaEve
         else tail_kernel<false><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
         ++*launches;
     }
+    if (a.n_slabs && a.ev_pairs1) cudaEventRecord(a.ev_pairs1, st); // sparse engine: slab join + tail
     if (a.n_req && a.first_streaming < a.count) {
         const std::uint64_t rows = a.n_req * std::uint64_t(a.count - a.first_streaming);
         if (deg) req_rows_kernel<true><<<unsigned((rows + 255) / 256), 256, 0, side>>>(a);
