@@ -73,34 +73,49 @@ __device__ __forceinline__ void mt_twist_warp(std::uint64_t* mt, int lane) {
 
 constexpr int kMtWarps = 4;
 
+// One CTA per (stream, {angles, radii}): warp 0 seeds ([rand.predef]
+// seeding recurrence, serial by definition) and regenerates the 312-word state
+// block k into buffer k % 2 while warps 1..3 temper block k - 1 and write its
+// outputs (x >> 11) * 2^-53 coalesced; one __syncthreads per block.  A long
+// stream then costs ~one twist per block instead of twist + tempering.
 // which: 0 = both streams of every job, 1 = angle streams only, 2 = radius streams only
 __global__ void __launch_bounds__(32 * kMtWarps) mt_uniforms_kernel(const StreamJob* __restrict__ jobs, int njobs,
                                                                      double* __restrict__ u_ang,
                                                                      double* __restrict__ u_rad, int which) {
-    __shared__ std::uint64_t state[kMtWarps][kMtN];
+    __shared__ std::uint64_t state[kMtN], out[2][kMtN];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gw   = blockIdx.x * kMtWarps + warp;
+    const int gw   = blockIdx.x;
     if (gw >= (which ? 1 : 2) * njobs) return;
-    const StreamJob& J   = jobs[which ? gw : gw >> 1];
-    const bool       ang = which ? which == 1 : (gw & 1) == 0;
-    double*          out = (ang ? u_ang : u_rad) + J.out_off;
-    std::uint64_t*   mt  = state[warp];
-    if (J.count == 0) return;
-    if (lane == 0) { // [rand.predef] seeding recurrence (serial by definition)
+    const StreamJob&    J   = jobs[which ? gw : gw >> 1];
+    const bool          ang = which ? which == 1 : (gw & 1) == 0;
+    double*             dst = (ang ? u_ang : u_rad) + J.out_off;
+    const std::uint64_t n   = J.count;
+    if (n == 0) return;
+    if (warp == 0 && lane == 0) {
         std::uint64_t x = ang ? J.seed_ang : J.seed_rad;
-        mt[0]           = x;
+        state[0]        = x;
         for (int i = 1; i < kMtN; ++i) {
-            x     = 6364136223846793005ull * (x ^ (x >> 62)) + std::uint64_t(i);
-            mt[i] = x;
+            x        = 6364136223846793005ull * (x ^ (x >> 62)) + std::uint64_t(i);
+            state[i] = x;
         }
     }
-    __syncwarp();
-    for (std::uint64_t base = 0; base < J.count; base += kMtN) {
-        mt_twist_warp(mt, lane);
-        const std::uint64_t left = J.count - base;
-        const int           nout = left < kMtN ? int(left) : kMtN;
-        for (int i = lane; i < nout; i += 32) out[base + i] = double(mt_temper(mt[i]) >> 11) * 0x1.0p-53;
-        __syncwarp();
+    __syncthreads();
+    const std::uint64_t nblk = (n + kMtN - 1) / kMtN;
+    for (std::uint64_t k = 0; k <= nblk; ++k) {
+        if (warp == 0) {
+            if (k < nblk) {
+                mt_twist_warp(state, lane);
+                std::uint64_t* o = out[k & 1];
+                for (int i = lane; i < kMtN; i += 32) o[i] = state[i];
+            }
+        } else if (k > 0) { // temper and store block k - 1
+            const std::uint64_t  base = (k - 1) * kMtN;
+            const int            cnt  = n - base < std::uint64_t(kMtN) ? int(n - base) : kMtN;
+            const std::uint64_t* o    = out[(k - 1) & 1];
+            for (int i = threadIdx.x - 32; i < cnt; i += 32 * (kMtWarps - 1))
+                dst[base + i] = double(mt_temper(o[i]) >> 11) * 0x1.0p-53;
+        }
+        __syncthreads();
     }
 }
 
@@ -245,7 +260,7 @@ __global__ void frames_from_points_kernel(const StreamJob* __restrict__ jobs, in
 // beside it on a second stream; the angular kernel joins both.
 void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
     if (S.total == 0 || S.njobs == 0) return;
-    const int      mt_blocks = (S.njobs + kMtWarps - 1) / kMtWarps;
+    const int      mt_blocks = S.njobs; // one CTA per stream
     const unsigned pblocks   = unsigned((S.total + 255) / 256);
     cudaStream_t   side      = S.side ? S.side : st;
     if (S.side) {
@@ -271,8 +286,7 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
 
 void launch_mt_uniforms(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
     if (S.total == 0 || S.njobs == 0) return;
-    const int mt_blocks = (2 * S.njobs + kMtWarps - 1) / kMtWarps;
-    mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 0);
+    mt_uniforms_kernel<<<2 * S.njobs, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 0);
     *launches += 1;
 }
 
