@@ -71,6 +71,26 @@ __device__ __forceinline__ void mt_twist_warp(std::uint64_t* mt, int lane) {
     __syncwarp();
 }
 
+// Out-of-place twist: B = twist(A), equal to the in-place sequential twist of
+// [rand.predef] (words 0..155 read old words only, 156..310 read new words
+// i-156, word 311 reads new words 0 and 155).
+__device__ __forceinline__ void mt_twist_to(const std::uint64_t* __restrict__ A, std::uint64_t* __restrict__ B,
+                                            int lane) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = lane + 32 * k;
+        if (i < kMtN - kMtM) B[i] = mt_mix(A[i], A[i + 1], A[i + kMtM]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = kMtN - kMtM + lane + 32 * k;
+        if (i < kMtN - 1) B[i] = mt_mix(A[i], A[i + 1], B[i - (kMtN - kMtM)]);
+    }
+    if (lane == 0) B[kMtN - 1] = mt_mix(A[kMtN - 1], B[0], B[kMtM - 1]);
+    __syncwarp();
+}
+
 constexpr int kMtWarps = 4;
 
 // One CTA per (stream, {angles, radii}): warp 0 seeds ([rand.predef]
@@ -82,7 +102,7 @@ constexpr int kMtWarps = 4;
 __global__ void __launch_bounds__(32 * kMtWarps) mt_uniforms_kernel(const StreamJob* __restrict__ jobs, int njobs,
                                                                      double* __restrict__ u_ang,
                                                                      double* __restrict__ u_rad, int which) {
-    __shared__ std::uint64_t state[kMtN], out[2][kMtN];
+    __shared__ std::uint64_t st[2][kMtN]; // st[k & 1]: the state after k twists
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gw   = blockIdx.x;
     if (gw >= (which ? 1 : 2) * njobs) return;
@@ -93,25 +113,21 @@ __global__ void __launch_bounds__(32 * kMtWarps) mt_uniforms_kernel(const Stream
     if (n == 0) return;
     if (warp == 0 && lane == 0) {
         std::uint64_t x = ang ? J.seed_ang : J.seed_rad;
-        state[0]        = x;
+        st[0][0]        = x;
         for (int i = 1; i < kMtN; ++i) {
             x        = 6364136223846793005ull * (x ^ (x >> 62)) + std::uint64_t(i);
-            state[i] = x;
+            st[0][i] = x;
         }
     }
     __syncthreads();
     const std::uint64_t nblk = (n + kMtN - 1) / kMtN;
     for (std::uint64_t k = 0; k <= nblk; ++k) {
         if (warp == 0) {
-            if (k < nblk) {
-                mt_twist_warp(state, lane);
-                std::uint64_t* o = out[k & 1];
-                for (int i = lane; i < kMtN; i += 32) o[i] = state[i];
-            }
-        } else if (k > 0) { // temper and store block k - 1
+            if (k < nblk) mt_twist_to(st[k & 1], st[(k + 1) & 1], lane); // block k
+        } else if (k > 0) { // temper and store block k - 1 (the state after k twists)
             const std::uint64_t  base = (k - 1) * kMtN;
             const int            cnt  = n - base < std::uint64_t(kMtN) ? int(n - base) : kMtN;
-            const std::uint64_t* o    = out[(k - 1) & 1];
+            const std::uint64_t* o    = st[k & 1];
             for (int i = threadIdx.x - 32; i < cnt; i += 32 * (kMtWarps - 1))
                 dst[base + i] = double(mt_temper(o[i]) >> 11) * 0x1.0p-53;
         }
