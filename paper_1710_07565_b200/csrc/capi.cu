@@ -122,6 +122,7 @@ struct Plan {
     std::uint32_t           e0 = 0, e1 = 0, T = 0;
     std::vector<AnnulusDev> ann;
     std::vector<StreamJob>  jobs;
+    std::vector<std::uint32_t> job_order;   // jobs by descending count
     std::vector<std::uint64_t> gt_prefix;   // dense-engine warps (512-node owned strips) before annulus j
     std::vector<std::uint64_t> gseg;        // global-point annulus offsets (segments of the theta sort)
     std::vector<unsigned long long> dense_mask; // [count] bit j: (a, j) runs on the dense engine
@@ -229,6 +230,10 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
             pl.jobs.push_back(J);
         }
     pl.total = pl.n_ext + pl.n_glob;
+    pl.job_order.resize(pl.jobs.size());
+    for (std::uint32_t k = 0; k < pl.job_order.size(); ++k) pl.job_order[k] = k;
+    std::stable_sort(pl.job_order.begin(), pl.job_order.end(),
+                     [&](std::uint32_t x, std::uint32_t y) { return pl.jobs[x].count > pl.jobs[y].count; });
     for (std::uint32_t i = 0; i < L.first_streaming; ++i) pl.gseg.push_back(L.chunk_id_base(i, 0));
     pl.gseg.push_back(pl.n_glob);
     // (annulus, target) pairs whose windows hold >= kDenseMin nodes on average run on the dense
@@ -314,6 +319,7 @@ struct Tables {
     unsigned long long* dense_mask;
     std::uint64_t*      req_off;
     StreamJob*          jobs;
+    std::uint32_t*      job_order;
     std::uint64_t*      gt_prefix;
     std::uint64_t*      gseg;
     std::uint32_t*      ann_blk;
@@ -340,7 +346,7 @@ Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr)
     const std::size_t i_ann = add(pl.ann), i_dm = add(pl.dense_mask), i_ro = add(pl.req_off), i_jobs = add(pl.jobs);
     const std::size_t i_gt = add(pl.gt_prefix), i_gs = add(pl.gseg), i_ab = add(pl.ann_blk), i_sm = add(pl.src_mask);
     const std::size_t i_hb = add(pl.hbound), i_sp = add(pl.slab_tab), i_tp = add(pl.tail_prefix);
-    const std::size_t i_tl = add(pl.tail_lam);
+    const std::size_t i_tl = add(pl.tail_lam), i_jo = add(pl.job_order);
     bytes += 256;
     ctx->staging.ensure(bytes);
     char* h = static_cast<char*>(ctx->staging.p);
@@ -353,6 +359,7 @@ Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr)
     auto  at = [&](std::size_t i) { return static_cast<void*>(d + parts[i].off); };
     return {static_cast<AnnulusDev*>(at(i_ann)),        static_cast<unsigned long long*>(at(i_dm)),
             static_cast<std::uint64_t*>(at(i_ro)),      static_cast<StreamJob*>(at(i_jobs)),
+            static_cast<std::uint32_t*>(at(i_jo)),
             static_cast<std::uint64_t*>(at(i_gt)),      static_cast<std::uint64_t*>(at(i_gs)),
             static_cast<std::uint32_t*>(at(i_ab)),      static_cast<unsigned long long*>(at(i_sm)),
             static_cast<double*>(at(i_hb)),             static_cast<unsigned long long*>(at(i_sp)),
@@ -374,7 +381,7 @@ void ensure_points(rhg_ctx* ctx, std::uint64_t total, bool with_export) {
 
 SamplerArgs sampler_args(rhg_ctx* ctx, const Plan& pl, const Tables& t) {
     SamplerArgs s;
-    s.jobs = t.jobs, s.njobs = int(pl.jobs.size()), s.ann = t.ann, s.alpha = pl.L.alpha, s.total = pl.total;
+    s.jobs = t.jobs, s.job_order = t.job_order, s.njobs = int(pl.jobs.size()), s.ann = t.ann, s.alpha = pl.L.alpha, s.total = pl.total;
     s.beta = ctx->beta.as<double>(), s.hw = ctx->hw.as<double>();
     s.rec0 = ctx->rec0.as<double2>(), s.rec1 = ctx->rec1.as<double2>(), s.rec2 = ctx->rec2.as<double2>();
     s.side = ctx->side, s.ev_fork = ctx->fork, s.ev_join = ctx->join;

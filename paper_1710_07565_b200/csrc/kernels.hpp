@@ -11,6 +11,7 @@ namespace rhgb {
 struct SamplerArgs {
     const StreamJob*  jobs = nullptr;
     int               njobs = 0;
+    const std::uint32_t* job_order = nullptr; // jobs by descending count (chain kernel schedule)
     const AnnulusDev* ann   = nullptr;
     double            alpha = 1.0;
     std::uint64_t     total = 0; // points (streaming extended arrays + global points)

@@ -183,11 +183,14 @@ __global__ void point_radial_kernel(const StreamJob* __restrict__ jobs, int njob
 // arrive by shuffle, so the loop-carried dependency is one DMUL per point —
 // and lane k%32 keeps beta_k for a coalesced store.
 __global__ void __launch_bounds__(128) sorted_chain_kernel(const StreamJob* __restrict__ jobs, int njobs,
+                                                           const std::uint32_t* __restrict__ order,
                                                            double* __restrict__ x) {
     const int lane = threadIdx.x & 31;
-    const int w    = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // warp w of CTA b runs the (b + w gridDim)-th longest stream: the first CTA on every SM
+    // leads with one of the longest chains (a chain is issue-bound when it shares its scheduler)
+    const int w = blockIdx.x + (threadIdx.x >> 5) * gridDim.x;
     if (w >= njobs) return;
-    const StreamJob&    J = jobs[w];
+    const StreamJob&    J = jobs[order[w]];
     double*             p = x + J.out_off;
     const std::uint64_t n = J.count;
     const double        a = J.a, b = J.b, wd = fsub(b, a);
@@ -287,7 +290,7 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
     point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
     mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 1);
     point_pow_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.total, S.beta);
-    sorted_chain_kernel<<<(S.njobs + 3) / 4, 128, 0, st>>>(S.jobs, S.njobs, S.beta);
+    sorted_chain_kernel<<<(S.njobs + 3) / 4, 128, 0, st>>>(S.jobs, S.njobs, S.job_order, S.beta);
     if (S.side) {
         cudaEventRecord(S.ev_join, side);
         cudaStreamWaitEvent(st, S.ev_join, 0);
