@@ -142,7 +142,7 @@ struct Plan {
 // Expected number of annulus-j nodes in the window of an annulus-a request
 // at a's median radius (density ~ sinh(alpha r)); same-annulus windows count
 // half (dedup).  Only chooses the engine for (a, j); never affects results.
-constexpr double kDenseMin = 32.0;
+constexpr double kDenseMin = 96.0;
 double expected_window_nodes(const Layout& L, std::uint32_t a, std::uint32_t j) {
     const double r    = std::acosh(0.5 * (L.cosh_alpha_lower[a] + L.cosh_alpha_upper[a])) / L.alpha;
     const double ex   = std::exp(r), mex = 1.0 / ex, sh = 0.5 * (ex - mex);
@@ -237,7 +237,7 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
     for (std::uint32_t i = 0; i < L.first_streaming; ++i) pl.gseg.push_back(L.chunk_id_base(i, 0));
     pl.gseg.push_back(pl.n_glob);
     // (annulus, target) pairs whose windows hold >= kDenseMin nodes on average run on the dense
-    // engine (node tiles x streamed requests); the rest on the streaming kernel
+    // engine (node tiles x streamed requests); the rest on the slab join (96: measured optimum band 64..128 at cfg2)
     pl.dense_mask.assign(L.count, 0ull);
     pl.req_off.assign(L.count, 0);
     pl.n_req = pl.n_glob;
