@@ -105,9 +105,11 @@ double ms_between(cudaEvent_t a, cudaEvent_t b) {
 
 struct rhg_ctx {
     int          device = 0;
-    cudaStream_t stream = nullptr, side = nullptr;
+    cudaStream_t stream = nullptr, side = nullptr, late = nullptr;
     cudaEvent_t  ev[6]{};
     cudaEvent_t  fork = nullptr, join = nullptr; // timing-free events for the side stream
+    cudaEvent_t  ev_pow = nullptr, ev_late = nullptr; // the wave-2 chains (late stream)
+    cudaEvent_t  evw[4]{};                            // sparse-engine timing of the two edge waves
     DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, cells, counters, degrees, dbg, nid;
     DevBuf       lcells, perm, s_beta, s_hw, s_lt, s_rec1, s_rec2, gsort, gbuf;
     HostPinned   staging;
@@ -122,7 +124,10 @@ struct Plan {
     std::uint32_t           e0 = 0, e1 = 0, T = 0;
     std::vector<AnnulusDev> ann;
     std::vector<StreamJob>  jobs;
-    std::vector<std::uint32_t> job_order;   // jobs by descending count
+    std::vector<std::uint32_t> job_order;   // wave-1 jobs then wave-2 jobs, each by descending count
+    std::uint32_t              wave_j = 0;  // first annulus of wave 2 (count: no split)
+    int                        wave2_jobs = 0;
+    std::uint64_t              n_slabs1 = 0; // slabs of wave-1 targets (they come first in slab_tab)
     std::vector<std::uint64_t> gt_prefix;   // dense-engine warps (512-node owned strips) before annulus j
     std::vector<std::uint64_t> gseg;        // global-point annulus offsets (segments of the theta sort)
     std::vector<unsigned long long> dense_mask; // [count] bit j: (a, j) runs on the dense engine
@@ -230,10 +235,6 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
             pl.jobs.push_back(J);
         }
     pl.total = pl.n_ext + pl.n_glob;
-    pl.job_order.resize(pl.jobs.size());
-    for (std::uint32_t k = 0; k < pl.job_order.size(); ++k) pl.job_order[k] = k;
-    std::stable_sort(pl.job_order.begin(), pl.job_order.end(),
-                     [&](std::uint32_t x, std::uint32_t y) { return pl.jobs[x].count > pl.jobs[y].count; });
     for (std::uint32_t i = 0; i < L.first_streaming; ++i) pl.gseg.push_back(L.chunk_id_base(i, 0));
     pl.gseg.push_back(pl.n_glob);
     // (annulus, target) pairs whose windows hold >= kDenseMin nodes on average run on the dense
@@ -247,6 +248,19 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
         pl.req_off[a] = pl.n_req;
         if (pl.dense_mask[a]) pl.n_req += pl.ann[a].end - pl.ann[a].off;
     }
+    // wave split (generate mode): the outermost streaming annulus (the longest sorted-uniform
+    // chains) forms wave 2 when it is not a dense-engine source; everything else is wave 1
+    pl.wave_j = L.count;
+    if (L.count >= L.first_streaming + 2 && pl.T > 0 && !pl.dense_mask[L.count - 1]) pl.wave_j = L.count - 1;
+    pl.job_order.resize(pl.jobs.size());
+    for (std::uint32_t k = 0; k < pl.job_order.size(); ++k) pl.job_order[k] = k;
+    auto in_wave2 = [&](std::uint32_t k) { return pl.jobs[k].annulus >= pl.wave_j && pl.jobs[k].annulus < L.count; };
+    std::stable_sort(pl.job_order.begin(), pl.job_order.end(), [&](std::uint32_t x, std::uint32_t y) {
+        if (in_wave2(x) != in_wave2(y)) return !in_wave2(x);
+        return pl.jobs[x].count > pl.jobs[y].count;
+    });
+    pl.wave2_jobs = 0;
+    for (std::uint32_t k = 0; k < pl.jobs.size(); ++k) pl.wave2_jobs += in_wave2(k);
     // slab join for the sparse pairs: slabs of every target annulus with sparse sources, the
     // half-width bounds that find a slab's requests, and the tail (wrap / halo) requests
     const std::uint32_t K = L.count;
@@ -273,8 +287,13 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
             for (std::uint64_t i = 0; i < ns; ++i)
                 order.push_back({(double(i) + 0.5) / double(ns), (static_cast<unsigned long long>(j) << 32) | i});
         }
-        std::stable_sort(order.begin(), order.end(),
-                         [](const auto& x, const auto& y) { return x.first < y.first; });
+        const auto wave = [&](unsigned long long v) { return (v >> 32) >= pl.wave_j ? 1 : 0; };
+        std::stable_sort(order.begin(), order.end(), [&](const auto& x, const auto& y) {
+            if (wave(x.second) != wave(y.second)) return wave(x.second) < wave(y.second);
+            return x.first < y.first;
+        });
+        pl.n_slabs1 = 0;
+        for (const auto& o: order) pl.n_slabs1 += wave(o.second) == 0;
         pl.slab_tab.resize(order.size());
         for (std::size_t i = 0; i < order.size(); ++i) pl.slab_tab[i] = order[i].second;
     }
@@ -390,7 +409,7 @@ SamplerArgs sampler_args(rhg_ctx* ctx, const Plan& pl, const Tables& t) {
 
 // Cell index + every edge kernel + counters back to the host.
 void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out, std::uint32_t* degrees,
-               bool gen, std::uint64_t* launches) {
+               bool gen, bool split_wave, std::uint64_t* launches) {
     const std::uint32_t K         = pl.L.count;
     const std::size_t   o_dmax    = align256(3 * sizeof(Counters));
     const std::size_t   o_hmax    = o_dmax + align256(K * sizeof(unsigned long long));
@@ -470,7 +489,6 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     e.lift_part   = pl.e1 == pl.L.chunks && pl.T > 0;
     e.slab_tab = t.slab_tab, e.n_slabs = pl.n_slabs, e.src_mask = t.src_mask, e.hbound = t.hbound;
     e.tail_prefix = t.tail_prefix, e.tail_lam = t.tail_lam, e.n_tail = pl.n_tail;
-    e.ev_pairs0 = ctx->ev[4], e.ev_pairs1 = ctx->ev[5];
     e.gg_tile_begin = pl.gg_t0, e.gg_tile_end = pl.gg_t1;
     e.degrees       = degrees ? ctx->degrees.as<unsigned>() : nullptr;
     if (const char* ab = std::getenv("RHG_ABLATE")) e.ablate = std::atoi(ab);
@@ -483,17 +501,36 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     }
     e.ann_blk = t.ann_blk;
     e.gen = gen ? 1 : 0;
-    launch_cell_index(e, pl.ann_blk[pl.L.count], gen, ctx->stream, launches);
-    // dense chain on the side stream, concurrent with the sparse pairs
-    CK(cudaEventRecord(ctx->fork, ctx->stream));
-    CK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
-    if (pl.n_req && pl.L.first_streaming < pl.L.count) { // dense-engine requests in (source, class, angle) order
+    // Two waves when the sampler split its chains (generate mode): wave 1 = every annulus below
+    // pl.wave_j (sort phase, dense prep, rows / node tiles / slabs of those targets, the global
+    // unit) overlaps the outermost annulus's chains on ctx->late; wave 2 = the outermost annulus
+    // after ev_late, then the tail pairs, the deferred ranges and the counter fold.
+    const std::uint32_t fs = pl.L.first_streaming;
+    const bool          split = split_wave && pl.wave_j < K;
+    const std::uint32_t jw    = split ? pl.wave_j : K;
+    launch_cell_index(e, pl.ann_blk[fs], pl.ann_blk[jw], int(fs), int(jw), gen, ctx->stream, launches);
+    if (pl.n_req && fs < K) { // dense-engine requests in (source, class, angle) order
         std::size_t need = 0;
-        launch_sort_globals(e, nullptr, 0, &need, ctx->side, launches);
+        launch_sort_globals(e, nullptr, 0, &need, ctx->stream, launches);
         ctx->gsort.ensure(need);
-        launch_sort_globals(e, ctx->gsort.p, ctx->gsort.cap, &need, ctx->side, launches);
+        launch_sort_globals(e, ctx->gsort.p, ctx->gsort.cap, &need, ctx->stream, launches);
     }
-    launch_edges(e, ctx->stream, ctx->side, ctx->join, launches);
+    EdgeWave w1;
+    w1.j0 = int(fs), w1.j1 = int(jw), w1.tile_warps = pl.gt_prefix[jw] - pl.gt_prefix[fs];
+    w1.slab_begin = 0, w1.slab_end = split ? pl.n_slabs1 : pl.n_slabs;
+    w1.global_unit = true, w1.tail = !split, w1.finish = !split;
+    w1.ev0 = ctx->evw[0], w1.ev1 = ctx->evw[1];
+    launch_edges(e, w1, ctx->stream, launches);
+    if (split) {
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_late, 0));
+        launch_cell_index(e, pl.ann_blk[jw], pl.ann_blk[K], int(jw), int(K), gen, ctx->stream, launches);
+        EdgeWave w2;
+        w2.j0 = int(jw), w2.j1 = int(K), w2.tile_warps = pl.gt_prefix[K] - pl.gt_prefix[jw];
+        w2.slab_begin = pl.n_slabs1, w2.slab_end = pl.n_slabs;
+        w2.tail = true, w2.finish = true;
+        w2.ev0 = ctx->evw[2], w2.ev1 = ctx->evw[3];
+        launch_edges(e, w2, ctx->stream, launches);
+    }
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[2], ctx->stream));
     ctx->staging.ensure(4096);
@@ -523,7 +560,10 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     out->global_comps = hc[2].comps;
     out->stream_comps = hc[0].comps;
     out->dense_comps  = hc[1].comps;
-    out->pairs_ms     = pl.n_slabs ? ms_between(ctx->ev[4], ctx->ev[5]) : 0.0;
+    out->pairs_ms     = 0.0; // sparse engine (slab join + tail), both waves
+    const bool split_used = split_wave && pl.wave_j < pl.L.count;
+    if (pl.n_slabs1 || !split_used) out->pairs_ms += (split_used ? pl.n_slabs1 : pl.n_slabs) ? ms_between(ctx->evw[0], ctx->evw[1]) : 0.0;
+    if (split_used && pl.n_slabs > pl.n_slabs1) out->pairs_ms += ms_between(ctx->evw[2], ctx->evw[3]);
     out->d2h_bytes += 3 * sizeof(Counters) + (degrees ? pl.L.n * sizeof(unsigned) : 0);
 }
 
@@ -588,6 +628,10 @@ int rhg_create(int device, rhg_ctx** out) {
         c->device = device;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->late, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_pow, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_late, cudaEventDisableTiming));
+        for (auto& e: c->evw) CK(cudaEventCreate(&e));
         for (auto& e: c->ev) CK(cudaEventCreate(&e));
         CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
@@ -609,6 +653,11 @@ void rhg_destroy(rhg_ctx* c) {
     cudaEventDestroy(c->fork);
     cudaEventDestroy(c->join);
     cudaStreamDestroy(c->side);
+    cudaStreamSynchronize(c->late);
+    cudaStreamDestroy(c->late);
+    cudaEventDestroy(c->ev_pow);
+    cudaEventDestroy(c->ev_late);
+    for (auto& e: c->evw) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -629,9 +678,12 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         SamplerArgs sa  = sampler_args(ctx, pl, t);
         sa.angular_from = pl.n_ext; // streaming frames are built while scattering (sort phase)
+        const char* ns    = std::getenv("RHG_NO_WAVES"); // A/B switch for timing experiments
+        const bool  split = pl.wave_j < pl.L.count && !(ns && ns[0] == '1');
+        if (split) sa.wave2_jobs = pl.wave2_jobs, sa.late = ctx->late, sa.ev_pow = ctx->ev_pow, sa.ev_late = ctx->ev_late;
         launch_sampler(sa, ctx->stream, &launches);
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
-        run_edges(ctx, pl, t, out, degrees, true, &launches);
+        run_edges(ctx, pl, t, out, degrees, true, split, &launches);
         fill_common(pl, out);
         out->sample_ms       = ms_between(ctx->ev[0], ctx->ev[1]);
         out->edges_ms        = ms_between(ctx->ev[1], ctx->ev[2]);
@@ -747,7 +799,7 @@ int rhg_count_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rh
         CK(cudaEventRecord(ctx->ev[0], st));
         launch_frames_from_points(sampler_args(ctx, pl, t), st, &launches);
         CK(cudaEventRecord(ctx->ev[1], st));
-        run_edges(ctx, pl, t, out, degrees, false, &launches);
+        run_edges(ctx, pl, t, out, degrees, false, false, &launches);
         fill_common(pl, out);
         out->sample_ms       = ms_between(ctx->ev[0], ctx->ev[1]);
         out->edges_ms        = ms_between(ctx->ev[1], ctx->ev[2]);

@@ -81,7 +81,7 @@ __device__ __forceinline__ std::uint32_t cellf(const AnnulusDev& A, double x) {
 // (prefix table A.ann_blk), so every block knows its annulus without a search
 // per thread.  Returns the annulus of this block and sets i (maybe >= end).
 __device__ __forceinline__ int block_annulus(const EdgeArgs& A, std::uint64_t& i) {
-    const std::uint32_t b  = blockIdx.x;
+    const std::uint32_t b  = A.blk0 + blockIdx.x; // waves launch a sub-range of the blocks
     int                 lo = A.first_streaming, hi = A.count - 1; // last annulus with ann_blk <= b
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -124,7 +124,7 @@ __device__ __forceinline__ double frame_lambda(const EdgeArgs& A, const AnnulusD
 template <bool GEN>
 __global__ void __launch_bounds__(256) beta_cells_kernel(EdgeArgs A) {
     const int lane = threadIdx.x & 31;
-    if (blockIdx.x == 0 && int(threadIdx.x) < A.count && int(threadIdx.x) >= A.first_streaming) {
+    if (blockIdx.x == 0 && A.blk0 == 0 && int(threadIdx.x) < A.count && int(threadIdx.x) >= A.first_streaming) {
         const AnnulusDev& E = A.ann[threadIdx.x]; // empty blocks: [off, off]
         if (E.end == E.off)
             for (std::uint32_t k = 0; k <= E.ncells; ++k) A.cellstart[E.cell_off + k] = E.off;
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(256) lambda_cells_kernel(EdgeArgs A) {
 // Tails of both cell tables: cells after the last point of a block hold the
 // block end (beta table: whole annulus array; lambda table: owned block).
 __global__ void cell_tail_kernel(EdgeArgs A, int lambda) {
-    const int           j = A.first_streaming + int(blockIdx.y);
+    const int           j = A.j0 + int(blockIdx.y);
     const AnnulusDev&   J = A.ann[j];
     const std::uint64_t e = lambda ? J.halo : J.end;
     if (e == J.off) return; // empty: initialised by beta_cells_kernel
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kSlabThreads, 4) slab_kernel(EdgeArgs A) {
     extern __shared__ __align__(16) unsigned char slab_raw[];
     SlabSmem&                S    = *reinterpret_cast<SlabSmem*>(slab_raw);
     const int                lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned long long sl   = A.slab_tab[blockIdx.x]; // (j << 32) | slab index in j (angle-interleaved order)
+    const unsigned long long sl   = A.slab_tab[A.slab0 + blockIdx.x]; // (j << 32) | slab index in j, angle order per wave
     const int                j    = int(sl >> 32);
     const AnnulusDev&        Aj   = A.ann[j];
     const std::uint64_t      N0   = Aj.off + (sl & 0xffffffffull) * kSlab;
@@ -803,16 +803,17 @@ __global__ void __launch_bounds__(256) deferred_kernel(EdgeArgs A) {
 template <bool DEG>
 __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
     const std::uint64_t nR  = A.n_req;
-    const int           nst = A.count - A.first_streaming;
+    const int           nst = A.j1 - A.j0; // targets of this wave
     const std::uint64_t idx = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool          ok  = idx < nR * std::uint64_t(nst);
     Acc                 acc;
     int                 hkey  = -1;
     unsigned long long  hbits = 0;
     if (ok) {
-        const int           jt = int(idx / nR);
-        const std::uint64_t s  = idx - std::uint64_t(jt) * nR;
-        const int           j  = A.first_streaming + jt;
+        const int           jw = int(idx / nR);
+        const std::uint64_t s  = idx - std::uint64_t(jw) * nR;
+        const int           j  = A.j0 + jw;
+        const int           jt = j - A.first_streaming;
         const std::uint32_t u  = A.g_u[s];
         const AnnulusDev&   Aj = A.ann[j];
         std::uint32_t       pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -960,8 +961,8 @@ template <bool DEG>
 __global__ void __launch_bounds__(256, 2) glob_tiles_kernel(EdgeArgs A) {
     __shared__ GWarp    smem[8];
     const int           lane = threadIdx.x & 31;
-    const std::uint64_t w    = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (w >= A.gt_prefix[A.count]) return;
+    const std::uint64_t w    = A.gt_prefix[A.j0] + ((std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    if (w >= A.gt_prefix[A.j1]) return;
     GWarp* ws = &smem[threadIdx.x >> 5];
     int    j  = A.first_streaming, hj = A.count - 1; // last annulus with gt_prefix <= w
     while (j < hj) {
@@ -1198,10 +1199,14 @@ __global__ void __launch_bounds__(1024) reduce_counters_kernel(EdgeArgs A) {
 
 } // namespace
 
-void launch_cell_index(const EdgeArgs& a, std::uint64_t nblocks, bool gen, cudaStream_t st, std::uint64_t* launches) {
-    if (a.first_streaming >= a.count) return;
-    const unsigned g = unsigned(nblocks ? nblocks : 1); // >= 1: block 0 also initialises empty annuli
-    const dim3     tails(64, unsigned(a.count - a.first_streaming));
+void launch_cell_index(const EdgeArgs& a0, std::uint32_t blk_begin, std::uint32_t blk_end, int j_begin, int j_end,
+                       bool gen, cudaStream_t st, std::uint64_t* launches) {
+    if (a0.first_streaming >= a0.count || j_end <= j_begin) return;
+    EdgeArgs a = a0;
+    a.blk0 = blk_begin, a.j0 = j_begin, a.j1 = j_end;
+    const std::uint32_t nblocks = blk_end - blk_begin;
+    const unsigned      g = unsigned(nblocks ? nblocks : 1); // >= 1: block 0 of wave 1 initialises empty annuli
+    const dim3          tails(64, unsigned(j_end - j_begin));
     if (gen) beta_cells_kernel<true><<<g, 256, 0, st>>>(a);
     else beta_cells_kernel<false><<<g, 256, 0, st>>>(a);
     cell_tail_kernel<<<tails, 256, 0, st>>>(a, 0);
@@ -1250,13 +1255,28 @@ void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, 
     *launches += 6;
 }
 
-// Sparse pairs (slab join + tail) on st; the dense chain (rows, node tiles,
-// global unit) on side, concurrently (both are latency-bound at modest
-// occupancy); side joins st before the counters are folded.  The dense
-// requests must already be sorted on side (launch_sort_globals).
-void launch_edges(const EdgeArgs& a, cudaStream_t st, cudaStream_t side, cudaEvent_t join, std::uint64_t* launches) {
-    const bool deg = a.degrees != nullptr;
-    if (a.n_slabs) {
+// One wave of edge work on st: dense rows and node tiles of the targets
+// [W.j0, W.j1), the slab join over slabs [W.slab_begin, W.slab_end), and
+// optionally the global unit, the tail pairs, the deferred ranges and the
+// final counter fold.  The dense requests must already be sorted
+// (launch_sort_globals) and the targets' annuli indexed (launch_cell_index).
+void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::uint64_t* launches) {
+    const bool deg = a0.degrees != nullptr;
+    EdgeArgs   a   = a0;
+    a.j0 = W.j0, a.j1 = W.j1, a.slab0 = W.slab_begin;
+    if (W.j1 > W.j0 && a.n_req && a.first_streaming < a.count) {
+        const std::uint64_t rows = a.n_req * std::uint64_t(W.j1 - W.j0);
+        if (deg) req_rows_kernel<true><<<unsigned((rows + 255) / 256), 256, 0, st>>>(a);
+        else req_rows_kernel<false><<<unsigned((rows + 255) / 256), 256, 0, st>>>(a);
+        ++*launches;
+        const std::uint64_t tw = W.tile_warps;
+        if (tw) {
+            if (deg) glob_tiles_kernel<true><<<unsigned((tw + 7) / 8), 256, 0, st>>>(a);
+            else glob_tiles_kernel<false><<<unsigned((tw + 7) / 8), 256, 0, st>>>(a);
+            ++*launches;
+        }
+    }
+    if (W.slab_end > W.slab_begin) {
         const int   smem = int(sizeof(SlabSmem));
         static bool attr = false;
         if (!attr) {
@@ -1264,45 +1284,38 @@ void launch_edges(const EdgeArgs& a, cudaStream_t st, cudaStream_t side, cudaEve
             cudaFuncSetAttribute(slab_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             attr = true;
         }
-        if (a.ev_pairs0) cudaEventRecord(a.ev_pairs0, st);
-        if (deg) slab_kernel<true><<<unsigned(a.n_slabs), kSlabThreads, smem, st>>>(a);
-        else slab_kernel<false><<<unsigned(a.n_slabs), kSlabThreads, smem, st>>>(a);
+        if (W.ev0) cudaEventRecord(W.ev0, st);
+        const unsigned n = unsigned(W.slab_end - W.slab_begin);
+        if (deg) slab_kernel<true><<<n, kSlabThreads, smem, st>>>(a);
+        else slab_kernel<false><<<n, kSlabThreads, smem, st>>>(a);
         ++*launches;
-    }
-    if (a.n_tail) {
+        if (W.tail && a.n_tail) {
+            if (deg) tail_kernel<true><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
+            else tail_kernel<false><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
+            ++*launches;
+        }
+        if (W.ev1) cudaEventRecord(W.ev1, st); // sparse engine of this wave (slab join [+ tail])
+    } else if (W.tail && a.n_tail) {
         if (deg) tail_kernel<true><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
         else tail_kernel<false><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
         ++*launches;
     }
-    if (a.n_slabs && a.ev_pairs1) cudaEventRecord(a.ev_pairs1, st); // sparse engine: slab join + tail
-    if (a.n_req && a.first_streaming < a.count) {
-        const std::uint64_t rows = a.n_req * std::uint64_t(a.count - a.first_streaming);
-        if (deg) req_rows_kernel<true><<<unsigned((rows + 255) / 256), 256, 0, side>>>(a);
-        else req_rows_kernel<false><<<unsigned((rows + 255) / 256), 256, 0, side>>>(a);
-        ++*launches;
-        if (a.glob_tile_warps) {
-            const unsigned blocks = unsigned((a.glob_tile_warps + 7) / 8);
-            if (deg) glob_tiles_kernel<true><<<blocks, 256, 0, side>>>(a);
-            else glob_tiles_kernel<false><<<blocks, 256, 0, side>>>(a);
-            ++*launches;
-        }
-        if (deg) deferred_kernel<true><<<148 * 4, 256, 0, side>>>(a);
-        else deferred_kernel<false><<<148 * 4, 256, 0, side>>>(a);
-        ++*launches;
-    }
-    if (a.gg_tile_end > a.gg_tile_begin) {
+    if (W.global_unit && a.gg_tile_end > a.gg_tile_begin) {
         const std::uint64_t nT     = (a.n_glob + kGGTile - 1) / kGGTile;
         const unsigned      blocks = unsigned(a.gg_tile_end - a.gg_tile_begin);
-        if (deg) glob_pairs_kernel<true><<<blocks, kGGTile, 0, side>>>(a, nT);
-        else glob_pairs_kernel<false><<<blocks, kGGTile, 0, side>>>(a, nT);
+        if (deg) glob_pairs_kernel<true><<<blocks, kGGTile, 0, st>>>(a, nT);
+        else glob_pairs_kernel<false><<<blocks, kGGTile, 0, st>>>(a, nT);
         ++*launches;
     }
-    if (side != st) {
-        cudaEventRecord(join, side);
-        cudaStreamWaitEvent(st, join, 0);
+    if (W.finish) {
+        if (a.n_req) {
+            if (deg) deferred_kernel<true><<<148 * 4, 256, 0, st>>>(a);
+            else deferred_kernel<false><<<148 * 4, 256, 0, st>>>(a);
+            ++*launches;
+        }
+        reduce_counters_kernel<<<3, 1024, 0, st>>>(a);
+        ++*launches;
     }
-    reduce_counters_kernel<<<3, 1024, 0, st>>>(a);
-    ++*launches;
 }
 
 } // namespace rhgb

@@ -25,6 +25,9 @@ struct SamplerArgs {
     std::uint64_t     angular_from = 0; // point_angular_kernel runs on [angular_from, total) (generate mode: n_ext)
     cudaStream_t      side = nullptr;                // optional second stream (fork/join with events)
     cudaEvent_t       ev_fork = nullptr, ev_join = nullptr;
+    int               wave2_jobs = 0;     // the last wave2_jobs entries of job_order chain on `late`
+    cudaStream_t      late = nullptr;
+    cudaEvent_t       ev_pow = nullptr, ev_late = nullptr; // pow done (main) / wave-2 chains done (late)
 };
 
 void launch_sampler(const SamplerArgs& a, cudaStream_t st, std::uint64_t* launches);
@@ -84,6 +87,11 @@ struct EdgeArgs {
     double            chunk0_upper = 0.0; // chunk_upper_bound(0, P)
     int               lift_part = 0;      // shard owns engine P-1 (halo = lifted chunk 0)
     int               gen = 0;            // generate mode (see launch_cell_index)
+    // wave parameters (set by the launch functions): sort-phase block offset, target annuli
+    // [j0, j1) (cell tails, rows, node tiles), first slab of the wave
+    std::uint32_t     blk0 = 0;
+    int               j0 = 0, j1 = 0;
+    std::uint64_t     slab0 = 0;
     // slab join (sparse pairs): slabs of 1024 owned nodes of every target annulus with sparse sources
     const unsigned long long* slab_tab = nullptr; // [n_slabs] (j << 32) | slab index in j, angle-interleaved order
     std::uint64_t     n_slabs = 0;
@@ -103,8 +111,16 @@ struct EdgeArgs {
 
 // gen: the beta array holds the sampler's unlifted beta and no frames yet (rank from beta + hw, the
 // frames are computed while scattering); otherwise frames_from_points already built beta/rec0/rec1.
-void launch_cell_index(const EdgeArgs& a, std::uint64_t nblocks, bool gen, cudaStream_t st, std::uint64_t* launches);
-void launch_edges(const EdgeArgs& a, cudaStream_t st, cudaStream_t side, cudaEvent_t join, std::uint64_t* launches);
+void launch_cell_index(const EdgeArgs& a, std::uint32_t blk_begin, std::uint32_t blk_end, int j_begin, int j_end,
+                       bool gen, cudaStream_t st, std::uint64_t* launches);
+struct EdgeWave {
+    int           j0 = 0, j1 = 0;                 // target annuli of the dense rows / node tiles
+    std::uint64_t tile_warps = 0;                 // gt_prefix[j1] - gt_prefix[j0]
+    std::uint64_t slab_begin = 0, slab_end = 0;   // slab-join CTAs (slab_tab range)
+    bool          global_unit = false, tail = false, finish = false;
+    cudaEvent_t   ev0 = nullptr, ev1 = nullptr;   // optional: time the wave's sparse engine
+};
+void launch_edges(const EdgeArgs& a, const EdgeWave& w, cudaStream_t st, std::uint64_t* launches);
 // Sorts the global points by (annulus, theta) into a.gperm (scratch layout
 // internal); with scratch == nullptr only reports the bytes needed in *need.
 void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, std::size_t* need, cudaStream_t st,

@@ -290,7 +290,18 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
     point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
     mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 1);
     point_pow_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.total, S.beta);
-    sorted_chain_kernel<<<(S.njobs + 3) / 4, 128, 0, st>>>(S.jobs, S.njobs, S.job_order, S.beta);
+    // chains: wave 1 on st; wave 2 (the outermost annulus, the longest chains) on S.late,
+    // signalling S.ev_late, so the inner annuli's edge work overlaps its tail
+    const int n1 = S.njobs - S.wave2_jobs;
+    if (S.wave2_jobs && S.late) {
+        cudaEventRecord(S.ev_pow, st);
+        cudaStreamWaitEvent(S.late, S.ev_pow, 0);
+        sorted_chain_kernel<<<(S.wave2_jobs + 3) / 4, 128, 0, S.late>>>(S.jobs, S.wave2_jobs, S.job_order + n1, S.beta);
+        cudaEventRecord(S.ev_late, S.late);
+        ++*launches;
+    }
+    if (n1) sorted_chain_kernel<<<(n1 + 3) / 4, 128, 0, st>>>(S.jobs, S.wave2_jobs && S.late ? n1 : S.njobs,
+                                                             S.job_order, S.beta);
     if (S.side) {
         cudaEventRecord(S.ev_join, side);
         cudaStreamWaitEvent(st, S.ev_join, 0);
