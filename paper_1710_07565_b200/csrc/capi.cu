@@ -110,12 +110,43 @@ struct rhg_ctx {
     cudaEvent_t  fork = nullptr, join = nullptr; // timing-free events for the side stream
     cudaEvent_t  ev_pow = nullptr, ev_late = nullptr; // the wave-2 chains (late stream)
     cudaEvent_t  evw[4]{};                            // sparse-engine timing of the two edge waves
+    std::vector<std::pair<std::string, cudaEvent_t>> tl; // RHG_TIMELINE marks of the current call
+    std::vector<cudaEvent_t> tl_pool;
     DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, cells, counters, degrees, dbg, nid;
     DevBuf       lcells, perm, s_beta, s_hw, s_lt, s_rec1, s_rec2, gsort, gbuf;
     HostPinned   staging;
 };
 
 namespace {
+
+void timeline_mark(void* self, const char* name, cudaStream_t st) {
+    auto* c = static_cast<rhg_ctx*>(self);
+    if (c->tl.size() >= c->tl_pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        c->tl_pool.push_back(e);
+    }
+    cudaEvent_t e = c->tl_pool[c->tl.size()];
+    cudaEventRecord(e, st);
+    c->tl.push_back({name, e});
+}
+Timeline timeline_of(rhg_ctx* c) {
+    Timeline t;
+    const char* v = std::getenv("RHG_TIMELINE");
+    if (v && v[0] == '1') t.fn = timeline_mark, t.self = c;
+    return t;
+}
+void timeline_report(rhg_ctx* c, cudaEvent_t start) {
+    if (c->tl.empty()) return;
+    std::fprintf(stderr, "RHG_TIMELINE");
+    for (auto& m: c->tl) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, start, m.second);
+        std::fprintf(stderr, " %s=%.3f", m.first.c_str(), ms);
+    }
+    std::fprintf(stderr, "\n");
+    c->tl.clear();
+}
 
 // The shard plan: which (annulus, chunk) streams this rank draws, where they
 // land in the extended arrays, and the pair-kernel work lists.
@@ -404,6 +435,7 @@ SamplerArgs sampler_args(rhg_ctx* ctx, const Plan& pl, const Tables& t) {
     s.beta = ctx->beta.as<double>(), s.hw = ctx->hw.as<double>();
     s.rec0 = ctx->rec0.as<double2>(), s.rec1 = ctx->rec1.as<double2>(), s.rec2 = ctx->rec2.as<double2>();
     s.side = ctx->side, s.ev_fork = ctx->fork, s.ev_join = ctx->join;
+    s.mark = timeline_of(ctx);
     return s;
 }
 
@@ -501,6 +533,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     }
     e.ann_blk = t.ann_blk;
     e.gen = gen ? 1 : 0;
+    e.mark = timeline_of(ctx);
     // Two waves when the sampler split its chains (generate mode): wave 1 = every annulus below
     // pl.wave_j (sort phase, dense prep, rows / node tiles / slabs of those targets, the global
     // unit) overlaps the outermost annulus's chains on ctx->late; wave 2 = the outermost annulus
@@ -509,6 +542,11 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     const bool          split = split_wave && pl.wave_j < K;
     const std::uint32_t jw    = split ? pl.wave_j : K;
     launch_cell_index(e, pl.ann_blk[fs], pl.ann_blk[jw], int(fs), int(jw), gen, ctx->stream, launches);
+    if (split) { // wave 2's sort phase right after its chains, beside wave 1 (needs the radius side too)
+        CK(cudaStreamWaitEvent(ctx->late, ctx->join, 0));
+        launch_cell_index(e, pl.ann_blk[jw], pl.ann_blk[K], int(jw), int(K), gen, ctx->late, launches);
+        CK(cudaEventRecord(ctx->ev_late, ctx->late));
+    }
     if (pl.n_req && fs < K) { // dense-engine requests in (source, class, angle) order
         std::size_t need = 0;
         launch_sort_globals(e, nullptr, 0, &need, ctx->stream, launches);
@@ -523,7 +561,6 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     launch_edges(e, w1, ctx->stream, launches);
     if (split) {
         CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_late, 0));
-        launch_cell_index(e, pl.ann_blk[jw], pl.ann_blk[K], int(jw), int(K), gen, ctx->stream, launches);
         EdgeWave w2;
         w2.j0 = int(jw), w2.j1 = int(K), w2.tile_warps = pl.gt_prefix[K] - pl.gt_prefix[jw];
         w2.slab_begin = pl.n_slabs1, w2.slab_end = pl.n_slabs;
@@ -544,6 +581,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     if (degrees)
         CK(cudaMemcpyAsync(degrees, ctx->degrees.p, pl.L.n * sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    timeline_report(ctx, ctx->ev[0]);
     if (*h_ncls > kMaxCls) throw Invariant("dense engine: too many request segments");
     if (*h_drop) throw Invariant("dense engine: deferred-range list overflow");
     if (dbg) {
@@ -658,6 +696,7 @@ void rhg_destroy(rhg_ctx* c) {
     cudaEventDestroy(c->ev_pow);
     cudaEventDestroy(c->ev_late);
     for (auto& e: c->evw) cudaEventDestroy(e);
+    for (auto& e: c->tl_pool) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     delete c;
 }

@@ -1223,6 +1223,7 @@ void launch_cell_index(const EdgeArgs& a0, std::uint32_t blk_begin, std::uint32_
         cell_tail_kernel<<<tails, 256, 0, st>>>(a, 1);
         *launches += 4;
     }
+    a0.mark("sort_phase", st);
 }
 
 void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, std::size_t* need, cudaStream_t st,
@@ -1253,6 +1254,7 @@ void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, 
     a.gperm = perm;
     req_gather_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a);
     *launches += 6;
+    a.mark("dense_prep", st);
 }
 
 // One wave of edge work on st: dense rows and node tiles of the targets
@@ -1269,11 +1271,13 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         if (deg) req_rows_kernel<true><<<unsigned((rows + 255) / 256), 256, 0, st>>>(a);
         else req_rows_kernel<false><<<unsigned((rows + 255) / 256), 256, 0, st>>>(a);
         ++*launches;
+        a.mark("rows", st);
         const std::uint64_t tw = W.tile_warps;
         if (tw) {
             if (deg) glob_tiles_kernel<true><<<unsigned((tw + 7) / 8), 256, 0, st>>>(a);
             else glob_tiles_kernel<false><<<unsigned((tw + 7) / 8), 256, 0, st>>>(a);
             ++*launches;
+            a.mark("tiles", st);
         }
     }
     if (W.slab_end > W.slab_begin) {
@@ -1295,6 +1299,7 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
             ++*launches;
         }
         if (W.ev1) cudaEventRecord(W.ev1, st); // sparse engine of this wave (slab join [+ tail])
+        a.mark("slab(+tail)", st);
     } else if (W.tail && a.n_tail) {
         if (deg) tail_kernel<true><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
         else tail_kernel<false><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
@@ -1306,6 +1311,7 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         if (deg) glob_pairs_kernel<true><<<blocks, kGGTile, 0, st>>>(a, nT);
         else glob_pairs_kernel<false><<<blocks, kGGTile, 0, st>>>(a, nT);
         ++*launches;
+        a.mark("global_unit", st);
     }
     if (W.finish) {
         if (a.n_req) {

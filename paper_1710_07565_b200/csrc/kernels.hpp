@@ -8,6 +8,16 @@
 
 namespace rhgb {
 
+// Optional phase timeline (RHG_TIMELINE=1): launch code calls mark(...) at phase
+// boundaries; the context records an event on the given stream per mark.
+struct Timeline {
+    void (*fn)(void* self, const char* name, cudaStream_t st) = nullptr;
+    void* self = nullptr;
+    void  operator()(const char* name, cudaStream_t st) const {
+        if (fn) fn(self, name, st);
+    }
+};
+
 struct SamplerArgs {
     const StreamJob*  jobs = nullptr;
     int               njobs = 0;
@@ -25,6 +35,7 @@ struct SamplerArgs {
     std::uint64_t     angular_from = 0; // point_angular_kernel runs on [angular_from, total) (generate mode: n_ext)
     cudaStream_t      side = nullptr;                // optional second stream (fork/join with events)
     cudaEvent_t       ev_fork = nullptr, ev_join = nullptr;
+    Timeline          mark;
     int               wave2_jobs = 0;     // the last wave2_jobs entries of job_order chain on `late`
     cudaStream_t      late = nullptr;
     cudaEvent_t       ev_pow = nullptr, ev_late = nullptr; // pow done (main) / wave-2 chains done (late)
@@ -87,6 +98,7 @@ struct EdgeArgs {
     double            chunk0_upper = 0.0; // chunk_upper_bound(0, P)
     int               lift_part = 0;      // shard owns engine P-1 (halo = lifted chunk 0)
     int               gen = 0;            // generate mode (see launch_cell_index)
+    Timeline          mark;
     // wave parameters (set by the launch functions): sort-phase block offset, target annuli
     // [j0, j1) (cell tails, rows, node tiles), first slab of the wave
     std::uint32_t     blk0 = 0;

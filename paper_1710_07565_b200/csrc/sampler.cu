@@ -287,9 +287,13 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
         cudaStreamWaitEvent(side, S.ev_fork, 0);
     }
     mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, side>>>(S.jobs, S.njobs, S.beta, S.hw, 2);
+    S.mark("mt_radii", side);
     point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
+    S.mark("radial", side);
     mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 1);
+    S.mark("mt_angles", st);
     point_pow_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.total, S.beta);
+    S.mark("pow", st);
     // chains: wave 1 on st; wave 2 (the outermost annulus, the longest chains) on S.late,
     // signalling S.ev_late, so the inner annuli's edge work overlaps its tail
     const int n1 = S.njobs - S.wave2_jobs;
@@ -298,10 +302,12 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
         cudaStreamWaitEvent(S.late, S.ev_pow, 0);
         sorted_chain_kernel<<<(S.wave2_jobs + 3) / 4, 128, 0, S.late>>>(S.jobs, S.wave2_jobs, S.job_order + n1, S.beta);
         cudaEventRecord(S.ev_late, S.late);
+        S.mark("chain_wave2(late)", S.late);
         ++*launches;
     }
     if (n1) sorted_chain_kernel<<<(n1 + 3) / 4, 128, 0, st>>>(S.jobs, S.wave2_jobs && S.late ? n1 : S.njobs,
                                                              S.job_order, S.beta);
+    S.mark("chain_wave1", st);
     if (S.side) {
         cudaEventRecord(S.ev_join, side);
         cudaStreamWaitEvent(st, S.ev_join, 0);
