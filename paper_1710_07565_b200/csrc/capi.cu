@@ -542,7 +542,10 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     const bool          split = split_wave && pl.wave_j < K;
     const std::uint32_t jw    = split ? pl.wave_j : K;
     launch_cell_index(e, pl.ann_blk[fs], pl.ann_blk[jw], int(fs), int(jw), gen, ctx->stream, launches);
-    if (split) { // wave 2's sort phase right after its chains, beside wave 1 (needs the radius side too)
+    if (split) { // wave 2's sort phase right after its chains, beside wave 1 (needs the radius side
+                 // and this call's zeroed counters / dmax table from the main stream)
+        CK(cudaEventRecord(ctx->fork, ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->late, ctx->fork, 0));
         CK(cudaStreamWaitEvent(ctx->late, ctx->join, 0));
         launch_cell_index(e, pl.ann_blk[jw], pl.ann_blk[K], int(jw), int(K), gen, ctx->late, launches);
         CK(cudaEventRecord(ctx->ev_late, ctx->late));
