@@ -669,7 +669,9 @@ int rhg_create(int device, rhg_ctx** out) {
         c->device = device;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&c->late, cudaStreamNonBlocking));
+        int prio_lo = 0, prio_hi = 0; // the late stream (outermost annulus) gets block-scheduling priority
+        CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        CK(cudaStreamCreateWithPriority(&c->late, cudaStreamNonBlocking, prio_hi));
         CK(cudaEventCreateWithFlags(&c->ev_pow, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_late, cudaEventDisableTiming));
         for (auto& e: c->evw) CK(cudaEventCreate(&e));

@@ -286,14 +286,20 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
         cudaEventRecord(S.ev_fork, st);
         cudaStreamWaitEvent(side, S.ev_fork, 0);
     }
+    // the radius attributes are needed only by the sort phase: they run beside the (few-SM)
+    // chains, after pow, instead of competing with pow for the FP64 pipes
     mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, side>>>(S.jobs, S.njobs, S.beta, S.hw, 2);
     S.mark("mt_radii", side);
-    point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
-    S.mark("radial", side);
     mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 1);
     S.mark("mt_angles", st);
     point_pow_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.total, S.beta);
     S.mark("pow", st);
+    if (S.side) {
+        cudaEventRecord(S.ev_fork, st);
+        cudaStreamWaitEvent(side, S.ev_fork, 0);
+    }
+    point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
+    S.mark("radial", side);
     // chains: wave 1 on st; wave 2 (the outermost annulus, the longest chains) on S.late,
     // signalling S.ev_late, so the inner annuli's edge work overlaps its tail
     const int n1 = S.njobs - S.wave2_jobs;
