@@ -34,6 +34,8 @@
 //                       nodes held in registers x every global request whose
 //                       window can reach them (theta-sorted candidate ranges)
 //   glob_pairs_kernel   global unit, 128x128 tiles of the upper triangle
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 
 #include "device.cuh"
@@ -356,19 +358,19 @@ __device__ __forceinline__ void serial_range(const EdgeArgs& A, const SRow& q, d
 // after the request (index order == (theta, id) dedup order); everything
 // else - halo requests, halo nodes, wrapped points - runs in tail_kernel.
 constexpr int kSlab        = kSlabNodes;
-constexpr int kSlabThreads = 256;
 
 
 struct SlabWarp {
     SRow          rows[32]; // the warp's current requests (pad = local node of pair 0)
     std::uint32_t incl[32]; // inclusive prefix of the lanes' pair counts
 };
+template <int NT>
 struct SlabSmem {
     double             lam[kSlab];
     double2            r1[kSlab], r2[kSlab];
     unsigned long long id[kSlab];
     std::uint16_t      bstart[kSlab + 1]; // bucket b: first local node with bucket(lambda) >= b
-    SlabWarp           w[kSlabThreads / 32];
+    SlabWarp           w[NT / 32];
 };
 
 // Bucket of an angle inside the slab: monotone in x (fsub, fmul, clamp), so
@@ -379,7 +381,8 @@ __device__ __forceinline__ std::uint32_t slab_bucket(double x, double org, doubl
     if (t >= double(kSlab - 1)) return kSlab - 1;
     return std::uint32_t(t);
 }
-__device__ __forceinline__ std::uint32_t slab_lb(const SlabSmem& S, double x, double org, double inv_w) {
+template <class SM>
+__device__ __forceinline__ std::uint32_t slab_lb(const SM& S, double x, double org, double inv_w) {
     const std::uint32_t b = slab_bucket(x, org, inv_w);
     std::uint32_t       k = S.bstart[b];
     const std::uint32_t e = S.bstart[b + 1];
@@ -387,10 +390,11 @@ __device__ __forceinline__ std::uint32_t slab_lb(const SlabSmem& S, double x, do
     return k;
 }
 
-template <bool DEG>
-__global__ void __launch_bounds__(kSlabThreads, 4) slab_kernel(EdgeArgs A) {
+template <bool DEG, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
+    constexpr int kSlabThreads = NT;
     extern __shared__ __align__(16) unsigned char slab_raw[];
-    SlabSmem&                S    = *reinterpret_cast<SlabSmem*>(slab_raw);
+    SlabSmem<NT>&            S    = *reinterpret_cast<SlabSmem<NT>*>(slab_raw);
     const int                lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned long long sl   = A.slab_tab[A.slab0 + blockIdx.x]; // (j << 32) | slab index in j, angle order per wave
     const int                j    = int(sl >> 32);
@@ -506,7 +510,7 @@ __global__ void __launch_bounds__(kSlabThreads, 4) slab_kernel(EdgeArgs A) {
             // lane L runs the contiguous pairs [L c, (L + 1) c) of the warp's sequence: its
             // request stays in registers until the owner changes (rarely), only node records
             // come from shared memory
-            const std::uint32_t c  = (T + 31) >> 5;
+            const std::uint32_t c  = ((T + 31) >> 5) | 1u; // odd: lane starts fall in distinct smem banks
             std::uint32_t       t  = std::uint32_t(lane) * c;
             const std::uint32_t te = t + c < T ? t + c : T;
             if (t < te) {
@@ -1257,6 +1261,19 @@ void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, 
     a.mark("dense_prep", st);
 }
 
+template <int NT, int MINB>
+void launch_slab(const EdgeArgs& a, unsigned n, bool deg, cudaStream_t st) {
+    const int   smem = int(sizeof(SlabSmem<NT>));
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(slab_kernel<true, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(slab_kernel<false, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    if (deg) slab_kernel<true, NT, MINB><<<n, NT, smem, st>>>(a);
+    else slab_kernel<false, NT, MINB><<<n, NT, smem, st>>>(a);
+}
+
 // One wave of edge work on st: dense rows and node tiles of the targets
 // [W.j0, W.j1), the slab join over slabs [W.slab_begin, W.slab_end), and
 // optionally the global unit, the tail pairs, the deferred ranges and the
@@ -1281,17 +1298,9 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         }
     }
     if (W.slab_end > W.slab_begin) {
-        const int   smem = int(sizeof(SlabSmem));
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(slab_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            cudaFuncSetAttribute(slab_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            attr = true;
-        }
         if (W.ev0) cudaEventRecord(W.ev0, st);
-        const unsigned n = unsigned(W.slab_end - W.slab_begin);
-        if (deg) slab_kernel<true><<<n, kSlabThreads, smem, st>>>(a);
-        else slab_kernel<false><<<n, kSlabThreads, smem, st>>>(a);
+        const unsigned n   = unsigned(W.slab_end - W.slab_begin);
+        launch_slab<256, 4>(a, n, deg, st); // measured best of 128/256/512 threads x occupancy
         ++*launches;
         if (W.tail && a.n_tail) {
             if (deg) tail_kernel<true><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
