@@ -173,6 +173,7 @@ struct Plan {
     std::vector<double>        tail_lam;    // [count] owned requests with lambda >= this are tail requests
     std::uint64_t           n_ext = 0, n_glob = 0, total = 0, gtwarps = 0, ncells = 0, n_slabs = 0, n_tail = 0;
     std::uint64_t           gg_t0 = 0, gg_t1 = 0;
+    double                  layout_ms = 0;
 };
 
 // Expected number of annulus-j nodes in the window of an annulus-a request
@@ -204,8 +205,10 @@ double half_width_bound(const Layout& L, std::uint32_t a, std::uint32_t j) {
 }
 
 Plan make_plan(const Params& P, const rhg_shard* shard) {
-    Plan pl;
-    pl.L                  = make_layout(P);
+    Plan       pl;
+    const auto tl0 = std::chrono::steady_clock::now();
+    pl.L           = make_layout(P);
+    pl.layout_ms   = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count();
     const Layout&       L = pl.L;
     const std::uint32_t W = shard ? shard->world : 1, r = shard ? shard->rank : 0;
     if (W < 1 || r >= W) throw InvalidArgument("rhg_shard: rank must lie in [0, world)");
@@ -310,23 +313,27 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
         pl.slab_prefix[j + 1]   = pl.slab_prefix[j] + (own + kSlabNodes - 1) / kSlabNodes;
     }
     pl.n_slabs = pl.slab_prefix[K];
-    { // slabs in angular order across targets: requests are re-read from L2 by the next target's slab
-        std::vector<std::pair<double, unsigned long long>> order;
-        order.reserve(pl.n_slabs);
+    { // slabs in angular order across targets (requests are re-read from L2 by the next target's
+      // slab), wave-1 targets first: a counting sort on (wave, angle bucket) - the order only
+      // shapes cache locality
+        const std::uint64_t nb = std::max<std::uint64_t>(pl.n_slabs, 1);
+        std::vector<std::uint32_t> cnt(2 * nb + 1, 0);
+        auto key = [&](std::uint32_t j, std::uint64_t i, std::uint64_t ns) {
+            const std::uint64_t b = (2 * i + 1) * nb / (2 * ns); // bucket of the slab's mid angle
+            return (j >= pl.wave_j ? nb : 0) + std::min<std::uint64_t>(b, nb - 1);
+        };
+        for (std::uint32_t j = 0; j < K; ++j) {
+            const std::uint64_t ns = pl.slab_prefix[j + 1] - pl.slab_prefix[j];
+            for (std::uint64_t i = 0; i < ns; ++i) ++cnt[key(j, i, ns) + 1];
+        }
+        for (std::size_t b = 1; b < cnt.size(); ++b) cnt[b] += cnt[b - 1];
+        pl.n_slabs1 = cnt[nb];
+        pl.slab_tab.resize(pl.n_slabs);
         for (std::uint32_t j = 0; j < K; ++j) {
             const std::uint64_t ns = pl.slab_prefix[j + 1] - pl.slab_prefix[j];
             for (std::uint64_t i = 0; i < ns; ++i)
-                order.push_back({(double(i) + 0.5) / double(ns), (static_cast<unsigned long long>(j) << 32) | i});
+                pl.slab_tab[cnt[key(j, i, ns)]++] = (static_cast<unsigned long long>(j) << 32) | i;
         }
-        const auto wave = [&](unsigned long long v) { return (v >> 32) >= pl.wave_j ? 1 : 0; };
-        std::stable_sort(order.begin(), order.end(), [&](const auto& x, const auto& y) {
-            if (wave(x.second) != wave(y.second)) return wave(x.second) < wave(y.second);
-            return x.first < y.first;
-        });
-        pl.n_slabs1 = 0;
-        for (const auto& o: order) pl.n_slabs1 += wave(o.second) == 0;
-        pl.slab_tab.resize(order.size());
-        for (std::size_t i = 0; i < order.size(); ++i) pl.slab_tab[i] = order[i].second;
     }
     const double Bnd = chunk_lower_bound(pl.e1, Pc); // halo nodes and wrapped points have lambda >= Bnd
     for (std::uint32_t a = 0; a < K; ++a) {
@@ -715,10 +722,15 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
         CK(cudaSetDevice(ctx->device));
         const Params  P  = to_params(params);
         const Plan    pl = make_plan(P, shard);
+        const auto    t1 = Clock::now();
         std::uint64_t launches = 0;
         ensure_points(ctx, pl.total, false);
         const Tables t = upload_tables(ctx, pl, &out->h2d_bytes);
         const double host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+        if (const char* v = std::getenv("RHG_TIMELINE"); v && v[0] == '1')
+            std::fprintf(stderr, "RHG_HOST plan=%.3f ms (layout=%.3f) upload=%.3f ms\n",
+                         std::chrono::duration<double, std::milli>(t1 - t0).count(), pl.layout_ms,
+                         std::chrono::duration<double, std::milli>(Clock::now() - t1).count());
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         SamplerArgs sa  = sampler_args(ctx, pl, t);
         sa.angular_from = pl.n_ext; // streaming frames are built while scattering (sort phase)

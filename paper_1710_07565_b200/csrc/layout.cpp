@@ -5,6 +5,9 @@
 #include <atomic>
 #include <cmath>
 #include <exception>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
 
 namespace rhgb {
@@ -47,6 +50,78 @@ private:
     }
     std::uint64_t mt_[312];
     int           idx_ = 312;
+};
+
+// A persistent host worker pool for the layout's independent binomial trees
+// (spawning threads per call would cost more than the work at P ~ 64).
+class Pool {
+public:
+    static Pool& get() {
+        static Pool p;
+        return p;
+    }
+    unsigned size() const { return unsigned(workers_.size()) + 1; }
+    // body(k) for k < n on the pool and the calling thread; rethrows the first exception.
+    template <class F>
+    void run(std::uint32_t n, F&& body) {
+        std::lock_guard<std::mutex> serial(call_mu_); // one parallel region at a time
+        std::atomic<std::uint32_t>  next{0};
+        std::exception_ptr          err;
+        std::atomic<bool>           failed{false};
+        std::function<void()>       work = [&] {
+            try {
+                for (std::uint32_t k = next++; k < n && !failed; k = next++) body(k);
+            } catch (...) {
+                if (!failed.exchange(true)) err = std::current_exception();
+            }
+        };
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            job_ = &work, pending_ = unsigned(workers_.size()), ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> g(mu_);
+        done_.wait(g, [&] { return pending_ == 0; });
+        job_ = nullptr;
+        if (err) std::rethrow_exception(err);
+    }
+
+private:
+    Pool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        for (unsigned t = 1; t < std::min(hw, 16u); ++t) workers_.emplace_back([this] { loop(); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t: workers_) t.join();
+    }
+    void loop() {
+        std::uint64_t seen = 0;
+        for (;;) {
+            std::function<void()>* job;
+            {
+                std::unique_lock<std::mutex> g(mu_);
+                cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_, job = job_;
+            }
+            (*job)();
+            std::lock_guard<std::mutex> g(mu_);
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    std::vector<std::thread>  workers_;
+    std::mutex                mu_, call_mu_;
+    std::condition_variable   cv_, done_;
+    std::function<void()>*    job_     = nullptr;
+    unsigned                  pending_ = 0;
+    std::uint64_t             gen_     = 0;
+    bool                      stop_    = false;
 };
 
 double normal(Mt64& s) { // rng.hpp:75-79
@@ -228,32 +303,58 @@ Layout make_layout(const Params& p) {
         L.counts[L.count - 1] = remaining;
     }
     L.chunk_counts.assign(std::size_t(L.count) * p.chunks, 0);
-    // per-annulus binomial trees are independent (seeded by their own paths):
-    // spread them over host threads when there is enough work
+    // The per-annulus binomial trees are independent (every split node has its own seed path),
+    // and so are the subtrees below any node: the first levels are split here, and the
+    // subtrees run on host threads (the splits dominate the host time: ~1 us per MT seeding
+    // plus up to ~1000 inversion steps each).
     {
-        const unsigned hw      = std::max(1u, std::thread::hardware_concurrency());
-        const unsigned threads = p.chunks >= 256 ? std::min<unsigned>(hw, std::min<unsigned>(L.count, 16)) : 1;
-        std::atomic<std::uint32_t> next{0};
-        std::exception_ptr         err;
-        std::atomic<bool>          failed{false};
-        auto work = [&] {
-            try {
-                for (std::uint32_t i = next++; i < L.count && !failed; i = next++)
-                    split_chunk_range(p.seed, i, L.counts[i], 0, p.chunks, 1,
-                                      L.chunk_counts.data() + std::size_t(i) * p.chunks);
-            } catch (...) {
-                if (!failed.exchange(true)) err = std::current_exception();
+        struct Task {
+            std::uint32_t annulus, lo, hi;
+            std::uint64_t total, node;
+        };
+        const unsigned threads = p.chunks >= 16 ? Pool::get().size() : 1;
+        auto run = [&](std::uint32_t ntasks, auto&& body) { // body(k) for k < ntasks
+            if (threads <= 1 || ntasks <= 1) {
+                for (std::uint32_t k = 0; k < ntasks; ++k) body(k);
+            } else {
+                Pool::get().run(ntasks, body);
             }
         };
-        if (threads <= 1) {
-            work();
-        } else {
-            std::vector<std::thread> pool;
-            for (unsigned t = 1; t < threads; ++t) pool.emplace_back(work);
-            work();
-            for (auto& t: pool) t.join();
-        }
-        if (err) std::rethrow_exception(err);
+        // phase 1, one task per annulus: the top levels of its tree (up to 8 subtrees)
+        const int         levels = threads > 1 ? 3 : 0;
+        std::vector<Task> per(std::size_t(L.count) << levels);
+        std::vector<int>  nper(L.count, 0);
+        run(L.count, [&](std::uint32_t i) {
+            std::vector<Task> cur{{i, 0, p.chunks, L.counts[i], 1}};
+            for (int level = 0; level < levels; ++level) {
+                std::vector<Task> next;
+                for (const Task& t: cur) {
+                    if (t.hi - t.lo < 4) {
+                        next.push_back(t);
+                        continue;
+                    }
+                    const std::uint32_t mid = t.lo + (t.hi - t.lo + 1) / 2;
+                    const double        ml = double(mid - t.lo), mr = double(t.hi - mid);
+                    Mt64                s(derive_seed3(p.seed, kPhaseChunks, t.annulus, t.node));
+                    const std::uint64_t left = binomial(t.total, ml / (ml + mr), s); // rng.hpp:197-204
+                    next.push_back({t.annulus, t.lo, mid, left, 2 * t.node});
+                    next.push_back({t.annulus, mid, t.hi, t.total - left, 2 * t.node + 1});
+                }
+                cur.swap(next);
+            }
+            for (std::size_t k = 0; k < cur.size(); ++k) per[(std::size_t(i) << levels) + k] = cur[k];
+            nper[i] = int(cur.size());
+        });
+        std::vector<Task> tasks;
+        for (std::uint32_t i = 0; i < L.count; ++i)
+            for (int k = 0; k < nper[i]; ++k) tasks.push_back(per[(std::size_t(i) << levels) + k]);
+        std::sort(tasks.begin(), tasks.end(), [](const Task& x, const Task& y) { return x.total > y.total; });
+        // phase 2: the subtrees
+        run(std::uint32_t(tasks.size()), [&](std::uint32_t k) {
+            const Task& t = tasks[k];
+            split_chunk_range(p.seed, t.annulus, t.total, t.lo, t.hi, t.node,
+                              L.chunk_counts.data() + std::size_t(t.annulus) * p.chunks);
+        });
     }
 
     // classify, partition.hpp:195-217

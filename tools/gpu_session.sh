@@ -1,2 +1,3 @@
-timeout 600 python -m pytest tests -m gpu -x -q -k "same_points_parity_cfg2 or golden" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu.log
-for c in 0 1 2 3 4; do RHG_SLAB_CFG=$c timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "cfg=$c $(tail -1 gpurun_out/bench.log | python3 -c 'import sys,json; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["roofline"]["kernel_ms"])')"; done
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu.log
+RHG_TIMELINE=1 timeout 300 python tools/host_times.py cfg2 2>&1 | grep -E "RHG_HOST|wall" | tail -2
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench $(tail -1 gpurun_out/bench.log | python3 -c 'import sys,json; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["value"], d["e2e"]["value"], d["roofline"]["kernel_ms"])')"
