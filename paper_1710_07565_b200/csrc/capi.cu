@@ -155,7 +155,9 @@ struct Plan {
     std::uint32_t           e0 = 0, e1 = 0, T = 0;
     std::vector<AnnulusDev> ann;
     std::vector<StreamJob>  jobs;
-    std::vector<std::uint32_t> job_order;   // wave-1 jobs then wave-2 jobs, each by descending count
+    std::vector<std::uint32_t> job_order;   // wave-1 jobs then wave-2 jobs, grouped by chain bin
+    std::vector<std::uint32_t> chain_bins;  // bin b runs job_order[chain_bins[b], chain_bins[b + 1])
+    std::uint32_t              chain_bins1 = 0; // wave-1 bins (wave-2 bins follow)
     std::uint32_t              wave_j = 0;  // first annulus of wave 2 (count: no split)
     int                        wave2_jobs = 0;
     std::uint64_t              n_slabs1 = 0; // slabs of wave-1 targets (they come first in slab_tab)
@@ -295,6 +297,33 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
     });
     pl.wave2_jobs = 0;
     for (std::uint32_t k = 0; k < pl.jobs.size(); ++k) pl.wave2_jobs += in_wave2(k);
+    // chain bins: each wave's streams packed longest-processing-time-first into bins whose
+    // load stays near the wave's longest chain; one warp runs one bin's chains back to back,
+    // so few chain warps share an SM (their shared-memory traffic, not the DMUL latency,
+    // is what slows a chain that shares its SM with many others)
+    pl.chain_bins.assign(1, 0);
+    pl.chain_bins1 = 0;
+    for (int wv = 0; wv < 2; ++wv) {
+        const std::uint32_t j0 = wv ? std::uint32_t(pl.jobs.size() - pl.wave2_jobs) : 0;
+        const std::uint32_t j1 = wv ? std::uint32_t(pl.jobs.size()) : std::uint32_t(pl.jobs.size() - pl.wave2_jobs);
+        if (j1 <= j0) continue;
+        std::uint64_t sum = 0, mx = 0;
+        for (std::uint32_t k = j0; k < j1; ++k) sum += pl.jobs[pl.job_order[k]].count, mx = std::max(mx, pl.jobs[pl.job_order[k]].count);
+        const std::uint64_t nb = std::min<std::uint64_t>(j1 - j0, mx ? (sum + mx - 1) / mx + (sum + 7 * mx) / (8 * mx) : 1);
+        std::vector<std::uint64_t>              load(nb, 0);
+        std::vector<std::vector<std::uint32_t>> bin(nb);
+        for (std::uint32_t k = j0; k < j1; ++k) { // job_order is by descending count inside a wave
+            const std::size_t b = std::min_element(load.begin(), load.end()) - load.begin();
+            load[b] += pl.jobs[pl.job_order[k]].count + 64; // + per-stream overhead
+            bin[b].push_back(pl.job_order[k]);
+        }
+        std::uint32_t k = j0;
+        for (const auto& v: bin) {
+            for (std::uint32_t x: v) pl.job_order[k++] = x;
+            pl.chain_bins.push_back(k);
+        }
+        if (!wv) pl.chain_bins1 = std::uint32_t(nb);
+    }
     // slab join for the sparse pairs: slabs of every target annulus with sparse sources, the
     // half-width bounds that find a slab's requests, and the tail (wrap / halo) requests
     const std::uint32_t K = L.count;
@@ -377,6 +406,7 @@ struct Tables {
     std::uint64_t*      req_off;
     StreamJob*          jobs;
     std::uint32_t*      job_order;
+    std::uint32_t*      chain_bins;
     std::uint64_t*      gt_prefix;
     std::uint64_t*      gseg;
     std::uint32_t*      ann_blk;
@@ -403,7 +433,7 @@ Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr)
     const std::size_t i_ann = add(pl.ann), i_dm = add(pl.dense_mask), i_ro = add(pl.req_off), i_jobs = add(pl.jobs);
     const std::size_t i_gt = add(pl.gt_prefix), i_gs = add(pl.gseg), i_ab = add(pl.ann_blk), i_sm = add(pl.src_mask);
     const std::size_t i_hb = add(pl.hbound), i_sp = add(pl.slab_tab), i_tp = add(pl.tail_prefix);
-    const std::size_t i_tl = add(pl.tail_lam), i_jo = add(pl.job_order);
+    const std::size_t i_tl = add(pl.tail_lam), i_jo = add(pl.job_order), i_cb = add(pl.chain_bins);
     bytes += 256;
     ctx->staging.ensure(bytes);
     char* h = static_cast<char*>(ctx->staging.p);
@@ -416,7 +446,7 @@ Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr)
     auto  at = [&](std::size_t i) { return static_cast<void*>(d + parts[i].off); };
     return {static_cast<AnnulusDev*>(at(i_ann)),        static_cast<unsigned long long*>(at(i_dm)),
             static_cast<std::uint64_t*>(at(i_ro)),      static_cast<StreamJob*>(at(i_jobs)),
-            static_cast<std::uint32_t*>(at(i_jo)),
+            static_cast<std::uint32_t*>(at(i_jo)),      static_cast<std::uint32_t*>(at(i_cb)),
             static_cast<std::uint64_t*>(at(i_gt)),      static_cast<std::uint64_t*>(at(i_gs)),
             static_cast<std::uint32_t*>(at(i_ab)),      static_cast<unsigned long long*>(at(i_sm)),
             static_cast<double*>(at(i_hb)),             static_cast<unsigned long long*>(at(i_sp)),
@@ -438,6 +468,7 @@ void ensure_points(rhg_ctx* ctx, std::uint64_t total, bool with_export) {
 
 SamplerArgs sampler_args(rhg_ctx* ctx, const Plan& pl, const Tables& t) {
     SamplerArgs s;
+    s.chain_bins = t.chain_bins, s.chain_bins1 = int(pl.chain_bins1), s.chain_bins_total = int(pl.chain_bins.size()) - 1;
     s.jobs = t.jobs, s.job_order = t.job_order, s.njobs = int(pl.jobs.size()), s.ann = t.ann, s.alpha = pl.L.alpha, s.total = pl.total;
     s.beta = ctx->beta.as<double>(), s.hw = ctx->hw.as<double>();
     s.rec0 = ctx->rec0.as<double2>(), s.rec1 = ctx->rec1.as<double2>(), s.rec2 = ctx->rec2.as<double2>();

@@ -493,6 +493,14 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                 if (lane >= o) incl += x;
             }
             const std::uint32_t T = __shfl_sync(kFull, incl, 31);
+            if (A.dbg) { // slab-join path statistics (RHG_DEBUG_STATS=1)
+                const unsigned nv = __popc(__ballot_sync(kFull, valid)), nl = __popc(__ballot_sync(kFull, len > 0));
+                if (lane == 0) {
+                    atomicAdd(&A.dbg[10], 1ull), atomicAdd(&A.dbg[11], (unsigned long long)nv);
+                    atomicAdd(&A.dbg[12], (unsigned long long)nl), atomicAdd(&A.dbg[13], (unsigned long long)T);
+                    atomicAdd(&A.dbg[14], 32ull * (((T + 31) >> 5) | 1u)), atomicAdd(&A.dbg[own ? 15 : 16], 1ull);
+                }
+            }
             if (T == 0 || (A.ablate & 2)) { acc.comps += len; continue; }
             const std::uint32_t excl = incl - len;
             acc.comps += len;

@@ -21,7 +21,9 @@ struct Timeline {
 struct SamplerArgs {
     const StreamJob*  jobs = nullptr;
     int               njobs = 0;
-    const std::uint32_t* job_order = nullptr; // jobs by descending count (chain kernel schedule)
+    const std::uint32_t* job_order = nullptr; // jobs grouped by chain bin (chain kernel schedule)
+    const std::uint32_t* chain_bins = nullptr; // bin b = job_order[chain_bins[b], chain_bins[b + 1])
+    int                  chain_bins1 = 0, chain_bins_total = 0; // wave-1 bins come first
     const AnnulusDev* ann   = nullptr;
     double            alpha = 1.0;
     std::uint64_t     total = 0; // points (streaming extended arrays + global points)

@@ -17,6 +17,8 @@
 //                           engine-frame beta/lambda (sweep.hpp:135-139, 478-480).
 //
 // All exact-rounding steps use __dmul_rn/__dadd_rn (no FMA contraction).
+#include <cstdlib>
+
 #include "device.cuh"
 #include "kernels.hpp"
 
@@ -177,62 +179,85 @@ __global__ void point_radial_kernel(const StreamJob* __restrict__ jobs, int njob
     if (r_out) r_out[i] = r;
 }
 
-// rng.hpp:218-229.  One warp per stream: the 32 lanes stage the pow
-// factors (coalesced, next tile prefetched into registers), then every lane
-// runs the identical serial chain cur = fl(cur * x_k) over the tile — values
-// arrive by shuffle, so the loop-carried dependency is one DMUL per point —
-// and lane k%32 keeps beta_k for a coalesced store.
-__global__ void __launch_bounds__(128) sorted_chain_kernel(const StreamJob* __restrict__ jobs, int njobs,
-                                                           const std::uint32_t* __restrict__ order,
-                                                           double* __restrict__ x) {
-    const int lane = threadIdx.x & 31;
-    // warp w of CTA b runs the (b + w gridDim)-th longest stream: the first CTA on every SM
-    // leads with one of the longest chains (a chain is issue-bound when it shares its scheduler)
-    const int w = blockIdx.x + (threadIdx.x >> 5) * gridDim.x;
-    if (w >= njobs) return;
-    const StreamJob&    J = jobs[order[w]];
-    double*             p = x + J.out_off;
-    const std::uint64_t n = J.count;
-    const double        a = J.a, b = J.b, wd = fsub(b, a);
-    const double        bmax = nextafter(b, a);
-    constexpr int       kQ   = 8; // tile = 32 * kQ points
-    double              cur  = 1.0;
-    double              nxt[kQ];
+// rng.hpp:218-229.  One single-warp CTA per chain bin (the host packs the
+// streams into bins whose lengths add up to about the longest chain, so few
+// chain warps share an SM): for each stream of its bin the 32 lanes stage a
+// tile of pow factors into shared memory (coalesced, the next tile prefetched
+// into registers), lane 0 alone runs the serial chain cur = fl(cur * x_k)
+// over the tile from shared memory (vector loads two batches ahead in
+// ping-pong registers, so the loop-carried dependency is one DMUL per point
+// and no shuffles), and the warp maps the tile's products to
+// beta = a + w (1 - cur), clamped, with a coalesced store.  Past-the-end
+// factors are 1.0: fl(cur * 1.0) == cur.
+constexpr int kChainQ = 16;               // tile = 32 * kChainQ points
+constexpr int kChainT = 32 * kChainQ;
+__global__ void __launch_bounds__(32) sorted_chain_kernel(const StreamJob* __restrict__ jobs,
+                                                          const std::uint32_t* __restrict__ bins,
+                                                          const std::uint32_t* __restrict__ order,
+                                                          double* __restrict__ x) {
+    __shared__ __align__(16) double tile[kChainT];
+    const int lane = threadIdx.x;
+    for (std::uint32_t jb = bins[blockIdx.x]; jb < bins[blockIdx.x + 1]; ++jb) {
+        const StreamJob&    J = jobs[order[jb]];
+        double*             p = x + J.out_off;
+        const std::uint64_t n = J.count;
+        const double        a = J.a, b = J.b, wd = fsub(b, a);
+        const double        bmax = nextafter(b, a);
+        double              cur  = 1.0; // lane 0's chain state
+        double              nxt[kChainQ];
 #pragma unroll
-    for (int q = 0; q < kQ; ++q) {
-        const std::uint64_t k = std::uint64_t(lane) + 32u * q;
-        nxt[q]                = k < n ? p[k] : 1.0;
-    }
-    for (std::uint64_t base = 0; base < n; base += 32 * kQ) {
-        double v[kQ], out[kQ];
-#pragma unroll
-        for (int q = 0; q < kQ; ++q) v[q] = nxt[q];
-        const std::uint64_t nb = base + 32 * kQ;
-#pragma unroll
-        for (int q = 0; q < kQ; ++q) { // prefetch the next tile while the chain runs
-            const std::uint64_t k = nb + std::uint64_t(lane) + 32u * q;
+        for (int q = 0; q < kChainQ; ++q) {
+            const std::uint64_t k = std::uint64_t(lane) + 32u * q;
             nxt[q]                = k < n ? p[k] : 1.0;
         }
-        // past-the-end factors are 1.0: fl(cur * 1.0) == cur, so the tail
-        // needs no branch and the shuffles can all be hoisted.
+        for (std::uint64_t base = 0; base < n; base += kChainT) {
 #pragma unroll
-        for (int q = 0; q < kQ; ++q) {
-            double xs[32];
+            for (int q = 0; q < kChainQ; ++q) tile[lane + 32 * q] = nxt[q];
+            const std::uint64_t nb = base + kChainT;
 #pragma unroll
-            for (int L = 0; L < 32; ++L) xs[L] = __shfl_sync(0xffffffffu, v[q], L);
-            double mine = 1.0;
-#pragma unroll
-            for (int L = 0; L < 32; ++L) {
-                cur  = fmul(cur, xs[L]);
-                mine = lane == L ? cur : mine;
+            for (int q = 0; q < kChainQ; ++q) { // prefetch the next tile while the chain runs
+                const std::uint64_t k = nb + std::uint64_t(lane) + 32u * q;
+                nxt[q]                = k < n ? p[k] : 1.0;
             }
-            const double y = fadd(a, fmul(wd, fsub(1.0, mine)));
-            out[q]         = y >= b ? bmax : y;
-        }
+            __syncwarp();
+            if (lane == 0) {
+                const double2* t2 = reinterpret_cast<const double2*>(tile);
+                double2*       o2 = reinterpret_cast<double2*>(tile);
+                constexpr int  kB = 8; // double2 per batch (16 points); batches A, B alternate
+                double2        A[kB], B[kB];
 #pragma unroll
-        for (int q = 0; q < kQ; ++q) {
-            const std::uint64_t k = base + std::uint64_t(lane) + 32u * q;
-            if (k < n) p[k] = out[q];
+                for (int i = 0; i < kB; ++i) A[i] = t2[i];
+#pragma unroll 1
+                for (int bb = 0; bb < kChainT / 2; bb += 2 * kB) {
+#pragma unroll
+                    for (int i = 0; i < kB; ++i) B[i] = t2[bb + kB + i];
+#pragma unroll
+                    for (int i = 0; i < kB; ++i) {
+                        double2 o;
+                        cur = fmul(cur, A[i].x), o.x = cur;
+                        cur = fmul(cur, A[i].y), o.y = cur;
+                        o2[bb + i] = o;
+                    }
+                    const int na = bb + 2 * kB < kChainT / 2 ? bb + 2 * kB : 0;
+#pragma unroll
+                    for (int i = 0; i < kB; ++i) A[i] = t2[na + i];
+#pragma unroll
+                    for (int i = 0; i < kB; ++i) {
+                        double2 o;
+                        cur = fmul(cur, B[i].x), o.x = cur;
+                        cur = fmul(cur, B[i].y), o.y = cur;
+                        o2[bb + kB + i] = o;
+                    }
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < kChainQ; ++q) {
+                const std::uint64_t k = base + std::uint64_t(lane) + 32u * q;
+                const double        y = fadd(a, fmul(wd, fsub(1.0, tile[lane + 32 * q])));
+                if (k < n) p[k] = y >= b ? bmax : y;
+            }
+            __syncwarp();
         }
     }
 }
@@ -292,27 +317,39 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
     S.mark("mt_radii", side);
     mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 1);
     S.mark("mt_angles", st);
+    static const int sched = std::getenv("RHG_SCHED") ? std::atoi(std::getenv("RHG_SCHED")) : 0;
+    if (sched == 1) {
+        point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
+        S.mark("radial", side);
+    }
     point_pow_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.total, S.beta);
     S.mark("pow", st);
+    if (sched == 2) {
+        point_radial_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
+        S.mark("radial", st);
+    }
     if (S.side) {
         cudaEventRecord(S.ev_fork, st);
         cudaStreamWaitEvent(side, S.ev_fork, 0);
     }
-    point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
-    S.mark("radial", side);
+    if (sched == 0) {
+        point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
+        S.mark("radial", side);
+    }
     // chains: wave 1 on st; wave 2 (the outermost annulus, the longest chains) on S.late,
     // signalling S.ev_late, so the inner annuli's edge work overlaps its tail
-    const int n1 = S.njobs - S.wave2_jobs;
-    if (S.wave2_jobs && S.late) {
+    const bool split = S.wave2_jobs && S.late;
+    const int  nb1   = split ? S.chain_bins1 : S.chain_bins_total;
+    if (split && S.chain_bins_total > nb1) {
         cudaEventRecord(S.ev_pow, st);
         cudaStreamWaitEvent(S.late, S.ev_pow, 0);
-        sorted_chain_kernel<<<(S.wave2_jobs + 3) / 4, 128, 0, S.late>>>(S.jobs, S.wave2_jobs, S.job_order + n1, S.beta);
+        sorted_chain_kernel<<<S.chain_bins_total - nb1, 32, 0, S.late>>>(S.jobs, S.chain_bins + nb1, S.job_order,
+                                                                         S.beta);
         cudaEventRecord(S.ev_late, S.late);
         S.mark("chain_wave2(late)", S.late);
         ++*launches;
     }
-    if (n1) sorted_chain_kernel<<<(n1 + 3) / 4, 128, 0, st>>>(S.jobs, S.wave2_jobs && S.late ? n1 : S.njobs,
-                                                             S.job_order, S.beta);
+    if (nb1) sorted_chain_kernel<<<nb1, 32, 0, st>>>(S.jobs, S.chain_bins, S.job_order, S.beta);
     S.mark("chain_wave1", st);
     if (S.side) {
         cudaEventRecord(S.ev_join, side);
