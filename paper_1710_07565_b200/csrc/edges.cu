@@ -360,19 +360,6 @@ __device__ __forceinline__ void serial_range(const EdgeArgs& A, const SRow& q, d
 constexpr int kSlab        = kSlabNodes;
 
 
-struct SlabWarp {
-    SRow          rows[32]; // the warp's current requests (pad = local node of pair 0)
-    std::uint32_t incl[32]; // inclusive prefix of the lanes' pair counts
-};
-template <int NT>
-struct SlabSmem {
-    double             lam[kSlab];
-    double2            r1[kSlab], r2[kSlab];
-    unsigned long long id[kSlab];
-    std::uint16_t      bstart[kSlab + 1]; // bucket b: first local node with bucket(lambda) >= b
-    SlabWarp           w[NT / 32];
-};
-
 // Bucket of an angle inside the slab: monotone in x (fsub, fmul, clamp), so
 // lower_bound(x) lies in [bstart[b], bstart[b + 1]] for b = bucket(x).
 __device__ __forceinline__ std::uint32_t slab_bucket(double x, double org, double inv_w) {
@@ -390,6 +377,51 @@ __device__ __forceinline__ std::uint32_t slab_lb(const SM& S, double x, double o
     return k;
 }
 
+// FP32 pre-filter of the reference predicate (sweep.hpp:531-533), exact by
+// construction: with the stored doubles of request r and node n,
+//   D = lhs - rhs = (c_r c_n + s_r s_n) - coth_r coth_n + rci_r inv_n
+// is rewritten with three non-negative, well-conditioned terms
+//   P = rci_r inv_n,  Q = coth_r coth_n - 1 = m_r + m_n + m_r m_n  (m = coth - 1, exact in FP64),
+//   S = 1 - cos(theta_r - theta_n) = Delta^2 / 2 - Delta^4 / 24 + ...  (Delta = lambda_n - lambda_r),
+// D ~= P - (Q + S), evaluated in FP32 from float copies (lambda as offsets from
+// the slab's first node).  |D32 - D_ref| is bounded by
+//   * FP32 rounding of P, Q, S and their inputs        <= 1.1e-6 (P + Q + S)
+//   * the float offsets of lambda                      <= |Delta| ed + ed^2,   ed = 2^-24 (|off_r| + span) + 1.5e-15
+//   * the reference's own FP64 rounding (6 roundings)  <= 2.3e-16 (2 + P + Q)
+//   * the stored cos/sin vs cos(theta) (CUDA sincos, <= 2 ulp) and the 2pi wrap
+//     of theta (theta = lambda - 2pi_d)                <= 6.5e-16 + 1.4e-15 |Delta|
+// (Appendix of DESIGN.md); tau below covers the sum with a 25% margin.  Only when
+// |D32| > tau does the FP32 sign decide; otherwise (and for |Delta| > 2^-6, where
+// the truncated series is not used) the pair takes the exact FP64 predicate.
+constexpr float kPreMaxDelta = 0.015625f;
+
+struct __align__(16) SlabRow32 { // one request with pairs in the slab (rows of a group are compacted)
+    float         lamf;  // lambda_r - lam_first (float)
+    float         m;     // coth_r - 1
+    float         rcif;  // coshR / sinh r_r (the reference's rounded rci), float
+    float         e1;    // tau coefficient of |Delta|
+    float         c0;    // tau constant
+    std::uint32_t qoff;  // request id - id base of its source annulus's owned block
+    std::uint32_t pad;   // local node of pair t: pad + t (mod 2^32)
+    std::uint32_t incl;  // inclusive prefix of the rows' pair counts
+};
+struct __align__(16) SlabRow64 { // the same request for the exact predicate
+    double cs, sn, coth, rci;
+};
+template <int NT>
+struct SlabSmem {
+    float4             nd[kSlab];         // (lambda - lam_first, coth - 1, 1 / sinh, id offset bits)
+    double2            r1[kSlab], r2[kSlab];
+    double             lam[kSlab];
+    std::uint16_t      bstart[kSlab + 1]; // bucket b: first local node with bucket(lambda) >= b
+    SlabRow32          rows[NT / 32][32];
+    SlabRow64          rows64[NT / 32][32];
+    std::uint64_t      run_r0[64];        // compacted non-empty sources of the slab
+    std::uint32_t      run_g[65];         // group prefix over the compacted sources
+    std::uint8_t       run_a[64];
+    std::uint32_t      n_run;
+};
+
 template <bool DEG, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     constexpr int kSlabThreads = NT;
@@ -401,15 +433,21 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     const AnnulusDev&        Aj   = A.ann[j];
     const std::uint64_t      N0   = Aj.off + (sl & 0xffffffffull) * kSlab;
     const std::uint32_t      m    = std::uint32_t(Aj.halo - N0 < std::uint64_t(kSlab) ? Aj.halo - N0 : kSlab);
+    const std::uint64_t      base_j = Aj.off + std::uint64_t(Aj.dlt0); // owned ids of j: [base_j, base_j + n)
+    const double             lam_first = A.s_lam[N0];
     for (std::uint32_t i = threadIdx.x; i < m; i += kSlabThreads) {
-        S.lam[i] = A.s_lam[N0 + i];
+        const double  l  = A.s_lam[N0 + i];
+        const double2 r2 = A.s_rec2[N0 + i];
+        S.lam[i] = l;
         S.r1[i]  = A.s_rec1[N0 + i];
-        S.r2[i]  = A.s_rec2[N0 + i];
-        S.id[i]  = A.s_id[N0 + i];
+        S.r2[i]  = r2;
+        S.nd[i]  = make_float4(float(fsub(l, lam_first)), float(fsub(r2.x, 1.0)), float(r2.y),
+                               __uint_as_float(std::uint32_t(A.s_id[N0 + i] - base_j)));
     }
     __syncthreads();
-    const double lam_first = S.lam[0], lam_last = S.lam[m - 1];
-    const double inv_w     = lam_last > lam_first ? double(kSlab - 1) / (lam_last - lam_first) : 0.0;
+    const double lam_last = S.lam[m - 1];
+    const double inv_w    = lam_last > lam_first ? double(kSlab - 1) / (lam_last - lam_first) : 0.0;
+    const float  span     = float(fsub(lam_last, lam_first)) * 1.0001f;
     for (std::uint32_t i = threadIdx.x; i < m; i += kSlabThreads) { // bucket starts (cell_fill pattern)
         const std::uint32_t b  = slab_bucket(S.lam[i], lam_first, inv_w);
         const std::int32_t  bp = i ? std::int32_t(slab_bucket(S.lam[i - 1], lam_first, inv_w)) : -1;
@@ -417,15 +455,13 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
         if (i == m - 1)
             for (std::uint32_t c = b + 1; c <= kSlab; ++c) S.bstart[c] = std::uint16_t(m);
     }
-    __syncthreads();
-    // request runs of every sparse source annulus a <= j (lambda within
-    // hbound(a, j) of the slab: a superset from a's cell table), numbered as
+    // request runs of every sparse source annulus a <= j (lambda within hbound(a, j) of the
+    // slab: a superset from a's cell table), compacted to the non-empty ones and numbered as
     // one CTA-wide list of 32-request groups shared by all warps
-    __shared__ std::uint64_t run_r0[64];
-    __shared__ std::uint32_t run_g[65]; // group prefix over the sources
     if (warp == 0) {
         const unsigned long long srcs = (A.ablate & 1) ? 0ull : A.src_mask[j]; // ablate: timing experiments only
-        for (int a0 = 0; a0 < 64; a0 += 32) {
+        std::uint32_t            nrun = 0, gsum = 0;
+        for (int a0 = 0; a0 <= j; a0 += 32) {
             const int     a  = a0 + lane;
             std::uint64_t r0 = 0, r1 = 0;
             if (a <= j && ((srcs >> a) & 1ull)) {
@@ -436,113 +472,152 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                 if (a == j && r1 > Aa.wrap) r1 = Aa.wrap; // own annulus: unwrapped requests only
                 if (r1 < r0) r1 = r0;
             }
-            const std::uint32_t ng   = std::uint32_t((r1 - r0 + 31) / 32);
+            const std::uint32_t ng = std::uint32_t((r1 - r0 + 31) / 32);
+            const unsigned      nz = __ballot_sync(kFull, ng > 0);
             std::uint32_t       incl = ng;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const std::uint32_t x = __shfl_up_sync(kFull, incl, o);
                 if (lane >= o) incl += x;
             }
-            const std::uint32_t base = a0 ? run_g[a0] : 0u;
-            run_r0[a]                = r0;
-            run_g[a + 1]             = base + incl;
-            if (a == 0) run_g[0] = 0;
-            __syncwarp();
+            if (ng) {
+                const std::uint32_t r = nrun + __popc(nz & ((1u << lane) - 1u));
+                S.run_r0[r] = r0, S.run_a[r] = std::uint8_t(a), S.run_g[r + 1] = gsum + incl;
+            }
+            nrun += __popc(nz);
+            gsum += __shfl_sync(kFull, incl, 31);
         }
+        if (lane == 0) S.run_g[0] = 0, S.n_run = nrun;
     }
     __syncthreads();
-    const std::uint32_t ngroups = run_g[64];
+    const std::uint32_t ngroups = S.run_g[S.n_run];
+    SlabRow32* const    rows    = S.rows[warp];
+    SlabRow64* const    rows64  = S.rows64[warp];
     Acc                 acc;
-    int a = 0; // source of group gi: last a with run_g[a] <= gi (gi only grows)
+    unsigned long long  n_exact = 0;
+    int ri = 0; // run of group gi: last ri with run_g[ri] <= gi (gi only grows)
     for (std::uint32_t gi = warp; gi < ngroups; gi += kSlabThreads / 32) {
-        while (run_g[a + 1] <= gi) ++a;
-        {
-            const AnnulusDev&   Aa = A.ann[a];
-            const bool          own = a == j;
-            const std::uint64_t g   = run_r0[a] + std::uint64_t(gi - run_g[a]) * 32;
-            const std::uint64_t R1  = run_r0[a] + std::uint64_t(run_g[a + 1] - run_g[a]) * 32; // group end bound
-            const std::uint64_t Rend = own ? (Aa.wrap < Aa.halo ? Aa.wrap : Aa.halo) : Aa.halo;
-            const std::uint32_t wl = own ? std::uint32_t(Aa.wrap > N0 ? (Aa.wrap - N0 < m ? Aa.wrap - N0 : m) : 0) : m;
-            const std::uint64_t p     = g + std::uint64_t(lane);
-            const bool          valid = p < R1 && p < Rend;
-            const std::uint64_t pc    = valid ? p : g;
-            const double2       r2 = A.s_rec2[pc];
-            double              lo, hi;
-            if (own) {
-                const double b = A.s_beta[pc], hw = A.s_hw[pc];
-                lo = b, hi = fadd(b, fmul(2.0, hw));
-            } else {
-                const double lam = A.s_lam[pc];
-                const double h   = half_width_in(Aj, r2.x, r2.y);
-                lo = fsub(lam, h), hi = fadd(lam, h);
-            }
-            std::uint32_t l0 = 0, l1 = 0;
-            if (valid && hi > lo && hi > lam_first && lo <= lam_last) {
-                l0 = slab_lb(S, lo, lam_first, inv_w), l1 = slab_lb(S, hi, lam_first, inv_w);
-                if (own) {
-                    if (p + 1 > N0 && l0 < std::uint32_t(p + 1 - N0)) l0 = std::uint32_t(p + 1 - N0 < m ? p + 1 - N0 : m);
-                    if (l1 > wl) l1 = wl;
-                }
-            }
-            // flattened pair list over the warp: pair t belongs to the lane whose prefix covers it
-            const std::uint32_t len  = l1 > l0 ? l1 - l0 : 0u;
-            std::uint32_t       incl = len;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const std::uint32_t x = __shfl_up_sync(kFull, incl, o);
-                if (lane >= o) incl += x;
-            }
-            const std::uint32_t T = __shfl_sync(kFull, incl, 31);
-            if (A.dbg) { // slab-join path statistics (RHG_DEBUG_STATS=1)
-                const unsigned nv = __popc(__ballot_sync(kFull, valid)), nl = __popc(__ballot_sync(kFull, len > 0));
-                if (lane == 0) {
-                    atomicAdd(&A.dbg[10], 1ull), atomicAdd(&A.dbg[11], (unsigned long long)nv);
-                    atomicAdd(&A.dbg[12], (unsigned long long)nl), atomicAdd(&A.dbg[13], (unsigned long long)T);
-                    atomicAdd(&A.dbg[14], 32ull * (((T + 31) >> 5) | 1u)), atomicAdd(&A.dbg[own ? 15 : 16], 1ull);
-                }
-            }
-            if (T == 0 || (A.ablate & 2)) { acc.comps += len; continue; }
-            const std::uint32_t excl = incl - len;
-            acc.comps += len;
-            SlabWarp& W = S.w[warp];
-            __syncwarp();
-            {
-                const double2 r1 = A.s_rec1[pc];
-                SRow          q;
-                q.cs = r1.x, q.sn = r1.y, q.coth = r2.x, q.rci = fmul(A.cosh_R, r2.y), q.id = A.s_id[pc];
-                q.pad        = std::uint32_t(l0 - excl); // local node of pair t: pad + t (mod 2^32)
-                W.rows[lane] = q;
-                W.incl[lane] = incl;
-            }
-            __syncwarp();
-            // lane L runs the contiguous pairs [L c, (L + 1) c) of the warp's sequence: its
-            // request stays in registers until the owner changes (rarely), only node records
-            // come from shared memory
-            const std::uint32_t c  = ((T + 31) >> 5) | 1u; // odd: lane starts fall in distinct smem banks
-            std::uint32_t       t  = std::uint32_t(lane) * c;
-            const std::uint32_t te = t + c < T ? t + c : T;
-            if (t < te) {
-                int o = 0, ho = 31; // first lane whose inclusive prefix exceeds t
-                while (o < ho) {
-                    const int mid = (o + ho) >> 1;
-                    if (W.incl[mid] > t) ho = mid;
-                    else o = mid + 1;
-                }
-                SRow          q   = W.rows[o];
-                std::uint32_t end = W.incl[o];
-                for (; t < te; ++t) {
-                    if (t >= end) { // next non-empty owner
-                        do ++o;
-                        while (W.incl[o] <= t);
-                        q = W.rows[o], end = W.incl[o];
-                    }
-                    const std::uint32_t k = std::uint32_t(q.pad) + t;
-                    count_edge<DEG>(A, edge_test(q.cs, q.sn, q.coth, q.rci, S.r1[k], S.r2[k]), q.id, S.id[k], acc);
-                }
-            }
-            __syncwarp();
+        while (S.run_g[ri + 1] <= gi) ++ri;
+        const int           a   = S.run_a[ri];
+        const AnnulusDev&   Aa  = A.ann[a];
+        const bool          own = a == j;
+        const std::uint64_t g    = S.run_r0[ri] + std::uint64_t(gi - S.run_g[ri]) * 32;
+        const std::uint64_t R1   = S.run_r0[ri] + std::uint64_t(S.run_g[ri + 1] - S.run_g[ri]) * 32; // group end bound
+        const std::uint64_t Rend = own ? (Aa.wrap < Aa.halo ? Aa.wrap : Aa.halo) : Aa.halo;
+        const std::uint64_t p     = g + std::uint64_t(lane);
+        const bool          valid = p < R1 && p < Rend;
+        const std::uint64_t pc    = valid ? p : g;
+        const double2       r2  = A.s_rec2[pc];
+        const double        lam = A.s_lam[pc];
+        double              lo, hi;
+        if (own) {
+            const double b = A.s_beta[pc], hw = A.s_hw[pc];
+            lo = b, hi = fadd(b, fmul(2.0, hw));
+        } else {
+            const double h = half_width_in(Aj, r2.x, r2.y);
+            lo = fsub(lam, h), hi = fadd(lam, h);
         }
+        std::uint32_t l0 = 0, l1 = 0;
+        if (valid && hi > lo && hi > lam_first && lo <= lam_last) {
+            l0 = slab_lb(S, lo, lam_first, inv_w), l1 = slab_lb(S, hi, lam_first, inv_w);
+            if (own) {
+                const std::uint32_t wl = std::uint32_t(Aa.wrap > N0 ? (Aa.wrap - N0 < m ? Aa.wrap - N0 : m) : 0);
+                if (p + 1 > N0 && l0 < std::uint32_t(p + 1 - N0)) l0 = std::uint32_t(p + 1 - N0 < m ? p + 1 - N0 : m);
+                if (l1 > wl) l1 = wl;
+            }
+        }
+        const std::uint32_t len = l1 > l0 ? l1 - l0 : 0u;
+        const unsigned      nz  = __ballot_sync(kFull, len > 0);
+        if (A.dbg) { // slab-join path statistics (RHG_DEBUG_STATS=1)
+            const unsigned nv = __popc(__ballot_sync(kFull, valid));
+            if (lane == 0)
+                atomicAdd(&A.dbg[10], 1ull), atomicAdd(&A.dbg[11], (unsigned long long)nv),
+                    atomicAdd(&A.dbg[12], (unsigned long long)__popc(nz)), atomicAdd(&A.dbg[own ? 15 : 16], 1ull);
+        }
+        if (nz == 0) continue;
+        // flattened pair list over the warp: pair t belongs to the row whose prefix covers it
+        std::uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const std::uint32_t x = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += x;
+        }
+        const std::uint32_t T  = __shfl_sync(kFull, incl, 31);
+        const std::uint32_t nr = __popc(nz);
+        acc.comps += len;
+        if (A.dbg && lane == 0) atomicAdd(&A.dbg[13], (unsigned long long)T), atomicAdd(&A.dbg[14], 32ull * (((T + 31) >> 5) | 1u));
+        if (A.ablate & 2) continue;
+        const std::uint64_t base_a = Aa.off + std::uint64_t(Aa.dlt0);
+        __syncwarp();
+        if (len) {
+            const double2 r1  = A.s_rec1[pc];
+            const double  rci = fmul(A.cosh_R, r2.y);
+            const int     w   = __popc(nz & ((1u << lane) - 1u));
+            rows64[w]         = SlabRow64{r1.x, r1.y, r2.x, rci};
+            const float lamf  = float(fsub(lam, lam_first));
+            const float ed    = 5.9604645e-8f * (fabsf(lamf) + span) + 1.5e-15f;
+            SlabRow32 R;
+            R.lamf = lamf, R.m = float(fsub(r2.x, 1.0)), R.rcif = float(rci);
+            R.e1 = 1.3f * ed + 3e-15f, R.c0 = 1.3f * ed * ed + 2e-15f;
+            R.qoff = std::uint32_t(A.s_id[pc] - base_a), R.pad = l0 - (incl - len), R.incl = incl;
+            rows[w] = R;
+        }
+        __syncwarp();
+        // lane L runs the contiguous pairs [L c, (L + 1) c) of the warp's sequence: its request
+        // stays in registers until the owner changes (one step: rows are non-empty), node
+        // records (16 B) come from shared memory.  Edge ids are summed as 32-bit offsets from
+        // the two annuli's id bases, rebased once per group.
+        const std::uint32_t c  = ((T + 31) >> 5) | 1u; // odd: lane starts fall in distinct smem banks
+        std::uint32_t       t  = std::uint32_t(lane) * c;
+        const std::uint32_t te = t + c < T ? t + c : T;
+        if (t < te) {
+            std::uint32_t o = 0, ho = nr - 1; // first row whose inclusive prefix exceeds t
+            while (o < ho) {
+                const std::uint32_t mid = (o + ho) >> 1;
+                if (rows[mid].incl > t) ho = mid;
+                else o = mid + 1;
+            }
+            const float4* rf = reinterpret_cast<const float4*>(rows); // row o: rf[2 o] floats, ru[2 o + 1]
+            const uint4*  ru = reinterpret_cast<const uint4*>(rows);
+            float4        q  = rf[2 * o];     // (lamf, m, rcif, e1)
+            uint4         u  = ru[2 * o + 1]; // (c0 bits, qoff, pad, incl)
+            std::uint32_t cnt = 0;
+            unsigned long long sum = 0;
+            for (; t < te; ++t) {
+                if (t >= u.w) { // next row
+                    ++o;
+                    q = rf[2 * o], u = ru[2 * o + 1];
+                }
+                const std::uint32_t k  = u.z + t;
+                const float4        nd = S.nd[k];
+                const float         df = nd.x - q.x;
+                const float         y2 = df * df;
+                const float         Sv = y2 * fmaf(y2, -1.0f / 24.0f, 0.5f);
+                const float         P  = q.z * nd.z;
+                const float         M  = fmaf(q.y, nd.y, q.y + nd.y) + Sv;
+                const float         D  = P - M;
+                const float         tau = fmaf(fabsf(df), q.w, fmaf(P + M, 1.4e-6f, __uint_as_float(u.x)));
+                bool                e  = D > 0.0f;
+                if (!(fabsf(D) > tau) || fabsf(df) > kPreMaxDelta) { // near the threshold: exact FP64
+                    const SlabRow64& R = rows64[o];
+                    e = edge_test(R.cs, R.sn, R.coth, R.rci, S.r1[k], S.r2[k]);
+                    ++n_exact;
+                }
+                if (e) {
+                    const std::uint32_t nid = __float_as_uint(nd.w);
+                    sum += nid + u.y, ++cnt; // < 2^32: a shard holds < 2^31 points
+                    if (DEG) {
+                        atomicAdd(&A.degrees[base_a + u.y], 1u);
+                        atomicAdd(&A.degrees[base_j + nid], 1u);
+                    }
+                }
+            }
+            acc.edges += cnt;
+            acc.fp += sum + static_cast<unsigned long long>(cnt) * (base_a + base_j);
+        }
+        __syncwarp();
     }
+    if (A.dbg && n_exact) atomicAdd(&A.dbg[17], n_exact);
     flush(acc, A, 0, lane);
 }
 
@@ -1308,7 +1383,9 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
     if (W.slab_end > W.slab_begin) {
         if (W.ev0) cudaEventRecord(W.ev0, st);
         const unsigned n   = unsigned(W.slab_end - W.slab_begin);
-        launch_slab<256, 4>(a, n, deg, st); // measured best of 128/256/512 threads x occupancy
+        static const int scfg = std::getenv("RHG_SLAB_CFG") ? std::atoi(std::getenv("RHG_SLAB_CFG")) : 0;
+        if (scfg == 0) launch_slab<256, 4>(a, n, deg, st);
+        else launch_slab<256, 3>(a, n, deg, st);
         ++*launches;
         if (W.tail && a.n_tail) {
             if (deg) tail_kernel<true><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
