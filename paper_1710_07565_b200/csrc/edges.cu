@@ -393,7 +393,8 @@ __device__ __forceinline__ std::uint32_t slab_lb(const SM& S, double x, double o
 // (Appendix of DESIGN.md); tau below covers the sum with a 25% margin.  Only when
 // |D32| > tau does the FP32 sign decide; otherwise (and for |Delta| > 2^-6, where
 // the truncated series is not used) the pair takes the exact FP64 predicate.
-constexpr float kPreMaxDelta = 0.015625f;
+constexpr float  kPreMaxDelta = 0.015625f;
+constexpr double kPreMinS     = 4e-14; // groups whose windows give S below this skip the pre-filter
 
 struct __align__(16) SlabRow32 { // one request with pairs in the slab (rows of a group are compacted)
     float         lamf;  // lambda_r - lam_first (float)
@@ -493,8 +494,8 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     const std::uint32_t ngroups = S.run_g[S.n_run];
     SlabRow32* const    rows    = S.rows[warp];
     SlabRow64* const    rows64  = S.rows64[warp];
-    Acc                 acc;
-    unsigned long long  n_exact = 0;
+    std::uint32_t       acc_e = 0, acc_c = 0; // per-thread totals of one slab fit 32 bits
+    unsigned long long  acc_fp = 0;
     int ri = 0; // run of group gi: last ri with run_g[ri] <= gi (gi only grows)
     for (std::uint32_t gi = warp; gi < ngroups; gi += kSlabThreads / 32) {
         while (S.run_g[ri + 1] <= gi) ++ri;
@@ -509,13 +510,13 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
         const std::uint64_t pc    = valid ? p : g;
         const double2       r2  = A.s_rec2[pc];
         const double        lam = A.s_lam[pc];
-        double              lo, hi;
+        double              lo, hi, hw_own = 0.0, h_oth = 0.0;
         if (own) {
             const double b = A.s_beta[pc], hw = A.s_hw[pc];
-            lo = b, hi = fadd(b, fmul(2.0, hw));
+            lo = b, hi = fadd(b, fmul(2.0, hw)), hw_own = hw;
         } else {
             const double h = half_width_in(Aj, r2.x, r2.y);
-            lo = fsub(lam, h), hi = fadd(lam, h);
+            lo = fsub(lam, h), hi = fadd(lam, h), h_oth = h;
         }
         std::uint32_t l0 = 0, l1 = 0;
         if (valid && hi > lo && hi > lam_first && lo <= lam_last) {
@@ -528,6 +529,11 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
         }
         const std::uint32_t len = l1 > l0 ? l1 - l0 : 0u;
         const unsigned      nz  = __ballot_sync(kFull, len > 0);
+        // the pre-filter decides a pair only when its distance term S = 1 - cos(dtheta) is
+        // well above the FP64 rounding floor (~2e-15); groups with windows narrower than
+        // that (outer annuli at R >~ 33) run the exact FP64 predicate directly
+        const double        hwin = own ? hw_own : h_oth;
+        const bool          fp64 = __any_sync(kFull, len > 0 && 0.5 * hwin * hwin < kPreMinS);
         if (A.dbg) { // slab-join path statistics (RHG_DEBUG_STATS=1)
             const unsigned nv = __popc(__ballot_sync(kFull, valid));
             if (lane == 0)
@@ -544,7 +550,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
         }
         const std::uint32_t T  = __shfl_sync(kFull, incl, 31);
         const std::uint32_t nr = __popc(nz);
-        acc.comps += len;
+        acc_c += len;
         if (A.dbg && lane == 0) atomicAdd(&A.dbg[13], (unsigned long long)T), atomicAdd(&A.dbg[14], 32ull * (((T + 31) >> 5) | 1u));
         if (A.ablate & 2) continue;
         const std::uint64_t base_a = Aa.off + std::uint64_t(Aa.dlt0);
@@ -583,41 +589,62 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
             uint4         u  = ru[2 * o + 1]; // (c0 bits, qoff, pad, incl)
             std::uint32_t cnt = 0;
             unsigned long long sum = 0;
-            for (; t < te; ++t) {
-                if (t >= u.w) { // next row
-                    ++o;
-                    q = rf[2 * o], u = ru[2 * o + 1];
+            if (!fp64) {
+                for (; t < te; ++t) {
+                    if (t >= u.w) { // next row
+                        ++o;
+                        q = rf[2 * o], u = ru[2 * o + 1];
+                    }
+                    const std::uint32_t k  = u.z + t;
+                    const float4        nd = S.nd[k];
+                    const float         df = nd.x - q.x;
+                    const float         y2 = df * df;
+                    const float         Sv = y2 * fmaf(y2, -1.0f / 24.0f, 0.5f);
+                    const float         P  = q.z * nd.z;
+                    const float         M  = fmaf(q.y, nd.y, q.y + nd.y) + Sv;
+                    const float         D  = P - M;
+                    const float         tau = fmaf(fabsf(df), q.w, fmaf(P + M, 1.4e-6f, __uint_as_float(u.x)));
+                    bool                e  = D > 0.0f;
+                    if (!(fabsf(D) > tau) || fabsf(df) > kPreMaxDelta) { // near the threshold: exact FP64
+                        const SlabRow64& R = rows64[o];
+                        e = edge_test(R.cs, R.sn, R.coth, R.rci, S.r1[k], S.r2[k]);
+                        if (A.dbg) atomicAdd(&A.dbg[17], 1ull);
+                    }
+                    if (e) {
+                        const std::uint32_t nid = __float_as_uint(nd.w);
+                        sum += nid + u.y, ++cnt; // < 2^32: a shard holds < 2^31 points
+                        if (DEG) {
+                            atomicAdd(&A.degrees[base_a + u.y], 1u);
+                            atomicAdd(&A.degrees[base_j + nid], 1u);
+                        }
+                    }
                 }
-                const std::uint32_t k  = u.z + t;
-                const float4        nd = S.nd[k];
-                const float         df = nd.x - q.x;
-                const float         y2 = df * df;
-                const float         Sv = y2 * fmaf(y2, -1.0f / 24.0f, 0.5f);
-                const float         P  = q.z * nd.z;
-                const float         M  = fmaf(q.y, nd.y, q.y + nd.y) + Sv;
-                const float         D  = P - M;
-                const float         tau = fmaf(fabsf(df), q.w, fmaf(P + M, 1.4e-6f, __uint_as_float(u.x)));
-                bool                e  = D > 0.0f;
-                if (!(fabsf(D) > tau) || fabsf(df) > kPreMaxDelta) { // near the threshold: exact FP64
-                    const SlabRow64& R = rows64[o];
-                    e = edge_test(R.cs, R.sn, R.coth, R.rci, S.r1[k], S.r2[k]);
-                    ++n_exact;
-                }
-                if (e) {
-                    const std::uint32_t nid = __float_as_uint(nd.w);
-                    sum += nid + u.y, ++cnt; // < 2^32: a shard holds < 2^31 points
-                    if (DEG) {
-                        atomicAdd(&A.degrees[base_a + u.y], 1u);
-                        atomicAdd(&A.degrees[base_j + nid], 1u);
+            } else { // windows so narrow that the FP64 rounding noise dominates: exact predicate only
+                const double2* r64 = reinterpret_cast<const double2*>(rows64);
+                double2        q0 = r64[2 * o], q1 = r64[2 * o + 1]; // (cs, sn), (coth, rci)
+                for (; t < te; ++t) {
+                    if (t >= u.w) { // next row
+                        ++o;
+                        q0 = r64[2 * o], q1 = r64[2 * o + 1], u = ru[2 * o + 1];
+                    }
+                    const std::uint32_t k = u.z + t;
+                    if (edge_test(q0.x, q0.y, q1.x, q1.y, S.r1[k], S.r2[k])) {
+                        const std::uint32_t nid = __float_as_uint(S.nd[k].w);
+                        sum += nid + u.y, ++cnt;
+                        if (DEG) {
+                            atomicAdd(&A.degrees[base_a + u.y], 1u);
+                            atomicAdd(&A.degrees[base_j + nid], 1u);
+                        }
                     }
                 }
             }
-            acc.edges += cnt;
-            acc.fp += sum + static_cast<unsigned long long>(cnt) * (base_a + base_j);
+            acc_e += cnt;
+            acc_fp += sum + static_cast<unsigned long long>(cnt) * (base_a + base_j);
         }
         __syncwarp();
     }
-    if (A.dbg && n_exact) atomicAdd(&A.dbg[17], n_exact);
+    Acc acc;
+    acc.edges = acc_e, acc.comps = acc_c, acc.fp = acc_fp;
     flush(acc, A, 0, lane);
 }
 
