@@ -594,21 +594,42 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         ctx->gsort.ensure(need);
         launch_sort_globals(e, ctx->gsort.p, ctx->gsort.cap, &need, ctx->stream, launches);
     }
-    EdgeWave w1;
-    w1.j0 = int(fs), w1.j1 = int(jw), w1.tile_warps = pl.gt_prefix[jw] - pl.gt_prefix[fs];
-    w1.slab_begin = 0, w1.slab_end = split ? pl.n_slabs1 : pl.n_slabs;
-    w1.global_unit = true, w1.tail = !split, w1.finish = !split;
-    w1.ev0 = ctx->evw[0], w1.ev1 = ctx->evw[1];
-    launch_edges(e, w1, ctx->stream, launches);
+    // Per wave: the dense engine (rows + node tiles) and the global unit, then the slab join.
+    // RHG_CONCURRENT_ENGINES=1 puts the dense side on ctx->side beside the slab join
+    // (independent counter families, both only read the sorted arrays; measured: no gain at
+    // cfg2 — each engine fills the GPU on its own); the deferred ranges and the counter fold
+    // wait for both.
+    const bool conc = std::getenv("RHG_CONCURRENT_ENGINES") != nullptr;
+    cudaStream_t dst = conc ? ctx->side : ctx->stream;
+    auto fork_to = [&](cudaStream_t from, cudaStream_t to) {
+        if (from == to) return;
+        CK(cudaEventRecord(ctx->fork, from));
+        CK(cudaStreamWaitEvent(to, ctx->fork, 0));
+    };
+    EdgeWave d1; // wave 1 dense targets + the global unit
+    d1.j0 = int(fs), d1.j1 = int(jw), d1.tile_warps = pl.gt_prefix[jw] - pl.gt_prefix[fs];
+    d1.global_unit = true;
+    EdgeWave s1; // wave 1 slab join (tail pairs too when there is no wave 2)
+    s1.slab_begin = 0, s1.slab_end = split ? pl.n_slabs1 : pl.n_slabs;
+    s1.tail = !split, s1.ev0 = ctx->evw[0], s1.ev1 = ctx->evw[1];
+    fork_to(ctx->stream, dst);
+    launch_edges(e, d1, dst, launches);
+    launch_edges(e, s1, ctx->stream, launches);
     if (split) {
         CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_late, 0));
-        EdgeWave w2;
-        w2.j0 = int(jw), w2.j1 = int(K), w2.tile_warps = pl.gt_prefix[K] - pl.gt_prefix[jw];
-        w2.slab_begin = pl.n_slabs1, w2.slab_end = pl.n_slabs;
-        w2.tail = true, w2.finish = true;
-        w2.ev0 = ctx->evw[2], w2.ev1 = ctx->evw[3];
-        launch_edges(e, w2, ctx->stream, launches);
+        CK(cudaStreamWaitEvent(dst, ctx->ev_late, 0));
+        EdgeWave d2;
+        d2.j0 = int(jw), d2.j1 = int(K), d2.tile_warps = pl.gt_prefix[K] - pl.gt_prefix[jw];
+        EdgeWave s2;
+        s2.slab_begin = pl.n_slabs1, s2.slab_end = pl.n_slabs;
+        s2.tail = true, s2.ev0 = ctx->evw[2], s2.ev1 = ctx->evw[3];
+        launch_edges(e, d2, dst, launches);
+        launch_edges(e, s2, ctx->stream, launches);
     }
+    fork_to(dst, ctx->stream); // join
+    EdgeWave fin;
+    fin.finish = true;
+    launch_edges(e, fin, ctx->stream, launches);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[2], ctx->stream));
     ctx->staging.ensure(4096);
