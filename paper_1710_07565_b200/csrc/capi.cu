@@ -13,6 +13,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <queue>
 #include <vector>
 
 #include "../../include/rhg_b200.h"
@@ -112,9 +113,9 @@ struct rhg_ctx {
     cudaEvent_t  evw[4]{};                            // sparse-engine timing of the two edge waves
     std::vector<std::pair<std::string, cudaEvent_t>> tl; // RHG_TIMELINE marks of the current call
     std::vector<cudaEvent_t> tl_pool;
-    DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, cells, counters, degrees, dbg, nid;
+    DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, tables2, cells, counters, degrees, dbg, nid;
     DevBuf       lcells, perm, s_beta, s_hw, s_lt, s_rec1, s_rec2, gsort, gbuf;
-    HostPinned   staging;
+    HostPinned   staging, staging2, readback; // table parts 1 and 2, counter readback
 };
 
 namespace {
@@ -152,7 +153,7 @@ void timeline_report(rhg_ctx* c, cudaEvent_t start) {
 // land in the extended arrays, and the pair-kernel work lists.
 struct Plan {
     Layout                  L;
-    std::uint32_t           e0 = 0, e1 = 0, T = 0;
+    std::uint32_t           e0 = 0, e1 = 0, T = 0, rank = 0, world = 1;
     std::vector<AnnulusDev> ann;
     std::vector<StreamJob>  jobs;
     std::vector<std::uint32_t> job_order;   // wave-1 jobs then wave-2 jobs, grouped by chain bin
@@ -176,6 +177,7 @@ struct Plan {
     std::uint64_t           n_ext = 0, n_glob = 0, total = 0, gtwarps = 0, ncells = 0, n_slabs = 0, n_tail = 0;
     std::uint64_t           gg_t0 = 0, gg_t1 = 0;
     double                  layout_ms = 0;
+    double                  sub_ms[4] = {0, 0, 0, 0}; // RHG_TIMELINE: plan phases after the layout
 };
 
 // Expected number of annulus-j nodes in the window of an annulus-a request
@@ -206,7 +208,7 @@ double half_width_bound(const Layout& L, std::uint32_t a, std::uint32_t j) {
     return std::min(kPi, h * (1.0 + 1e-6) + 1e-9);
 }
 
-Plan make_plan(const Params& P, const rhg_shard* shard) {
+Plan make_plan_head(const Params& P, const rhg_shard* shard) {
     Plan       pl;
     const auto tl0 = std::chrono::steady_clock::now();
     pl.L           = make_layout(P);
@@ -215,6 +217,7 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
     const std::uint32_t W = shard ? shard->world : 1, r = shard ? shard->rank : 0;
     if (W < 1 || r >= W) throw InvalidArgument("rhg_shard: rank must lie in [0, world)");
     const std::uint32_t Pc = L.chunks;
+    pl.rank = r, pl.world = W;
     pl.e0 = std::uint32_t(std::uint64_t(Pc) * r / W);
     pl.e1 = std::uint32_t(std::uint64_t(Pc) * (r + 1) / W);
     pl.T  = pl.e1 - pl.e0;
@@ -297,6 +300,8 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
     });
     pl.wave2_jobs = 0;
     for (std::uint32_t k = 0; k < pl.jobs.size(); ++k) pl.wave2_jobs += in_wave2(k);
+    const auto tl1 = std::chrono::steady_clock::now();
+    pl.sub_ms[0] = std::chrono::duration<double, std::milli>(tl1 - tl0).count() - pl.layout_ms;
     // chain bins: each wave's streams packed longest-processing-time-first into bins whose
     // load stays near the wave's longest chain; one warp runs one bin's chains back to back,
     // so few chain warps share an SM (their shared-memory traffic, not the DMUL latency,
@@ -310,12 +315,16 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
         std::uint64_t sum = 0, mx = 0;
         for (std::uint32_t k = j0; k < j1; ++k) sum += pl.jobs[pl.job_order[k]].count, mx = std::max(mx, pl.jobs[pl.job_order[k]].count);
         const std::uint64_t nb = std::min<std::uint64_t>(j1 - j0, mx ? (sum + mx - 1) / mx + (sum + 7 * mx) / (8 * mx) : 1);
-        std::vector<std::uint64_t>              load(nb, 0);
         std::vector<std::vector<std::uint32_t>> bin(nb);
+        using LB = std::pair<std::uint64_t, std::uint32_t>; // (load, bin): min-heap on load
+        std::priority_queue<LB, std::vector<LB>, std::greater<LB>> heap;
+        for (std::uint32_t b = 0; b < nb; ++b) heap.push({0, b});
         for (std::uint32_t k = j0; k < j1; ++k) { // job_order is by descending count inside a wave
-            const std::size_t b = std::min_element(load.begin(), load.end()) - load.begin();
-            load[b] += pl.jobs[pl.job_order[k]].count + 64; // + per-stream overhead
-            bin[b].push_back(pl.job_order[k]);
+            LB lb = heap.top();
+            heap.pop();
+            lb.first += pl.jobs[pl.job_order[k]].count + 64; // + per-stream overhead
+            bin[lb.second].push_back(pl.job_order[k]);
+            heap.push(lb);
         }
         std::uint32_t k = j0;
         for (const auto& v: bin) {
@@ -324,6 +333,19 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
         }
         if (!wv) pl.chain_bins1 = std::uint32_t(nb);
     }
+    pl.sub_ms[1] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl1).count();
+    if (pl.n_ext >= (std::uint64_t(1) << 32) || pl.n_req >= (std::uint64_t(1) << 31) || L.n >= (std::uint64_t(1) << 32))
+        throw InvalidArgument("rhg: more than 2^32 points (per device) are not supported");
+    return pl;
+}
+
+// The edge-phase part of the plan (slab join work lists, tail requests, node-tile strips,
+// global-unit tiles): only the edge kernels read it, so rhg_generate_stats builds and uploads
+// it while the device sampler runs.
+void plan_edges(Plan& pl) {
+    const Layout&       L  = pl.L;
+    const std::uint32_t Pc = L.chunks;
+    const auto          tl2 = std::chrono::steady_clock::now();
     // slab join for the sparse pairs: slabs of every target annulus with sparse sources, the
     // half-width bounds that find a slab's requests, and the tail (wrap / halo) requests
     const std::uint32_t K = L.count;
@@ -347,23 +369,31 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
       // shapes cache locality
         const std::uint64_t nb = std::max<std::uint64_t>(pl.n_slabs, 1);
         std::vector<std::uint32_t> cnt(2 * nb + 1, 0);
-        auto key = [&](std::uint32_t j, std::uint64_t i, std::uint64_t ns) {
-            const std::uint64_t b = (2 * i + 1) * nb / (2 * ns); // bucket of the slab's mid angle
-            return (j >= pl.wave_j ? nb : 0) + std::min<std::uint64_t>(b, nb - 1);
-        };
+        std::vector<std::uint32_t> bkt(pl.n_slabs); // bucket of each slab's mid angle (wave-major)
         for (std::uint32_t j = 0; j < K; ++j) {
             const std::uint64_t ns = pl.slab_prefix[j + 1] - pl.slab_prefix[j];
-            for (std::uint64_t i = 0; i < ns; ++i) ++cnt[key(j, i, ns) + 1];
+            if (!ns) continue;
+            const double        f    = double(nb) / double(2 * ns);
+            const std::uint32_t base = j >= pl.wave_j ? std::uint32_t(nb) : 0u;
+            std::uint32_t*      out  = bkt.data() + pl.slab_prefix[j];
+            for (std::uint64_t i = 0; i < ns; ++i) {
+                const std::uint64_t b = std::min<std::uint64_t>(std::uint64_t(double(2 * i + 1) * f), nb - 1);
+                out[i]                = base + std::uint32_t(b);
+                ++cnt[out[i] + 1];
+            }
         }
         for (std::size_t b = 1; b < cnt.size(); ++b) cnt[b] += cnt[b - 1];
         pl.n_slabs1 = cnt[nb];
         pl.slab_tab.resize(pl.n_slabs);
         for (std::uint32_t j = 0; j < K; ++j) {
             const std::uint64_t ns = pl.slab_prefix[j + 1] - pl.slab_prefix[j];
+            const std::uint32_t* in = bkt.data() + pl.slab_prefix[j];
             for (std::uint64_t i = 0; i < ns; ++i)
-                pl.slab_tab[cnt[key(j, i, ns)]++] = (static_cast<unsigned long long>(j) << 32) | i;
+                pl.slab_tab[cnt[in[i]]++] = (static_cast<unsigned long long>(j) << 32) | i;
         }
     }
+    const auto tl3 = std::chrono::steady_clock::now();
+    pl.sub_ms[2] = std::chrono::duration<double, std::milli>(tl3 - tl2).count();
     const double Bnd = chunk_lower_bound(pl.e1, Pc); // halo nodes and wrapped points have lambda >= Bnd
     for (std::uint32_t a = 0; a < K; ++a) {
         std::uint64_t n = 0;
@@ -393,10 +423,14 @@ Plan make_plan(const Params& P, const rhg_shard* shard) {
         pl.gt_prefix[j + 1]     = pl.gt_prefix[j] + (own + 127) / 128; // one 128-node tile per warp
     }
     pl.gtwarps = pl.gt_prefix[L.count];
-    if (pl.n_ext >= (std::uint64_t(1) << 32) || pl.n_req >= (std::uint64_t(1) << 31) || L.n >= (std::uint64_t(1) << 32))
-        throw InvalidArgument("rhg: more than 2^32 points (per device) are not supported");
     const std::uint64_t nT = (pl.n_glob + kGGTile - 1) / kGGTile, tiles = nT * (nT + 1) / 2;
-    pl.gg_t0 = tiles * r / W, pl.gg_t1 = tiles * (r + 1) / W;
+    pl.gg_t0 = tiles * pl.rank / pl.world, pl.gg_t1 = tiles * (pl.rank + 1) / pl.world;
+    pl.sub_ms[3] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl3).count();
+}
+
+Plan make_plan(const Params& P, const rhg_shard* shard) {
+    Plan pl = make_plan_head(P, shard);
+    plan_edges(pl);
     return pl;
 }
 
@@ -417,40 +451,59 @@ struct Tables {
     double*             tail_lam;
 };
 
-// Pack all tables into one pinned blob and send it with one copy.
-Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr) {
-    struct Part {
-        const void* src;
-        std::size_t bytes, off;
-    };
-    std::vector<Part> parts;
-    std::size_t       bytes = 0;
-    auto add = [&](const auto& v) {
-        parts.push_back({v.data(), v.size() * sizeof(v[0]), bytes});
-        bytes = align256(bytes + v.size() * sizeof(v[0]));
-        return parts.size() - 1;
-    };
-    const std::size_t i_ann = add(pl.ann), i_dm = add(pl.dense_mask), i_ro = add(pl.req_off), i_jobs = add(pl.jobs);
-    const std::size_t i_gt = add(pl.gt_prefix), i_gs = add(pl.gseg), i_ab = add(pl.ann_blk), i_sm = add(pl.src_mask);
-    const std::size_t i_hb = add(pl.hbound), i_sp = add(pl.slab_tab), i_tp = add(pl.tail_prefix);
-    const std::size_t i_tl = add(pl.tail_lam), i_jo = add(pl.job_order), i_cb = add(pl.chain_bins);
+// Pack tables into one pinned blob and send it with one copy: part 1 = what the sampler
+// (and everything after it) reads, part 2 = the edge-phase work lists (plan_edges).
+// Each part has its own pinned staging and device buffer, so part 2 can be staged while
+// part 1's copy and the sampler are still in flight.
+void upload_part(rhg_ctx* ctx, int part, const std::vector<std::pair<const void*, std::size_t>>& src,
+                 std::vector<void*>& dst, std::uint64_t* h2d) {
+    std::vector<std::size_t> off(src.size());
+    std::size_t              bytes = 0;
+    for (std::size_t i = 0; i < src.size(); ++i) off[i] = bytes, bytes = align256(bytes + src[i].second);
     bytes += 256;
-    ctx->staging.ensure(bytes);
-    char* h = static_cast<char*>(ctx->staging.p);
-    for (const Part& q: parts)
-        if (q.bytes) std::memcpy(h + q.off, q.src, q.bytes);
-    ctx->tables.ensure(bytes);
-    CK(cudaMemcpyAsync(ctx->tables.p, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    HostPinned& stg = part ? ctx->staging2 : ctx->staging;
+    DevBuf&     dev = part ? ctx->tables2 : ctx->tables;
+    stg.ensure(bytes);
+    dev.ensure(bytes);
+    char* h = static_cast<char*>(stg.p);
+    for (std::size_t i = 0; i < src.size(); ++i)
+        if (src[i].second) std::memcpy(h + off[i], src[i].first, src[i].second);
+    CK(cudaMemcpyAsync(dev.p, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
     if (h2d) *h2d += bytes;
-    char* d  = ctx->tables.as<char>();
-    auto  at = [&](std::size_t i) { return static_cast<void*>(d + parts[i].off); };
-    return {static_cast<AnnulusDev*>(at(i_ann)),        static_cast<unsigned long long*>(at(i_dm)),
-            static_cast<std::uint64_t*>(at(i_ro)),      static_cast<StreamJob*>(at(i_jobs)),
-            static_cast<std::uint32_t*>(at(i_jo)),      static_cast<std::uint32_t*>(at(i_cb)),
-            static_cast<std::uint64_t*>(at(i_gt)),      static_cast<std::uint64_t*>(at(i_gs)),
-            static_cast<std::uint32_t*>(at(i_ab)),      static_cast<unsigned long long*>(at(i_sm)),
-            static_cast<double*>(at(i_hb)),             static_cast<unsigned long long*>(at(i_sp)),
-            static_cast<std::uint64_t*>(at(i_tp)),      static_cast<double*>(at(i_tl))};
+    dst.resize(src.size());
+    for (std::size_t i = 0; i < src.size(); ++i) dst[i] = dev.as<char>() + off[i];
+}
+template <class V>
+std::pair<const void*, std::size_t> blob(const V& v) {
+    return {v.data(), v.size() * sizeof(v[0])};
+}
+
+void upload_tables_head(rhg_ctx* ctx, const Plan& pl, Tables& t, std::uint64_t* h2d) {
+    std::vector<void*> d;
+    upload_part(ctx, 0,
+                {blob(pl.ann), blob(pl.dense_mask), blob(pl.req_off), blob(pl.jobs), blob(pl.job_order),
+                 blob(pl.chain_bins), blob(pl.gseg), blob(pl.ann_blk)},
+                d, h2d);
+    t.ann = static_cast<AnnulusDev*>(d[0]), t.dense_mask = static_cast<unsigned long long*>(d[1]);
+    t.req_off = static_cast<std::uint64_t*>(d[2]), t.jobs = static_cast<StreamJob*>(d[3]);
+    t.job_order = static_cast<std::uint32_t*>(d[4]), t.chain_bins = static_cast<std::uint32_t*>(d[5]);
+    t.gseg = static_cast<std::uint64_t*>(d[6]), t.ann_blk = static_cast<std::uint32_t*>(d[7]);
+}
+void upload_tables_edges(rhg_ctx* ctx, const Plan& pl, Tables& t, std::uint64_t* h2d) {
+    std::vector<void*> d;
+    upload_part(ctx, 1,
+                {blob(pl.gt_prefix), blob(pl.src_mask), blob(pl.hbound), blob(pl.slab_tab), blob(pl.tail_prefix),
+                 blob(pl.tail_lam)},
+                d, h2d);
+    t.gt_prefix = static_cast<std::uint64_t*>(d[0]), t.src_mask = static_cast<unsigned long long*>(d[1]);
+    t.hbound = static_cast<double*>(d[2]), t.slab_tab = static_cast<unsigned long long*>(d[3]);
+    t.tail_prefix = static_cast<std::uint64_t*>(d[4]), t.tail_lam = static_cast<double*>(d[5]);
+}
+Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr) {
+    Tables t{};
+    upload_tables_head(ctx, pl, t, h2d);
+    upload_tables_edges(ctx, pl, t, h2d);
+    return t;
 }
 
 void ensure_points(rhg_ctx* ctx, std::uint64_t total, bool with_export) {
@@ -632,8 +685,8 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     launch_edges(e, fin, ctx->stream, launches);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[2], ctx->stream));
-    ctx->staging.ensure(4096);
-    auto* hc = static_cast<Counters*>(ctx->staging.p);
+    ctx->readback.ensure(4096);
+    auto* hc = static_cast<Counters*>(ctx->readback.p);
     CK(cudaMemcpyAsync(hc, ctx->counters.p, 3 * sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
     int* h_ncls = reinterpret_cast<int*>(hc + 3);
     auto* h_drop = reinterpret_cast<unsigned long long*>(hc + 4);
@@ -751,6 +804,8 @@ void rhg_destroy(rhg_ctx* c) {
                      &c->s_hw, &c->s_lt, &c->s_rec1, &c->s_rec2, &c->gsort, &c->gbuf})
         b->release();
     if (c->staging.p) cudaFreeHost(c->staging.p);
+    if (c->staging2.p) cudaFreeHost(c->staging2.p);
+    if (c->readback.p) cudaFreeHost(c->readback.p);
     for (auto& e: c->ev) cudaEventDestroy(e);
     cudaEventDestroy(c->fork);
     cudaEventDestroy(c->join);
@@ -773,15 +828,17 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
         std::memset(out, 0, sizeof *out);
         CK(cudaSetDevice(ctx->device));
         const Params  P  = to_params(params);
-        const Plan    pl = make_plan(P, shard);
+        Plan          pl = make_plan_head(P, shard);
         const auto    t1 = Clock::now();
         std::uint64_t launches = 0;
         ensure_points(ctx, pl.total, false);
-        const Tables t = upload_tables(ctx, pl, &out->h2d_bytes);
-        const double host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+        Tables t{};
+        upload_tables_head(ctx, pl, t, &out->h2d_bytes);
+        double host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
         if (const char* v = std::getenv("RHG_TIMELINE"); v && v[0] == '1')
-            std::fprintf(stderr, "RHG_HOST plan=%.3f ms (layout=%.3f) upload=%.3f ms\n",
-                         std::chrono::duration<double, std::milli>(t1 - t0).count(), pl.layout_ms,
+            std::fprintf(stderr, "RHG_HOST plan=%.3f ms (layout=%.3f jobs=%.3f bins=%.3f slabs=%.3f rest=%.3f) upload=%.3f ms\n",
+                         std::chrono::duration<double, std::milli>(t1 - t0).count(), pl.layout_ms, pl.sub_ms[0],
+                         pl.sub_ms[1], pl.sub_ms[2], pl.sub_ms[3],
                          std::chrono::duration<double, std::milli>(Clock::now() - t1).count());
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         SamplerArgs sa  = sampler_args(ctx, pl, t);
@@ -791,6 +848,12 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
         if (split) sa.wave2_jobs = pl.wave2_jobs, sa.late = ctx->late, sa.ev_pow = ctx->ev_pow, sa.ev_late = ctx->ev_late;
         launch_sampler(sa, ctx->stream, &launches);
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        { // the edge-phase plan is built and staged while the device samples
+            const auto t2 = Clock::now();
+            plan_edges(pl);
+            upload_tables_edges(ctx, pl, t, &out->h2d_bytes);
+            host_ms += std::chrono::duration<double, std::milli>(Clock::now() - t2).count();
+        }
         run_edges(ctx, pl, t, out, degrees, true, split, &launches);
         fill_common(pl, out);
         out->sample_ms       = ms_between(ctx->ev[0], ctx->ev[1]);
@@ -799,7 +862,7 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
         out->host_ms         = host_ms;
         out->kernel_launches = launches;
         out->device_bytes    = ctx->beta.cap + ctx->hw.cap + ctx->rec0.cap + ctx->rec1.cap + ctx->rec2.cap +
-                            ctx->r_out.cap + ctx->beta_raw.cap + ctx->tables.cap + ctx->cells.cap + ctx->counters.cap +
+                            ctx->r_out.cap + ctx->beta_raw.cap + ctx->tables.cap + ctx->tables2.cap + ctx->cells.cap + ctx->counters.cap +
                             ctx->degrees.cap + ctx->nid.cap + ctx->lcells.cap + ctx->perm.cap + ctx->s_beta.cap +
                             ctx->s_hw.cap + ctx->s_lt.cap + ctx->s_rec1.cap + ctx->s_rec2.cap + ctx->gbuf.cap;
         out->seconds = std::chrono::duration<double>(Clock::now() - t0).count();
