@@ -502,6 +502,8 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
         const int           a   = S.run_a[ri];
         const AnnulusDev&   Aa  = A.ann[a];
         const bool          own = a == j;
+        if ((A.ablate & 4) && own) continue; // timing experiments only
+        if ((A.ablate & 8) && !own) continue;
         const std::uint64_t g    = S.run_r0[ri] + std::uint64_t(gi - S.run_g[ri]) * 32;
         const std::uint64_t R1   = S.run_r0[ri] + std::uint64_t(S.run_g[ri + 1] - S.run_g[ri]) * 32; // group end bound
         const std::uint64_t Rend = own ? (Aa.wrap < Aa.halo ? Aa.wrap : Aa.halo) : Aa.halo;
