@@ -1413,8 +1413,8 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         if (W.ev0) cudaEventRecord(W.ev0, st);
         const unsigned n   = unsigned(W.slab_end - W.slab_begin);
         static const int scfg = std::getenv("RHG_SLAB_CFG") ? std::atoi(std::getenv("RHG_SLAB_CFG")) : 0;
-        if (scfg == 0) launch_slab<256, 4>(a, n, deg, st);
-        else launch_slab<256, 3>(a, n, deg, st);
+        if (scfg == 0) launch_slab<256, 4>(a, n, deg, st); // measured best of 128..512 threads x 256..1024-node slabs
+        else launch_slab<128, 8>(a, n, deg, st);
         ++*launches;
         if (W.tail && a.n_tail) {
             if (deg) tail_kernel<true><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
