@@ -17,6 +17,9 @@
  *   materialize_points / the      oracle.hpp:26-39,       rhg_sample_points (device sampler,
  *     ChunkPointSource stream     sweep.hpp:102-151         points copied back in id order)
  *   (parity hook, no ref. twin)                           rhg_count_edges_from_points
+ *   generate(params, opts, edge)  generator.hpp:135-215   rhg_generate_edges (canonical order)
+ *   TextEdgeWriter/BinaryEdgeWriter io.hpp:20-68           rhg_write_edges_text / _binary
+ *   read_binary_edges             io.hpp:70-96            rhg_read_edges_binary
  *
  * Conventions: plain pointers and sizes, no exceptions across the ABI.
  * Every call returns RHG_OK (0) or an error code; rhg_last_error() gives the
@@ -36,7 +39,7 @@
 extern "C" {
 #endif
 
-#define RHG_ABI_VERSION 2
+#define RHG_ABI_VERSION 3
 
 enum {
     RHG_OK = 0,
@@ -143,6 +146,31 @@ int rhg_sample_uniforms(rhg_ctx* ctx, const rhg_params* params, double* u_angle,
  * reference's edges / fingerprint / comps bit for bit. */
 int rhg_count_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard,
                                 const rhg_points* pts, rhg_run_stats* out, uint32_t* degrees);
+
+/* Materialised edge stream (generator.hpp:135-215
+ * generate(params, opts, edge_sink)).  Every edge this shard owns as a
+ * canonical pair (u < v), `edges` = 2 * cap uint64 (u0, v0, u1, v1, ...),
+ * sorted ascending by (u, v).  The reference emits the same multiset in its
+ * unit / sweep order (its own tests compare sorted multisets, oracle.hpp:
+ * 70-104).  *n_edges always receives the edge count; edges == NULL only
+ * counts; cap < count fails with RHG_INVALID_ARGUMENT (retry with
+ * cap >= *n_edges).  Requires n < 2^32 and < 2^31 edges per call. */
+int rhg_generate_edges(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, rhg_run_stats* out,
+                       uint64_t* edges, uint64_t cap, uint64_t* n_edges);
+/* The same for a GIVEN point set ("same points" mode, as rhg_count_edges_from_points). */
+int rhg_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, const rhg_points* pts,
+                          rhg_run_stats* out, uint64_t* edges, uint64_t cap, uint64_t* n_edges);
+
+/* Edge stream file formats, byte-compatible with io.hpp:20-96:
+ * text = one "u v\n" per edge (decimal); binary = 8-byte magic "RHGE0001"
+ * then little-endian uint64 pairs, no length prefix.  Host-only. */
+int rhg_write_edges_text(const char* path, const uint64_t* edges, uint64_t m);
+int rhg_write_edges_binary(const char* path, const uint64_t* edges, uint64_t m);
+/* io.hpp:70-96 read_binary_edges: bad magic / truncated pair -> RHG_INVALID_ARGUMENT
+ * (std::runtime_error in the reference).  edges == NULL only counts. */
+int rhg_read_edges_binary(const char* path, uint64_t* edges, uint64_t cap, uint64_t* m);
+/* message of the last failed edge-file call (this thread) */
+const char* rhg_io_last_error(void);
 
 /* Diagnostic (not part of the reference interface): measured non-FMA FP64
  * DMUL+DADD instruction rate of `device` (the edge kernels' roofline

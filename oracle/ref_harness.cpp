@@ -11,6 +11,7 @@
 // reference's own functions.
 
 #include <rhg/generator.hpp>
+#include <rhg/io.hpp>
 #include <rhg/geometry.hpp>
 #include <rhg/oracle.hpp>
 #include <rhg/partition.hpp>
@@ -18,6 +19,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <exception>
 #include <string>
 #include <thread>
@@ -206,6 +208,30 @@ int ref_naive_edges(std::uint64_t n, double alpha, double C, std::uint64_t seed,
                 edges[2 * k]     = e[k].first;
                 edges[2 * k + 1] = e[k].second;
             }
+    });
+}
+
+// io.hpp:20-68 TextEdgeWriter / BinaryEdgeWriter over an edge list (byte-level
+// parity of the B200 library's writers) and io.hpp:70-96 read_binary_edges.
+int ref_write_edges(const char* path, const std::uint64_t* edges, std::uint64_t m, int binary) {
+    return guarded([&] {
+        std::ofstream os(path, std::ios::binary);
+        if (binary) {
+            rhg::BinaryEdgeWriter w(os);
+            for (std::uint64_t k = 0; k < m; ++k) w.edge(edges[2 * k], edges[2 * k + 1]);
+        } else {
+            rhg::TextEdgeWriter w(os);
+            for (std::uint64_t k = 0; k < m; ++k) w.edge(edges[2 * k], edges[2 * k + 1]);
+        }
+    });
+}
+int ref_read_edges_binary(const char* path, std::uint64_t* m, std::uint64_t* edges) {
+    return guarded([&] {
+        std::ifstream is(path, std::ios::binary);
+        const auto    e = rhg::read_binary_edges(is);
+        *m              = e.size();
+        if (edges)
+            for (std::size_t k = 0; k < e.size(); ++k) edges[2 * k] = e[k].first, edges[2 * k + 1] = e[k].second;
     });
 }
 

@@ -96,6 +96,8 @@ class Ref(_Base):
         L.ref_points.argtypes = [u64, f64, f64, u64, u32, u32] + [P_f64] * 8 + [P_u32]
         L.ref_generate_edges.argtypes = [u64, f64, f64, u64, u32, u32, P_u64, P_u64]
         L.ref_naive_edges.argtypes = [u64, f64, f64, u64, u32, P_u64, P_u64]
+        L.ref_write_edges.argtypes = [C.c_char_p, P_u64, u64, C.c_int]
+        L.ref_read_edges_binary.argtypes = [C.c_char_p, P_u64, P_u64]
         L.ref_derive_seed.argtypes = [u64, P_u64, u32]
         L.ref_derive_seed.restype = u64
         L.ref_mt_outputs.argtypes = [u64, u64, P_u64]
@@ -165,6 +167,17 @@ class Ref(_Base):
         self._check(self.L.ref_generate_edges(n, alpha, Cc, seed, chunks, workers, C.byref(m), None))
         buf = np.zeros(2 * m.value, np.uint64)
         self._check(self.L.ref_generate_edges(n, alpha, Cc, seed, chunks, workers, C.byref(m), _p(buf, P_u64)))
+        return buf.reshape(-1, 2)
+
+    def write_edges(self, path, edges, binary):
+        e = np.ascontiguousarray(edges, np.uint64).reshape(-1, 2)
+        self._check(self.L.ref_write_edges(str(path).encode(), _p(e, P_u64), len(e), 1 if binary else 0))
+
+    def read_edges_binary(self, path):
+        m = u64()
+        self._check(self.L.ref_read_edges_binary(str(path).encode(), C.byref(m), None))
+        buf = np.zeros(2 * m.value, np.uint64)
+        self._check(self.L.ref_read_edges_binary(str(path).encode(), C.byref(m), _p(buf, P_u64)))
         return buf.reshape(-1, 2)
 
     def naive_edges(self, n, alpha, Cc, seed, chunks):

@@ -22,7 +22,7 @@ from typing import Optional
 import numpy as np
 
 from . import _native
-from ._native import RhgCudaError, check, lib
+from ._native import RHG_OK, RhgCudaError, check, lib
 
 __all__ = ["alpha_from_gamma", "gamma_from_alpha", "radial_const_from_avg_degree", "radius_from_size",
            "expected_avg_degree", "ModelParams", "GenOptions", "ChunkStats", "RunStats", "generate_stats",
@@ -264,3 +264,70 @@ def count_edges_from_points(params: ModelParams, points, opts: GenOptions = GenO
     out = RunStats._from_c(st)
     out.degrees = deg
     return out
+
+
+# ------------------------------------------------------- edge streams ---
+# the materialised edge stream (generator.hpp:135-215
+# generate(params, opts, edge sink)) and its file formats (io.hpp:20-96).
+
+def _edges_call(fn, params: ModelParams, opts: GenOptions, *pre):
+    ctx = _Context.get(opts.device)
+    st = _native.rhg_run_stats()
+    m = C.c_uint64(0)
+    est = expected_avg_degree(params.C, params.alpha) * params.n / 2.0 / max(1, opts.world)
+    cap = int(est * 1.25) + 4096
+    for _ in range(2):
+        buf = np.empty((cap, 2), np.uint64)
+        rc = fn(ctx, C.byref(params._c()), C.byref(_shard(opts)), *pre, C.byref(st),
+                buf.ctypes.data_as(C.POINTER(C.c_uint64)), cap, C.byref(m))
+        if rc == _native.RHG_INVALID_ARGUMENT and m.value > cap:
+            cap = int(m.value)  # the estimate was low: rerun with the exact count
+            continue
+        check(rc)
+        return buf[: m.value], RunStats._from_c(st)
+    raise RuntimeError("generate_edges: edge count changed between runs")
+
+
+def generate_edges(params: ModelParams, opts: GenOptions = GenOptions()):
+    """Every edge of the graph (or of this shard) as a (m, 2) uint64 array of
+    canonical pairs u < v, sorted by (u, v), plus the RunStats of the run.
+    The reference's generate() emits the same multiset in its unit order."""
+    return _edges_call(lib().rhg_generate_edges, params, opts)
+
+
+def edges_from_points(params: ModelParams, points, opts: GenOptions = GenOptions()):
+    """generate_edges for a GIVEN point set ("same points" mode)."""
+    pts = Points(*[getattr(points, k, None) for k in Points.FIELDS])
+    return _edges_call(lib().rhg_edges_from_points, params, opts, C.byref(pts._c()))
+
+
+def _io_check(rc: int) -> None:
+    if rc != RHG_OK:
+        raise ValueError(lib().rhg_io_last_error().decode())
+
+
+def _edge_ptr(edges):
+    e = np.ascontiguousarray(edges, np.uint64).reshape(-1, 2)
+    return e, e.ctypes.data_as(C.POINTER(C.c_uint64))
+
+
+def write_edges_text(path: str, edges) -> None:
+    """io.hpp TextEdgeWriter: one "u v" line per edge (decimal)."""
+    e, p = _edge_ptr(edges)
+    _io_check(lib().rhg_write_edges_text(str(path).encode(), p, len(e)))
+
+
+def write_edges_binary(path: str, edges) -> None:
+    """io.hpp BinaryEdgeWriter: magic "RHGE0001" then little-endian u64 pairs."""
+    e, p = _edge_ptr(edges)
+    _io_check(lib().rhg_write_edges_binary(str(path).encode(), p, len(e)))
+
+
+def read_edges_binary(path: str) -> np.ndarray:
+    """io.hpp read_binary_edges (bad magic / truncated pair raise ValueError)."""
+    m = C.c_uint64(0)
+    _io_check(lib().rhg_read_edges_binary(str(path).encode(), None, 0, C.byref(m)))
+    buf = np.empty((m.value, 2), np.uint64)
+    _io_check(lib().rhg_read_edges_binary(str(path).encode(), buf.ctypes.data_as(C.POINTER(C.c_uint64)), m.value,
+                                          C.byref(m)))
+    return buf

@@ -49,7 +49,8 @@ class RhgCudaError(RuntimeError):
 EXPORTS = ["rhg_last_error", "rhg_abi_version", "rhg_alpha_from_gamma", "rhg_radial_const_from_avg_degree",
            "rhg_params_validate", "rhg_params_from_avg_degree", "rhg_create", "rhg_destroy", "rhg_generate_stats",
            "rhg_sample_points", "rhg_sample_uniforms", "rhg_count_edges_from_points",
-           "rhg_fp64_peak"]
+           "rhg_fp64_peak", "rhg_generate_edges", "rhg_edges_from_points", "rhg_write_edges_text", "rhg_write_edges_binary",
+           "rhg_read_edges_binary", "rhg_io_last_error"]
 
 _lib = None
 
@@ -81,6 +82,15 @@ def lib():
                                               C.POINTER(C.c_uint32)]
     L.rhg_sample_uniforms.argtypes = [C.c_void_p, C.POINTER(rhg_params), P_f64, P_f64]
     L.rhg_fp64_peak.argtypes = [C.c_int, P_f64, P_f64, P_f64]
+    P_u64 = C.POINTER(C.c_uint64)
+    L.rhg_generate_edges.argtypes = [C.c_void_p, C.POINTER(rhg_params), C.POINTER(rhg_shard),
+                                     C.POINTER(rhg_run_stats), P_u64, C.c_uint64, P_u64]
+    L.rhg_edges_from_points.argtypes = [C.c_void_p, C.POINTER(rhg_params), C.POINTER(rhg_shard),
+                                        C.POINTER(rhg_points), C.POINTER(rhg_run_stats), P_u64, C.c_uint64, P_u64]
+    L.rhg_write_edges_text.argtypes = [C.c_char_p, P_u64, C.c_uint64]
+    L.rhg_write_edges_binary.argtypes = [C.c_char_p, P_u64, C.c_uint64]
+    L.rhg_read_edges_binary.argtypes = [C.c_char_p, P_u64, C.c_uint64, P_u64]
+    L.rhg_io_last_error.restype = C.c_char_p
     _lib = L
     return L
 

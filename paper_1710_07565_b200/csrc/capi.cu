@@ -115,6 +115,7 @@ struct rhg_ctx {
     std::vector<cudaEvent_t> tl_pool;
     DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, tables2, cells, counters, degrees, dbg, nid;
     DevBuf       lcells, perm, s_beta, s_hw, s_lt, s_rec1, s_rec2, gsort, gbuf;
+    DevBuf       ebuf, ecount, ekeys, esort; // materialised edges (rhg_generate_edges)
     HostPinned   staging, staging2, readback; // table parts 1 and 2, counter readback
 };
 
@@ -531,8 +532,17 @@ SamplerArgs sampler_args(rhg_ctx* ctx, const Plan& pl, const Tables& t) {
 }
 
 // Cell index + every edge kernel + counters back to the host.
+// Optional materialised edge stream (rhg_generate_edges / rhg_edges_from_points): the
+// kernels append canonical (u, v) pairs to ctx->ebuf (capacity dev_cap); run_edges
+// reports how many the graph has (*count, which may exceed dev_cap: the caller regrows
+// and reruns).
+struct EdgeSink {
+    std::uint64_t dev_cap = 0;
+    std::uint64_t count   = 0;
+};
+
 void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out, std::uint32_t* degrees,
-               bool gen, bool split_wave, std::uint64_t* launches) {
+               bool gen, bool split_wave, std::uint64_t* launches, EdgeSink* sink = nullptr) {
     const std::uint32_t K         = pl.L.count;
     const std::size_t   o_dmax    = align256(3 * sizeof(Counters));
     const std::size_t   o_hmax    = o_dmax + align256(K * sizeof(unsigned long long));
@@ -614,6 +624,13 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     e.tail_prefix = t.tail_prefix, e.tail_lam = t.tail_lam, e.n_tail = pl.n_tail;
     e.gg_tile_begin = pl.gg_t0, e.gg_tile_end = pl.gg_t1;
     e.degrees       = degrees ? ctx->degrees.as<unsigned>() : nullptr;
+    if (sink) {
+        ctx->ebuf.ensure(std::max<std::uint64_t>(sink->dev_cap, 1) * sizeof(ulonglong2));
+        ctx->ecount.ensure(256);
+        CK(cudaMemsetAsync(ctx->ecount.p, 0, 8, ctx->stream));
+        e.edge_out = ctx->ebuf.as<ulonglong2>(), e.edge_cap = sink->dev_cap;
+        e.edge_count = ctx->ecount.as<unsigned long long>();
+    }
     if (const char* ab = std::getenv("RHG_ABLATE")) e.ablate = std::atoi(ab);
     const char* dbg_env = std::getenv("RHG_DEBUG_STATS");
     const bool  dbg     = dbg_env && dbg_env[0] == '1';
@@ -695,7 +712,11 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     if (e.defer_ctr) CK(cudaMemcpyAsync(h_drop, e.defer_ctr + 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
     if (degrees)
         CK(cudaMemcpyAsync(degrees, ctx->degrees.p, pl.L.n * sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    auto* h_ecount = reinterpret_cast<unsigned long long*>(hc + 5);
+    *h_ecount      = 0;
+    if (sink) CK(cudaMemcpyAsync(h_ecount, ctx->ecount.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    if (sink) sink->count = *h_ecount;
     timeline_report(ctx, ctx->ev[0]);
     if (*h_ncls > kMaxCls) throw Invariant("dense engine: too many request segments");
     if (*h_drop) throw Invariant("dense engine: deferred-range list overflow");
@@ -820,9 +841,72 @@ void rhg_destroy(rhg_ctx* c) {
     delete c;
 }
 
+namespace {
+void generate_impl(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, rhg_run_stats* out,
+                   std::uint32_t* degrees, EdgeSink* sink);
+void from_points_impl(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, const rhg_points* pts,
+                      rhg_run_stats* out, std::uint32_t* degrees, EdgeSink* sink);
+// Sorts the sink's edges on the device and copies them to the caller's (u, v) array.
+void deliver_edges(rhg_ctx* ctx, const rhg_params* params, const EdgeSink& sink, std::uint64_t* edges,
+                   std::uint64_t cap, std::uint64_t* n_edges) {
+    *n_edges = sink.count;
+    if (!edges) return;
+    if (sink.count > cap)
+        throw InvalidArgument("rhg edges: the edge buffer holds " + std::to_string(cap) + " pairs, the graph has " +
+                              std::to_string(sink.count));
+    const std::uint64_t m = sink.count;
+    if (m >= (std::uint64_t(1) << 31)) throw InvalidArgument("rhg edges: more than 2^31 edges per call");
+    int bits = 1;
+    while (bits < 32 && (std::uint64_t(1) << bits) < params->n) ++bits;
+    ctx->ekeys.ensure(std::max<std::uint64_t>(m, 1) * 16);
+    auto*       ka  = ctx->ekeys.as<unsigned long long>();
+    auto*       kb  = ka + std::max<std::uint64_t>(m, 1);
+    std::size_t tmp = 0;
+    launch_sort_edges(ctx->ebuf.as<ulonglong2>(), m, ka, kb, nullptr, &tmp, 32 + bits, ctx->stream);
+    ctx->esort.ensure(std::max<std::size_t>(tmp, 256));
+    tmp = ctx->esort.cap;
+    launch_sort_edges(ctx->ebuf.as<ulonglong2>(), m, ka, kb, ctx->esort.p, &tmp, 32 + bits, ctx->stream);
+    if (m) CK(cudaMemcpyAsync(edges, ctx->ebuf.p, m * 16, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+}
+} // namespace
+
+int rhg_generate_edges(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, rhg_run_stats* out,
+                       std::uint64_t* edges, std::uint64_t cap, std::uint64_t* n_edges) {
+    return guarded([&] {
+        if (!ctx || !out || !n_edges || !params) throw InvalidArgument("rhg_generate_edges: null argument");
+        EdgeSink sink;
+        sink.dev_cap = edges ? cap : 0;
+        generate_impl(ctx, params, shard, out, nullptr, &sink);
+        deliver_edges(ctx, params, sink, edges, cap, n_edges);
+    });
+}
+
+int rhg_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, const rhg_points* pts,
+                          rhg_run_stats* out, std::uint64_t* edges, std::uint64_t cap, std::uint64_t* n_edges) {
+    return guarded([&] {
+        if (!ctx || !out || !n_edges || !params) throw InvalidArgument("rhg_edges_from_points: null argument");
+        EdgeSink sink;
+        sink.dev_cap = edges ? cap : 0;
+        from_points_impl(ctx, params, shard, pts, out, nullptr, &sink);
+        deliver_edges(ctx, params, sink, edges, cap, n_edges);
+    });
+}
+
 int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, rhg_run_stats* out,
                        std::uint32_t* degrees) {
-    return guarded([&] {
+    return guarded([&] { generate_impl(ctx, params, shard, out, degrees, nullptr); });
+}
+
+int rhg_count_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, const rhg_points* pts,
+                                rhg_run_stats* out, std::uint32_t* degrees) {
+    return guarded([&] { from_points_impl(ctx, params, shard, pts, out, degrees, nullptr); });
+}
+
+namespace {
+void generate_impl(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, rhg_run_stats* out,
+                   std::uint32_t* degrees, EdgeSink* sink) {
+    {
         if (!ctx || !out) throw InvalidArgument("rhg_generate_stats: null argument");
         const auto t0 = Clock::now();
         std::memset(out, 0, sizeof *out);
@@ -854,7 +938,7 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
             upload_tables_edges(ctx, pl, t, &out->h2d_bytes);
             host_ms += std::chrono::duration<double, std::milli>(Clock::now() - t2).count();
         }
-        run_edges(ctx, pl, t, out, degrees, true, split, &launches);
+        run_edges(ctx, pl, t, out, degrees, true, split, &launches, sink);
         fill_common(pl, out);
         out->sample_ms       = ms_between(ctx->ev[0], ctx->ev[1]);
         out->edges_ms        = ms_between(ctx->ev[1], ctx->ev[2]);
@@ -866,8 +950,9 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
                             ctx->degrees.cap + ctx->nid.cap + ctx->lcells.cap + ctx->perm.cap + ctx->s_beta.cap +
                             ctx->s_hw.cap + ctx->s_lt.cap + ctx->s_rec1.cap + ctx->s_rec2.cap + ctx->gbuf.cap;
         out->seconds = std::chrono::duration<double>(Clock::now() - t0).count();
-    });
+    }
 }
+} // namespace
 
 int rhg_sample_points(rhg_ctx* ctx, const rhg_params* params, rhg_points* o) {
     return guarded([&] {
@@ -935,9 +1020,10 @@ int rhg_sample_uniforms(rhg_ctx* ctx, const rhg_params* params, double* u_angle,
     });
 }
 
-int rhg_count_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, const rhg_points* pts,
-                                rhg_run_stats* out, std::uint32_t* degrees) {
-    return guarded([&] {
+namespace {
+void from_points_impl(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, const rhg_points* pts,
+                      rhg_run_stats* out, std::uint32_t* degrees, EdgeSink* sink) {
+    {
         if (!ctx || !out || !pts || !pts->beta || !pts->theta || !pts->half_width || !pts->coth_r ||
             !pts->inv_sinh_r || !pts->cos_theta || !pts->sin_theta)
             throw InvalidArgument("rhg_count_edges_from_points: null argument");
@@ -970,7 +1056,7 @@ int rhg_count_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rh
         CK(cudaEventRecord(ctx->ev[0], st));
         launch_frames_from_points(sampler_args(ctx, pl, t), st, &launches);
         CK(cudaEventRecord(ctx->ev[1], st));
-        run_edges(ctx, pl, t, out, degrees, false, false, &launches);
+        run_edges(ctx, pl, t, out, degrees, false, false, &launches, sink);
         fill_common(pl, out);
         out->sample_ms       = ms_between(ctx->ev[0], ctx->ev[1]);
         out->edges_ms        = ms_between(ctx->ev[1], ctx->ev[2]);
@@ -978,7 +1064,8 @@ int rhg_count_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rh
         out->host_ms         = host_ms;
         out->kernel_launches = launches;
         out->seconds         = std::chrono::duration<double>(Clock::now() - t0).count();
-    });
+    }
 }
+} // namespace
 
 } // extern "C"

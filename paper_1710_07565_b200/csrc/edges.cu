@@ -300,15 +300,31 @@ __device__ __forceinline__ bool edge_test(double cs, double sn, double coth, dou
     return lhs > rhs;
 }
 
-template <bool DEG>
+// Materialised edge stream (MODE 2): canonical (min id, max id) pairs appended
+// to A.edge_out with one warp-aggregated atomic per call site; the host sorts
+// them (rhg_generate_edges).  Pairs past edge_cap are counted, not written.
+__device__ __forceinline__ void emit_edge(const EdgeArgs& A, unsigned long long a, unsigned long long b) {
+    const unsigned           m      = __activemask();
+    const int                lane   = threadIdx.x & 31;
+    const int                leader = __ffs(m) - 1;
+    unsigned long long       base   = 0;
+    if (lane == leader) base = atomicAdd(A.edge_count, static_cast<unsigned long long>(__popc(m)));
+    base                          = __shfl_sync(m, base, leader);
+    const unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
+    if (slot < A.edge_cap) A.edge_out[slot] = make_ulonglong2(a < b ? a : b, a < b ? b : a);
+}
+
+// MODE: 0 = counters only, 1 = + per-vertex degrees, 2 = + materialised edges
+template <int MODE>
 __device__ __forceinline__ void count_edge(const EdgeArgs& A, bool e, unsigned long long id_r,
                                            unsigned long long id_n, Acc& acc) {
     acc.edges += e;
     acc.fp += e ? id_r + id_n : 0ull;
-    if (DEG && e) {
+    if (MODE == 1 && e) {
         atomicAdd(&A.degrees[id_r], 1u);
         atomicAdd(&A.degrees[id_n], 1u);
     }
+    if (MODE == 2 && e) emit_edge(A, id_r, id_n);
 }
 
 // ------------------------------------------------ streaming (sparse) ---
@@ -320,7 +336,7 @@ struct SRow { // one request as the cooperative loop reads it (broadcast from sh
 
 // Thread-serial pairs (rare): halo-block ranges and same-annulus pairs that
 // need the full (theta, id) dedup (sweep.hpp:517-526).
-template <bool DEG>
+template <int MODE>
 __device__ __forceinline__ void serial_range(const EdgeArgs& A, const SRow& q, double theta, bool dedup,
                                              std::uint64_t k0, std::uint64_t k1, Acc& acc) {
     for (std::uint64_t k = k0; k < k1; k += 4) { // four independent nodes in flight
@@ -340,7 +356,7 @@ __device__ __forceinline__ void serial_range(const EdgeArgs& A, const SRow& q, d
             if (!in) continue;
             if (A.dbg) atomicAdd(&A.dbg[5], 1ull);
             acc.comps += 1;
-            count_edge<DEG>(A, edge_test(q.cs, q.sn, q.coth, q.rci, n1[u], n2[u]), q.id, nid[u], acc);
+            count_edge<MODE>(A, edge_test(q.cs, q.sn, q.coth, q.rci, n1[u], n2[u]), q.id, nid[u], acc);
         }
     }
 }
@@ -423,7 +439,7 @@ struct SlabSmem {
     std::uint32_t      n_run;
 };
 
-template <bool DEG, int NT, int MINB>
+template <int MODE, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     constexpr int kSlabThreads = NT;
     extern __shared__ __align__(16) unsigned char slab_raw[];
@@ -615,10 +631,11 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                     if (e) {
                         const std::uint32_t nid = __float_as_uint(nd.w);
                         sum += nid + u.y, ++cnt; // < 2^32: a shard holds < 2^31 points
-                        if (DEG) {
+                        if (MODE == 1) {
                             atomicAdd(&A.degrees[base_a + u.y], 1u);
                             atomicAdd(&A.degrees[base_j + nid], 1u);
                         }
+                        if (MODE == 2) emit_edge(A, base_a + u.y, base_j + nid);
                     }
                 }
             } else { // windows so narrow that the FP64 rounding noise dominates: exact predicate only
@@ -633,10 +650,11 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                     if (edge_test(q0.x, q0.y, q1.x, q1.y, S.r1[k], S.r2[k])) {
                         const std::uint32_t nid = __float_as_uint(S.nd[k].w);
                         sum += nid + u.y, ++cnt;
-                        if (DEG) {
+                        if (MODE == 1) {
                             atomicAdd(&A.degrees[base_a + u.y], 1u);
                             atomicAdd(&A.degrees[base_j + nid], 1u);
                         }
+                        if (MODE == 2) emit_edge(A, base_a + u.y, base_j + nid);
                     }
                 }
             }
@@ -655,7 +673,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
 // request or node (full (theta, id) dedup, sweep.hpp:517-526).  Only the
 // requests near the end of the owned block (lambda >= tail_lam(a)) and the
 // halo requests can have such pairs; thread = one of them, all its sparse targets.
-template <bool DEG>
+template <int MODE>
 __global__ void __launch_bounds__(256) tail_kernel(EdgeArgs A) {
     const std::uint64_t t  = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     Acc                 acc;
@@ -698,11 +716,11 @@ __global__ void __launch_bounds__(256) tail_kernel(EdgeArgs A) {
                         if (p >= Aa.wrap) owned_range(A, Aj, lo, hi, g0, g1);
                         else g0 = Aj.wrap, g1 = lower_bound_owned(A, Aj, hi); // wrapped nodes
                     }
-                    if (g1 > g0) serial_range<DEG>(A, q, theta, own, g0, g1, acc);
+                    if (g1 > g0) serial_range<MODE>(A, q, theta, own, g0, g1, acc);
                 }
                 if (!halo_req && Aj.end > Aj.halo && hi > A.s_lam[Aj.halo] && lo <= A.s_lam[Aj.end - 1]) {
                     const std::uint64_t h0 = lower_bound_halo(A, Aj, lo), h1 = lower_bound_halo(A, Aj, hi);
-                    if (h1 > h0) serial_range<DEG>(A, q, theta, own, h0, h1, acc);
+                    if (h1 > h0) serial_range<MODE>(A, q, theta, own, h0, h1, acc);
                 }
             }
         }
@@ -879,7 +897,7 @@ __device__ __forceinline__ void defer_range(const EdgeArgs& A, std::uint32_t s, 
 }
 
 // One warp per deferred range: lanes stride its nodes.
-template <bool DEG>
+template <int MODE>
 __global__ void __launch_bounds__(256) deferred_kernel(EdgeArgs A) {
     const int                lane = threadIdx.x & 31;
     const unsigned long long n    = A.defer_ctr[0] < A.defer_cap ? A.defer_ctr[0] : A.defer_cap;
@@ -901,7 +919,7 @@ __global__ void __launch_bounds__(256) deferred_kernel(EdgeArgs A) {
             }
             if (!in) continue;
             acc.comps += 1;
-            count_edge<DEG>(A, edge_test(q.cs, q.sn, q.coth, q.rci, A.s_rec1[k], A.s_rec2[k]), q.id, nid, acc);
+            count_edge<MODE>(A, edge_test(q.cs, q.sn, q.coth, q.rci, A.s_rec1[k], A.s_rec2[k]), q.id, nid, acc);
         }
     }
     flush(acc, A, 1, lane);
@@ -916,7 +934,7 @@ __global__ void __launch_bounds__(256) deferred_kernel(EdgeArgs A) {
 // pairs that need the full (theta, id) dedup or live in the halo block run
 // right here, thread-serially.  Also writes the sorted request records and
 // the per-(segment, target) max half-width.
-template <bool DEG>
+template <int MODE>
 __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
     const std::uint64_t nR  = A.n_req;
     const int           nst = A.j1 - A.j0; // targets of this wave
@@ -1073,7 +1091,7 @@ __device__ __forceinline__ std::uint32_t gtheta_lb(const double* th, std::uint32
 // the nodes sit in registers, each chunk of 32 candidates is clipped to the
 // tile and compacted into (request, piece) entries in shared memory, and the
 // warp sweeps the entries (32-node slices outside an entry are skipped).
-template <bool DEG>
+template <int MODE>
 __global__ void __launch_bounds__(256, 2) glob_tiles_kernel(EdgeArgs A) {
     __shared__ GWarp    smem[8];
     const int           lane = threadIdx.x & 31;
@@ -1218,10 +1236,11 @@ __global__ void __launch_bounds__(256, 2) glob_tiles_kernel(EdgeArgs A) {
                             for (int q = 0; q < kQ; ++q) {
                                 const bool e = edge_test(cs, sn, coth, rci, n1[q], n2[q]);
                                 ecnt[q] += e, ce += e;
-                                if (DEG && e) {
+                                if (MODE == 1 && e) {
                                     atomicAdd(&A.degrees[E.id], 1u);
                                     atomicAdd(&A.degrees[A.s_id[t0 + std::uint32_t(lane + 32 * q)]], 1u);
                                 }
+                                if (MODE == 2 && e) emit_edge(A, E.id, A.s_id[t0 + std::uint32_t(lane + 32 * q)]);
                             }
                         } else {
 #pragma unroll
@@ -1230,10 +1249,11 @@ __global__ void __launch_bounds__(256, 2) glob_tiles_kernel(EdgeArgs A) {
                                 const std::uint32_t kl = std::uint32_t(lane + 32 * q);
                                 const bool e = kl >= el && kl < eh && edge_test(cs, sn, coth, rci, n1[q], n2[q]);
                                 ecnt[q] += e, ce += e;
-                                if (DEG && e) {
+                                if (MODE == 1 && e) {
                                     atomicAdd(&A.degrees[E.id], 1u);
                                     atomicAdd(&A.degrees[A.s_id[t0 + kl]], 1u);
                                 }
+                                if (MODE == 2 && e) emit_edge(A, E.id, A.s_id[t0 + kl]);
                             }
                         }
                         rsum += static_cast<unsigned long long>(__reduce_add_sync(kFull, ce)) * E.id;
@@ -1255,7 +1275,7 @@ __global__ void __launch_bounds__(256, 2) glob_tiles_kernel(EdgeArgs A) {
 }
 
 // generator.hpp:84-102: all pairs i < k of the global points, request = i.
-template <bool DEG>
+template <int MODE>
 __global__ void __launch_bounds__(kGGTile) glob_pairs_kernel(EdgeArgs A, std::uint64_t nT) {
     __shared__ double2 s1[kGGTile], s2[kGGTile];
     const std::uint64_t t = A.gg_tile_begin + blockIdx.x;
@@ -1283,7 +1303,7 @@ __global__ void __launch_bounds__(kGGTile) glob_pairs_kernel(EdgeArgs A, std::ui
         const std::uint64_t k1 = (J + 1) * kGGTile < nG ? (J + 1) * kGGTile : nG;
         acc.comps              = k1 > k0 ? k1 - k0 : 0;
         for (std::uint64_t k = k0; k < k1; ++k)
-            count_edge<DEG>(A, edge_test(cs, sn, coth, rci, s1[k - J * kGGTile], s2[k - J * kGGTile]), i, k, acc);
+            count_edge<MODE>(A, edge_test(cs, sn, coth, rci, s1[k - J * kGGTile], s2[k - J * kGGTile]), i, k, acc);
     }
     flush(acc, A, 2, threadIdx.x & 31);
 }
@@ -1313,6 +1333,17 @@ __global__ void __launch_bounds__(1024) reduce_counters_kernel(EdgeArgs A) {
     }
 }
 
+
+// ------------------------------------------------- materialised edges ---
+// Canonical order of an edge list (u < v, ascending by u then v): key = u << 32 | v.
+__global__ void edge_keys_kernel(const ulonglong2* __restrict__ e, std::uint64_t m, unsigned long long* __restrict__ k) {
+    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < m) k[i] = (e[i].x << 32) | e[i].y;
+}
+__global__ void edge_unpack_kernel(const unsigned long long* __restrict__ k, std::uint64_t m, ulonglong2* __restrict__ e) {
+    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < m) e[i] = make_ulonglong2(k[i] >> 32, k[i] & 0xffffffffull);
+}
 } // namespace
 
 void launch_cell_index(const EdgeArgs& a0, std::uint32_t blk_begin, std::uint32_t blk_end, int j_begin, int j_end,
@@ -1373,17 +1404,28 @@ void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, 
     a.mark("dense_prep", st);
 }
 
+// Launch kernel K<MODE> for the run-time mode (0 counters, 1 degrees, 2 edges).
+#define RHG_LAUNCH_MODE(K, mode, cfg, ...)                          \
+    do {                                                            \
+        if ((mode) == 2) K<2><<<cfg>>>(__VA_ARGS__);                \
+        else if ((mode) == 1) K<1><<<cfg>>>(__VA_ARGS__);           \
+        else K<0><<<cfg>>>(__VA_ARGS__);                            \
+    } while (0)
+#define RHG_CFG(...) __VA_ARGS__
+
 template <int NT, int MINB>
-void launch_slab(const EdgeArgs& a, unsigned n, bool deg, cudaStream_t st) {
+void launch_slab(const EdgeArgs& a, unsigned n, int mode, cudaStream_t st) {
     const int   smem = int(sizeof(SlabSmem<NT>));
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(slab_kernel<true, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(slab_kernel<false, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(slab_kernel<0, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(slab_kernel<1, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(slab_kernel<2, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    if (deg) slab_kernel<true, NT, MINB><<<n, NT, smem, st>>>(a);
-    else slab_kernel<false, NT, MINB><<<n, NT, smem, st>>>(a);
+    if (mode == 2) slab_kernel<2, NT, MINB><<<n, NT, smem, st>>>(a);
+    else if (mode == 1) slab_kernel<1, NT, MINB><<<n, NT, smem, st>>>(a);
+    else slab_kernel<0, NT, MINB><<<n, NT, smem, st>>>(a);
 }
 
 // One wave of edge work on st: dense rows and node tiles of the targets
@@ -1392,19 +1434,17 @@ void launch_slab(const EdgeArgs& a, unsigned n, bool deg, cudaStream_t st) {
 // final counter fold.  The dense requests must already be sorted
 // (launch_sort_globals) and the targets' annuli indexed (launch_cell_index).
 void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::uint64_t* launches) {
-    const bool deg = a0.degrees != nullptr;
+    const int  mode = a0.edge_out ? 2 : a0.degrees ? 1 : 0;
     EdgeArgs   a   = a0;
     a.j0 = W.j0, a.j1 = W.j1, a.slab0 = W.slab_begin;
     if (W.j1 > W.j0 && a.n_req && a.first_streaming < a.count) {
         const std::uint64_t rows = a.n_req * std::uint64_t(W.j1 - W.j0);
-        if (deg) req_rows_kernel<true><<<unsigned((rows + 255) / 256), 256, 0, st>>>(a);
-        else req_rows_kernel<false><<<unsigned((rows + 255) / 256), 256, 0, st>>>(a);
+        RHG_LAUNCH_MODE(req_rows_kernel, mode, RHG_CFG(unsigned((rows + 255) / 256), 256, 0, st), a);
         ++*launches;
         a.mark("rows", st);
         const std::uint64_t tw = W.tile_warps;
         if (tw) {
-            if (deg) glob_tiles_kernel<true><<<unsigned((tw + 7) / 8), 256, 0, st>>>(a);
-            else glob_tiles_kernel<false><<<unsigned((tw + 7) / 8), 256, 0, st>>>(a);
+            RHG_LAUNCH_MODE(glob_tiles_kernel, mode, RHG_CFG(unsigned((tw + 7) / 8), 256, 0, st), a);
             ++*launches;
             a.mark("tiles", st);
         }
@@ -1413,38 +1453,49 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         if (W.ev0) cudaEventRecord(W.ev0, st);
         const unsigned n   = unsigned(W.slab_end - W.slab_begin);
         static const int scfg = std::getenv("RHG_SLAB_CFG") ? std::atoi(std::getenv("RHG_SLAB_CFG")) : 0;
-        if (scfg == 0) launch_slab<256, 4>(a, n, deg, st); // measured best of 128..512 threads x 256..1024-node slabs
-        else launch_slab<128, 8>(a, n, deg, st);
+        if (scfg == 0) launch_slab<256, 4>(a, n, mode, st); // measured best of 128..512 threads x 256..1024-node slabs
+        else launch_slab<128, 8>(a, n, mode, st);
         ++*launches;
         if (W.tail && a.n_tail) {
-            if (deg) tail_kernel<true><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
-            else tail_kernel<false><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
+            RHG_LAUNCH_MODE(tail_kernel, mode, RHG_CFG(unsigned((a.n_tail + 255) / 256), 256, 0, st), a);
             ++*launches;
         }
         if (W.ev1) cudaEventRecord(W.ev1, st); // sparse engine of this wave (slab join [+ tail])
         a.mark("slab(+tail)", st);
     } else if (W.tail && a.n_tail) {
-        if (deg) tail_kernel<true><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
-        else tail_kernel<false><<<unsigned((a.n_tail + 255) / 256), 256, 0, st>>>(a);
+        RHG_LAUNCH_MODE(tail_kernel, mode, RHG_CFG(unsigned((a.n_tail + 255) / 256), 256, 0, st), a);
         ++*launches;
     }
     if (W.global_unit && a.gg_tile_end > a.gg_tile_begin) {
         const std::uint64_t nT     = (a.n_glob + kGGTile - 1) / kGGTile;
         const unsigned      blocks = unsigned(a.gg_tile_end - a.gg_tile_begin);
-        if (deg) glob_pairs_kernel<true><<<blocks, kGGTile, 0, st>>>(a, nT);
-        else glob_pairs_kernel<false><<<blocks, kGGTile, 0, st>>>(a, nT);
+        RHG_LAUNCH_MODE(glob_pairs_kernel, mode, RHG_CFG(blocks, kGGTile, 0, st), a, nT);
         ++*launches;
         a.mark("global_unit", st);
     }
     if (W.finish) {
         if (a.n_req) {
-            if (deg) deferred_kernel<true><<<148 * 4, 256, 0, st>>>(a);
-            else deferred_kernel<false><<<148 * 4, 256, 0, st>>>(a);
+            RHG_LAUNCH_MODE(deferred_kernel, mode, RHG_CFG(148 * 4, 256, 0, st), a);
             ++*launches;
         }
         reduce_counters_kernel<<<3, 1024, 0, st>>>(a);
         ++*launches;
     }
+}
+
+void launch_sort_edges(ulonglong2* edges, std::uint64_t m, unsigned long long* ka, unsigned long long* kb, void* tmp,
+                       std::size_t* tmp_bytes, int end_bit, cudaStream_t st) {
+    std::size_t need = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, need, ka, kb, int(m), 0, end_bit, st);
+    if (!tmp || *tmp_bytes < need) {
+        *tmp_bytes = need;
+        return;
+    }
+    if (m == 0) return;
+    const unsigned g = unsigned((m + 255) / 256);
+    edge_keys_kernel<<<g, 256, 0, st>>>(edges, m, ka);
+    cub::DeviceRadixSort::SortKeys(tmp, need, ka, kb, int(m), 0, end_bit, st);
+    edge_unpack_kernel<<<g, 256, 0, st>>>(kb, m, edges);
 }
 
 } // namespace rhgb

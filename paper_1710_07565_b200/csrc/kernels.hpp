@@ -119,6 +119,9 @@ struct EdgeArgs {
     Counters*         ctr = nullptr; // [0] streaming kernel, [1] dense engine, [2] global unit
     SlotCounter*      slots = nullptr; // [3 * kSlots] partial counters (folded into ctr at the end)
     int               ablate = 0;       // RHG_ABLATE bit flags: skip kernel phases (timing experiments; results invalid)
+    ulonglong2*         edge_out = nullptr;   // optional materialised edges (MODE 2): canonical (u, v)
+    unsigned long long  edge_cap = 0;
+    unsigned long long* edge_count = nullptr; // device counter of emitted edges (may exceed edge_cap)
     unsigned long long* dbg = nullptr; // optional path statistics (RHG_DEBUG_STATS=1), kDbgSlots entries
     unsigned int*     degrees = nullptr;
 };
@@ -135,6 +138,10 @@ struct EdgeWave {
     cudaEvent_t   ev0 = nullptr, ev1 = nullptr;   // optional: time the wave's sparse engine
 };
 void launch_edges(const EdgeArgs& a, const EdgeWave& w, cudaStream_t st, std::uint64_t* launches);
+// Sorts m canonical edges in place into (u, v) order (keys ka/kb: m each; ids < 2^32).
+// With tmp == nullptr or *tmp_bytes too small, only reports the scratch bytes needed.
+void launch_sort_edges(ulonglong2* edges, std::uint64_t m, unsigned long long* ka, unsigned long long* kb, void* tmp,
+                       std::size_t* tmp_bytes, int end_bit, cudaStream_t st);
 // Sorts the global points by (annulus, theta) into a.gperm (scratch layout
 // internal); with scratch == nullptr only reports the bytes needed in *need.
 void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, std::size_t* need, cudaStream_t st,
