@@ -20,6 +20,7 @@
  *   generate(params, opts, edge)  generator.hpp:135-215   rhg_generate_edges (canonical order)
  *   TextEdgeWriter/BinaryEdgeWriter io.hpp:20-68           rhg_write_edges_text / _binary
  *   read_binary_edges             io.hpp:70-96            rhg_read_edges_binary
+ *   naive_edges                   oracle.hpp:41-54        rhg_naive_edges (GPU brute force)
  *
  * Conventions: plain pointers and sizes, no exceptions across the ABI.
  * Every call returns RHG_OK (0) or an error code; rhg_last_error() gives the
@@ -160,6 +161,15 @@ int rhg_generate_edges(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
 /* The same for a GIVEN point set ("same points" mode, as rhg_count_edges_from_points). */
 int rhg_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, const rhg_points* pts,
                           rhg_run_stats* out, uint64_t* edges, uint64_t cap, uint64_t* n_edges);
+
+/* Brute-force oracle on the GPU (oracle.hpp:41-54 naive_edges): every pair
+ * u < v of the n given points (host arrays, id order) with
+ * hyperbolic_distance (geometry.hpp:117-123, direct formula) < R, as sorted
+ * canonical pairs.  n > 100000 fails like the reference's guard.  Same buffer
+ * protocol as rhg_generate_edges.  verify_against_oracle (oracle.hpp:70-111)
+ * is built on it in the Python mirror. */
+int rhg_naive_edges(rhg_ctx* ctx, uint64_t n, double R, const double* r, const double* theta, uint64_t* edges,
+                    uint64_t cap, uint64_t* n_edges);
 
 /* Edge stream file formats, byte-compatible with io.hpp:20-96:
  * text = one "u v\n" per edge (decimal); binary = 8-byte magic "RHGE0001"

@@ -331,3 +331,91 @@ def read_edges_binary(path: str) -> np.ndarray:
     _io_check(lib().rhg_read_edges_binary(str(path).encode(), buf.ctypes.data_as(C.POINTER(C.c_uint64)), m.value,
                                           C.byref(m)))
     return buf
+
+
+# ------------------------------------------------- brute-force oracle ---
+# the vertex stream (sample_points) and the brute-force
+# verifier of oracle.hpp:26-111, with the quadratic all-pairs check on the GPU.
+
+NAIVE_ORACLE_GUARD = 100000  # oracle.hpp:41
+
+
+def naive_edges(points, R: float, device: int = 0) -> np.ndarray:
+    """oracle.hpp:44-54 on the GPU: all pairs u < v (sorted) of the points
+    (id order; fields r, theta) with hyperbolic_distance < R."""
+    r = np.ascontiguousarray(points.r, np.float64)
+    th = np.ascontiguousarray(points.theta, np.float64)
+    n = len(r)
+    ctx = _Context.get(device)
+    m = C.c_uint64(0)
+    P64 = C.POINTER(C.c_uint64)
+    check(lib().rhg_naive_edges(ctx, n, float(R), r.ctypes.data_as(_native.P_f64), th.ctypes.data_as(_native.P_f64),
+                                None, 0, C.byref(m)))
+    buf = np.empty((m.value, 2), np.uint64)
+    check(lib().rhg_naive_edges(ctx, n, float(R), r.ctypes.data_as(_native.P_f64), th.ctypes.data_as(_native.P_f64),
+                                buf.ctypes.data_as(P64), m.value, C.byref(m)))
+    return buf
+
+
+def hyperbolic_distance(r1, t1, r2, t2):
+    """geometry.hpp:117-123 (host, float64, vectorised; canonical r1 <= r2)."""
+    a, b = np.minimum(r1, r2), np.maximum(r1, r2)
+    arg = np.cosh(b - a) + (1.0 - np.cos(np.abs(t1 - t2))) * np.sinh(a) * np.sinh(b)
+    return np.where(arg <= 1.0, 0.0, np.arccosh(np.maximum(arg, 1.0)))
+
+
+@dataclass
+class CompareReport:
+    """oracle.hpp:60-63."""
+    missing: int = 0
+    extra: int = 0
+    duplicates: int = 0
+    boundary_band: int = 0
+
+    def clean(self) -> bool:
+        return self.missing == 0 and self.extra == 0 and self.duplicates == 0
+
+
+def compare(generated, oracle_edges, points=None, R: float = 0.0) -> CompareReport:
+    """oracle.hpp:65-104: exact multiset diff of two edge streams; mismatches
+    within 1e-9 R of the threshold count as boundary_band, not as errors."""
+    def canon(e):
+        e = np.asarray(e, np.uint64).reshape(-1, 2)
+        lo, hi = np.minimum(e[:, 0], e[:, 1]), np.maximum(e[:, 0], e[:, 1])
+        return lo.astype(np.uint64), hi.astype(np.uint64)
+
+    rep = CompareReport()
+    glo, ghi = canon(generated)
+    olo, ohi = canon(oracle_edges)
+    if (len(ghi) and ghi.max() >= 2**32) or (len(ohi) and ohi.max() >= 2**32):
+        raise ValueError("compare: vertex ids must be < 2^32")
+    g = np.sort((glo << np.uint64(32)) | ghi)  # one 64-bit key per edge
+    o = np.unique((olo << np.uint64(32)) | ohi)
+    gu, gc = np.unique(g, return_counts=True)
+    rep.duplicates = int((gc - 1).sum())
+    only_g = np.setdiff1d(gu, o, assume_unique=True)
+    only_o = np.setdiff1d(o, gu, assume_unique=True)
+
+    def band(keys):
+        if points is None or R <= 0.0 or len(keys) == 0:
+            return np.zeros(len(keys), bool)
+        keys = np.asarray(keys, dtype=np.uint64)
+        u, v = keys >> np.uint64(32), keys & np.uint64(0xFFFFFFFF)
+        d = hyperbolic_distance(points.r[u], points.theta[u], points.r[v], points.theta[v])
+        return np.abs(d - R) < 1e-9 * R
+
+    bg, bo = band(only_g), band(only_o)
+    rep.boundary_band = int(bg.sum() + bo.sum())
+    rep.extra = int((~bg).sum())
+    rep.missing = int((~bo).sum())
+    return rep
+
+
+def verify_against_oracle(params: ModelParams, opts: GenOptions = GenOptions()) -> CompareReport:
+    """oracle.hpp:106-111: generate with params, diff against the brute-force
+    oracle on the generator's own vertex stream (both on the GPU)."""
+    if params.n > NAIVE_ORACLE_GUARD:
+        raise ValueError("verify_against_oracle: refusing quadratic work above n = 100000")
+    edges, _ = generate_edges(params, opts)
+    pts = sample_points(params, opts)
+    return compare(edges, naive_edges(pts, params.R, opts.device), pts, params.R)

@@ -898,6 +898,44 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
     return guarded([&] { generate_impl(ctx, params, shard, out, degrees, nullptr); });
 }
 
+int rhg_naive_edges(rhg_ctx* ctx, std::uint64_t n, double R, const double* r, const double* theta,
+                    std::uint64_t* edges, std::uint64_t cap, std::uint64_t* n_edges) {
+    return guarded([&] {
+        if (!ctx || !n_edges || (n && (!r || !theta))) throw InvalidArgument("rhg_naive_edges: null argument");
+        if (n > 100000) throw InvalidArgument("naive_edges: refusing quadratic work above n = 100000");
+        CK(cudaSetDevice(ctx->device));
+        cudaStream_t st = ctx->stream;
+        ctx->beta.ensure(std::max<std::uint64_t>(n, 1) * 8);
+        ctx->hw.ensure(std::max<std::uint64_t>(n, 1) * 8);
+        ctx->r_out.ensure(std::max<std::uint64_t>(n, 1) * 8);
+        ctx->ecount.ensure(256);
+        if (n) {
+            CK(cudaMemcpyAsync(ctx->beta.p, r, n * 8, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(ctx->hw.p, theta, n * 8, cudaMemcpyHostToDevice, st));
+        }
+        std::uint64_t dev_cap = edges ? cap : 0;
+        for (int pass = 0; pass < 2; ++pass) { // pass 2 only when the caller's capacity is unknown (count)
+            ctx->ebuf.ensure(std::max<std::uint64_t>(dev_cap, 1) * sizeof(ulonglong2));
+            launch_naive_pairs(ctx->beta.as<double>(), ctx->hw.as<double>(), ctx->r_out.as<double>(), n, R,
+                               ctx->ebuf.as<ulonglong2>(), dev_cap, ctx->ecount.as<unsigned long long>(), st);
+            unsigned long long m = 0;
+            CK(cudaMemcpyAsync(&m, ctx->ecount.p, 8, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            EdgeSink sink;
+            sink.count = m;
+            if (m <= dev_cap || !edges) {
+                rhg_params P{};
+                P.n = n;
+                deliver_edges(ctx, &P, sink, edges, cap, n_edges);
+                return;
+            }
+            *n_edges = m;
+            throw InvalidArgument("rhg_naive_edges: the edge buffer holds " + std::to_string(cap) +
+                                  " pairs, the oracle has " + std::to_string(m));
+        }
+    });
+}
+
 int rhg_count_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, const rhg_points* pts,
                                 rhg_run_stats* out, std::uint32_t* degrees) {
     return guarded([&] { from_points_impl(ctx, params, shard, pts, out, degrees, nullptr); });

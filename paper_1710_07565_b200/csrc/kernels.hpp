@@ -138,6 +138,9 @@ struct EdgeWave {
     cudaEvent_t   ev0 = nullptr, ev1 = nullptr;   // optional: time the wave's sparse engine
 };
 void launch_edges(const EdgeArgs& a, const EdgeWave& w, cudaStream_t st, std::uint64_t* launches);
+// naive.cu: brute-force pairs with hyperbolic distance < R (oracle.hpp:41-54), unsorted.
+void launch_naive_pairs(const double* r, const double* theta, double* sh, std::uint64_t n, double R, ulonglong2* out,
+                        unsigned long long cap, unsigned long long* count, cudaStream_t st);
 // Sorts m canonical edges in place into (u, v) order (keys ka/kb: m each; ids < 2^32).
 // With tmp == nullptr or *tmp_bytes too small, only reports the scratch bytes needed.
 void launch_sort_edges(ulonglong2* edges, std::uint64_t m, unsigned long long* ka, unsigned long long* kb, void* tmp,
