@@ -323,7 +323,7 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
         for (std::uint32_t k = j0; k < j1; ++k) { // job_order is by descending count inside a wave
             LB lb = heap.top();
             heap.pop();
-            lb.first += pl.jobs[pl.job_order[k]].count + 64; // + per-stream overhead
+            lb.first += pl.jobs[pl.job_order[k]].count + 1250; // + per-stream pipeline fill / seeding
             bin[lb.second].push_back(pl.job_order[k]);
             heap.push(lb);
         }

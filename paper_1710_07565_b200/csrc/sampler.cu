@@ -1,20 +1,23 @@
 // Device point sampler (sm_100a): the reference's ChunkPointSource
 // (sweep.hpp:102-141) for every (annulus, chunk) stream of a shard.
 //
-//   S1 mt_uniforms_kernel   one warp per (stream, {angles, radii}): std::mt19937_64
-//                           seeded by derive_seed(seed,{3|4,i,c}) (rng.hpp:41-69),
-//                           312-word twist done warp-parallel in shared memory,
-//                           output (x >> 11) * 2^-53 written coalesced.
-//   S2 point_pow_kernel     per point: x_k = pow(U_k, 1/remaining) for the
-//                           sorted stream (rng.hpp:221);
-//      point_radial_kernel  per point, on a side stream beside S2/S3: the
-//                           radius-only attributes r, coth r, 1/sinh r,
-//                           half-width (partition.hpp:64-70, sweep.hpp:121-134).
-//   S3 sorted_chain_kernel  one warp per angle stream: the serial product
-//                           chain cur *= x_k, beta = a + w (1 - cur), clamp
-//                           (rng.hpp:218-229) — the only serial dependency.
-//   S4 point_angular_kernel per point: theta = beta + hw (mod 2pi), cos, sin,
-//                           engine-frame beta/lambda (sweep.hpp:135-139, 478-480).
+//   S1 angle_side_kernel    one CTA per chain bin (the host packs each wave's
+//                           streams longest-first into bins of about the longest
+//                           chain): per stream, a 3-stage pipeline over 312-value
+//                           blocks — std::mt19937_64 seeded by derive_seed(seed,
+//                           {3,i,c}) (rng.hpp:41-69, warp-parallel twist), the
+//                           factors pow(U_k, 1/remaining) (rng.hpp:221), and the
+//                           serial product chain cur *= x_k with beta = a + w (1 -
+//                           cur), clamped (rng.hpp:218-229) — the only serial
+//                           dependency, run by one lane from shared memory.
+//   S2 mt_uniforms_kernel   one CTA per (stream, radii): the radius uniforms
+//                           (seed {4,i,c}), twist warp + tempering warps.
+//      point_radial_kernel  per point, on a side stream beside S1: the radius-only
+//                           attributes r, coth r, 1/sinh r, half-width
+//                           (partition.hpp:64-70, sweep.hpp:121-134).
+//   S3 point_angular_kernel per global point: theta = beta + hw (mod 2pi), cos, sin
+//                           (sweep.hpp:135-139); streaming points get theirs in the
+//                           sort phase (edges.cu angular_scatter_kernel).
 //
 // All exact-rounding steps use __dmul_rn/__dadd_rn (no FMA contraction).
 #include <cstdlib>
@@ -147,16 +150,6 @@ __device__ __forceinline__ int find_job(const StreamJob* __restrict__ jobs, int 
     return lo;
 }
 
-// rng.hpp:221: cur_max *= pow(U, 1.0 / remaining), remaining = count - k
-__global__ void point_pow_kernel(const StreamJob* __restrict__ jobs, int njobs, std::uint64_t total,
-                                 double* __restrict__ u_ang) {
-    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= total) return;
-    const StreamJob&    J   = jobs[find_job(jobs, njobs, i)];
-    const double        rem = double(J.count - (i - J.out_off));
-    u_ang[i]                = pow(u_ang[i], __ddiv_rn(1.0, rem));
-}
-
 // partition.hpp:64-70 radius_from_uniform, then sweep.hpp:125-134.
 __global__ void point_radial_kernel(const StreamJob* __restrict__ jobs, int njobs, const AnnulusDev* __restrict__ ann,
                                     double alpha, std::uint64_t total, double* __restrict__ hw_out,
@@ -179,85 +172,106 @@ __global__ void point_radial_kernel(const StreamJob* __restrict__ jobs, int njob
     if (r_out) r_out[i] = r;
 }
 
-// rng.hpp:218-229.  One single-warp CTA per chain bin (the host packs the
-// streams into bins whose lengths add up to about the longest chain, so few
-// chain warps share an SM): for each stream of its bin the 32 lanes stage a
-// tile of pow factors into shared memory (coalesced, the next tile prefetched
-// into registers), lane 0 alone runs the serial chain cur = fl(cur * x_k)
-// over the tile from shared memory (vector loads two batches ahead in
-// ping-pong registers, so the loop-carried dependency is one DMUL per point
-// and no shuffles), and the warp maps the tile's products to
-// beta = a + w (1 - cur), clamped, with a coalesced store.  Past-the-end
-// factors are 1.0: fl(cur * 1.0) == cur.
-constexpr int kChainQ = 16;               // tile = 32 * kChainQ points
-constexpr int kChainT = 32 * kChainQ;
-__global__ void __launch_bounds__(32) sorted_chain_kernel(const StreamJob* __restrict__ jobs,
-                                                          const std::uint32_t* __restrict__ bins,
-                                                          const std::uint32_t* __restrict__ order,
-                                                          double* __restrict__ x) {
-    __shared__ __align__(16) double tile[kChainT];
-    const int lane = threadIdx.x;
-    for (std::uint32_t jb = bins[blockIdx.x]; jb < bins[blockIdx.x + 1]; ++jb) {
-        const StreamJob&    J = jobs[order[jb]];
-        double*             p = x + J.out_off;
-        const std::uint64_t n = J.count;
+// The whole angle side of one chain bin in one CTA (rng.hpp:58-69 + 209-244):
+// warp 1 regenerates the stream's std::mt19937_64 output (seeding, warp-
+// parallel twist, tempering -> 53-bit uniforms) one 312-value block at a time,
+// warps 2.. turn block b-1 into the factors pow(U_k, 1/remaining_k) (about
+// one per thread: pow's latency, not its throughput, bounds the stage), and
+// warp 0 runs the serial chain cur = fl(cur * x_k) over block b-2 (lane 0,
+// from shared memory) and writes beta_k = a + w (1 - cur) (clamped) — a
+// three-stage pipeline with one __syncthreads per block, so the chain (the
+// only serial dependency) starts after the first two blocks instead of after
+// two full-array kernels.  Same arithmetic, same order as the separate
+// mt_uniforms / point_pow / sorted_chain kernels.
+#ifndef RHG_ANG_WARPS
+#define RHG_ANG_WARPS 8 // measured: 6 -> 4.35 ms, 8 -> 4.31, 10 -> 4.34, 12 -> 4.34 (cfg2 step)
+#endif
+constexpr int kAngWarps = RHG_ANG_WARPS; // warp 0: chain, warp 1: MT, warps 2..: pow factors
+struct AngSmem {
+    std::uint64_t st[2][kMtN];   // MT state, double-buffered (warp 1)
+    double        u[2][kMtN];    // uniforms of blocks b, b-1
+    double        x[2][kMtN];    // pow factors of blocks b-1, b-2 (products in place)
+};
+__global__ void __launch_bounds__(32 * kAngWarps) angle_side_kernel(const StreamJob* __restrict__ jobs,
+                                                                    const std::uint32_t* __restrict__ bins,
+                                                                    int nbins, const std::uint32_t* __restrict__ order,
+                                                                    double* __restrict__ beta_out) {
+    __shared__ __align__(16) AngSmem S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bin  = blockIdx.x;
+    if (bin >= nbins) return;
+    for (std::uint32_t jb = bins[bin]; jb < bins[bin + 1]; ++jb) {
+        const StreamJob&    J    = jobs[order[jb]];
+        const std::uint64_t n    = J.count;
+        const std::uint64_t nblk = (n + kMtN - 1) / kMtN;
+        double*             p    = beta_out + J.out_off;
         const double        a = J.a, b = J.b, wd = fsub(b, a);
         const double        bmax = nextafter(b, a);
-        double              cur  = 1.0; // lane 0's chain state
-        double              nxt[kChainQ];
-#pragma unroll
-        for (int q = 0; q < kChainQ; ++q) {
-            const std::uint64_t k = std::uint64_t(lane) + 32u * q;
-            nxt[q]                = k < n ? p[k] : 1.0;
-        }
-        for (std::uint64_t base = 0; base < n; base += kChainT) {
-#pragma unroll
-            for (int q = 0; q < kChainQ; ++q) tile[lane + 32 * q] = nxt[q];
-            const std::uint64_t nb = base + kChainT;
-#pragma unroll
-            for (int q = 0; q < kChainQ; ++q) { // prefetch the next tile while the chain runs
-                const std::uint64_t k = nb + std::uint64_t(lane) + 32u * q;
-                nxt[q]                = k < n ? p[k] : 1.0;
+        double              cur  = 1.0; // lane 0 of warp 0
+        if (warp == 1 && lane == 0) {   // [rand.predef] seeding recurrence (serial by definition)
+            std::uint64_t z = J.seed_ang;
+            S.st[0][0]      = z;
+            for (int i = 1; i < kMtN; ++i) {
+                z          = 6364136223846793005ull * (z ^ (z >> 62)) + std::uint64_t(i);
+                S.st[0][i] = z;
             }
-            __syncwarp();
-            if (lane == 0) {
-                const double2* t2 = reinterpret_cast<const double2*>(tile);
-                double2*       o2 = reinterpret_cast<double2*>(tile);
-                constexpr int  kB = 8; // double2 per batch (16 points); batches A, B alternate
-                double2        A[kB], B[kB];
+        }
+        __syncwarp();
+        for (std::uint64_t s = 0; s < nblk + 2; ++s) {
+            if (warp == 1 && s < nblk) { // block s: state after s + 1 twists
+                const std::uint64_t* A = S.st[s & 1];
+                std::uint64_t*       B = S.st[(s + 1) & 1];
+                mt_twist_to(A, B, lane);
+                double* u = S.u[s & 1];
+                for (int i = lane; i < kMtN; i += 32) u[i] = double(mt_temper(B[i]) >> 11) * 0x1.0p-53;
+            } else if (warp >= 2 && s >= 1 && s <= nblk) { // block s - 1: pow factors
+                const std::uint64_t base = (s - 1) * kMtN;
+                const double*       u    = S.u[(s - 1) & 1];
+                double*             x    = S.x[(s - 1) & 1];
+                for (int i = threadIdx.x - 64; i < kMtN; i += 32 * (kAngWarps - 2)) {
+                    const std::uint64_t k = base + std::uint64_t(i);
+                    x[i] = k < n ? pow(u[i], __ddiv_rn(1.0, double(n - k))) : 1.0; // rng.hpp:221, past the end: 1
+                }
+            } else if (warp == 0 && s >= 2) { // block s - 2: the chain, then beta
+                const std::uint64_t base = (s - 2) * kMtN;
+                double*             x    = S.x[s & 1]; // == (s - 2) & 1
+                if (lane == 0) {
+                    double2*      x2 = reinterpret_cast<double2*>(x);
+                    constexpr int kB = 6;              // 156 double2 = 13 batches of 12 values
+                    double2       A[kB], B[kB];
 #pragma unroll
-                for (int i = 0; i < kB; ++i) A[i] = t2[i];
+                    for (int i = 0; i < kB; ++i) A[i] = x2[i];
 #pragma unroll 1
-                for (int bb = 0; bb < kChainT / 2; bb += 2 * kB) {
+                    for (int bb = 0; bb < kMtN / 2; bb += 2 * kB) {
 #pragma unroll
-                    for (int i = 0; i < kB; ++i) B[i] = t2[bb + kB + i];
+                        for (int i = 0; i < kB; ++i) B[i] = bb + kB + i < kMtN / 2 ? x2[bb + kB + i] : make_double2(1.0, 1.0);
 #pragma unroll
-                    for (int i = 0; i < kB; ++i) {
-                        double2 o;
-                        cur = fmul(cur, A[i].x), o.x = cur;
-                        cur = fmul(cur, A[i].y), o.y = cur;
-                        o2[bb + i] = o;
-                    }
-                    const int na = bb + 2 * kB < kChainT / 2 ? bb + 2 * kB : 0;
+                        for (int i = 0; i < kB; ++i) {
+                            double2 o;
+                            cur = fmul(cur, A[i].x), o.x = cur;
+                            cur = fmul(cur, A[i].y), o.y = cur;
+                            x2[bb + i] = o;
+                        }
+                        if (bb + kB >= kMtN / 2) break;
 #pragma unroll
-                    for (int i = 0; i < kB; ++i) A[i] = t2[na + i];
+                        for (int i = 0; i < kB; ++i) A[i] = bb + 2 * kB + i < kMtN / 2 ? x2[bb + 2 * kB + i] : make_double2(1.0, 1.0);
 #pragma unroll
-                    for (int i = 0; i < kB; ++i) {
-                        double2 o;
-                        cur = fmul(cur, B[i].x), o.x = cur;
-                        cur = fmul(cur, B[i].y), o.y = cur;
-                        o2[bb + kB + i] = o;
+                        for (int i = 0; i < kB; ++i) {
+                            double2 o;
+                            cur = fmul(cur, B[i].x), o.x = cur;
+                            cur = fmul(cur, B[i].y), o.y = cur;
+                            x2[bb + kB + i] = o;
+                        }
                     }
                 }
+                __syncwarp();
+                for (int i = lane; i < kMtN; i += 32) {
+                    const std::uint64_t k = base + std::uint64_t(i);
+                    const double        y = fadd(a, fmul(wd, fsub(1.0, x[i])));
+                    if (k < n) p[k] = y >= b ? bmax : y;
+                }
             }
-            __syncwarp();
-#pragma unroll
-            for (int q = 0; q < kChainQ; ++q) {
-                const std::uint64_t k = base + std::uint64_t(lane) + 32u * q;
-                const double        y = fadd(a, fmul(wd, fsub(1.0, tile[lane + 32 * q])));
-                if (k < n) p[k] = y >= b ? bmax : y;
-            }
-            __syncwarp();
+            __syncthreads();
         }
     }
 }
@@ -299,68 +313,60 @@ __global__ void frames_from_points_kernel(const StreamJob* __restrict__ jobs, in
 
 } // namespace
 
-// Two streams: the angle side (MT -> pow -> serial chain) is latency-bound
-// and occupies few SMs, so the radius side (MT -> radial attributes) runs
-// beside it on a second stream; the angular kernel joins both.
+// Streams: the angle side of every chain bin is one fused kernel
+// (angle_side_kernel: MT -> pow -> serial chain -> beta), wave 1 on st and
+// wave 2 (the outermost annulus, the longest chains) on S.late, signalling
+// S.ev_late, so the inner annuli's sort and edge work overlaps its tail; the
+// radius side (MT -> radial attributes) runs on S.side and joins st.
 void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
     if (S.total == 0 || S.njobs == 0) return;
     const int      mt_blocks = S.njobs; // one CTA per stream
     const unsigned pblocks   = unsigned((S.total + 255) / 256);
     cudaStream_t   side      = S.side ? S.side : st;
+    static const int sched   = std::getenv("RHG_SCHED") ? std::atoi(std::getenv("RHG_SCHED")) : 0;
     if (S.side) {
         cudaEventRecord(S.ev_fork, st);
         cudaStreamWaitEvent(side, S.ev_fork, 0);
     }
-    // the radius attributes are needed only by the sort phase: they run beside the (few-SM)
-    // chains, after pow, instead of competing with pow for the FP64 pipes
-    mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, side>>>(S.jobs, S.njobs, S.beta, S.hw, 2);
-    S.mark("mt_radii", side);
-    mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 1);
-    S.mark("mt_angles", st);
-    static const int sched = std::getenv("RHG_SCHED") ? std::atoi(std::getenv("RHG_SCHED")) : 0;
-    if (sched == 1) {
-        point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
-        S.mark("radial", side);
-    }
-    point_pow_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.total, S.beta);
-    S.mark("pow", st);
-    if (sched == 2) {
-        point_radial_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
-        S.mark("radial", st);
-    }
-    if (S.side) {
-        cudaEventRecord(S.ev_fork, st);
-        cudaStreamWaitEvent(side, S.ev_fork, 0);
-    }
-    if (sched == 0) {
-        point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
-        S.mark("radial", side);
-    }
-    // chains: wave 1 on st; wave 2 (the outermost annulus, the longest chains) on S.late,
-    // signalling S.ev_late, so the inner annuli's edge work overlaps its tail
     const bool split = S.wave2_jobs && S.late;
     const int  nb1   = split ? S.chain_bins1 : S.chain_bins_total;
     if (split && S.chain_bins_total > nb1) {
         cudaEventRecord(S.ev_pow, st);
         cudaStreamWaitEvent(S.late, S.ev_pow, 0);
-        sorted_chain_kernel<<<S.chain_bins_total - nb1, 32, 0, S.late>>>(S.jobs, S.chain_bins + nb1, S.job_order,
-                                                                         S.beta);
+        angle_side_kernel<<<S.chain_bins_total - nb1, 32 * kAngWarps, 0, S.late>>>(
+            S.jobs, S.chain_bins + nb1, S.chain_bins_total - nb1, S.job_order, S.beta);
         cudaEventRecord(S.ev_late, S.late);
         S.mark("chain_wave2(late)", S.late);
         ++*launches;
     }
-    if (nb1) sorted_chain_kernel<<<nb1, 32, 0, st>>>(S.jobs, S.chain_bins, S.job_order, S.beta);
+    mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, side>>>(S.jobs, S.njobs, S.beta, S.hw, 2);
+    S.mark("mt_radii", side);
+    ++*launches;
+    if (sched != 2) {
+        point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
+        S.mark("radial", side);
+        ++*launches;
+    }
+    if (nb1) {
+        angle_side_kernel<<<nb1, 32 * kAngWarps, 0, st>>>(S.jobs, S.chain_bins, nb1, S.job_order, S.beta);
+        ++*launches;
+    }
     S.mark("chain_wave1", st);
     if (S.side) {
         cudaEventRecord(S.ev_join, side);
         cudaStreamWaitEvent(st, S.ev_join, 0);
+    }
+    if (sched == 2) {
+        point_radial_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
+        S.mark("radial", st);
+        ++*launches;
     }
     // generate mode: streaming points get their frames in the sort phase (edges.cu angular_scatter_kernel)
     const std::uint64_t first = S.angular_from;
     if (S.total > first)
         point_angular_kernel<<<unsigned((S.total - first + 255) / 256), 256, 0, st>>>(
             S.jobs, S.njobs, first, S.total, S.beta, S.hw, S.rec0, S.rec1, S.beta_unlifted_out);
-    *launches += 6;
+    *launches += 1;
 }
 
 void launch_mt_uniforms(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
