@@ -116,6 +116,7 @@ struct rhg_ctx {
     DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, tables2, cells, counters, degrees, dbg, nid;
     DevBuf       lcells, perm, s_beta, s_hw, s_lt, s_rec1, s_rec2, gsort, gbuf;
     DevBuf       ebuf, ecount, ekeys, esort; // materialised edges (rhg_generate_edges)
+    DevBuf       lam_tmp;
     HostPinned   staging, staging2, readback; // table parts 1 and 2, counter readback
 };
 
@@ -569,6 +570,8 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     {
         const std::size_t ne = pl.n_ext + 2;
         ctx->perm.ensure(ne * sizeof(std::uint64_t));
+        ctx->lam_tmp.ensure(ne * sizeof(double));
+        e.lam_tmp = ctx->lam_tmp.as<double>();
         ctx->s_beta.ensure(ne * sizeof(double));
         ctx->s_hw.ensure(ne * sizeof(double));
         ctx->s_lt.ensure(2 * ne * sizeof(double));

@@ -118,10 +118,6 @@ __device__ __forceinline__ double frame_beta(const EdgeArgs& A, const AnnulusDev
     const double b = A.beta[i];
     return GEN && A.lift_part && i >= J.halo ? fadd(b, kTwoPiD) : b;
 }
-template <bool GEN>
-__device__ __forceinline__ double frame_lambda(const EdgeArgs& A, const AnnulusDev& J, std::uint64_t i) {
-    return GEN ? fadd(frame_beta<true>(A, J, i), A.hw[i]) : A.rec0[i].x;
-}
 
 template <bool GEN>
 __global__ void __launch_bounds__(256) beta_cells_kernel(EdgeArgs A) {
@@ -138,10 +134,12 @@ __global__ void __launch_bounds__(256) beta_cells_kernel(EdgeArgs A) {
     const AnnulusDev&   J = A.ann[j];
     unsigned long long  hwbits = 0;
     if (i < J.end) {
-        const std::uint32_t k  = cellf(J, frame_beta<GEN>(A, J, i));
+        const double        bi = frame_beta<GEN>(A, J, i), hi = A.hw[i];
+        const std::uint32_t k  = cellf(J, bi);
         const std::int64_t  kp = i > J.off ? std::int64_t(cellf(J, frame_beta<GEN>(A, J, i - 1))) : -1;
         cell_fill(A.cellstart + J.cell_off, kp, k, i);
-        hwbits = static_cast<unsigned long long>(__double_as_longlong(A.hw[i])); // hw >= +0
+        hwbits     = static_cast<unsigned long long>(__double_as_longlong(hi)); // hw >= +0
+        A.lam_tmp[i] = GEN ? fadd(bi, hi) : A.rec0[i].x; // engine-frame lambda, read by rank_kernel
     }
     __shared__ unsigned long long wmax[8]; // one atomic per block (all its points share the annulus)
     const unsigned long long m = warp_max_u64(hwbits);
@@ -167,7 +165,7 @@ __global__ void __launch_bounds__(256) rank_kernel(EdgeArgs A) {
     if (i >= J.end) return;
     const bool          hb = i >= J.halo;
     const std::uint64_t bs = hb ? J.halo : J.off, be = hb ? J.end : J.halo;
-    const double        li = frame_lambda<GEN>(A, J, i);
+    const double        li = A.lam_tmp[i];
     const double        dm = __longlong_as_double(static_cast<long long>(A.dmax_bits[j]));
     std::uint64_t       k0 = A.cellstart[J.cell_off + cellf(J, fsub(fsub(li, dm), 1e-12))];
     std::uint64_t       k1 = A.cellstart[J.cell_off + cellf(J, li) + 1];
@@ -175,7 +173,7 @@ __global__ void __launch_bounds__(256) rank_kernel(EdgeArgs A) {
     k1 = k1 > be ? be : k1;
     std::uint64_t rank = k0 - bs;
     for (std::uint64_t k = k0; k < k1; ++k) {
-        const double lk = frame_lambda<GEN>(A, J, k);
+        const double lk = A.lam_tmp[k];
         rank += (lk < li) || (lk == li && k < i);
     }
     A.perm[i] = bs + rank;

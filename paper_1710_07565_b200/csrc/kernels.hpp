@@ -119,6 +119,7 @@ struct EdgeArgs {
     Counters*         ctr = nullptr; // [0] streaming kernel, [1] dense engine, [2] global unit
     SlotCounter*      slots = nullptr; // [3 * kSlots] partial counters (folded into ctr at the end)
     int               ablate = 0;       // RHG_ABLATE bit flags: skip kernel phases (timing experiments; results invalid)
+    double*             lam_tmp = nullptr;    // [n_ext] engine-frame lambda in sampler order (sort phase)
     ulonglong2*         edge_out = nullptr;   // optional materialised edges (MODE 2): canonical (u, v)
     unsigned long long  edge_cap = 0;
     unsigned long long* edge_count = nullptr; // device counter of emitted edges (may exceed edge_cap)
