@@ -83,15 +83,16 @@ __device__ __forceinline__ std::uint32_t cellf(const AnnulusDev& A, double x) {
 // (prefix table A.ann_blk), so every block knows its annulus without a search
 // per thread.  Returns the annulus of this block and sets i (maybe >= end).
 __device__ __forceinline__ int block_annulus(const EdgeArgs& A, std::uint64_t& i) {
-    const std::uint32_t b  = A.blk0 + blockIdx.x; // waves launch a sub-range of the blocks
-    int                 lo = A.first_streaming, hi = A.count - 1; // last annulus with ann_blk <= b
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (A.ann_blk[mid] <= b) lo = mid;
-        else hi = mid - 1;
+    const std::uint32_t b    = A.blk0 + blockIdx.x; // waves launch a sub-range of the blocks
+    const int           lane = threadIdx.x & 31;
+    int                 j    = A.first_streaming; // last annulus with ann_blk <= b (one ballot per 32 annuli)
+    for (int base = 0; base < A.count; base += 32) {
+        const int      a = base + lane;
+        const unsigned m = __ballot_sync(0xffffffffu, a < A.count && a >= A.first_streaming && A.ann_blk[a] <= b);
+        if (m) j = base + 31 - __clz(m);
     }
-    i = A.ann[lo].off + std::uint64_t(b - A.ann_blk[lo]) * 256u + threadIdx.x;
-    return lo;
+    i = A.ann[j].off + std::uint64_t(b - A.ann_blk[j]) * 256u + threadIdx.x;
+    return j;
 }
 
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
