@@ -176,9 +176,17 @@ def main():
     import torch.distributed as dist
     import paper_1710_07565_b200 as rhg
 
+    # RHG_BENCH_ONE_GPU=1: functional check of the N-rank path on a 1-GPU box (every rank on
+    # cuda:0, gloo for the counter all-reduce); its timings are not scaling numbers
+    one_gpu = os.environ.get("RHG_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n, d, g, seed, P = cfg
     params = rhg.ModelParams.from_avg_degree(n, rhg.alpha_from_gamma(g), d, seed, P)
     opts = rhg.GenOptions(device=local, rank=rank, world=world)
@@ -211,9 +219,10 @@ def main():
     barrier()
     # whole-graph counters: wrapping u64 sums over shards (the one collective)
     from paper_1710_07565_b200.distributed import ShardResult, reduce_shards
-    g = reduce_shards(ShardResult(st.total.edges, st.total.fingerprint, st.total.comps, dev_ms), device="cuda")
+    cdev = "cpu" if one_gpu else "cuda"
+    g = reduce_shards(ShardResult(st.total.edges, st.total.fingerprint, st.total.comps, dev_ms), device=cdev)
     edges, fp, comps = g.edges, g.fingerprint, g.comps
-    tm = torch.tensor([wall_s, edges_ms], dtype=torch.float64, device="cuda")
+    tm = torch.tensor([wall_s, edges_ms], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
     dev_ms, wall_s, edges_ms = g.max_device_ms, float(tm[0]), float(tm[1])
