@@ -1110,7 +1110,7 @@ __global__ void __launch_bounds__(256, 2) glob_tiles_kernel(EdgeArgs A) {
     const int           ncls = *A.n_cls < kMaxCls ? *A.n_cls : kMaxCls;
     const double        lam_lo = A.s_lam[sb0], lam_hi = A.s_lam[sb1 - 1];
     Acc                 acc;
-    unsigned long long  rsum = 0; // sum of request ids over the warp's edges (uniform; lane 0 reports it)
+    unsigned long long  rsum = 0; // this lane's sum of request ids over its edges
     for (int a0 = 0; a0 < ncls; a0 += 32) {
         // candidate ranges of sorted positions: lane = segment a0 + lane
         {
@@ -1255,7 +1255,7 @@ __global__ void __launch_bounds__(256, 2) glob_tiles_kernel(EdgeArgs A) {
                                 if (MODE == 2 && e) emit_edge(A, E.id, A.s_id[t0 + kl]);
                             }
                         }
-                        rsum += static_cast<unsigned long long>(__reduce_add_sync(kFull, ce)) * E.id;
+                        rsum += static_cast<unsigned long long>(ce) * E.id;
                     }
                 }
             }
@@ -1269,7 +1269,7 @@ __global__ void __launch_bounds__(256, 2) glob_tiles_kernel(EdgeArgs A) {
             }
         }
     }
-    if (lane == 0) acc.fp += rsum;
+    acc.fp += rsum; // flush() reduces over the warp
     flush(acc, A, 1, lane);
 }
 
