@@ -486,6 +486,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                 r0 = A.lcellstart[Aa.cell_off + cellf(Aa, lam_first - hb)];
                 r1 = A.lcellstart[Aa.cell_off + cellf(Aa, lam_last + hb) + 1];
                 if (a == j && r1 > Aa.wrap) r1 = Aa.wrap; // own annulus: unwrapped requests only
+                if (a == j && r1 > N0 + m - 1) r1 = N0 + m - 1; // own requests past the slab: no node after them
                 if (r1 < r0) r1 = r0;
             }
             const std::uint32_t ng = std::uint32_t((r1 - r0 + 31) / 32);
