@@ -451,30 +451,23 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     const std::uint32_t      m    = std::uint32_t(Aj.halo - N0 < std::uint64_t(kSlab) ? Aj.halo - N0 : kSlab);
     const std::uint64_t      base_j = Aj.off + std::uint64_t(Aj.dlt0); // owned ids of j: [base_j, base_j + n)
     const double             lam_first = A.s_lam[N0];
-    for (std::uint32_t i = threadIdx.x; i < m; i += kSlabThreads) {
-        const double  l  = A.s_lam[N0 + i];
-        const double2 r2 = A.s_rec2[N0 + i];
-        S.lam[i] = l;
-        S.r1[i]  = A.s_rec1[N0 + i];
-        S.r2[i]  = r2;
-        S.nd[i]  = make_float4(float(fsub(l, lam_first)), float(fsub(r2.x, 1.0)), float(r2.y),
-                               __uint_as_float(std::uint32_t(A.s_id[N0 + i] - base_j)));
-    }
-    __syncthreads();
-    const double lam_last = S.lam[m - 1];
-    const double inv_w    = lam_last > lam_first ? double(kSlab - 1) / (lam_last - lam_first) : 0.0;
-    const float  span     = float(fsub(lam_last, lam_first)) * 1.0001f;
-    for (std::uint32_t i = threadIdx.x; i < m; i += kSlabThreads) { // bucket starts (cell_fill pattern)
-        const std::uint32_t b  = slab_bucket(S.lam[i], lam_first, inv_w);
-        const std::int32_t  bp = i ? std::int32_t(slab_bucket(S.lam[i - 1], lam_first, inv_w)) : -1;
-        for (std::int32_t c = bp + 1; c <= std::int32_t(b); ++c) S.bstart[c] = std::uint16_t(i);
-        if (i == m - 1)
-            for (std::uint32_t c = b + 1; c <= kSlab; ++c) S.bstart[c] = std::uint16_t(m);
+    const double             lam_last  = A.s_lam[N0 + m - 1];
+    // warp 0 finds the slab's request runs (cell-table lookups) while warps 1.. stage the nodes
+    if (warp != 0) {
+        for (std::uint32_t i = threadIdx.x - 32; i < m; i += kSlabThreads - 32) {
+            const double  l  = A.s_lam[N0 + i];
+            const double2 r2 = A.s_rec2[N0 + i];
+            S.lam[i] = l;
+            S.r1[i]  = A.s_rec1[N0 + i];
+            S.r2[i]  = r2;
+            S.nd[i]  = make_float4(float(fsub(l, lam_first)), float(fsub(r2.x, 1.0)), float(r2.y),
+                                   __uint_as_float(std::uint32_t(A.s_id[N0 + i] - base_j)));
+        }
     }
     // request runs of every sparse source annulus a <= j (lambda within hbound(a, j) of the
     // slab: a superset from a's cell table), compacted to the non-empty ones and numbered as
     // one CTA-wide list of 32-request groups shared by all warps
-    if (warp == 0) {
+    else {
         const unsigned long long srcs = (A.ablate & 1) ? 0ull : A.src_mask[j]; // ablate: timing experiments only
         std::uint32_t            nrun = 0, gsum = 0;
         for (int a0 = 0; a0 <= j; a0 += 32) {
@@ -505,6 +498,16 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
             gsum += __shfl_sync(kFull, incl, 31);
         }
         if (lane == 0) S.run_g[0] = 0, S.n_run = nrun;
+    }
+    __syncthreads();
+    const double inv_w    = lam_last > lam_first ? double(kSlab - 1) / (lam_last - lam_first) : 0.0;
+    const float  span     = float(fsub(lam_last, lam_first)) * 1.0001f;
+    for (std::uint32_t i = threadIdx.x; i < m; i += kSlabThreads) { // bucket starts (cell_fill pattern)
+        const std::uint32_t b  = slab_bucket(S.lam[i], lam_first, inv_w);
+        const std::int32_t  bp = i ? std::int32_t(slab_bucket(S.lam[i - 1], lam_first, inv_w)) : -1;
+        for (std::int32_t c = bp + 1; c <= std::int32_t(b); ++c) S.bstart[c] = std::uint16_t(i);
+        if (i == m - 1)
+            for (std::uint32_t c = b + 1; c <= kSlab; ++c) S.bstart[c] = std::uint16_t(m);
     }
     __syncthreads();
     const std::uint32_t ngroups = S.run_g[S.n_run];
