@@ -453,15 +453,23 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     const double             lam_first = A.s_lam[N0];
     const double             lam_last  = A.s_lam[N0 + m - 1];
     // warp 0 finds the slab's request runs (cell-table lookups) while warps 1.. stage the nodes
-    if (warp != 0) {
+    const double inv_w = lam_last > lam_first ? double(kSlab - 1) / (lam_last - lam_first) : 0.0;
+    const float  span  = float(fsub(lam_last, lam_first)) * 1.0001f;
+    if (warp != 0) { // staging + bucket starts (cell_fill pattern; the predecessor's lambda from L1)
         for (std::uint32_t i = threadIdx.x - 32; i < m; i += kSlabThreads - 32) {
             const double  l  = A.s_lam[N0 + i];
+            const double  lp = i ? A.s_lam[N0 + i - 1] : 0.0;
             const double2 r2 = A.s_rec2[N0 + i];
             S.lam[i] = l;
             S.r1[i]  = A.s_rec1[N0 + i];
             S.r2[i]  = r2;
             S.nd[i]  = make_float4(float(fsub(l, lam_first)), float(fsub(r2.x, 1.0)), float(r2.y),
                                    __uint_as_float(std::uint32_t(A.s_id[N0 + i] - base_j)));
+            const std::uint32_t b  = slab_bucket(l, lam_first, inv_w);
+            const std::int32_t  bp = i ? std::int32_t(slab_bucket(lp, lam_first, inv_w)) : -1;
+            for (std::int32_t c = bp + 1; c <= std::int32_t(b); ++c) S.bstart[c] = std::uint16_t(i);
+            if (i == m - 1)
+                for (std::uint32_t c = b + 1; c <= kSlab; ++c) S.bstart[c] = std::uint16_t(m);
         }
     }
     // request runs of every sparse source annulus a <= j (lambda within hbound(a, j) of the
@@ -498,16 +506,6 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
             gsum += __shfl_sync(kFull, incl, 31);
         }
         if (lane == 0) S.run_g[0] = 0, S.n_run = nrun;
-    }
-    __syncthreads();
-    const double inv_w    = lam_last > lam_first ? double(kSlab - 1) / (lam_last - lam_first) : 0.0;
-    const float  span     = float(fsub(lam_last, lam_first)) * 1.0001f;
-    for (std::uint32_t i = threadIdx.x; i < m; i += kSlabThreads) { // bucket starts (cell_fill pattern)
-        const std::uint32_t b  = slab_bucket(S.lam[i], lam_first, inv_w);
-        const std::int32_t  bp = i ? std::int32_t(slab_bucket(S.lam[i - 1], lam_first, inv_w)) : -1;
-        for (std::int32_t c = bp + 1; c <= std::int32_t(b); ++c) S.bstart[c] = std::uint16_t(i);
-        if (i == m - 1)
-            for (std::uint32_t c = b + 1; c <= kSlab; ++c) S.bstart[c] = std::uint16_t(m);
     }
     __syncthreads();
     const std::uint32_t ngroups = S.run_g[S.n_run];
