@@ -154,3 +154,19 @@ def test_repeatable_and_context_reuse():
     c = rhg.generate_stats(p)
     assert triple(a) == triple(c) and a.total.edges > 0 and b.total.edges > 0
     assert a.kernel_launches > 0 and a.device_ms > 0
+
+
+@pytest.mark.parametrize("n,alpha,C,seed,P", [(1 << 20, 1.0, 8.0, 3, 8), (1 << 18, 0.6, 10.0, 5, 4),
+                                              (1 << 19, 0.8, 4.0, 9, 16)])
+def test_same_points_parity_large_R(oracle, n, alpha, C, seed, P):
+    """R = 2 ln n + C up to 35: outer-annulus windows fall below the FP64 rounding floor, so
+    the slab join runs those groups on the exact predicate and the FP32 pre-filter leaves
+    many pairs to the exact recheck — the counters must stay bit-exact."""
+    p = rhg.ModelParams(n, alpha, C, seed, P)
+    pts = oracle.points(n, alpha, C, seed, P)
+    want = oracle.generate_stats(n, alpha, C, seed, P)
+    st = rhg.count_edges_from_points(p, pts)
+    assert triple(st) == (want["edges"], want["fingerprint"], want["comps"])
+    dev = rhg.sample_points(p)
+    want2 = oracle.count_edges_from_points(n, alpha, C, seed, P, dev)
+    assert triple(rhg.generate_stats(p)) == (want2["edges"], want2["fingerprint"], want2["comps"])
