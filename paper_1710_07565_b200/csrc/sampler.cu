@@ -186,7 +186,11 @@ __global__ void point_radial_kernel(const StreamJob* __restrict__ jobs, int njob
 #ifndef RHG_ANG_WARPS
 #define RHG_ANG_WARPS 8 // measured: 6 -> 4.35 ms, 8 -> 4.31, 10 -> 4.34, 12 -> 4.34 (cfg2 step)
 #endif
-constexpr int kAngWarps = RHG_ANG_WARPS; // warp 0: chain, warp 1: MT, warps 2..: pow factors
+constexpr int kAngWarps = RHG_ANG_WARPS; // warp 0: chain, warp kMtWarp: MT, the others: pow factors
+#ifndef RHG_MT_WARP
+#define RHG_MT_WARP 4 // shares the chain warp's SM sub-partition (integer work only), so no pow warp does
+#endif
+constexpr int kMtWarp = RHG_MT_WARP;
 struct AngSmem {
     std::uint64_t st[2][kMtN];   // MT state, double-buffered (warp 1)
     double        u[2][kMtN];    // uniforms of blocks b, b-1
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(32 * kAngWarps) angle_side_kernel(const Stream
         const double        a = J.a, b = J.b, wd = fsub(b, a);
         const double        bmax = nextafter(b, a);
         double              cur  = 1.0; // lane 0 of warp 0
-        if (warp == 1 && lane == 0) {   // [rand.predef] seeding recurrence (serial by definition)
+        if (warp == kMtWarp && lane == 0) { // [rand.predef] seeding recurrence (serial by definition)
             std::uint64_t z = J.seed_ang;
             S.st[0][0]      = z;
             for (int i = 1; i < kMtN; ++i) {
@@ -218,17 +222,18 @@ __global__ void __launch_bounds__(32 * kAngWarps) angle_side_kernel(const Stream
         }
         __syncwarp();
         for (std::uint64_t s = 0; s < nblk + 2; ++s) {
-            if (warp == 1 && s < nblk) { // block s: state after s + 1 twists
+            if (warp == kMtWarp && s < nblk) { // block s: state after s + 1 twists
                 const std::uint64_t* A = S.st[s & 1];
                 std::uint64_t*       B = S.st[(s + 1) & 1];
                 mt_twist_to(A, B, lane);
                 double* u = S.u[s & 1];
                 for (int i = lane; i < kMtN; i += 32) u[i] = double(mt_temper(B[i]) >> 11) * 0x1.0p-53;
-            } else if (warp >= 2 && s >= 1 && s <= nblk) { // block s - 1: pow factors
+            } else if (warp != 0 && warp != kMtWarp && s >= 1 && s <= nblk) { // block s - 1: pow factors
                 const std::uint64_t base = (s - 1) * kMtN;
                 const double*       u    = S.u[(s - 1) & 1];
                 double*             x    = S.x[(s - 1) & 1];
-                for (int i = threadIdx.x - 64; i < kMtN; i += 32 * (kAngWarps - 2)) {
+                const int pw = warp - 1 - (warp > kMtWarp); // 0 .. kAngWarps - 3
+                for (int i = pw * 32 + lane; i < kMtN; i += 32 * (kAngWarps - 2)) {
                     const std::uint64_t k = base + std::uint64_t(i);
                     x[i] = k < n ? pow(u[i], __ddiv_rn(1.0, double(n - k))) : 1.0; // rng.hpp:221, past the end: 1
                 }
