@@ -422,7 +422,7 @@ void plan_edges(Plan& pl) {
     pl.gt_prefix.assign(L.count + 1, 0);
     for (std::uint32_t j = 0; j < L.count; ++j) {
         const std::uint64_t own = j >= L.first_streaming && pl.n_req ? pl.ann[j].halo - pl.ann[j].off : 0;
-        pl.gt_prefix[j + 1]     = pl.gt_prefix[j] + (own + 127) / 128; // one 128-node tile per warp
+        pl.gt_prefix[j + 1]     = pl.gt_prefix[j] + (own + kTileNodes - 1) / kTileNodes; // one node tile per warp
     }
     pl.gtwarps = pl.gt_prefix[L.count];
     const std::uint64_t nT = (pl.n_glob + kGGTile - 1) / kGGTile, tiles = nT * (nT + 1) / 2;

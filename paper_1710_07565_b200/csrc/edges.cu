@@ -1061,7 +1061,7 @@ __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
     flush(acc, A, 1, threadIdx.x & 31);
 }
 
-constexpr int kTN    = 128; // owned nodes per dense-engine tile (4 per lane, in registers)
+constexpr int kTN    = kTileNodes; // owned nodes per dense-engine tile (kTN / 32 per lane, in registers)
 constexpr int kQ     = kTN / 32;
 constexpr int kStrip = 1;   // tiles per warp sharing one candidate search
 
@@ -1093,7 +1093,7 @@ __device__ __forceinline__ std::uint32_t gtheta_lb(const double* th, std::uint32
 // tile and compacted into (request, piece) entries in shared memory, and the
 // warp sweeps the entries (32-node slices outside an entry are skipped).
 template <int MODE>
-__global__ void __launch_bounds__(256, 2) glob_tiles_kernel(EdgeArgs A) {
+__global__ void __launch_bounds__(256, kTN == 128 ? 2 : 3) glob_tiles_kernel(EdgeArgs A) {
     __shared__ GWarp    smem[8];
     const int           lane = threadIdx.x & 31;
     const std::uint64_t w    = A.gt_prefix[A.j0] + ((std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
