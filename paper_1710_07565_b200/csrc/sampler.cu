@@ -328,7 +328,6 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
     const int      mt_blocks = S.njobs; // one CTA per stream
     const unsigned pblocks   = unsigned((S.total + 255) / 256);
     cudaStream_t   side      = S.side ? S.side : st;
-    static const int sched   = std::getenv("RHG_SCHED") ? std::atoi(std::getenv("RHG_SCHED")) : 0;
     if (S.side) {
         cudaEventRecord(S.ev_fork, st);
         cudaStreamWaitEvent(side, S.ev_fork, 0);
@@ -347,11 +346,11 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
     mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, side>>>(S.jobs, S.njobs, S.beta, S.hw, 2);
     S.mark("mt_radii", side);
     ++*launches;
-    if (sched != 2) {
-        point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
-        S.mark("radial", side);
-        ++*launches;
-    }
+    // the radius attributes run beside the angle side (serialising them after the wave-1 chains
+    // measured slower: 4.19 -> 4.56 ms at cfg2)
+    point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
+    S.mark("radial", side);
+    ++*launches;
     if (nb1) {
         angle_side_kernel<<<nb1, 32 * kAngWarps, 0, st>>>(S.jobs, S.chain_bins, nb1, S.job_order, S.beta);
         ++*launches;
@@ -360,11 +359,6 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
     if (S.side) {
         cudaEventRecord(S.ev_join, side);
         cudaStreamWaitEvent(st, S.ev_join, 0);
-    }
-    if (sched == 2) {
-        point_radial_kernel<<<pblocks, 256, 0, st>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
-        S.mark("radial", st);
-        ++*launches;
     }
     // generate mode: streaming points get their frames in the sort phase (edges.cu angular_scatter_kernel)
     const std::uint64_t first = S.angular_from;
