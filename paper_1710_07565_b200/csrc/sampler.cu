@@ -347,7 +347,7 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
     S.mark("mt_radii", side);
     ++*launches;
     // the radius attributes run beside the angle side (serialising them after the wave-1 chains
-    // measured slower: 4.19 -> 4.56 ms at cfg2)
+    // measured slower at cfg2: the wave-1 sort then waits for the whole radius side)
     point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
     S.mark("radial", side);
     ++*launches;
