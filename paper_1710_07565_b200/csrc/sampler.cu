@@ -178,10 +178,11 @@ __global__ void point_radial_kernel(const StreamJob* __restrict__ jobs, int njob
 // warps 2.. turn block b-1 into the factors pow(U_k, 1/remaining_k) (about
 // one per thread: pow's latency, not its throughput, bounds the stage), and
 // warp 0 runs the serial chain cur = fl(cur * x_k) over block b-2 (lane 0,
-// from shared memory) and writes beta_k = a + w (1 - cur) (clamped) — a
-// three-stage pipeline with one __syncthreads per block, so the chain (the
-// only serial dependency) starts after the first two blocks instead of after
-// two full-array kernels.  Same arithmetic, same order as the separate
+// from shared memory), and the pow warps also map block b-3's products to
+// beta_k = a + w (1 - cur) (clamped) — a four-stage pipeline with one
+// __syncthreads per block in which the chain warp does nothing but the chain
+// (the only serial dependency), starting after the first two blocks instead
+// of after two full-array kernels.  Same arithmetic, same order as the separate
 // mt_uniforms / point_pow / sorted_chain kernels.
 #ifndef RHG_ANG_WARPS
 #define RHG_ANG_WARPS 8 // measured: 6 -> 4.35 ms, 8 -> 4.31, 10 -> 4.34, 12 -> 4.34 (cfg2 step)
@@ -194,7 +195,7 @@ constexpr int kMtWarp = RHG_MT_WARP;
 struct AngSmem {
     std::uint64_t st[2][kMtN];   // MT state, double-buffered (warp 1)
     double        u[2][kMtN];    // uniforms of blocks b, b-1
-    double        x[2][kMtN];    // pow factors of blocks b-1, b-2 (products in place)
+    double        x[3][kMtN];    // pow factors of block b-1, products of b-2, block b-3 being mapped to beta
 };
 __global__ void __launch_bounds__(32 * kAngWarps) angle_side_kernel(const StreamJob* __restrict__ jobs,
                                                                     const std::uint32_t* __restrict__ bins,
@@ -221,25 +222,35 @@ __global__ void __launch_bounds__(32 * kAngWarps) angle_side_kernel(const Stream
             }
         }
         __syncwarp();
-        for (std::uint64_t s = 0; s < nblk + 2; ++s) {
+        for (std::uint64_t s = 0; s < nblk + 3; ++s) {
             if (warp == kMtWarp && s < nblk) { // block s: state after s + 1 twists
                 const std::uint64_t* A = S.st[s & 1];
                 std::uint64_t*       B = S.st[(s + 1) & 1];
                 mt_twist_to(A, B, lane);
                 double* u = S.u[s & 1];
                 for (int i = lane; i < kMtN; i += 32) u[i] = double(mt_temper(B[i]) >> 11) * 0x1.0p-53;
-            } else if (warp != 0 && warp != kMtWarp && s >= 1 && s <= nblk) { // block s - 1: pow factors
-                const std::uint64_t base = (s - 1) * kMtN;
-                const double*       u    = S.u[(s - 1) & 1];
-                double*             x    = S.x[(s - 1) & 1];
+            } else if (warp != 0 && warp != kMtWarp) {
                 const int pw = warp - 1 - (warp > kMtWarp); // 0 .. kAngWarps - 3
-                for (int i = pw * 32 + lane; i < kMtN; i += 32 * (kAngWarps - 2)) {
-                    const std::uint64_t k = base + std::uint64_t(i);
-                    x[i] = k < n ? pow(u[i], __ddiv_rn(1.0, double(n - k))) : 1.0; // rng.hpp:221, past the end: 1
+                if (s >= 1 && s <= nblk) {                  // block s - 1: pow factors
+                    const std::uint64_t base = (s - 1) * kMtN;
+                    const double*       u    = S.u[(s - 1) & 1];
+                    double*             x    = S.x[(s - 1) % 3];
+                    for (int i = pw * 32 + lane; i < kMtN; i += 32 * (kAngWarps - 2)) {
+                        const std::uint64_t k = base + std::uint64_t(i);
+                        x[i] = k < n ? pow(u[i], __ddiv_rn(1.0, double(n - k))) : 1.0; // rng.hpp:221, past the end: 1
+                    }
                 }
-            } else if (warp == 0 && s >= 2) { // block s - 2: the chain, then beta
-                const std::uint64_t base = (s - 2) * kMtN;
-                double*             x    = S.x[s & 1]; // == (s - 2) & 1
+                if (s >= 3) { // block s - 3: the chain's products -> beta (off the chain warp's path)
+                    const std::uint64_t base = (s - 3) * kMtN;
+                    const double*       x    = S.x[(s - 3) % 3];
+                    for (int i = pw * 32 + lane; i < kMtN; i += 32 * (kAngWarps - 2)) {
+                        const std::uint64_t k = base + std::uint64_t(i);
+                        const double        y = fadd(a, fmul(wd, fsub(1.0, x[i])));
+                        if (k < n) p[k] = y >= b ? bmax : y;
+                    }
+                }
+            } else if (warp == 0 && s >= 2 && s <= nblk + 1) { // block s - 2: the chain
+                double* x = S.x[(s - 2) % 3];
                 if (lane == 0) {
                     double2*      x2 = reinterpret_cast<double2*>(x);
                     constexpr int kB = 6;              // 156 double2 = 13 batches of 12 values
@@ -270,11 +281,6 @@ __global__ void __launch_bounds__(32 * kAngWarps) angle_side_kernel(const Stream
                     }
                 }
                 __syncwarp();
-                for (int i = lane; i < kMtN; i += 32) {
-                    const std::uint64_t k = base + std::uint64_t(i);
-                    const double        y = fadd(a, fmul(wd, fsub(1.0, x[i])));
-                    if (k < n) p[k] = y >= b ? bmax : y;
-                }
             }
             __syncthreads();
         }
