@@ -21,6 +21,7 @@
  *   TextEdgeWriter/BinaryEdgeWriter io.hpp:20-68           rhg_write_edges_text / _binary
  *   read_binary_edges             io.hpp:70-96            rhg_read_edges_binary
  *   naive_edges                   oracle.hpp:41-54        rhg_naive_edges (GPU brute force)
+ *   powerlaw_mle                  stats.hpp:58-75         rhg_powerlaw_mle (host)
  *
  * Conventions: plain pointers and sizes, no exceptions across the ABI.
  * Every call returns RHG_OK (0) or an error code; rhg_last_error() gives the
@@ -40,7 +41,8 @@
 extern "C" {
 #endif
 
-#define RHG_ABI_VERSION 3
+#define RHG_ABI_VERSION 4
+#define RHG_MAX_ANNULI 64 /* layouts with more annuli are rejected (RHG_INVALID_ARGUMENT) */
 
 enum {
     RHG_OK = 0,
@@ -93,6 +95,15 @@ typedef struct {
     double pairs_ms;          /* the sparse engine (slab join + tail kernels, dominant) */
     uint64_t stream_comps;    /* predicate tests of the sparse engine (slab join + tail) */
     uint64_t dense_comps;     /* predicate tests of the dense engine (global + wide-window requests) */
+    /* ChunkStats::*_by_annulus (sweep.hpp:160, 472, 530-539; generator.hpp:82-98) of this shard:
+     * tests and edges counted for the node's annulus (global unit: the larger annulus of the
+     * pair), vertices for their home annulus (global points on rank 0).  Entries [0, annuli).
+     * annulus_edges / annulus_comps are filled (per_annulus = 1) by the calls that also track
+     * degrees or materialise edges — the `stats` path; the counters-only path skips them. */
+    uint32_t per_annulus, pad_;
+    uint64_t annulus_edges[RHG_MAX_ANNULI];
+    uint64_t annulus_comps[RHG_MAX_ANNULI];
+    uint64_t annulus_vertices[RHG_MAX_ANNULI];
 } rhg_run_stats;
 
 /* Host point arrays in vertex-id order (n entries each; any may be NULL
@@ -179,7 +190,10 @@ int rhg_write_edges_binary(const char* path, const uint64_t* edges, uint64_t m);
 /* io.hpp:70-96 read_binary_edges: bad magic / truncated pair -> RHG_INVALID_ARGUMENT
  * (std::runtime_error in the reference).  edges == NULL only counts. */
 int rhg_read_edges_binary(const char* path, uint64_t* edges, uint64_t cap, uint64_t* m);
-/* message of the last failed edge-file call (this thread) */
+/* stats.hpp:58-75 powerlaw_mle over a degree array (host; same order and libm as the
+ * reference).  Fewer than 100 degrees >= d_min -> RHG_INVALID_ARGUMENT. */
+int rhg_powerlaw_mle(const uint32_t* degrees, uint64_t n, uint32_t d_min, double* gamma_hat);
+/* message of the last failed edge-file / analytics call (this thread) */
 const char* rhg_io_last_error(void);
 
 /* Diagnostic (not part of the reference interface): measured non-FMA FP64

@@ -12,6 +12,7 @@
 
 #include <rhg/generator.hpp>
 #include <rhg/io.hpp>
+#include <rhg/stats.hpp>
 #include <rhg/geometry.hpp>
 #include <rhg/oracle.hpp>
 #include <rhg/partition.hpp>
@@ -83,6 +84,27 @@ int ref_generate_stats(std::uint64_t n, double alpha, double C, std::uint64_t se
         if (degrees)
             std::memcpy(degrees, deg.data(), deg.size() * sizeof(std::uint32_t));
     });
+}
+
+// ChunkStats::*_by_annulus of generate_stats (arrays sized layout.count).
+int ref_generate_annuli(std::uint64_t n, double alpha, double C, std::uint64_t seed, std::uint32_t chunks,
+                        std::uint32_t workers, std::uint64_t* edges, std::uint64_t* comps, std::uint64_t* vertices) {
+    return guarded([&] {
+        const rhg::ModelParams params(n, alpha, C, seed, chunks);
+        rhg::GenOptions        opts;
+        opts.workers  = workers;
+        const auto st = rhg::generate_stats(params, opts);
+        for (std::size_t i = 0; i < st.total.edges_by_annulus.size(); ++i) {
+            edges[i]    = st.total.edges_by_annulus[i];
+            comps[i]    = st.total.comps_by_annulus[i];
+            vertices[i] = st.total.vertices_by_annulus[i];
+        }
+    });
+}
+
+// stats.hpp:58-75 powerlaw_mle (std::invalid_argument -> error code).
+int ref_powerlaw_mle(const std::uint32_t* degrees, std::uint64_t n, std::uint32_t d_min, double* gamma) {
+    return guarded([&] { *gamma = rhg::powerlaw_mle(std::vector<std::uint32_t>(degrees, degrees + n), d_min); });
 }
 
 // Per-unit counters of generate_stats (unit 0 = global unit).  edges/comps

@@ -97,6 +97,8 @@ class Ref(_Base):
         L.ref_generate_edges.argtypes = [u64, f64, f64, u64, u32, u32, P_u64, P_u64]
         L.ref_naive_edges.argtypes = [u64, f64, f64, u64, u32, P_u64, P_u64]
         L.ref_write_edges.argtypes = [C.c_char_p, P_u64, u64, C.c_int]
+        L.ref_generate_annuli.argtypes = [u64, f64, f64, u64, u32, u32, P_u64, P_u64, P_u64]
+        L.ref_powerlaw_mle.argtypes = [P_u32, u64, u32, P_f64]
         L.ref_read_edges_binary.argtypes = [C.c_char_p, P_u64, P_u64]
         L.ref_derive_seed.argtypes = [u64, P_u64, u32]
         L.ref_derive_seed.restype = u64
@@ -168,6 +170,19 @@ class Ref(_Base):
         buf = np.zeros(2 * m.value, np.uint64)
         self._check(self.L.ref_generate_edges(n, alpha, Cc, seed, chunks, workers, C.byref(m), _p(buf, P_u64)))
         return buf.reshape(-1, 2)
+
+    def generate_annuli(self, n, alpha, Cc, seed, chunks, workers=0):
+        K = self.layout(n, alpha, Cc, seed, chunks).count
+        e, c, v = (np.zeros(K, np.uint64) for _ in range(3))
+        self._check(self.L.ref_generate_annuli(n, alpha, Cc, seed, chunks, workers, _p(e, P_u64), _p(c, P_u64),
+                                               _p(v, P_u64)))
+        return e, c, v
+
+    def powerlaw_mle(self, degrees, d_min):
+        d = np.ascontiguousarray(degrees, np.uint32)
+        g = np.zeros(1, np.float64)
+        self._check(self.L.ref_powerlaw_mle(_p(d, P_u32), len(d), d_min, _p(g, P_f64)))
+        return float(g[0])
 
     def write_edges(self, path, edges, binary):
         e = np.ascontiguousarray(edges, np.uint64).reshape(-1, 2)

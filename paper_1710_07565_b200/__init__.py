@@ -102,11 +102,16 @@ class GenOptions:
 
 @dataclass
 class ChunkStats:
-    """sweep.hpp:154-177 (totals only)."""
+    """sweep.hpp:154-177 (max_insertion_bucket is a sweep internal, not produced).
+    edges_by_annulus / comps_by_annulus are filled when degrees are tracked (the `stats`
+    path) or edges are materialised; the counters-only path leaves them empty."""
     edges: int = 0
     comps: int = 0
     streaming_vertices: int = 0
     fingerprint: int = 0
+    edges_by_annulus: list = field(default_factory=list)
+    comps_by_annulus: list = field(default_factory=list)
+    vertices_by_annulus: list = field(default_factory=list)
 
 
 @dataclass
@@ -143,8 +148,12 @@ class RunStats:
 
     @classmethod
     def _from_c(cls, s: _native.rhg_run_stats) -> "RunStats":
+        k = int(s.annuli)
         return cls(n=s.n, global_vertices=s.global_vertices, r_G=s.r_G,
-                   total=ChunkStats(s.edges, s.comps, s.streaming_vertices, s.fingerprint), seconds=s.seconds,
+                   total=ChunkStats(s.edges, s.comps, s.streaming_vertices, s.fingerprint,
+                                    list(s.annulus_edges[:k]) if s.per_annulus else [],
+                                    list(s.annulus_comps[:k]) if s.per_annulus else [],
+                                    list(s.annulus_vertices[:k])), seconds=s.seconds,
                    R=s.R, annuli=s.annuli, first_streaming=s.first_streaming, global_edges=s.global_edges,
                    global_comps=s.global_comps, device_ms=s.device_ms, sample_ms=s.sample_ms, edges_ms=s.edges_ms,
                    host_ms=s.host_ms, kernel_launches=s.kernel_launches, device_bytes=s.device_bytes,
@@ -419,3 +428,102 @@ def verify_against_oracle(params: ModelParams, opts: GenOptions = GenOptions()) 
     edges, _ = generate_edges(params, opts)
     pts = sample_points(params, opts)
     return compare(edges, naive_edges(pts, params.R, opts.device), pts, params.R)
+
+
+# ------------------------------------------------- degree analytics ---
+# the CLI `stats` path (proj/tools/rhg.cpp:144-164) — exact degrees
+# (generate_stats(degrees=True)), the power-law fit and the run report (stats.hpp:37-208).
+
+def degree_histogram(degrees) -> np.ndarray:
+    """stats.hpp:48-56: hist[d] = number of vertices of degree d."""
+    d = np.asarray(degrees, np.uint32)
+    return np.bincount(d, minlength=int(d.max()) + 1 if len(d) else 1).astype(np.uint64)
+
+
+def powerlaw_mle(degrees, d_min: int) -> float:
+    """stats.hpp:58-75 (bit-identical: the library sums in id order with glibc log, like the
+    reference).  Fewer than 100 tail samples raise ValueError (std::invalid_argument)."""
+    d = np.ascontiguousarray(degrees, np.uint32)
+    g = C.c_double()
+    rc = lib().rhg_powerlaw_mle(d.ctypes.data_as(C.POINTER(C.c_uint32)), len(d), int(d_min), C.byref(g))
+    if rc != RHG_OK:
+        raise ValueError(lib().rhg_io_last_error().decode())
+    return g.value
+
+
+def _fmt(x) -> str:
+    """std::ostream default formatting of a double (%g, 6 significant digits)."""
+    if isinstance(x, float):
+        if math.isnan(x):
+            return "nan" if math.copysign(1.0, x) > 0 else "-nan"
+        if math.isinf(x):
+            return "inf" if x > 0 else "-inf"
+        return f"{x:g}"
+    return str(x)
+
+
+@dataclass
+class RunReport:
+    """stats.hpp:120-208: the flat run summary of `rhg stats`.  Per-unit vectors are not
+    produced by the B200 path (its unit of work is not the reference's chunk engine)."""
+    n: int = 0
+    m: int = 0
+    avg_degree: float = 0.0
+    expected_avg_degree: float = 0.0
+    gamma_hat: float = float("nan")
+    distance_computations: int = 0
+    overestimation_ratio: float = 0.0
+    fingerprint: int = 0
+    global_vertices: int = 0
+    r_G: float = 0.0
+    seconds: float = 0.0
+    edges_per_sec: float = 0.0
+    annulus_edges: list = field(default_factory=list)
+    annulus_comps: list = field(default_factory=list)
+    annulus_vertices: list = field(default_factory=list)
+
+    @classmethod
+    def from_stats(cls, params: ModelParams, stats: RunStats) -> "RunReport":
+        return cls(n=params.n, m=stats.total.edges, avg_degree=stats.avg_degree(),
+                   expected_avg_degree=expected_avg_degree(params.C, params.alpha),
+                   distance_computations=stats.total.comps, overestimation_ratio=stats.overestimation_ratio(),
+                   fingerprint=stats.total.fingerprint, global_vertices=stats.global_vertices, r_G=stats.r_G,
+                   seconds=stats.seconds,
+                   edges_per_sec=stats.total.edges / stats.seconds if stats.seconds > 0 else 0.0,
+                   annulus_edges=list(stats.total.edges_by_annulus),
+                   annulus_comps=list(stats.total.comps_by_annulus),
+                   annulus_vertices=list(stats.total.vertices_by_annulus))
+
+    CSV_HEADER = ("n,m,avg_degree,expected_avg_degree,gamma_hat,distance_computations,overestimation_ratio,"
+                  "fingerprint,global_vertices,r_G,seconds,edges_per_sec")
+
+    def csv_row(self) -> str:
+        return ",".join(_fmt(v) for v in (self.n, self.m, float(self.avg_degree), float(self.expected_avg_degree),
+                                          float(self.gamma_hat), self.distance_computations,
+                                          float(self.overestimation_ratio), self.fingerprint, self.global_vertices,
+                                          float(self.r_G), float(self.seconds), float(self.edges_per_sec))) + "\n"
+
+    def text(self) -> str:
+        j = lambda v: ",".join(str(int(x)) for x in v)  # noqa: E731
+        return (f"n={self.n}\nm={self.m}\navg_degree={_fmt(float(self.avg_degree))}\n"
+                f"expected_avg_degree={_fmt(float(self.expected_avg_degree))}\n"
+                f"gamma_hat={_fmt(float(self.gamma_hat))}\ndistance_computations={self.distance_computations}\n"
+                f"overestimation_ratio={_fmt(float(self.overestimation_ratio))}\nfingerprint={self.fingerprint}\n"
+                f"global_vertices={self.global_vertices}\nr_G={_fmt(float(self.r_G))}\n"
+                f"seconds={_fmt(float(self.seconds))}\nedges_per_sec={_fmt(float(self.edges_per_sec))}\n"
+                f"annulus_vertices={j(self.annulus_vertices)}\nannulus_comps={j(self.annulus_comps)}\n"
+                f"annulus_edges={j(self.annulus_edges)}\nunit_edges=\nunit_comps=\n")
+
+
+def stats_report(params: ModelParams, opts: GenOptions = GenOptions()) -> RunReport:
+    """proj/tools/rhg.cpp:144-164 cmd_stats: generate with exact degrees, fit gamma_hat over
+    the degrees >= d_min = max(10, round(expected average degree)) (NaN when the tail has fewer
+    than 100 samples) and build the run report."""
+    st = generate_stats(params, opts, degrees=True)
+    rep = RunReport.from_stats(params, st)
+    d_min = int(max(10.0, float(math.floor(rep.expected_avg_degree + 0.5))))  # std::llround (x > 0)
+    try:
+        rep.gamma_hat = powerlaw_mle(st.degrees, d_min)
+    except ValueError:
+        pass
+    return rep

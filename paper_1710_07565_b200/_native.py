@@ -31,7 +31,9 @@ class rhg_run_stats(C.Structure):
                 ("sample_ms", C.c_double), ("edges_ms", C.c_double), ("host_ms", C.c_double),
                 ("seconds", C.c_double), ("kernel_launches", C.c_uint64), ("device_bytes", C.c_uint64),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("pairs_ms", C.c_double),
-                ("stream_comps", C.c_uint64), ("dense_comps", C.c_uint64)]
+                ("stream_comps", C.c_uint64), ("dense_comps", C.c_uint64),
+                ("per_annulus", C.c_uint32), ("pad_", C.c_uint32), ("annulus_edges", C.c_uint64 * 64), ("annulus_comps", C.c_uint64 * 64),
+                ("annulus_vertices", C.c_uint64 * 64)]
 
 
 P_f64 = C.POINTER(C.c_double)
@@ -50,7 +52,7 @@ EXPORTS = ["rhg_last_error", "rhg_abi_version", "rhg_alpha_from_gamma", "rhg_rad
            "rhg_params_validate", "rhg_params_from_avg_degree", "rhg_create", "rhg_destroy", "rhg_generate_stats",
            "rhg_sample_points", "rhg_sample_uniforms", "rhg_count_edges_from_points",
            "rhg_fp64_peak", "rhg_generate_edges", "rhg_edges_from_points", "rhg_write_edges_text", "rhg_write_edges_binary",
-           "rhg_read_edges_binary", "rhg_io_last_error", "rhg_naive_edges"]
+           "rhg_read_edges_binary", "rhg_io_last_error", "rhg_naive_edges", "rhg_powerlaw_mle"]
 
 _lib = None
 
@@ -91,6 +93,7 @@ def lib():
     L.rhg_write_edges_binary.argtypes = [C.c_char_p, P_u64, C.c_uint64]
     L.rhg_read_edges_binary.argtypes = [C.c_char_p, P_u64, C.c_uint64, P_u64]
     L.rhg_io_last_error.restype = C.c_char_p
+    L.rhg_powerlaw_mle.argtypes = [C.POINTER(C.c_uint32), C.c_uint64, C.c_uint32, P_f64]
     L.rhg_naive_edges.argtypes = [C.c_void_p, C.c_uint64, C.c_double, P_f64, P_f64, P_u64, C.c_uint64, P_u64]
     _lib = L
     return L

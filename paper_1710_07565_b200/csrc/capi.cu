@@ -338,6 +338,7 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
     pl.sub_ms[1] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl1).count();
     if (pl.n_ext >= (std::uint64_t(1) << 32) || pl.n_req >= (std::uint64_t(1) << 31) || L.n >= (std::uint64_t(1) << 32))
         throw InvalidArgument("rhg: more than 2^32 points (per device) are not supported");
+    if (L.count > std::uint32_t(kMaxAnnuli)) throw InvalidArgument("rhg: more than 64 annuli are not supported");
     return pl;
 }
 
@@ -551,7 +552,8 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     const std::size_t   o_bkoff   = o_cseg + align256((kMaxCls + 1) * sizeof(std::uint32_t));
     const std::size_t   o_bksh    = o_bkoff + align256((kMaxCls + 1) * sizeof(std::uint32_t));
     const std::size_t   o_slots   = o_bksh + align256(kMaxCls * sizeof(std::uint32_t));
-    const std::size_t   cnt_bytes = o_slots + 3 * kSlots * sizeof(SlotCounter) + 256;
+    const std::size_t   o_ann     = o_slots + align256(3 * kSlots * sizeof(SlotCounter));
+    const std::size_t   cnt_bytes = o_ann + align256(std::size_t(kAnnSlots) * 2 * kMaxAnnuli * sizeof(unsigned long long)) + 256;
     ctx->counters.ensure(cnt_bytes);
     CK(cudaMemsetAsync(ctx->counters.p, 0, cnt_bytes, ctx->stream));
     ctx->cells.ensure(std::max<std::uint64_t>(pl.ncells, 1) * sizeof(std::uint64_t));
@@ -620,6 +622,8 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     e.ann_rw = t.ann;
     e.ctr       = ctx->counters.as<Counters>();
     e.slots     = reinterpret_cast<SlotCounter*>(ctx->counters.as<char>() + o_slots);
+    e.ann_ctr   = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + o_ann);
+    e.gseg      = t.gseg;
     e.dmax_bits = reinterpret_cast<unsigned long long*>(ctx->counters.as<char>() + o_dmax);
     e.cosh_R = pl.L.cosh_R, e.chunk0_upper = chunk_upper_bound(0, pl.L.chunks);
     e.lift_part   = pl.e1 == pl.L.chunks && pl.T > 0;
@@ -717,6 +721,9 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         CK(cudaMemcpyAsync(degrees, ctx->degrees.p, pl.L.n * sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
     auto* h_ecount = reinterpret_cast<unsigned long long*>(hc + 5);
     *h_ecount      = 0;
+    auto* h_ann    = reinterpret_cast<unsigned long long*>(static_cast<char*>(ctx->readback.p) + 512);
+    CK(cudaMemcpyAsync(h_ann, e.ann_ctr, 2 * kMaxAnnuli * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ctx->stream));
     if (sink) CK(cudaMemcpyAsync(h_ecount, ctx->ecount.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (sink) sink->count = *h_ecount;
@@ -730,6 +737,9 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         for (int i = 0; i < kDbgSlots; ++i) std::fprintf(stderr, "%s%llu", i ? "," : "", h[i]);
         std::fprintf(stderr, "]\n");
     }
+    out->per_annulus = (degrees || sink) ? 1u : 0u; // the MODE 1 / 2 kernels count per annulus
+    for (int a = 0; a < kMaxAnnuli; ++a)
+        out->annulus_edges[a] = out->per_annulus ? h_ann[a] : 0, out->annulus_comps[a] = out->per_annulus ? h_ann[kMaxAnnuli + a] : 0;
     out->edges       = hc[0].edges + hc[1].edges + hc[2].edges;
     out->fingerprint = hc[0].fp + hc[1].fp + hc[2].fp;
     out->comps       = hc[0].comps + hc[1].comps + hc[2].comps;
@@ -755,6 +765,9 @@ void fill_common(const Plan& pl, rhg_run_stats* out) {
     std::uint64_t owned     = 0;
     for (std::uint32_t i = pl.L.first_streaming; i < pl.L.count; ++i) owned += pl.ann[i].halo - pl.ann[i].off;
     out->streaming_vertices = owned;
+    for (std::uint32_t i = 0; i < pl.L.count && i < std::uint32_t(kMaxAnnuli); ++i)
+        out->annulus_vertices[i] =
+            i < pl.L.first_streaming ? (pl.rank == 0 ? pl.L.counts[i] : 0) : pl.ann[i].halo - pl.ann[i].off;
 }
 
 

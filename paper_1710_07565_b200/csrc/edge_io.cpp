@@ -1,5 +1,9 @@
-// Edge stream files (host side), byte-compatible with the reference's
-// io.hpp:20-96: text "u v\n" (decimal), binary magic "RHGE0001" + LE u64 pairs.
+// Host-side edge-stream files and degree analytics.
+//   * edge stream files, byte-compatible with the reference's io.hpp:20-96:
+//     text "u v\n" (decimal), binary magic "RHGE0001" + LE u64 pairs;
+//   * the power-law exponent MLE of stats.hpp:58-75 (same summation order and
+//     libm as the reference, so the estimate is bit-identical).
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -105,6 +109,23 @@ int rhg_read_edges_binary(const char* path, std::uint64_t* edges, std::uint64_t 
     }
     *m = n;
     if (edges && n > cap) return fail("rhg_read_edges_binary: buffer too small");
+    return RHG_OK;
+}
+
+// stats.hpp:58-75 powerlaw_mle: continuous MLE with the -0.5 discreteness correction over
+// the degrees >= d_min, in id order; fewer than 100 tail samples -> RHG_INVALID_ARGUMENT.
+int rhg_powerlaw_mle(const std::uint32_t* degrees, std::uint64_t n, std::uint32_t d_min, double* gamma_hat) {
+    if (!gamma_hat || (n && !degrees)) return fail("rhg_powerlaw_mle: null argument");
+    double        log_sum = 0.0;
+    std::uint64_t k       = 0;
+    const double  x_min   = static_cast<double>(d_min) - 0.5;
+    for (std::uint64_t i = 0; i < n; ++i)
+        if (degrees[i] >= d_min) {
+            log_sum += std::log(static_cast<double>(degrees[i]) / x_min);
+            ++k;
+        }
+    if (k < 100) return fail("powerlaw_mle: fewer than 100 degrees above d_min");
+    *gamma_hat = 1.0 + static_cast<double>(k) / log_sum;
     return RHG_OK;
 }
 

@@ -54,7 +54,10 @@ struct Acc {
 // Warp-reduce the lane accumulators and add them to one of kSlots spread
 // counter slots of family f (same-address atomics from every warp would
 // serialise in L2); reduce_counters_kernel folds the slots at the end.
-__device__ __forceinline__ void flush(Acc& acc, const EdgeArgs& A, int f, int lane) {
+// With j >= 0 the warp's totals also go to the per-annulus counters of annulus j
+// (ChunkStats::edges_by_annulus / comps_by_annulus, sweep.hpp:530-539: the node's annulus).
+template <bool ANN = false>
+__device__ __forceinline__ void flush(Acc& acc, const EdgeArgs& A, int f, int lane, int j = -1) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         acc.edges += __shfl_down_sync(kFull, acc.edges, o);
@@ -67,6 +70,36 @@ __device__ __forceinline__ void flush(Acc& acc, const EdgeArgs& A, int f, int la
         atomicAdd(&slot.edges, acc.edges);
         atomicAdd(&slot.fp, acc.fp);
         atomicAdd(&slot.comps, acc.comps);
+        if (ANN && j >= 0) {
+            unsigned long long* c = A.ann_ctr + std::size_t(w & (kAnnSlots - 1)) * 2 * kMaxAnnuli;
+            atomicAdd(&c[j], acc.edges), atomicAdd(&c[kMaxAnnuli + j], acc.comps);
+        }
+    }
+}
+
+// Per-annulus counters accumulated in shared memory by a CTA whose threads see several
+// annuli (tail, rows, deferred, global unit), then added to A.ann_ctr once per CTA.
+struct AnnAcc {
+    unsigned long long e[kMaxAnnuli], c[kMaxAnnuli];
+};
+template <bool ANN>
+__device__ __forceinline__ void ann_zero(AnnAcc& S) {
+    if (!ANN) return;
+    for (int i = threadIdx.x; i < kMaxAnnuli; i += blockDim.x) S.e[i] = 0, S.c[i] = 0;
+}
+template <bool ANN>
+__device__ __forceinline__ void ann_add(AnnAcc& S, int j, unsigned long long e, unsigned long long c) {
+    if (!ANN) return;
+    if (e) atomicAdd(&S.e[j], e);
+    if (c) atomicAdd(&S.c[j], c);
+}
+template <bool ANN>
+__device__ __forceinline__ void ann_flush(const AnnAcc& S, const EdgeArgs& A) {
+    if (!ANN) return;
+    unsigned long long* c = A.ann_ctr + std::size_t(blockIdx.x & (kAnnSlots - 1)) * 2 * kMaxAnnuli;
+    for (int i = threadIdx.x; i < kMaxAnnuli; i += blockDim.x) {
+        if (S.e[i]) atomicAdd(&c[i], S.e[i]);
+        if (S.c[i]) atomicAdd(&c[kMaxAnnuli + i], S.c[i]);
     }
 }
 
@@ -666,7 +699,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     }
     Acc acc;
     acc.edges = acc_e, acc.comps = acc_c, acc.fp = acc_fp;
-    flush(acc, A, 0, lane);
+    flush<MODE != 0>(acc, A, 0, lane, j);
 }
 
 // Pairs the slab join leaves out: halo requests (Foreign replica) x owned
@@ -678,6 +711,9 @@ template <int MODE>
 __global__ void __launch_bounds__(256) tail_kernel(EdgeArgs A) {
     const std::uint64_t t  = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     Acc                 acc;
+    __shared__ AnnAcc   SA;
+    ann_zero<MODE != 0>(SA);
+    __syncthreads();
     if (t < A.tail_prefix[A.count]) {
         int a = A.first_streaming, ha = A.count - 1; // last annulus with tail_prefix <= t
         while (a < ha) {
@@ -709,6 +745,7 @@ __global__ void __launch_bounds__(256) tail_kernel(EdgeArgs A) {
                     lo = fsub(lam, h), hi = fadd(lam, h);
                 }
                 if (!(hi > lo)) continue;
+                const unsigned long long e0 = acc.edges, c0 = acc.comps;
                 if (Aj.halo > Aj.off) {
                     std::uint64_t g0 = 0, g1 = 0;
                     if (halo_req) {
@@ -723,10 +760,13 @@ __global__ void __launch_bounds__(256) tail_kernel(EdgeArgs A) {
                     const std::uint64_t h0 = lower_bound_halo(A, Aj, lo), h1 = lower_bound_halo(A, Aj, hi);
                     if (h1 > h0) serial_range<MODE>(A, q, theta, own, h0, h1, acc);
                 }
+                ann_add<MODE != 0>(SA, j, acc.edges - e0, acc.comps - c0);
             }
         }
     }
     flush(acc, A, 0, threadIdx.x & 31);
+    __syncthreads();
+    ann_flush<MODE != 0>(SA, A);
 }
 
 // --------------------------------------------------------- dense engine ---
@@ -904,9 +944,13 @@ __global__ void __launch_bounds__(256) deferred_kernel(EdgeArgs A) {
     const unsigned long long n    = A.defer_ctr[0] < A.defer_cap ? A.defer_ctr[0] : A.defer_cap;
     const unsigned long long nw   = (unsigned long long)(gridDim.x) * (blockDim.x >> 5);
     Acc                      acc;
+    __shared__ AnnAcc        SA;
+    ann_zero<MODE != 0>(SA);
+    __syncthreads();
     for (unsigned long long i = (unsigned long long)(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
          i += nw) {
         const uint4   E  = A.deferred[i];
+        const unsigned long long e0 = acc.edges, c0 = acc.comps;
         const double2 q1 = A.g_rec[2 * E.x], q2 = A.g_rec[2 * E.x + 1];
         SRow          q;
         q.cs = q1.x, q.sn = q1.y, q.coth = q2.x, q.rci = q2.y, q.id = A.g_id[E.x], q.pad = 0;
@@ -922,8 +966,19 @@ __global__ void __launch_bounds__(256) deferred_kernel(EdgeArgs A) {
             acc.comps += 1;
             count_edge<MODE>(A, edge_test(q.cs, q.sn, q.coth, q.rci, A.s_rec1[k], A.s_rec2[k]), q.id, nid, acc);
         }
+        { // the range's annulus: the one whose extended block holds node E.y
+            int j = A.first_streaming;
+            for (int base = 0; base < A.count; base += 32) {
+                const int      a = base + lane;
+                const unsigned m = __ballot_sync(kFull, a < A.count && a >= A.first_streaming && A.ann[a].off <= E.y);
+                if (m) j = base + 31 - __clz(m);
+            }
+            ann_add<MODE != 0>(SA, j, acc.edges - e0, acc.comps - c0);
+        }
     }
     flush(acc, A, 1, lane);
+    __syncthreads();
+    ann_flush<MODE != 0>(SA, A);
 }
 
 // Row (sorted request s, target annulus j): the exact index ranges ("pieces")
@@ -1057,6 +1112,17 @@ __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
         const unsigned mx  = __reduce_max_sync(grp, unsigned(hbits >> 32));
         if (hkey >= 0 && int(threadIdx.x & 31) == __ffs(grp) - 1 && hbits)
             atomicMax(&A.hmax_bits[hkey], (static_cast<unsigned long long>(mx) << 32) | 0xffffffffull);
+    }
+    if constexpr (MODE != 0) { // the rows' comps per target annulus (lanes of one target reduce together;
+                               // compiled out of the counters-only kernel, where it also miscompiled)
+        const int      jj  = ok ? A.j0 + int(idx / nR) : -1;
+        const unsigned grp = __match_any_sync(kFull, jj);
+        const unsigned cs  = __reduce_add_sync(grp, unsigned(acc.comps));
+        if (jj >= 0 && cs && int(threadIdx.x & 31) == __ffs(grp) - 1) {
+            const unsigned w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+            atomicAdd(&A.ann_ctr[std::size_t(w & (kAnnSlots - 1)) * 2 * kMaxAnnuli + kMaxAnnuli + jj],
+                      static_cast<unsigned long long>(cs));
+        }
     }
     flush(acc, A, 1, threadIdx.x & 31);
 }
@@ -1272,7 +1338,7 @@ __global__ void __launch_bounds__(256, kTN == 128 ? 2 : 3) glob_tiles_kernel(Edg
         }
     }
     acc.fp += rsum; // flush() reduces over the warp
-    flush(acc, A, 1, lane);
+    flush<MODE != 0>(acc, A, 1, lane, j);
 }
 
 // generator.hpp:84-102: all pairs i < k of the global points, request = i.
@@ -1289,6 +1355,10 @@ __global__ void __launch_bounds__(kGGTile) glob_pairs_kernel(EdgeArgs A, std::ui
     const std::uint64_t J   = I + (t - start(I));
     const std::uint64_t nG  = A.n_glob;
     const std::uint64_t col = J * kGGTile + threadIdx.x;
+    __shared__ AnnAcc        SA;
+    __shared__ std::uint64_t sg[kMaxAnnuli + 1];
+    ann_zero<MODE != 0>(SA);
+    for (int a = threadIdx.x; a <= A.first_streaming; a += blockDim.x) sg[a] = A.gseg[a];
     if (col < nG) {
         s1[threadIdx.x] = A.rec1[A.n_ext + col];
         s2[threadIdx.x] = A.rec2[A.n_ext + col];
@@ -1296,6 +1366,14 @@ __global__ void __launch_bounds__(kGGTile) glob_pairs_kernel(EdgeArgs A, std::ui
     __syncthreads();
     const std::uint64_t i = I * kGGTile + threadIdx.x;
     Acc                 acc;
+    int                 ai = 0, key = -1; // key: the annulus of all this row's pairs (single-annulus rows)
+    // annulus of a global point index: the last inner annulus whose id base is <= it (ids are
+    // annulus-major); a pair counts for max(annulus_i, annulus_k) (generator.hpp:89)
+    auto ann_of = [&](std::uint64_t g) {
+        int a = 0;
+        while (a + 1 < A.first_streaming && sg[a + 1] <= g) ++a;
+        return a;
+    };
     if (i < nG) {
         const double2 r1 = A.rec1[A.n_ext + i], r2 = A.rec2[A.n_ext + i];
         const double  cs = r1.x, sn = r1.y, coth = r2.x, rci = fmul(A.cosh_R, r2.y);
@@ -1303,15 +1381,53 @@ __global__ void __launch_bounds__(kGGTile) glob_pairs_kernel(EdgeArgs A, std::ui
         if (k0 <= i) k0 = i + 1;
         const std::uint64_t k1 = (J + 1) * kGGTile < nG ? (J + 1) * kGGTile : nG;
         acc.comps              = k1 > k0 ? k1 - k0 : 0;
-        for (std::uint64_t k = k0; k < k1; ++k)
-            count_edge<MODE>(A, edge_test(cs, sn, coth, rci, s1[k - J * kGGTile], s2[k - J * kGGTile]), i, k, acc);
+        if constexpr (MODE == 0) { // counters only (the bench path): no per-annulus bookkeeping
+            for (std::uint64_t k = k0; k < k1; ++k)
+                count_edge<MODE>(A, edge_test(cs, sn, coth, rci, s1[k - J * kGGTile], s2[k - J * kGGTile]), i, k, acc);
+        } else {
+        ai = ann_of(i);
+        const int a0 = k1 > k0 ? ann_of(k0) : ai, a1 = k1 > k0 ? ann_of(k1 - 1) : ai;
+        if (a0 == a1) { // the usual case: the row's columns lie in one annulus (booked below, per warp)
+            for (std::uint64_t k = k0; k < k1; ++k)
+                count_edge<MODE>(A, edge_test(cs, sn, coth, rci, s1[k - J * kGGTile], s2[k - J * kGGTile]), i, k, acc);
+            key = ai > a0 ? ai : a0;
+        } else { // one run per annulus of k (global ids are annulus-major)
+            for (std::uint64_t k = k0; k < k1;) {
+                const int           ak = ann_of(k);
+                const std::uint64_t kn = sg[ak + 1]; // a0 != a1: ak is not the last annulus
+                const std::uint64_t ks = k, ke = kn < k1 ? kn : k1;
+                const unsigned long long e0 = acc.edges;
+                for (; k < ke; ++k)
+                    count_edge<MODE>(A, edge_test(cs, sn, coth, rci, s1[k - J * kGGTile], s2[k - J * kGGTile]), i, k,
+                                     acc);
+                ann_add<MODE != 0>(SA, ai > ak ? ai : ak, acc.edges - e0, ke - ks);
+            }
+        }
+        }
+    }
+    if constexpr (MODE != 0) { // single-annulus rows: one shared-memory atomic per annulus per warp
+        const unsigned grp = __match_any_sync(kFull, key);
+        const unsigned ce  = __reduce_add_sync(grp, key >= 0 ? unsigned(acc.edges) : 0u);
+        const unsigned cc  = __reduce_add_sync(grp, key >= 0 ? unsigned(acc.comps) : 0u);
+        if (key >= 0 && int(threadIdx.x & 31) == __ffs(grp) - 1) ann_add<MODE != 0>(SA, key, ce, cc);
     }
     flush(acc, A, 2, threadIdx.x & 31);
+    __syncthreads();
+    ann_flush<MODE != 0>(SA, A);
 }
 
-// Fold the counter slots of the three families into A.ctr.
+// Fold the counter slots of the three families into A.ctr (blocks 0..2) and the
+// per-annulus slots into slot 0 (block 3).
 __global__ void __launch_bounds__(1024) reduce_counters_kernel(EdgeArgs A) {
     const int          f = blockIdx.x;
+    if (f == 3) {
+        for (int i = threadIdx.x; i < 2 * kMaxAnnuli; i += blockDim.x) {
+            unsigned long long v = 0;
+            for (int s = 0; s < kAnnSlots; ++s) v += A.ann_ctr[std::size_t(s) * 2 * kMaxAnnuli + i];
+            A.ann_ctr[i] = v; // slot 0 holds the totals (slots 1.. are left as they are)
+        }
+        return;
+    }
     unsigned long long e = 0, fp = 0, c = 0;
     for (int i = threadIdx.x; i < kSlots; i += blockDim.x) {
         const SlotCounter& s = A.slots[f * kSlots + i];
@@ -1479,7 +1595,7 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
             RHG_LAUNCH_MODE(deferred_kernel, mode, RHG_CFG(148 * 4, 256, 0, st), a);
             ++*launches;
         }
-        reduce_counters_kernel<<<3, 1024, 0, st>>>(a);
+        reduce_counters_kernel<<<4, 1024, 0, st>>>(a);
         ++*launches;
     }
 }

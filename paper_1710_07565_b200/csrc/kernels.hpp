@@ -119,6 +119,8 @@ struct EdgeArgs {
     Counters*         ctr = nullptr; // [0] streaming kernel, [1] dense engine, [2] global unit
     SlotCounter*      slots = nullptr; // [3 * kSlots] partial counters (folded into ctr at the end)
     int               ablate = 0;       // RHG_ABLATE bit flags: skip kernel phases (timing experiments; results invalid)
+    unsigned long long* ann_ctr = nullptr;    // [kAnnSlots][2 * kMaxAnnuli]: per-annulus edges, then comps
+    const std::uint64_t* gseg = nullptr;      // [first_streaming + 1] global-id base of each inner annulus
     double*             lam_tmp = nullptr;    // [n_ext] engine-frame lambda in sampler order (sort phase)
     ulonglong2*         edge_out = nullptr;   // optional materialised edges (MODE 2): canonical (u, v)
     unsigned long long  edge_cap = 0;
@@ -152,6 +154,8 @@ void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, 
                          std::uint64_t* launches);
 
 constexpr int kGGTile = 128;
+constexpr int kMaxAnnuli = 64;  // annulus masks are 64-bit
+constexpr int kAnnSlots  = 64;  // spread per-annulus counter slots (folded by reduce_counters_kernel)
 constexpr int kTileNodes = 128; // owned nodes per dense-engine node tile (edges.cu glob_tiles_kernel; 64: 0.64 vs 0.58 ms)
 constexpr int kSlabNodes = 512; // owned nodes per slab of the slab join (edges.cu)
 constexpr int kMaxCls = 1024; // (source, radial class) segments of the dense-engine requests

@@ -170,3 +170,16 @@ def test_same_points_parity_large_R(oracle, n, alpha, C, seed, P):
     dev = rhg.sample_points(p)
     want2 = oracle.count_edges_from_points(n, alpha, C, seed, P, dev)
     assert triple(rhg.generate_stats(p)) == (want2["edges"], want2["fingerprint"], want2["comps"])
+
+
+def test_counter_modes_agree(oracle, golden):
+    """The counters-only kernels (MODE 0), the degree/per-annulus kernels (MODE 1) and the
+    edge-stream kernels (MODE 2) are separate instantiations: all must give the golden counters."""
+    for s in rows(golden, {"grid"}, 2000)[::3]:
+        p = params_of(s)
+        pts = oracle.points(p.n, p.alpha, p.C, p.seed, p.chunks)
+        want = (s["edges"], s["fingerprint"], s["comps"])
+        assert triple(rhg.count_edges_from_points(p, pts)) == want, s
+        assert triple(rhg.count_edges_from_points(p, pts, degrees=True)) == want, s
+        _, st = rhg.edges_from_points(p, pts)
+        assert triple(st) == want, s
