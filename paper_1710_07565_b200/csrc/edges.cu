@@ -735,6 +735,10 @@ __global__ void __launch_bounds__(256) tail_kernel(EdgeArgs A) {
             for (int j = a; j < A.count; ++j) {
                 const AnnulusDev& Aj = A.ann[j];
                 if (Aj.end == Aj.off || !((srcm >> j) & 1ull)) continue;
+                // a halo request tests owned nodes only: skip targets whose owned block ends before
+                // the request's window can begin (host bound on the half-width; no acos needed)
+                if (halo_req && (Aj.halo == Aj.off || fsub(lam, A.hbound[a * A.count + j]) > A.s_lam[Aj.halo - 1]))
+                    continue;
                 const bool own = j == a;
                 double     lo, hi;
                 if (own) {
