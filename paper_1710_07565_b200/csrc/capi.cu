@@ -186,6 +186,11 @@ struct Plan {
 // at a's median radius (density ~ sinh(alpha r)); same-annulus windows count
 // half (dedup).  Only chooses the engine for (a, j); never affects results.
 constexpr double kDenseMin = 96.0;
+// Outer streaming annuli whose chains run in wave 2 (generate mode)
+#ifndef RHG_WAVE2_DEFAULT
+#define RHG_WAVE2_DEFAULT 1
+#endif
+constexpr std::uint32_t kWave2Annuli = RHG_WAVE2_DEFAULT;
 double expected_window_nodes(const Layout& L, std::uint32_t a, std::uint32_t j) {
     const double r    = std::acosh(0.5 * (L.cosh_alpha_lower[a] + L.cosh_alpha_upper[a])) / L.alpha;
     const double ex   = std::exp(r), mex = 1.0 / ex, sh = 0.5 * (ex - mex);
@@ -224,6 +229,7 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
     pl.e1 = std::uint32_t(std::uint64_t(Pc) * (r + 1) / W);
     pl.T  = pl.e1 - pl.e0;
     pl.ann.resize(L.count);
+    pl.jobs.reserve(std::size_t(L.count) * (std::size_t(pl.T) + 1) + std::size_t(L.first_streaming) * Pc);
     std::uint64_t run = 0;
     for (std::uint32_t i = 0; i < L.count; ++i) {
         AnnulusDev& A = pl.ann[i];
@@ -292,16 +298,32 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
     // wave split (generate mode): the outermost streaming annulus (the longest sorted-uniform
     // chains) forms wave 2 when it is not a dense-engine source; everything else is wave 1
     pl.wave_j = L.count;
-    if (L.count >= L.first_streaming + 2 && pl.T > 0 && !pl.dense_mask[L.count - 1]) pl.wave_j = L.count - 1;
-    pl.job_order.resize(pl.jobs.size());
-    for (std::uint32_t k = 0; k < pl.job_order.size(); ++k) pl.job_order[k] = k;
-    auto in_wave2 = [&](std::uint32_t k) { return pl.jobs[k].annulus >= pl.wave_j && pl.jobs[k].annulus < L.count; };
-    std::stable_sort(pl.job_order.begin(), pl.job_order.end(), [&](std::uint32_t x, std::uint32_t y) {
-        if (in_wave2(x) != in_wave2(y)) return !in_wave2(x);
-        return pl.jobs[x].count > pl.jobs[y].count;
-    });
-    pl.wave2_jobs = 0;
-    for (std::uint32_t k = 0; k < pl.jobs.size(); ++k) pl.wave2_jobs += in_wave2(k);
+    {
+        const char*         wv = std::getenv("RHG_WAVE2_ANNULI"); // A/B switch: outer annuli in wave 2
+        const std::uint32_t w2 = wv ? std::uint32_t(std::max(1, std::atoi(wv))) : kWave2Annuli;
+        if (L.count >= L.first_streaming + 1 + w2 && pl.T > 0) {
+            bool dense_src = false;
+            for (std::uint32_t a = L.count - w2; a < L.count; ++a) dense_src |= pl.dense_mask[a] != 0;
+            if (!dense_src) pl.wave_j = L.count - w2;
+        }
+    }
+    // job order: wave 1 then wave 2, each by descending count, ties by job index (a stable
+    // sort), as one u64 key per job: wave bit | complemented count (< 2^39) | index (< 2^24)
+    if (pl.jobs.size() >= (std::size_t(1) << 24)) throw InvalidArgument("rhg: too many sampler streams");
+    {
+        std::vector<std::uint64_t> key(pl.jobs.size());
+        pl.wave2_jobs = 0;
+        for (std::uint32_t k = 0; k < key.size(); ++k) {
+            const StreamJob&    J  = pl.jobs[k];
+            const bool          w2 = J.annulus >= pl.wave_j && J.annulus < L.count;
+            const std::uint64_t c  = std::min<std::uint64_t>(J.count, (std::uint64_t(1) << 39) - 1);
+            key[k] = (std::uint64_t(w2) << 63) | ((((std::uint64_t(1) << 39) - 1) - c) << 24) | k;
+            pl.wave2_jobs += w2;
+        }
+        std::sort(key.begin(), key.end());
+        pl.job_order.resize(key.size());
+        for (std::uint32_t k = 0; k < key.size(); ++k) pl.job_order[k] = std::uint32_t(key[k] & 0xffffffu);
+    }
     const auto tl1 = std::chrono::steady_clock::now();
     pl.sub_ms[0] = std::chrono::duration<double, std::milli>(tl1 - tl0).count() - pl.layout_ms;
     // chain bins: each wave's streams packed longest-processing-time-first into bins whose
@@ -317,22 +339,38 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
         std::uint64_t sum = 0, mx = 0;
         for (std::uint32_t k = j0; k < j1; ++k) sum += pl.jobs[pl.job_order[k]].count, mx = std::max(mx, pl.jobs[pl.job_order[k]].count);
         const std::uint64_t nb = std::min<std::uint64_t>(j1 - j0, mx ? (sum + mx - 1) / mx + (sum + 7 * mx) / (8 * mx) : 1);
-        std::vector<std::vector<std::uint32_t>> bin(nb);
-        using LB = std::pair<std::uint64_t, std::uint32_t>; // (load, bin): min-heap on load
-        std::priority_queue<LB, std::vector<LB>, std::greater<LB>> heap;
-        for (std::uint32_t b = 0; b < nb; ++b) heap.push({0, b});
+        // min-heap on (load, bin) in a flat array; bin ids per job, then a stable counting sort
+        // (per-bin vectors cost more in allocations than the packing itself)
+        std::vector<std::uint64_t> heap(nb);
+        // key = load << 24 | bin: bins < 2^24 (jobs), loads < 2^35 (n < 2^32 plus 1250 per job)
+        if (nb >= (1u << 24)) throw InvalidArgument("rhg: too many sampler streams");
+        for (std::uint32_t b = 0; b < nb; ++b) heap[b] = b; // load 0
+        std::vector<std::uint32_t> bin_of(j1 - j0), fill(nb + 1, 0);
         for (std::uint32_t k = j0; k < j1; ++k) { // job_order is by descending count inside a wave
-            LB lb = heap.top();
-            heap.pop();
-            lb.first += pl.jobs[pl.job_order[k]].count + 1250; // + per-stream pipeline fill / seeding
-            bin[lb.second].push_back(pl.job_order[k]);
-            heap.push(lb);
+            const std::uint64_t top = heap[0];
+            const std::uint32_t b   = std::uint32_t(top & 0xffffffu);
+            bin_of[k - j0]          = b;
+            ++fill[b + 1];
+            // + per-stream pipeline fill / seeding
+            const std::uint64_t v = top + ((pl.jobs[pl.job_order[k]].count + 1250) << 24);
+            std::size_t         h = 0;
+            for (;;) { // sift the grown root down
+                std::size_t c = 2 * h + 1;
+                if (c >= nb) break;
+                if (c + 1 < nb && heap[c + 1] < heap[c]) ++c;
+                if (heap[c] >= v) break;
+                heap[h] = heap[c], h = c;
+            }
+            heap[h] = v;
         }
-        std::uint32_t k = j0;
-        for (const auto& v: bin) {
-            for (std::uint32_t x: v) pl.job_order[k++] = x;
-            pl.chain_bins.push_back(k);
+        for (std::uint32_t b = 0; b < nb; ++b) fill[b + 1] += fill[b];
+        std::vector<std::uint32_t> ordered(j1 - j0);
+        {
+            std::vector<std::uint32_t> pos(fill.begin(), fill.end() - 1);
+            for (std::uint32_t k = j0; k < j1; ++k) ordered[pos[bin_of[k - j0]]++] = pl.job_order[k];
         }
+        std::copy(ordered.begin(), ordered.end(), pl.job_order.begin() + j0);
+        for (std::uint32_t b = 0; b < nb; ++b) pl.chain_bins.push_back(j0 + fill[b + 1]);
         if (!wv) pl.chain_bins1 = std::uint32_t(nb);
     }
     pl.sub_ms[1] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl1).count();

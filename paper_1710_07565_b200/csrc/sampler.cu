@@ -11,7 +11,7 @@
 //                           cur), clamped (rng.hpp:218-229) — the only serial
 //                           dependency, run by one lane from shared memory.
 //   S2 mt_uniforms_kernel   one CTA per (stream, radii): the radius uniforms
-//                           (seed {4,i,c}), twist warp + tempering warps.
+//                           (seed {4,i,c}), a block-wide two-phase twist.
 //      point_radial_kernel  per point, on a side stream beside S1: the radius-only
 //                           attributes r, coth r, 1/sinh r, half-width
 //                           (partition.hpp:64-70, sweep.hpp:121-134).
@@ -42,40 +42,6 @@ __device__ __forceinline__ std::uint64_t mt_mix(std::uint64_t cur, std::uint64_t
     return far ^ (x >> 1) ^ ((x & 1ull) ? 0xB5026F5AA96619E9ull : 0ull);
 }
 
-// Warp-parallel regeneration of the 312-word state, equal to the sequential
-// in-place twist of [rand.predef] mersenne_twister_engine.
-__device__ __forceinline__ void mt_twist_warp(std::uint64_t* mt, int lane) {
-    std::uint64_t nv[5];
-    // words 0..155 read only old words
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-        const int i = lane + 32 * k;
-        if (i < kMtN - kMtM) nv[k] = mt_mix(mt[i], mt[i + 1], mt[i + kMtM]);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-        const int i = lane + 32 * k;
-        if (i < kMtN - kMtM) mt[i] = nv[k];
-    }
-    __syncwarp();
-    // words 156..310 read new words i-156 and old words i, i+1
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-        const int i = kMtN - kMtM + lane + 32 * k;
-        if (i < kMtN - 1) nv[k] = mt_mix(mt[i], mt[i + 1], mt[i - (kMtN - kMtM)]);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-        const int i = kMtN - kMtM + lane + 32 * k;
-        if (i < kMtN - 1) mt[i] = nv[k];
-    }
-    __syncwarp();
-    if (lane == 0) mt[kMtN - 1] = mt_mix(mt[kMtN - 1], mt[0], mt[kMtM - 1]);
-    __syncwarp();
-}
-
 // Out-of-place twist: B = twist(A), equal to the in-place sequential twist of
 // [rand.predef] (words 0..155 read old words only, 156..310 read new words
 // i-156, word 311 reads new words 0 and 155).
@@ -96,27 +62,34 @@ __device__ __forceinline__ void mt_twist_to(const std::uint64_t* __restrict__ A,
     __syncwarp();
 }
 
-constexpr int kMtWarps = 4;
+#ifndef RHG_MT_THREADS
+#define RHG_MT_THREADS 320 // measured cfg2: 160 -> 4.12 ms/step, 320 -> 4.07
+#endif
+constexpr int kMtThreads = RHG_MT_THREADS; // >= 156: one state word per thread and twist phase
 
-// One CTA per (stream, {angles, radii}): warp 0 seeds ([rand.predef]
-// seeding recurrence, serial by definition) and regenerates the 312-word state
-// block k into buffer k % 2 while warps 1..3 temper block k - 1 and write its
-// outputs (x >> 11) * 2^-53 coalesced; one __syncthreads per block.  A long
-// stream then costs ~one twist per block instead of twist + tempering.
+// One CTA per (stream, {angles, radii}): thread 0 seeds ([rand.predef]
+// seeding recurrence, serial by definition); then per 312-word block the
+// whole CTA regenerates the state out of place in two phases (words 0..155
+// read old words only; 156..311 read new words 0..155), one word per thread
+// and phase, while tempering the previous block into (x >> 11) * 2^-53,
+// written coalesced — two barriers per block.  A long stream's serial chain of
+// twists (the radius side's critical path) is then two shared-memory round
+// trips per block instead of a warp walking 5 words per phase.
 // which: 0 = both streams of every job, 1 = angle streams only, 2 = radius streams only
-__global__ void __launch_bounds__(32 * kMtWarps) mt_uniforms_kernel(const StreamJob* __restrict__ jobs, int njobs,
-                                                                     double* __restrict__ u_ang,
-                                                                     double* __restrict__ u_rad, int which) {
+__global__ void __launch_bounds__(kMtThreads) mt_uniforms_kernel(const StreamJob* __restrict__ jobs, int njobs,
+                                                                 double* __restrict__ u_ang,
+                                                                 double* __restrict__ u_rad, int which) {
+    static_assert(kMtThreads >= kMtN - kMtM && kMtThreads % 32 == 0, "one twist word per thread and phase");
     __shared__ std::uint64_t st[2][kMtN]; // st[k & 1]: the state after k twists
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gw   = blockIdx.x;
+    const int t  = threadIdx.x;
+    const int gw = blockIdx.x;
     if (gw >= (which ? 1 : 2) * njobs) return;
     const StreamJob&    J   = jobs[which ? gw : gw >> 1];
     const bool          ang = which ? which == 1 : (gw & 1) == 0;
     double*             dst = (ang ? u_ang : u_rad) + J.out_off;
     const std::uint64_t n   = J.count;
     if (n == 0) return;
-    if (warp == 0 && lane == 0) {
+    if (t == 0) {
         std::uint64_t x = ang ? J.seed_ang : J.seed_rad;
         st[0][0]        = x;
         for (int i = 1; i < kMtN; ++i) {
@@ -127,14 +100,20 @@ __global__ void __launch_bounds__(32 * kMtWarps) mt_uniforms_kernel(const Stream
     __syncthreads();
     const std::uint64_t nblk = (n + kMtN - 1) / kMtN;
     for (std::uint64_t k = 0; k <= nblk; ++k) {
-        if (warp == 0) {
-            if (k < nblk) mt_twist_to(st[k & 1], st[(k + 1) & 1], lane); // block k
-        } else if (k > 0) { // temper and store block k - 1 (the state after k twists)
-            const std::uint64_t  base = (k - 1) * kMtN;
-            const int            cnt  = n - base < std::uint64_t(kMtN) ? int(n - base) : kMtN;
-            const std::uint64_t* o    = st[k & 1];
-            for (int i = threadIdx.x - 32; i < cnt; i += 32 * (kMtWarps - 1))
-                dst[base + i] = double(mt_temper(o[i]) >> 11) * 0x1.0p-53;
+        const std::uint64_t* A = st[k & 1];       // the state after k twists (block k - 1)
+        std::uint64_t*       B = st[(k + 1) & 1]; // block k
+        if (k > 0) { // temper and store block k - 1
+            const std::uint64_t base = (k - 1) * kMtN;
+            const int           cnt  = n - base < std::uint64_t(kMtN) ? int(n - base) : kMtN;
+            for (int i = t; i < cnt; i += kMtThreads) dst[base + i] = double(mt_temper(A[i]) >> 11) * 0x1.0p-53;
+        }
+        if (k < nblk) {
+            if (t < kMtN - kMtM) B[t] = mt_mix(A[t], A[t + 1], A[t + kMtM]);
+            __syncthreads();
+            if (t < kMtN - kMtM) {
+                const int i = kMtN - kMtM + t;
+                B[i] = i < kMtN - 1 ? mt_mix(A[i], A[i + 1], B[t]) : mt_mix(A[kMtN - 1], B[0], B[kMtM - 1]);
+            }
         }
         __syncthreads();
     }
@@ -192,6 +171,10 @@ constexpr int kAngWarps = RHG_ANG_WARPS; // warp 0: chain, warp kMtWarp: MT, the
 #define RHG_MT_WARP 4 // shares the chain warp's SM sub-partition (integer work only), so no pow warp does
 #endif
 constexpr int kMtWarp = RHG_MT_WARP;
+#ifndef RHG_CHAIN_KB
+#define RHG_CHAIN_KB 6 // double2 per register batch of the chain lane (must divide 78)
+#endif
+static_assert(78 % RHG_CHAIN_KB == 0, "the chain's batches must tile a 312-value block");
 struct AngSmem {
     std::uint64_t st[2][kMtN];   // MT state, double-buffered (warp 1)
     double        u[2][kMtN];    // uniforms of blocks b, b-1
@@ -253,7 +236,7 @@ __global__ void __launch_bounds__(32 * kAngWarps) angle_side_kernel(const Stream
                 double* x = S.x[(s - 2) % 3];
                 if (lane == 0) {
                     double2*      x2 = reinterpret_cast<double2*>(x);
-                    constexpr int kB = 6;              // 156 double2 = 13 batches of 12 values
+                    constexpr int kB = RHG_CHAIN_KB;   // 156 double2 = (78 / kB) batches of 2 kB values
                     double2       A[kB], B[kB];
 #pragma unroll
                     for (int i = 0; i < kB; ++i) A[i] = x2[i];
@@ -331,9 +314,7 @@ __global__ void frames_from_points_kernel(const StreamJob* __restrict__ jobs, in
 // radius side (MT -> radial attributes) runs on S.side and joins st.
 void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
     if (S.total == 0 || S.njobs == 0) return;
-    const int      mt_blocks = S.njobs; // one CTA per stream
-    const unsigned pblocks   = unsigned((S.total + 255) / 256);
-    cudaStream_t   side      = S.side ? S.side : st;
+    cudaStream_t side = S.side ? S.side : st;
     if (S.side) {
         cudaEventRecord(S.ev_fork, st);
         cudaStreamWaitEvent(side, S.ev_fork, 0);
@@ -349,14 +330,15 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
         S.mark("chain_wave2(late)", S.late);
         ++*launches;
     }
-    mt_uniforms_kernel<<<mt_blocks, 32 * kMtWarps, 0, side>>>(S.jobs, S.njobs, S.beta, S.hw, 2);
+    mt_uniforms_kernel<<<S.njobs, kMtThreads, 0, side>>>(S.jobs, S.njobs, S.beta, S.hw, 2);
     S.mark("mt_radii", side);
-    ++*launches;
-    // the radius attributes run beside the angle side (serialising them after the wave-1 chains
-    // measured slower at cfg2: the wave-1 sort then waits for the whole radius side)
-    point_radial_kernel<<<pblocks, 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total, S.hw, S.rec2, S.r_out);
+    // the radius attributes run beside the angle side (measured at cfg2: serialising them after
+    // the wave-1 chains is slower — the wave-1 sort then waits for the whole radius side — and
+    // so is splitting them by wave: the GPU is saturated either way)
+    point_radial_kernel<<<unsigned((S.total + 255) / 256), 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total,
+                                                                          S.hw, S.rec2, S.r_out);
     S.mark("radial", side);
-    ++*launches;
+    *launches += 2;
     if (nb1) {
         angle_side_kernel<<<nb1, 32 * kAngWarps, 0, st>>>(S.jobs, S.chain_bins, nb1, S.job_order, S.beta);
         ++*launches;
@@ -376,7 +358,7 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
 
 void launch_mt_uniforms(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
     if (S.total == 0 || S.njobs == 0) return;
-    mt_uniforms_kernel<<<2 * S.njobs, 32 * kMtWarps, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 0);
+    mt_uniforms_kernel<<<2 * S.njobs, kMtThreads, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 0);
     *launches += 1;
 }
 
