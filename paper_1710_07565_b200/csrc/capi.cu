@@ -246,8 +246,6 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
             if (cnt) {
                 StreamJob J{};
                 J.out_off = run, J.count = cnt, J.annulus = i, J.chunk = c, J.lift = (pl.e0 + t == Pc) ? 1u : 0u;
-                J.seed_ang = derive_seed3(L.seed, kPhaseAngles, i, c);
-                J.seed_rad = derive_seed3(L.seed, kPhaseRadii, i, c);
                 J.a = chunk_lower_bound(c, Pc), J.b = chunk_upper_bound(c, Pc);
                 pl.jobs.push_back(J);
             }
@@ -276,8 +274,6 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
             if (!cnt) continue;
             StreamJob J{};
             J.out_off = pl.n_ext + L.chunk_id_base(i, c), J.count = cnt, J.annulus = i, J.chunk = c, J.lift = 0;
-            J.seed_ang = derive_seed3(L.seed, kPhaseAngles, i, c);
-            J.seed_rad = derive_seed3(L.seed, kPhaseRadii, i, c);
             J.a = chunk_lower_bound(c, Pc), J.b = chunk_upper_bound(c, Pc);
             pl.jobs.push_back(J);
         }
@@ -564,6 +560,7 @@ SamplerArgs sampler_args(rhg_ctx* ctx, const Plan& pl, const Tables& t) {
     SamplerArgs s;
     s.chain_bins = t.chain_bins, s.chain_bins1 = int(pl.chain_bins1), s.chain_bins_total = int(pl.chain_bins.size()) - 1;
     s.jobs = t.jobs, s.job_order = t.job_order, s.njobs = int(pl.jobs.size()), s.ann = t.ann, s.alpha = pl.L.alpha, s.total = pl.total;
+    s.seed = pl.L.seed;
     s.beta = ctx->beta.as<double>(), s.hw = ctx->hw.as<double>();
     s.rec0 = ctx->rec0.as<double2>(), s.rec1 = ctx->rec1.as<double2>(), s.rec2 = ctx->rec2.as<double2>();
     s.side = ctx->side, s.ev_fork = ctx->fork, s.ev_join = ctx->join;

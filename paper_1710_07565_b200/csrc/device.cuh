@@ -31,11 +31,26 @@ struct AnnulusDev {
 // source (sweep.hpp:102-111), written to [out_off, out_off + count).
 struct StreamJob {
     std::uint64_t out_off, count;
-    std::uint64_t seed_ang, seed_rad; // derive_seed(seed, {3|4, annulus, chunk})
     double        a, b;               // chunk angular bounds (sweep.hpp:80-85)
     std::uint32_t annulus, lift;      // lift: halo copy of chunk 0 seen from chunk P-1
     std::uint32_t chunk, pad;
 };
+
+// rng.hpp:15-19 + 41-46: derive_seed(root, {phase, annulus, chunk}) of a stream,
+// computed where the stream is drawn (the host plan no longer carries seeds).
+__device__ __forceinline__ std::uint64_t splitmix_mix_d(std::uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ std::uint64_t stream_seed(std::uint64_t root, std::uint64_t phase, std::uint64_t annulus,
+                                                     std::uint64_t chunk) {
+    constexpr std::uint64_t kG = 0x9E3779B97F4A7C15ull;
+    std::uint64_t           h  = splitmix_mix_d(root + kG);
+    h                          = splitmix_mix_d((h + kG) ^ phase);
+    h                          = splitmix_mix_d((h + kG) ^ annulus);
+    return splitmix_mix_d((h + kG) ^ chunk);
+}
 
 struct Counters { // one per edge-producing kernel family
     unsigned long long edges, fp, comps;

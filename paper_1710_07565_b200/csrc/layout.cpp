@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <exception>
 #include <condition_variable>
@@ -22,16 +23,33 @@ std::uint64_t splitmix_mix(std::uint64_t z) { // rng.hpp:15-19
 constexpr std::uint64_t kGolden = 0x9E3779B97F4A7C15ull;
 
 // std::mt19937_64 state machine ([rand.predef]); host copy used by the
-// binomial draws only.
+// binomial draws only.  Most split draws consume a handful of outputs, so the
+// seeding recurrence and the first twist run lazily: output k of the first
+// block needs seed words up to k + 156 (k < 156: new[k] = f(old[k], old[k+1],
+// old[k+156]); k >= 156: f(old[k], old[k+1], new[k-156]); k = 311: f(old[311],
+// new[0], new[155])), later blocks twist in place as usual — the same stream.
 class Mt64 {
 public:
-    explicit Mt64(std::uint64_t s) {
-        mt_[0] = s;
-        for (int i = 1; i < 312; ++i) mt_[i] = 6364136223846793005ull * (mt_[i - 1] ^ (mt_[i - 1] >> 62)) + std::uint64_t(i);
-    }
+    explicit Mt64(std::uint64_t s) { old_[0] = s; }
     std::uint64_t bits() {
-        if (idx_ >= 312) twist();
-        std::uint64_t y = mt_[idx_++];
+        std::uint64_t y;
+        if (first_) {
+            const int k = idx_++;
+            if (k < 156) {
+                seed_to(k + 156);
+                y = mix(old_[k], old_[k + 1], old_[k + 156]);
+            } else if (k < 311) {
+                seed_to(k + 1);
+                y = mix(old_[k], old_[k + 1], mt_[k - 156]);
+            } else {
+                y = mix(old_[311], mt_[0], mt_[155]);
+            }
+            mt_[k] = y;
+            if (idx_ == 312) first_ = false;
+        } else {
+            if (idx_ >= 312) twist();
+            y = mt_[idx_++];
+        }
         y ^= (y >> 29) & 0x5555555555555555ull;
         y ^= (y << 17) & 0x71D67FFFEDA60000ull;
         y ^= (y << 37) & 0xFFF7EEE000000000ull;
@@ -40,16 +58,23 @@ public:
     double uniform() { return double(bits() >> 11) * 0x1.0p-53; } // rng.hpp:63
 
 private:
+    static std::uint64_t mix(std::uint64_t cur, std::uint64_t nxt, std::uint64_t far) {
+        const std::uint64_t x = (cur & 0xFFFFFFFF80000000ull) | (nxt & 0x7FFFFFFFull);
+        return far ^ (x >> 1) ^ ((x & 1) ? 0xB5026F5AA96619E9ull : 0ull);
+    }
+    void seed_to(int k) { // old_[0..k] hold the seeding recurrence
+        for (; seeded_ < k; ++seeded_)
+            old_[seeded_ + 1] = 6364136223846793005ull * (old_[seeded_] ^ (old_[seeded_] >> 62)) + std::uint64_t(seeded_ + 1);
+    }
     void twist() {
-        constexpr std::uint64_t UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull, A = 0xB5026F5AA96619E9ull;
-        for (int i = 0; i < 312; ++i) {
-            const std::uint64_t x = (mt_[i] & UM) | (mt_[(i + 1) % 312] & LM);
-            mt_[i] = mt_[(i + 156) % 312] ^ (x >> 1) ^ ((x & 1) ? A : 0);
-        }
+        for (int i = 0; i < 312; ++i) mt_[i] = mix(mt_[i], mt_[(i + 1) % 312], mt_[(i + 156) % 312]);
         idx_ = 0;
     }
+    std::uint64_t old_[312];
     std::uint64_t mt_[312];
-    int           idx_ = 312;
+    int           seeded_ = 0; // old_[0..seeded_] are valid
+    int           idx_    = 0;
+    bool          first_  = true;
 };
 
 // A persistent host worker pool for the layout's independent binomial trees
@@ -81,8 +106,9 @@ public:
         }
         cv_.notify_all();
         work();
+        spin([&] { return pending_.load(std::memory_order_acquire) == 0; });
         std::unique_lock<std::mutex> g(mu_);
-        done_.wait(g, [&] { return pending_ == 0; });
+        done_.wait(g, [&] { return pending_.load() == 0; });
         job_ = nullptr;
         if (err) std::rethrow_exception(err);
     }
@@ -100,27 +126,38 @@ private:
         cv_.notify_all();
         for (auto& t: workers_) t.join();
     }
+    // Busy-wait up to ~50 us before blocking: the layout runs two parallel regions back to
+    // back, and a futex wake-up per worker and region costs more than the regions' work.
+    template <class P>
+    static void spin(P&& ready) {
+        const auto t0 = std::chrono::steady_clock::now();
+        for (unsigned k = 1; !ready(); ++k)
+            if ((k & 255) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(50)) return;
+    }
     void loop() {
         std::uint64_t seen = 0;
         for (;;) {
+            spin([&] { return gen_.load(std::memory_order_acquire) != seen; });
             std::function<void()>* job;
             {
                 std::unique_lock<std::mutex> g(mu_);
-                cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+                cv_.wait(g, [&] { return stop_ || gen_.load() != seen; });
                 if (stop_) return;
-                seen = gen_, job = job_;
+                seen = gen_.load(), job = job_;
             }
             (*job)();
-            std::lock_guard<std::mutex> g(mu_);
-            if (--pending_ == 0) done_.notify_one();
+            if (pending_.fetch_sub(1, std::memory_order_acq_rel) == 1) {
+                std::lock_guard<std::mutex> g(mu_);
+                done_.notify_one();
+            }
         }
     }
     std::vector<std::thread>  workers_;
     std::mutex                mu_, call_mu_;
     std::condition_variable   cv_, done_;
     std::function<void()>*    job_     = nullptr;
-    unsigned                  pending_ = 0;
-    std::uint64_t             gen_     = 0;
+    std::atomic<unsigned>      pending_{0};
+    std::atomic<std::uint64_t> gen_{0};
     bool                      stop_    = false;
 };
 

@@ -78,7 +78,8 @@ constexpr int kMtThreads = RHG_MT_THREADS; // >= 156: one state word per thread 
 // which: 0 = both streams of every job, 1 = angle streams only, 2 = radius streams only
 __global__ void __launch_bounds__(kMtThreads) mt_uniforms_kernel(const StreamJob* __restrict__ jobs, int njobs,
                                                                  double* __restrict__ u_ang,
-                                                                 double* __restrict__ u_rad, int which) {
+                                                                 double* __restrict__ u_rad, int which,
+                                                                 std::uint64_t seed) {
     static_assert(kMtThreads >= kMtN - kMtM && kMtThreads % 32 == 0, "one twist word per thread and phase");
     __shared__ std::uint64_t st[2][kMtN]; // st[k & 1]: the state after k twists
     const int t  = threadIdx.x;
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(kMtThreads) mt_uniforms_kernel(const StreamJob
     const std::uint64_t n   = J.count;
     if (n == 0) return;
     if (t == 0) {
-        std::uint64_t x = ang ? J.seed_ang : J.seed_rad;
+        std::uint64_t x = stream_seed(seed, ang ? 3 : 4, J.annulus, J.chunk); // kPhaseAngles / kPhaseRadii
         st[0][0]        = x;
         for (int i = 1; i < kMtN; ++i) {
             x        = 6364136223846793005ull * (x ^ (x >> 62)) + std::uint64_t(i);
@@ -183,7 +184,7 @@ struct AngSmem {
 __global__ void __launch_bounds__(32 * kAngWarps) angle_side_kernel(const StreamJob* __restrict__ jobs,
                                                                     const std::uint32_t* __restrict__ bins,
                                                                     int nbins, const std::uint32_t* __restrict__ order,
-                                                                    double* __restrict__ beta_out) {
+                                                                    double* __restrict__ beta_out, std::uint64_t seed) {
     __shared__ __align__(16) AngSmem S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int bin  = blockIdx.x;
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(32 * kAngWarps) angle_side_kernel(const Stream
         const double        bmax = nextafter(b, a);
         double              cur  = 1.0; // lane 0 of warp 0
         if (warp == kMtWarp && lane == 0) { // [rand.predef] seeding recurrence (serial by definition)
-            std::uint64_t z = J.seed_ang;
+            std::uint64_t z = stream_seed(seed, 3, J.annulus, J.chunk); // kPhaseAngles
             S.st[0][0]      = z;
             for (int i = 1; i < kMtN; ++i) {
                 z          = 6364136223846793005ull * (z ^ (z >> 62)) + std::uint64_t(i);
@@ -325,12 +326,12 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
         cudaEventRecord(S.ev_pow, st);
         cudaStreamWaitEvent(S.late, S.ev_pow, 0);
         angle_side_kernel<<<S.chain_bins_total - nb1, 32 * kAngWarps, 0, S.late>>>(
-            S.jobs, S.chain_bins + nb1, S.chain_bins_total - nb1, S.job_order, S.beta);
+            S.jobs, S.chain_bins + nb1, S.chain_bins_total - nb1, S.job_order, S.beta, S.seed);
         cudaEventRecord(S.ev_late, S.late);
         S.mark("chain_wave2(late)", S.late);
         ++*launches;
     }
-    mt_uniforms_kernel<<<S.njobs, kMtThreads, 0, side>>>(S.jobs, S.njobs, S.beta, S.hw, 2);
+    mt_uniforms_kernel<<<S.njobs, kMtThreads, 0, side>>>(S.jobs, S.njobs, S.beta, S.hw, 2, S.seed);
     S.mark("mt_radii", side);
     // the radius attributes run beside the angle side (measured at cfg2: serialising them after
     // the wave-1 chains is slower — the wave-1 sort then waits for the whole radius side — and
@@ -340,7 +341,7 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
     S.mark("radial", side);
     *launches += 2;
     if (nb1) {
-        angle_side_kernel<<<nb1, 32 * kAngWarps, 0, st>>>(S.jobs, S.chain_bins, nb1, S.job_order, S.beta);
+        angle_side_kernel<<<nb1, 32 * kAngWarps, 0, st>>>(S.jobs, S.chain_bins, nb1, S.job_order, S.beta, S.seed);
         ++*launches;
     }
     S.mark("chain_wave1", st);
@@ -358,7 +359,7 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
 
 void launch_mt_uniforms(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
     if (S.total == 0 || S.njobs == 0) return;
-    mt_uniforms_kernel<<<2 * S.njobs, kMtThreads, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 0);
+    mt_uniforms_kernel<<<2 * S.njobs, kMtThreads, 0, st>>>(S.jobs, S.njobs, S.beta, S.hw, 0, S.seed);
     *launches += 1;
 }
 
