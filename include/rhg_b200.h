@@ -10,6 +10,7 @@
  *   radial_const_from_avg_degree  geometry.hpp:26-33      rhg_radial_const_from_avg_degree
  *   ModelParams(n,alpha,C,seed,P) geometry.hpp:49-67      rhg_params + rhg_params_validate
  *   ModelParams::from_avg_degree  geometry.hpp:69-72      rhg_params_from_avg_degree
+ *   make_layout                   partition.hpp:233-240   rhg_layout (host only)
  *   GenOptions                    generator.hpp:27-32     rhg_create(device) / rhg_shard
  *   RunStats                      generator.hpp:34-46     rhg_run_stats
  *   generate_stats(params, opts,  generator.hpp:219-291   rhg_generate_stats
@@ -41,7 +42,7 @@
 extern "C" {
 #endif
 
-#define RHG_ABI_VERSION 4
+#define RHG_ABI_VERSION 5
 #define RHG_MAX_ANNULI 64 /* layouts with more annuli are rejected (RHG_INVALID_ARGUMENT) */
 
 enum {
@@ -131,6 +132,13 @@ int rhg_params_validate(rhg_params* p);
 /* geometry.hpp:69-72 */
 int rhg_params_from_avg_degree(uint64_t n, double alpha, double d_bar, uint64_t seed, uint32_t chunks,
                                rhg_params* out);
+/* partition.hpp:233-240 make_layout, on the host (no device needed): *n_annuli and
+ * *first_streaming always; when the arrays are non-NULL (room for n_annuli, resp.
+ * n_annuli * chunks entries) the per-annulus vertex counts, the per-(annulus, chunk) counts
+ * and first vertex ids (row-major by annulus) and the classes (0 clique, 1 global, 2
+ * streaming).  Call once with NULL arrays to size them. */
+int rhg_layout(const rhg_params* params, uint32_t* n_annuli, uint32_t* first_streaming, uint64_t* counts,
+               uint64_t* chunk_counts, uint64_t* id_base, uint8_t* classes);
 
 typedef struct rhg_ctx rhg_ctx;
 int rhg_create(int device, rhg_ctx** out);

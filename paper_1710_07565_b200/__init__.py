@@ -25,7 +25,7 @@ from . import _native
 from ._native import RHG_OK, RhgCudaError, check, lib
 
 __all__ = ["alpha_from_gamma", "gamma_from_alpha", "radial_const_from_avg_degree", "radius_from_size",
-           "expected_avg_degree", "ModelParams", "GenOptions", "ChunkStats", "RunStats", "generate_stats",
+           "expected_avg_degree", "ModelParams", "AnnulusLayout", "make_layout", "GenOptions", "ChunkStats", "RunStats", "generate_stats",
            "sample_points", "sample_uniforms", "fp64_peak", "count_edges_from_points", "Points", "RhgCudaError", "two_pi"]
 
 two_pi = 6.283185307179586476925286766559  # geometry.hpp:11
@@ -85,6 +85,35 @@ class ModelParams:
     def __repr__(self):
         return (f"ModelParams(n={self.n}, alpha={self.alpha!r}, C={self.C!r}, seed={self.seed}, "
                 f"chunks={self.chunks}, R={self.R!r})")
+
+
+@dataclass
+class AnnulusLayout:
+    """partition.hpp:22-82 (the graph-defining part): annulus vertex counts, the
+    per-(annulus, chunk) counts and first vertex ids, classes (0 clique, 1 global,
+    2 streaming), the first streaming annulus."""
+    count: int
+    first_streaming: int
+    counts: np.ndarray        # [count] uint64
+    chunk_counts: np.ndarray  # [count, chunks] uint64
+    id_base: np.ndarray       # [count, chunks] uint64
+    classes: np.ndarray       # [count] uint8
+
+
+def make_layout(params: ModelParams) -> AnnulusLayout:
+    """partition.hpp:233-240: the host layout the generator samples from (no GPU needed)."""
+    p = params._c()
+    k, fs = C.c_uint32(), C.c_uint32()
+    check(lib().rhg_layout(C.byref(p), C.byref(k), C.byref(fs), None, None, None, None))
+    n = k.value
+    counts = np.zeros(n, np.uint64)
+    cc = np.zeros(n * params.chunks, np.uint64)
+    ib = np.zeros(n * params.chunks, np.uint64)
+    cls = np.zeros(n, np.uint8)
+    u64 = C.POINTER(C.c_uint64)
+    check(lib().rhg_layout(C.byref(p), C.byref(k), C.byref(fs), counts.ctypes.data_as(u64), cc.ctypes.data_as(u64),
+                           ib.ctypes.data_as(u64), cls.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return AnnulusLayout(n, fs.value, counts, cc.reshape(n, params.chunks), ib.reshape(n, params.chunks), cls)
 
 
 @dataclass

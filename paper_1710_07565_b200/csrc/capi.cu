@@ -838,6 +838,19 @@ int rhg_params_from_avg_degree(std::uint64_t n, double alpha, double d_bar, std:
     });
 }
 
+int rhg_layout(const rhg_params* params, std::uint32_t* n_annuli, std::uint32_t* first_streaming,
+               std::uint64_t* counts, std::uint64_t* chunk_counts, std::uint64_t* id_base, std::uint8_t* classes) {
+    return guarded([&] {
+        if (!params || !n_annuli || !first_streaming) throw InvalidArgument("rhg_layout: null argument");
+        const Layout L = make_layout(to_params(params));
+        *n_annuli = L.count, *first_streaming = L.first_streaming;
+        if (counts) std::copy(L.counts.begin(), L.counts.end(), counts);
+        if (chunk_counts) std::copy(L.chunk_counts.begin(), L.chunk_counts.end(), chunk_counts);
+        if (id_base) std::copy(L.id_base.begin(), L.id_base.end(), id_base);
+        if (classes) std::copy(L.classes.begin(), L.classes.end(), classes);
+    });
+}
+
 int rhg_create(int device, rhg_ctx** out) {
     return guarded([&] {
         *out = nullptr;

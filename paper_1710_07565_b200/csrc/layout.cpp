@@ -11,6 +11,8 @@
 #include <mutex>
 #include <thread>
 
+#include <unistd.h>
+
 namespace rhgb {
 
 namespace {
@@ -81,9 +83,15 @@ private:
 // (spawning threads per call would cost more than the work at P ~ 64).
 class Pool {
 public:
+    // One pool per process: a forked child (whose copy of the parent's pool has no threads)
+    // starts its own.  Pools are never destroyed — their workers block until process exit.
     static Pool& get() {
-        static Pool p;
-        return p;
+        static std::mutex m;
+        static Pool*      p     = nullptr;
+        static pid_t      owner = 0;
+        std::lock_guard<std::mutex> g(m);
+        if (!p || owner != getpid()) p = new Pool(), owner = getpid();
+        return *p;
     }
     unsigned size() const { return unsigned(workers_.size()) + 1; }
     // body(k) for k < n on the pool and the calling thread; rethrows the first exception.
@@ -118,14 +126,6 @@ private:
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         for (unsigned t = 1; t < std::min(hw, 16u); ++t) workers_.emplace_back([this] { loop(); });
     }
-    ~Pool() {
-        {
-            std::lock_guard<std::mutex> g(mu_);
-            stop_ = true;
-        }
-        cv_.notify_all();
-        for (auto& t: workers_) t.join();
-    }
     // Busy-wait up to ~50 us before blocking: the layout runs two parallel regions back to
     // back, and a futex wake-up per worker and region costs more than the regions' work.
     template <class P>
@@ -141,8 +141,7 @@ private:
             std::function<void()>* job;
             {
                 std::unique_lock<std::mutex> g(mu_);
-                cv_.wait(g, [&] { return stop_ || gen_.load() != seen; });
-                if (stop_) return;
+                cv_.wait(g, [&] { return gen_.load() != seen; });
                 seen = gen_.load(), job = job_;
             }
             (*job)();
@@ -158,7 +157,6 @@ private:
     std::function<void()>*    job_     = nullptr;
     std::atomic<unsigned>      pending_{0};
     std::atomic<std::uint64_t> gen_{0};
-    bool                      stop_    = false;
 };
 
 double normal(Mt64& s) { // rng.hpp:75-79

@@ -43,7 +43,7 @@ def test_library_is_sm100a():
 
 
 def test_abi_version():
-    assert _native.lib().rhg_abi_version() == 4
+    assert _native.lib().rhg_abi_version() == 5
 
 
 def test_params_mirror_oracle(oracle):
