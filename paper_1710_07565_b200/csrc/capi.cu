@@ -166,6 +166,7 @@ struct Plan {
     std::uint64_t              n_slabs1 = 0; // slabs of wave-1 targets (they come first in slab_tab)
     std::vector<std::uint64_t> gt_prefix;   // dense-engine warps (512-node owned strips) before annulus j
     std::vector<std::uint64_t> gseg;        // global-point annulus offsets (segments of the theta sort)
+    std::vector<std::uint64_t> pseg;        // point segments in index order: first point << 8 | annulus; total << 8
     std::vector<unsigned long long> dense_mask; // [count] bit j: (a, j) runs on the dense engine
     std::vector<std::uint64_t> req_off;     // [count] unified dense-request index of annulus a's first request
     std::uint64_t              n_req = 0;
@@ -280,6 +281,9 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
     pl.total = pl.n_ext + pl.n_glob;
     for (std::uint32_t i = 0; i < L.first_streaming; ++i) pl.gseg.push_back(L.chunk_id_base(i, 0));
     pl.gseg.push_back(pl.n_glob);
+    for (std::uint32_t i = L.first_streaming; i < L.count; ++i) pl.pseg.push_back((pl.ann[i].off << 8) | i);
+    for (std::uint32_t i = 0; i < L.first_streaming; ++i) pl.pseg.push_back(((pl.n_ext + pl.gseg[i]) << 8) | i);
+    pl.pseg.push_back(pl.total << 8);
     // (annulus, target) pairs whose windows hold >= kDenseMin nodes on average run on the dense
     // engine (node tiles x streamed requests); the rest on the slab join (96: measured optimum band 64..128 at cfg2)
     pl.dense_mask.assign(L.count, 0ull);
@@ -481,6 +485,7 @@ struct Tables {
     std::uint64_t*      gt_prefix;
     std::uint64_t*      gseg;
     std::uint32_t*      ann_blk;
+    std::uint64_t*      pseg;
     unsigned long long* src_mask;
     double*             hbound;
     unsigned long long* slab_tab;
@@ -519,8 +524,9 @@ void upload_tables_head(rhg_ctx* ctx, const Plan& pl, Tables& t, std::uint64_t* 
     std::vector<void*> d;
     upload_part(ctx, 0,
                 {blob(pl.ann), blob(pl.dense_mask), blob(pl.req_off), blob(pl.jobs), blob(pl.job_order),
-                 blob(pl.chain_bins), blob(pl.gseg), blob(pl.ann_blk)},
+                 blob(pl.chain_bins), blob(pl.gseg), blob(pl.ann_blk), blob(pl.pseg)},
                 d, h2d);
+    t.pseg = static_cast<std::uint64_t*>(d[8]);
     t.ann = static_cast<AnnulusDev*>(d[0]), t.dense_mask = static_cast<unsigned long long*>(d[1]);
     t.req_off = static_cast<std::uint64_t*>(d[2]), t.jobs = static_cast<StreamJob*>(d[3]);
     t.job_order = static_cast<std::uint32_t*>(d[4]), t.chain_bins = static_cast<std::uint32_t*>(d[5]);
@@ -561,6 +567,7 @@ SamplerArgs sampler_args(rhg_ctx* ctx, const Plan& pl, const Tables& t) {
     s.chain_bins = t.chain_bins, s.chain_bins1 = int(pl.chain_bins1), s.chain_bins_total = int(pl.chain_bins.size()) - 1;
     s.jobs = t.jobs, s.job_order = t.job_order, s.njobs = int(pl.jobs.size()), s.ann = t.ann, s.alpha = pl.L.alpha, s.total = pl.total;
     s.seed = pl.L.seed;
+    s.pseg = t.pseg, s.npseg = int(pl.pseg.size()) - 1;
     s.beta = ctx->beta.as<double>(), s.hw = ctx->hw.as<double>();
     s.rec0 = ctx->rec0.as<double2>(), s.rec1 = ctx->rec1.as<double2>(), s.rec2 = ctx->rec2.as<double2>();
     s.side = ctx->side, s.ev_fork = ctx->fork, s.ev_join = ctx->join;

@@ -25,6 +25,8 @@ struct SamplerArgs {
     const std::uint32_t* chain_bins = nullptr; // bin b = job_order[chain_bins[b], chain_bins[b + 1])
     int                  chain_bins1 = 0, chain_bins_total = 0; // wave-1 bins come first
     const AnnulusDev* ann   = nullptr;
+    const std::uint64_t* pseg = nullptr; // [npseg + 1] point segments: first point << 8 | annulus, total << 8
+    int               npseg = 0;
     std::uint64_t     seed  = 0; // root seed: stream seeds are derive_seed(seed, {3|4, annulus, chunk})
     double            alpha = 1.0;
     std::uint64_t     total = 0; // points (streaming extended arrays + global points)

@@ -131,13 +131,33 @@ __device__ __forceinline__ int find_job(const StreamJob* __restrict__ jobs, int 
 }
 
 // partition.hpp:64-70 radius_from_uniform, then sweep.hpp:125-134.
-__global__ void point_radial_kernel(const StreamJob* __restrict__ jobs, int njobs, const AnnulusDev* __restrict__ ann,
+// The annulus of point i from the point-segment table (pseg[s] = first point << 8 | annulus,
+// ascending, pseg[nseg] = total << 8): one search per block for its first point, and a
+// per-thread search only past that segment's end (blocks rarely straddle two annuli).
+__device__ __forceinline__ int pseg_find(const std::uint64_t* __restrict__ pseg, int nseg, std::uint64_t i) {
+    int lo = 0, hi = nseg - 1; // last segment starting at or before i
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((pseg[mid] >> 8) <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+__global__ void point_radial_kernel(const std::uint64_t* __restrict__ pseg, int nseg, const AnnulusDev* __restrict__ ann,
                                     double alpha, std::uint64_t total, double* __restrict__ hw_out,
                                     double2* __restrict__ rec2, double* __restrict__ r_out) {
-    const std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const std::uint64_t i0 = std::uint64_t(blockIdx.x) * blockDim.x;
+    const std::uint64_t i  = i0 + threadIdx.x;
+    __shared__ int           s_a;
+    __shared__ std::uint64_t s_end;
+    if (threadIdx.x == 0) {
+        const int sg = pseg_find(pseg, nseg, i0);
+        s_a = int(pseg[sg] & 0xffu), s_end = pseg[sg + 1] >> 8;
+    }
+    __syncthreads();
     if (i >= total) return;
-    const StreamJob&  J = jobs[find_job(jobs, njobs, i)];
-    const AnnulusDev& A = ann[J.annulus];
+    const int         a = i < s_end ? s_a : int(pseg[pseg_find(pseg, nseg, i)] & 0xffu);
+    const AnnulusDev& A = ann[a];
     const double      u = hw_out[i];
     const double      c = fadd(A.cal, fmul(u, fsub(A.cau, A.cal)));
     double            r = __ddiv_rn(acosh(c < 1.0 ? 1.0 : c), alpha);
@@ -336,7 +356,7 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
     // the radius attributes run beside the angle side (measured at cfg2: serialising them after
     // the wave-1 chains is slower — the wave-1 sort then waits for the whole radius side — and
     // so is splitting them by wave: the GPU is saturated either way)
-    point_radial_kernel<<<unsigned((S.total + 255) / 256), 256, 0, side>>>(S.jobs, S.njobs, S.ann, S.alpha, S.total,
+    point_radial_kernel<<<unsigned((S.total + 255) / 256), 256, 0, side>>>(S.pseg, S.npseg, S.ann, S.alpha, S.total,
                                                                           S.hw, S.rec2, S.r_out);
     S.mark("radial", side);
     *launches += 2;
