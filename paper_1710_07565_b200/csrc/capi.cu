@@ -114,7 +114,7 @@ struct rhg_ctx {
     std::vector<std::pair<std::string, cudaEvent_t>> tl; // RHG_TIMELINE marks of the current call
     std::vector<cudaEvent_t> tl_pool;
     DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, tables2, cells, counters, degrees, dbg, nid;
-    DevBuf       lcells, perm, s_beta, s_hw, s_lt, s_rec1, s_rec2, gsort, gbuf;
+    DevBuf       lcells, s_beta, s_hw, s_lt, s_rec1, s_rec2, gsort, gbuf;
     DevBuf       ebuf, ecount, ekeys, esort; // materialised edges (rhg_generate_edges)
     DevBuf       lam_tmp;
     HostPinned   staging, staging2, readback; // table parts 1 and 2, counter readback
@@ -613,7 +613,6 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     e.lcellstart = ctx->lcells.as<std::uint64_t>();
     {
         const std::size_t ne = pl.n_ext + 2;
-        ctx->perm.ensure(ne * sizeof(std::uint64_t));
         ctx->lam_tmp.ensure(ne * sizeof(double));
         e.lam_tmp = ctx->lam_tmp.as<double>();
         ctx->s_beta.ensure(ne * sizeof(double));
@@ -622,7 +621,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         ctx->s_rec1.ensure(ne * sizeof(double2));
         ctx->s_rec2.ensure(ne * sizeof(double2));
         ctx->nid.ensure(ne * sizeof(unsigned long long));
-        e.perm = ctx->perm.as<std::uint64_t>(), e.s_beta = ctx->s_beta.as<double>(), e.s_hw = ctx->s_hw.as<double>();
+        e.s_beta = ctx->s_beta.as<double>(), e.s_hw = ctx->s_hw.as<double>();
         e.s_lam = ctx->s_lt.as<double>(), e.s_theta = ctx->s_lt.as<double>() + ne;
         e.s_rec1 = ctx->s_rec1.as<double2>(), e.s_rec2 = ctx->s_rec2.as<double2>();
         e.s_id = ctx->nid.as<unsigned long long>();
@@ -892,7 +891,7 @@ void rhg_destroy(rhg_ctx* c) {
     cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->side);
     for (DevBuf* b: {&c->beta, &c->hw, &c->rec0, &c->rec1, &c->rec2, &c->r_out, &c->beta_raw, &c->tables, &c->cells,
-                     &c->counters, &c->degrees, &c->dbg, &c->nid, &c->lcells, &c->perm, &c->s_beta,
+                     &c->counters, &c->degrees, &c->dbg, &c->nid, &c->lcells, &c->s_beta,
                      &c->s_hw, &c->s_lt, &c->s_rec1, &c->s_rec2, &c->gsort, &c->gbuf})
         b->release();
     if (c->staging.p) cudaFreeHost(c->staging.p);
@@ -1056,7 +1055,7 @@ void generate_impl(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shar
         out->kernel_launches = launches;
         out->device_bytes    = ctx->beta.cap + ctx->hw.cap + ctx->rec0.cap + ctx->rec1.cap + ctx->rec2.cap +
                             ctx->r_out.cap + ctx->beta_raw.cap + ctx->tables.cap + ctx->tables2.cap + ctx->cells.cap + ctx->counters.cap +
-                            ctx->degrees.cap + ctx->nid.cap + ctx->lcells.cap + ctx->perm.cap + ctx->s_beta.cap +
+                            ctx->degrees.cap + ctx->nid.cap + ctx->lcells.cap + ctx->s_beta.cap +
                             ctx->s_hw.cap + ctx->s_lt.cap + ctx->s_rec1.cap + ctx->s_rec2.cap + ctx->gbuf.cap;
         out->seconds = std::chrono::duration<double>(Clock::now() - t0).count();
     }

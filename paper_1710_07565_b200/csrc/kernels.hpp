@@ -63,7 +63,6 @@ struct EdgeArgs {
     const double2*    rec2 = nullptr;
     std::uint64_t*    cellstart = nullptr;  // beta cells (sampler order)
     std::uint64_t*    lcellstart = nullptr; // lambda cells (sorted owned blocks)
-    std::uint64_t*    perm = nullptr;       // sampler index -> sorted index
     // lambda-sorted copies (per annulus: owned block, halo block)
     double*           s_beta = nullptr;
     double*           s_hw   = nullptr;

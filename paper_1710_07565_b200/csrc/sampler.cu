@@ -17,7 +17,7 @@
 //                           (partition.hpp:64-70, sweep.hpp:121-134).
 //   S3 point_angular_kernel per global point: theta = beta + hw (mod 2pi), cos, sin
 //                           (sweep.hpp:135-139); streaming points get theirs in the
-//                           sort phase (edges.cu angular_scatter_kernel).
+//                           sort phase (edges.cu rank_kernel, angular_scatter_point).
 //
 // All exact-rounding steps use __dmul_rn/__dadd_rn (no FMA contraction).
 #include <cstdlib>
@@ -369,7 +369,7 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
         cudaEventRecord(S.ev_join, side);
         cudaStreamWaitEvent(st, S.ev_join, 0);
     }
-    // generate mode: streaming points get their frames in the sort phase (edges.cu angular_scatter_kernel)
+    // generate mode: streaming points get their frames in the sort phase (edges.cu rank_kernel, angular_scatter_point)
     const std::uint64_t first = S.angular_from;
     if (S.total > first)
         point_angular_kernel<<<unsigned((S.total - first + 255) / 256), 256, 0, st>>>(
