@@ -454,10 +454,18 @@ struct __align__(16) SlabRow32 { // one request with pairs in the slab (rows of 
 struct __align__(16) SlabRow64 { // the same request for the exact predicate
     double cs, sn, coth, rci;
 };
-template <int NT>
-struct SlabSmem {
+// The exact-path node doubles (cos, sin), (coth, 1/sinh): staged in shared memory (R12), or
+// read from the sorted arrays in global memory by the rare exact rechecks, which frees 16 KB
+// per CTA for a fifth CTA per SM.
+template <bool R12>
+struct SlabNodes64 {
+    double2 r1[kSlabNodes], r2[kSlabNodes];
+};
+template <>
+struct SlabNodes64<false> {};
+template <int NT, bool R12 = true>
+struct SlabSmem : SlabNodes64<R12> {
     float4             nd[kSlab];         // (lambda - lam_first, coth - 1, 1 / sinh, id offset bits)
-    double2            r1[kSlab], r2[kSlab];
     double             lam[kSlab];
     std::uint16_t      bstart[kSlab + 1]; // bucket b: first local node with bucket(lambda) >= b
     SlabRow32          rows[NT / 32][32];
@@ -472,7 +480,8 @@ template <int MODE, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     constexpr int kSlabThreads = NT;
     extern __shared__ __align__(16) unsigned char slab_raw[];
-    SlabSmem<NT>&            S    = *reinterpret_cast<SlabSmem<NT>*>(slab_raw);
+    constexpr bool           kR12 = MINB < 5; // exact-path node doubles in shared memory
+    SlabSmem<NT, kR12>&      S    = *reinterpret_cast<SlabSmem<NT, kR12>*>(slab_raw);
     const int                lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned long long sl   = A.slab_tab[A.slab0 + blockIdx.x]; // (j << 32) | slab index in j, angle order per wave
     const int                j    = int(sl >> 32);
@@ -480,6 +489,14 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     const std::uint64_t      N0   = Aj.off + (sl & 0xffffffffull) * kSlab;
     const std::uint32_t      m    = std::uint32_t(Aj.halo - N0 < std::uint64_t(kSlab) ? Aj.halo - N0 : kSlab);
     const std::uint64_t      base_j = Aj.off + std::uint64_t(Aj.dlt0); // owned ids of j: [base_j, base_j + n)
+    auto node_r1 = [&](std::uint32_t k) {
+        if constexpr (kR12) return S.r1[k];
+        else return A.s_rec1[N0 + k];
+    };
+    auto node_r2 = [&](std::uint32_t k) {
+        if constexpr (kR12) return S.r2[k];
+        else return A.s_rec2[N0 + k];
+    };
     const double             lam_first = A.s_lam[N0];
     const double             lam_last  = A.s_lam[N0 + m - 1];
     // warp 0 finds the slab's request runs (cell-table lookups) while warps 1.. stage the nodes
@@ -491,8 +508,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
             const double  lp = i ? A.s_lam[N0 + i - 1] : 0.0;
             const double2 r2 = A.s_rec2[N0 + i];
             S.lam[i] = l;
-            S.r1[i]  = A.s_rec1[N0 + i];
-            S.r2[i]  = r2;
+            if constexpr (kR12) S.r1[i] = A.s_rec1[N0 + i], S.r2[i] = r2;
             S.nd[i]  = make_float4(float(fsub(l, lam_first)), float(fsub(r2.x, 1.0)), float(r2.y),
                                    __uint_as_float(std::uint32_t(A.s_id[N0 + i] - base_j)));
             const std::uint32_t b  = slab_bucket(l, lam_first, inv_w);
@@ -656,7 +672,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                     bool                e  = D > 0.0f;
                     if (!(fabsf(D) > tau) || fabsf(df) > kPreMaxDelta) { // near the threshold: exact FP64
                         const SlabRow64& R = rows64[o];
-                        e = edge_test(R.cs, R.sn, R.coth, R.rci, S.r1[k], S.r2[k]);
+                        e = edge_test(R.cs, R.sn, R.coth, R.rci, node_r1(k), node_r2(k));
                         if (A.dbg) atomicAdd(&A.dbg[17], 1ull);
                     }
                     if (e) {
@@ -678,7 +694,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                         q0 = r64[2 * o], q1 = r64[2 * o + 1], u = ru[2 * o + 1];
                     }
                     const std::uint32_t k = u.z + t;
-                    if (edge_test(q0.x, q0.y, q1.x, q1.y, S.r1[k], S.r2[k])) {
+                    if (edge_test(q0.x, q0.y, q1.x, q1.y, node_r1(k), node_r2(k))) {
                         const std::uint32_t nid = __float_as_uint(S.nd[k].w);
                         sum += nid + u.y, ++cnt;
                         if (MODE == 1) {
@@ -1528,7 +1544,7 @@ void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, 
 
 template <int NT, int MINB>
 void launch_slab(const EdgeArgs& a, unsigned n, int mode, cudaStream_t st) {
-    const int   smem = int(sizeof(SlabSmem<NT>));
+    const int   smem = int(sizeof(SlabSmem<NT, (MINB < 5)>));
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(slab_kernel<0, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1566,8 +1582,13 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         if (W.ev0) cudaEventRecord(W.ev0, st);
         const unsigned n   = unsigned(W.slab_end - W.slab_begin);
         static const int scfg = std::getenv("RHG_SLAB_CFG") ? std::atoi(std::getenv("RHG_SLAB_CFG")) : 0;
-        if (scfg == 0) launch_slab<256, 4>(a, n, mode, st); // measured best of 128..512 threads x 256..1024-node slabs
-        else launch_slab<128, 8>(a, n, mode, st);
+        // 256 threads x 6 CTAs/SM (40 registers; the exact path's node doubles read from global
+        // memory, so 31.5 KB of shared memory per CTA): measured best at cfg2 (x4 with the node
+        // doubles staged, 64 registers: 3.96 -> 3.80 ms/step; x5 3.87; x7 4.13, spills), also
+        // cfg3 / cfg4 (-1.6% / -3.4%); RHG_SLAB_CFG selects the others for A/B runs
+        if (scfg == 4) launch_slab<256, 4>(a, n, mode, st);
+        else if (scfg == 1) launch_slab<128, 8>(a, n, mode, st);
+        else launch_slab<256, 6>(a, n, mode, st);
         ++*launches;
         if (W.tail && a.n_tail) {
             RHG_LAUNCH_MODE(tail_kernel, mode, RHG_CFG(unsigned((a.n_tail + 255) / 256), 256, 0, st), a);
