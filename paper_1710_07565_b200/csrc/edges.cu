@@ -1175,8 +1175,10 @@ __device__ __forceinline__ std::uint32_t gtheta_lb(const double* th, std::uint32
 // the nodes sit in registers, each chunk of 32 candidates is clipped to the
 // tile and compacted into (request, piece) entries in shared memory, and the
 // warp sweeps the entries (32-node slices outside an entry are skipped).
-template <int MODE>
-__global__ void __launch_bounds__(256, kTN == 128 ? 2 : 3) glob_tiles_kernel(EdgeArgs A) {
+// MINB: CTAs per SM the register budget targets (measured cfg2: wave 1's targets 0.40 ms at 2,
+// 0.43 at 3 with small spills; wave 2's outermost target 0.18 at 2, 0.15 at 3)
+template <int MODE, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) glob_tiles_kernel(EdgeArgs A) {
     __shared__ GWarp    smem[8];
     const int           lane = threadIdx.x & 31;
     const std::uint64_t w    = A.gt_prefix[A.j0] + ((std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
@@ -1573,7 +1575,11 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         a.mark("rows", st);
         const std::uint64_t tw = W.tile_warps;
         if (tw) {
-            RHG_LAUNCH_MODE(glob_tiles_kernel, mode, RHG_CFG(unsigned((tw + 7) / 8), 256, 0, st), a);
+            const unsigned g = unsigned((tw + 7) / 8);
+            if (W.global_unit) RHG_LAUNCH_MODE(glob_tiles_kernel, mode, RHG_CFG(g, 256, 0, st), a); // wave 1
+            else if (mode == 2) glob_tiles_kernel<2, 3><<<g, 256, 0, st>>>(a);
+            else if (mode == 1) glob_tiles_kernel<1, 3><<<g, 256, 0, st>>>(a);
+            else glob_tiles_kernel<0, 3><<<g, 256, 0, st>>>(a);
             ++*launches;
             a.mark("tiles", st);
         }
