@@ -209,6 +209,15 @@ const char* rhg_io_last_error(void);
  * denominator) and the dependent-DMUL latency in SM cycles. */
 int rhg_fp64_peak(int device, double* ops_per_s, double* dmul_latency_cycles, double* kernel_ms);
 
+/* Diagnostic (not part of the reference interface): the device restatement of the glibc 2.39
+ * routines the reference's point set passes through (csrc/glibc_libm.cuh: std::exp, log, log1p,
+ * acosh, acos, pow and the gcc-merged sincos of sweep.hpp:125-139, partition.hpp:66,
+ * rng.hpp:221), evaluated elementwise on host arrays of n doubles on `device`:
+ * fn 0 exp(x), 1 log(x), 2 log1p(x), 3 acosh(x), 4 acos(x), 5 pow(x, y), 6 sin(x), 7 cos(x)
+ * (6/7: the two outputs of one sincos call; y is read only for fn 5).  The results must equal
+ * the host glibc's bit for bit (tests/test_gpu_libm.py). */
+int rhg_libm_eval(int device, int fn, const double* x, const double* y, double* out, uint64_t n);
+
 #ifdef __cplusplus
 }
 #endif

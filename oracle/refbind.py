@@ -258,6 +258,17 @@ class Oracle(_Base):
         L.orc_count_edges_from_points.argtypes = [u64, f64, f64, u64, u32, u32] + [P_f64] * 7 + [
             C.POINTER(OrcStats), P_u32]
         L.orc_generate_stats_shard.argtypes = [u64, f64, f64, u64, u32, u32, u32, u32, C.POINTER(OrcStats)]
+        L.orc_libm_eval.argtypes = [C.c_int, P_f64, P_f64, P_f64, u64, u32]
+        L.orc_libm_eval.restype = None
+
+    def libm_eval(self, fn: int, x: np.ndarray, y: np.ndarray | None = None, threads: int | None = None):
+        """Host glibc exp/log/log1p/acosh/acos/pow/sin/cos (fn 0..7) elementwise."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        yy = None if y is None else np.ascontiguousarray(y, dtype=np.float64)
+        out = np.empty_like(x)
+        self.L.orc_libm_eval(fn, _p(x, P_f64), _p(yy, P_f64), _p(out, P_f64), x.size,
+                             threads or os.cpu_count() or 1)
+        return out
 
     def radial_const_from_avg_degree(self, d_bar, alpha):
         out = f64()

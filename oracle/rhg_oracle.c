@@ -1081,3 +1081,52 @@ int orc_generate_stats_shard(uint64_t n, double alpha, double C, uint64_t seed, 
     out->seconds = now_s() - t0;
     return rc;
 }
+
+/* ---- host libm evaluator (checker for the device glibc restatement) ---- */
+typedef struct {
+    int fn;
+    const double *x, *y;
+    double* out;
+    uint64_t lo, hi;
+} libm_job;
+
+/* volatile pointers: the calls must reach libm.so.6's ifunc-selected entry
+ * points, exactly as the reference's do (no builtin folding or inlining). */
+static double (*volatile lm_exp)(double) = exp;
+static double (*volatile lm_log)(double) = log;
+static double (*volatile lm_log1p)(double) = log1p;
+static double (*volatile lm_acosh)(double) = acosh;
+static double (*volatile lm_acos)(double) = acos;
+static double (*volatile lm_pow)(double, double) = pow;
+static void (*volatile lm_sincos)(double, double*, double*) = sincos;
+
+static void* libm_worker(void* arg) {
+    libm_job* j = (libm_job*)arg;
+    for (uint64_t i = j->lo; i < j->hi; ++i) {
+        const double a = j->x[i];
+        double r = 0.0, s, c;
+        switch (j->fn) {
+        case 0: r = lm_exp(a); break;
+        case 1: r = lm_log(a); break;
+        case 2: r = lm_log1p(a); break;
+        case 3: r = lm_acosh(a); break;
+        case 4: r = lm_acos(a); break;
+        case 5: r = lm_pow(a, j->y[i]); break;
+        default: lm_sincos(a, &s, &c); r = j->fn == 6 ? s : c; break;
+        }
+        j->out[i] = r;
+    }
+    return NULL;
+}
+
+void orc_libm_eval(int fn, const double* x, const double* y, double* out, uint64_t n, uint32_t threads) {
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pthread_t th[256];
+    libm_job jobs[256];
+    for (uint32_t t = 0; t < threads; ++t) {
+        jobs[t] = (libm_job){fn, x, y, out, n * t / threads, n * (t + 1) / threads};
+        pthread_create(&th[t], NULL, libm_worker, &jobs[t]);
+    }
+    for (uint32_t t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+}

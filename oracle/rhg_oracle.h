@@ -79,6 +79,11 @@ int orc_generate_stats_shard(uint64_t n, double alpha, double C, uint64_t seed, 
 int orc_comps_matrix(uint64_t n, double alpha, double C, uint64_t seed, uint32_t chunks, uint32_t threads,
                      uint64_t* mat);
 
+/* The HOST glibc routines the reference calls, elementwise (the checker of
+ * rhg_libm_eval): fn 0 exp, 1 log, 2 log1p, 3 acosh, 4 acos, 5 pow(x, y),
+ * 6 / 7 sin / cos from one sincos call (what gcc -O3 makes of sweep.hpp:138-139). */
+void orc_libm_eval(int fn, const double* x, const double* y, double* out, uint64_t n, uint32_t threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -284,6 +284,27 @@ def fp64_peak(device: int = 0):
     return a.value, b.value, c.value
 
 
+LIBM_FUNCTIONS = ("exp", "log", "log1p", "acosh", "acos", "pow", "sin", "cos")
+
+
+def libm_eval(fn: str, x, y=None, device: int = 0):
+    """The device restatement of the glibc 2.39 routine `fn` (csrc/glibc_libm.cuh; one of
+    LIBM_FUNCTIONS, "sin"/"cos" being the outputs of one sincos call) on array x (and y for
+    pow), elementwise on `device`.  Equal to the host glibc bit for bit (tests/test_gpu_libm.py)."""
+    code = LIBM_FUNCTIONS.index(fn)
+    xa = np.ascontiguousarray(x, dtype=np.float64)
+    ya = None
+    if fn == "pow":
+        ya = np.ascontiguousarray(y, dtype=np.float64)
+        if ya.shape != xa.shape:
+            raise ValueError("pow: x and y must have the same shape")
+    out = np.empty_like(xa)
+    P = C.POINTER(C.c_double)
+    check(lib().rhg_libm_eval(int(device), code, xa.ctypes.data_as(P),
+                              ya.ctypes.data_as(P) if ya is not None else None, out.ctypes.data_as(P), xa.size))
+    return out
+
+
 def count_edges_from_points(params: ModelParams, points, opts: GenOptions = GenOptions(),
                             degrees: bool = False) -> RunStats:
     """Parity hook: run the device edge kernels on a given point set (any

@@ -52,7 +52,8 @@ EXPORTS = ["rhg_last_error", "rhg_abi_version", "rhg_alpha_from_gamma", "rhg_rad
            "rhg_params_validate", "rhg_params_from_avg_degree", "rhg_create", "rhg_destroy", "rhg_generate_stats",
            "rhg_sample_points", "rhg_sample_uniforms", "rhg_count_edges_from_points",
            "rhg_fp64_peak", "rhg_generate_edges", "rhg_edges_from_points", "rhg_write_edges_text", "rhg_write_edges_binary",
-           "rhg_read_edges_binary", "rhg_io_last_error", "rhg_naive_edges", "rhg_powerlaw_mle", "rhg_layout"]
+           "rhg_read_edges_binary", "rhg_io_last_error", "rhg_naive_edges", "rhg_powerlaw_mle", "rhg_layout",
+           "rhg_libm_eval"]
 
 _lib = None
 
@@ -97,6 +98,7 @@ def lib():
     L.rhg_naive_edges.argtypes = [C.c_void_p, C.c_uint64, C.c_double, P_f64, P_f64, P_u64, C.c_uint64, P_u64]
     L.rhg_layout.argtypes = [C.POINTER(rhg_params), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), P_u64, P_u64,
                              P_u64, C.POINTER(C.c_uint8)]
+    L.rhg_libm_eval.argtypes = [C.c_int, C.c_int, P_f64, P_f64, P_f64, C.c_uint64]
     _lib = L
     return L
 

@@ -9,6 +9,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "glibc_libm.cuh"
+
 namespace rhgb {
 
 constexpr double kTwoPiD = 6.283185307179586476925286766559; // geometry.hpp:11
@@ -64,12 +66,12 @@ __device__ __forceinline__ double fmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double fadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double fsub(double a, double b) { return __dsub_rn(a, b); }
 
-// sweep.hpp:60-67 request_half_width_raw; acos branch via CUDA libm.
+// sweep.hpp:60-67 request_half_width_raw; acos is glibc's (glibc_libm.cuh), bit for bit.
 __device__ __forceinline__ double request_half_width(double coth_r, double inv_r, double coth_b, double cris_b) {
     const double arg = fsub(fmul(coth_r, coth_b), fmul(cris_b, inv_r));
     if (arg <= -1.0) return kPiD;
     if (arg >= 1.0) return 0.0;
-    return acos(arg);
+    return gl::gl_acos(arg);
 }
 // sweep.hpp:365-370 half_width_in
 __device__ __forceinline__ double half_width_in(const AnnulusDev& A, double coth_r, double inv_r) {

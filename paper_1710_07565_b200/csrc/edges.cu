@@ -212,7 +212,7 @@ __device__ __forceinline__ void angular_scatter_point(const EdgeArgs& A, const A
     double       th = fadd(b0, h);
     if (th >= kTwoPiD) th = fsub(th, kTwoPiD);
     double sn, cs;
-    sincos(th, &sn, &cs);
+    gl::gl_sincos(th, &sn, &cs);
     const double bf = A.lift_part && i >= J.halo ? fadd(b0, kTwoPiD) : b0;
     A.s_beta[d]     = bf;
     A.s_hw[d]       = h;

@@ -19,7 +19,8 @@
 //                           (sweep.hpp:135-139); streaming points get theirs in the
 //                           sort phase (edges.cu rank_kernel, angular_scatter_point).
 //
-// All exact-rounding steps use __dmul_rn/__dadd_rn (no FMA contraction).
+// All exact-rounding steps use __dmul_rn/__dadd_rn (no FMA contraction); pow, acosh,
+// exp, acos and sincos are glibc 2.39's, restated bit for bit in glibc_libm.cuh.
 #include <cstdlib>
 
 #include "device.cuh"
@@ -160,9 +161,9 @@ __global__ void point_radial_kernel(const std::uint64_t* __restrict__ pseg, int 
     const AnnulusDev& A = ann[a];
     const double      u = hw_out[i];
     const double      c = fadd(A.cal, fmul(u, fsub(A.cau, A.cal)));
-    double            r = __ddiv_rn(acosh(c < 1.0 ? 1.0 : c), alpha);
+    double            r = __ddiv_rn(gl::gl_acosh(c < 1.0 ? 1.0 : c), alpha);
     r                   = r > 1e-12 ? r : 1e-12;
-    const double ex   = exp(r);
+    const double ex   = gl::gl_exp(r);
     const double mex  = __ddiv_rn(1.0, ex);
     const double sh   = fmul(0.5, fsub(ex, mex));
     const double coth = __ddiv_rn(fmul(0.5, fadd(ex, mex)), sh);
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(32 * kAngWarps) angle_side_kernel(const Stream
                     double*             x    = S.x[(s - 1) % 3];
                     for (int i = pw * 32 + lane; i < kMtN; i += 32 * (kAngWarps - 2)) {
                         const std::uint64_t k = base + std::uint64_t(i);
-                        x[i] = k < n ? pow(u[i], __ddiv_rn(1.0, double(n - k))) : 1.0; // rng.hpp:221, past the end: 1
+                        x[i] = k < n ? gl::gl_pow(u[i], __ddiv_rn(1.0, double(n - k))) : 1.0; // rng.hpp:221, past the end: 1
                     }
                 }
                 if (s >= 3) { // block s - 3: the chain's products -> beta (off the chain warp's path)
@@ -304,7 +305,7 @@ __global__ void point_angular_kernel(const StreamJob* __restrict__ jobs, int njo
     double           th = fadd(b0, h);
     if (th >= kTwoPiD) th = fsub(th, kTwoPiD);
     double s, c;
-    sincos(th, &s, &c);
+    gl::gl_sincos(th, &s, &c);
     const double bf = J.lift ? fadd(b0, kTwoPiD) : b0;
     rec0[i]         = make_double2(fadd(bf, h), th);
     rec1[i]         = make_double2(c, s);

@@ -42,7 +42,10 @@ CONFIGS = [
     ("cfg4_1gpu", 1 << 28, 4.0, 3.0, 13, 4096),
     ("cfg4_2gpu", 1 << 29, 4.0, 3.0, 13, 8192),
     ("cfg5", 1 << 30, 16.0, 2.6, 17, 2048),
+    ("cfg4_4gpu", 1 << 30, 4.0, 3.0, 13, 16384),
+    ("cfg4_8gpu", 1 << 31, 4.0, 3.0, 13, 32768),
 ]
+BIG = ("cfg3", "cfg4_1gpu", "cfg4_2gpu", "cfg5", "cfg4_4gpu", "cfg4_8gpu")
 
 
 def sha(a: np.ndarray) -> str:
@@ -114,9 +117,24 @@ def stats_record(r: Ref, name, n, alpha, C, seed, P, extra=None) -> dict:
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--big", action="store_true", help="also cfg3..cfg5 (minutes of CPU)")
+    ap.add_argument("--big", action="store_true", help="also cfg3..cfg5 and cfg4 at 2^30/2^31 (tens of minutes of CPU)")
+    ap.add_argument("--only", nargs="+", choices=BIG,
+                    help="(re)compute just these big stats rows and merge them into stats.json")
     args = ap.parse_args()
     r = Ref()
+    path = os.path.join(OUT, "stats.json")
+    if args.only:
+        rows = [s for s in json.load(open(path)) if s["name"] not in args.only]
+        for name, n, d, g, seed, P in CONFIGS:
+            if name in args.only:
+                alpha = r.alpha_from_gamma(g)
+                C = r.radial_const_from_avg_degree(d, alpha)
+                print("stats", name, P, flush=True)
+                rows.append(stats_record(r, name, n, alpha, C, seed, P, {"d": d, "gamma": g}))
+        with open(path, "w") as f:
+            json.dump(rows, f, indent=1)
+        print("wrote", path)
+        return
     with open(os.path.join(OUT, "known_answers.json"), "w") as f:
         json.dump(known_answers(r), f, indent=1)
     with open(os.path.join(OUT, "layouts.json"), "w") as f:
@@ -143,7 +161,7 @@ def main():
         stats.append(stats_record(r, "odd_P", 20000, 0.75, C, 77, P, {"d": 12.0}))
     C = r.radial_const_from_avg_degree(16.0, 0.8)
     stats.append(stats_record(r, "smoke", 20000, 0.8, C, 5, 4, {"d": 16.0}))
-    big = {"cfg1", "cfg2"} | ({"cfg3", "cfg4_1gpu", "cfg4_2gpu", "cfg5"} if args.big else set())
+    big = {"cfg1", "cfg2"} | (set(BIG) if args.big else set())
     for name, n, d, g, seed, P in CONFIGS:
         if name not in big:
             continue
@@ -153,9 +171,8 @@ def main():
         for PP in Ps:
             print("stats", name, PP, flush=True)
             stats.append(stats_record(r, name, n, alpha, C, seed, PP, {"d": d, "gamma": g}))
-    path = os.path.join(OUT, "stats.json")
     if not args.big and os.path.exists(path):  # keep previously generated big rows
-        old = [s for s in json.load(open(path)) if s["name"] in ("cfg3", "cfg4_1gpu", "cfg4_2gpu", "cfg5")]
+        old = [s for s in json.load(open(path)) if s["name"] in BIG]
         stats.extend(old)
     with open(path, "w") as f:
         json.dump(stats, f, indent=1)
