@@ -1,27 +1,34 @@
 """Benchmark: threshold-RHG edges/s on B200 (driver contract, one JSON line).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfgX] [--impl ours|reference]
 
 A "step" is one full stats-only generation (generator.hpp:219-291) of the
-workload: host layout, device sampler, cell index, every edge kernel, and the
-counters back on the host.  The workload at N=1 is BASELINE.json configs[1]
-(n=2^24, d=64, gamma=2.2, seed=7) at the survey's recommended chunk count
-P=64; with N>1 (torchrun, one process per GPU) the same graph is
-split into N engine shards (chunks [r*P/N, (r+1)*P/N)) — strong scaling — and
-the only collective is an all-reduce of the (edges, fingerprint, comps) counters.
+workload: host layout, device sampler, cell index, every edge kernel, the
+counter all-reduce (N > 1) and the counters back on the host.
 
-value = whole-graph edges / (max over ranks of the summed per-step device
-time, CUDA events on the library's stream).  e2e = the same metric through the
-public API call (host layout + table upload + kernels + counter readback),
-host wall clock per call.  --impl reference times the reference's own CPU
-generator (oracle/_ref, the unmodified reference headers compiled in place)
-on the host cores with all threads.
+Workloads (BASELINE.json configs, SURVEY 8(d) chunk counts P):
+  N = 1: cfg2 (configs[1], n=2^24, d=64, gamma=2.2, seed=7, P=64) -- the 1-B200 config.
+  N > 1: cfg3 (configs[2], n=2^26, d=256, gamma=3, seed=11, P=512) -- strong scaling;
+         --config cfg4 is the weak-scaling line (n = 2^28 N, P = 4096 N, d=4, seed=13).
+  With N > 1 and no WORLD_SIZE in the environment, bench.py re-launches itself under
+  torchrun with N ranks (one per GPU; fewer visible GPUs is an error).  Each rank owns
+  engines [r P/N, (r+1) P/N), regenerates its halo from the seeds, and every step ends
+  with ONE device-side ncclAllReduce(uint64) of the (edges, fingerprint, comps) counters
+  inside the library (rhg_attach_comm), on the timed stream.
+
+value = whole-graph edges per step x K / (max over ranks of the summed per-step device
+time: CUDA events on the library's stream).  e2e = the same metric through the public
+API call (host layout + table upload + kernels + all-reduce + counter readback), host
+wall clock, max over ranks.  --impl reference times the reference's own CPU generator
+(oracle/_ref, the unmodified reference headers compiled in place) on the host cores.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
+import statistics
 import subprocess
 import sys
 import time
@@ -32,13 +39,35 @@ sys.path.insert(0, ROOT)
 METRIC = "edges/sec (device-timed, max over ranks) at 1/2/4/8 B200; % of FP64 roofline"
 UNIT = "edges/s"
 
-CONFIGS = {  # name: (n, avg degree, gamma, seed, chunks)  -- BASELINE.json configs, SURVEY §8(d) P
-    "cfg1": (1 << 20, 16.0, 3.0, 1, 8),
-    "cfg2": (1 << 24, 64.0, 2.2, 7, 64),
-    "cfg3": (1 << 26, 256.0, 3.0, 11, 512),
-    "cfg4": (1 << 28, 4.0, 3.0, 13, 4096),
-    "cfg5": (1 << 30, 16.0, 2.6, 17, 2048),
+# name: (n, avg degree, gamma, seed, chunks, weak) -- weak: n and P scale with the GPU count
+CONFIGS = {
+    "cfg1": (1 << 20, 16.0, 3.0, 1, 8, False),
+    "cfg2": (1 << 24, 64.0, 2.2, 7, 64, False),
+    "cfg3": (1 << 26, 256.0, 3.0, 11, 512, False),
+    "cfg4": (1 << 28, 4.0, 3.0, 13, 4096, True),
+    "cfg5": (1 << 30, 16.0, 2.6, 17, 2048, False),
 }
+GOLDEN_NAME = {"cfg1": "cfg1", "cfg2": "cfg2", "cfg3": "cfg3", "cfg5": "cfg5"}
+
+
+def workload(name, world):
+    n, d, g, seed, P, weak = CONFIGS[name]
+    if weak:
+        n, P = n * world, P * world
+    return n, d, g, seed, P, weak
+
+
+def golden_row(name, n, P):
+    """The reference's (edges, fingerprint, comps) for this workload, from the goldens the
+    reference produced (tests/golden/stats.json, make_golden.py)."""
+    try:
+        rows = json.load(open(os.path.join(ROOT, "tests", "golden", "stats.json")))
+    except (OSError, ValueError):
+        return None
+    for s in rows:
+        if s["n"] == n and s["P"] == P and s["name"].startswith(name):
+            return s
+    return None
 
 
 def dist_env():
@@ -46,6 +75,16 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class Clocks:
@@ -102,87 +141,131 @@ class Clocks:
 
 
 def kernel_profile():
-    """Pipe / L1 / issue utilisation of the slab join from the committed ncu summary
-    (profiles/r01/ncu_kernels_cfg2_latest.json): what bounds the dominant kernel."""
-    p = os.path.join(ROOT, "profiles", "r01", "ncu_kernels_cfg2_latest.json")
-    try:
-        rows = [k for k in json.load(open(p)) if "slab_kernel" in k.get("kernel", "")]
-    except (OSError, ValueError):
-        return None
-    if not rows:
-        return None
-    keys = {"fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-            "fp32_fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-            "l1_pct": "l1tex__throughput.avg.pct_of_peak_sustained_active",
-            "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
-            "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active"}
-    out = {"source": "profiles/r01/ncu_kernels_cfg2_latest.json (ncu --set full, both slab launches of a step)"}
-    for name, key in keys.items():
-        vals = []
-        for r in rows:
-            try:
-                vals.append(float(str(r.get(key, "")).split()[0]))
-            except (ValueError, IndexError):
-                pass
-        out[name] = round(sum(vals) / len(vals), 1) if vals else None
-    out["bound"] = ("latency/issue: the FP32 pre-filter replaced the FP64 predicate for 99.9% of the pairs "
-                    "(exact FP64 recheck near the threshold), so the FP64 pipe is not the limit")
-    return out
+    """Pipe / L1 / issue utilisation of the slab join from the committed ncu summary."""
+    for p in (os.path.join(ROOT, "profiles", "r02", "ncu_kernels_cfg2.json"),
+              os.path.join(ROOT, "profiles", "r01", "ncu_kernels_cfg2_latest.json")):
+        try:
+            rows = [k for k in json.load(open(p)) if "slab_kernel" in k.get("kernel", "")]
+        except (OSError, ValueError):
+            continue
+        if not rows:
+            continue
+        keys = {"fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                "fp32_fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+                "l1_pct": "l1tex__throughput.avg.pct_of_peak_sustained_active",
+                "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active"}
+        out = {"source": os.path.relpath(p, ROOT) + " (ncu --set full, the slab launches of a step)"}
+        for name, key in keys.items():
+            vals = []
+            for r in rows:
+                try:
+                    vals.append(float(str(r.get(key, "")).split()[0]))
+                except (ValueError, IndexError):
+                    pass
+            out[name] = round(sum(vals) / len(vals), 1) if vals else None
+        out["bound"] = ("latency/issue: the FP32 pre-filter replaced the FP64 predicate for 99.9% of the pairs "
+                        "(exact FP64 recheck near the threshold), so the FP64 pipe is not the limit")
+        return out
+    return None
 
 
 def traffic_from_profile():
     """DRAM bytes per launch of the dominant kernel from the committed ncu summary."""
-    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
-    try:
-        return json.load(open(p))
-    except (OSError, ValueError):
-        return None
+    for p in (os.path.join(ROOT, "profiles", "r02", "roofline_traffic.json"),
+              os.path.join(ROOT, "profiles", "roofline_traffic.json")):
+        try:
+            return json.load(open(p))
+        except (OSError, ValueError):
+            continue
+    return None
 
 
-def cpu_reference_run(cfg, threads=0):
+def cpu_reference_run(n, d, g, seed, P, threads=0):
     """The reference's generate_stats on the host cores (oracle/_ref)."""
     from oracle.refbind import Ref
     ref = Ref()
-    n, d, g, seed, P = cfg
     alpha = ref.alpha_from_gamma(g)
     C = ref.radial_const_from_avg_degree(d, alpha)
     t = time.perf_counter()
     st = ref.generate_stats(n, alpha, C, seed, P, threads)
-    wall = time.perf_counter() - t
-    return st, wall
+    return st, time.perf_counter() - t
 
 
-def run_reference(args, cfg, world, rank):
+def workload_config(name, wl, world):
+    n, d, g, seed, P, weak = wl
+    return {"workload": f"{name}: threshold RHG n={n}, avg degree {d:g}, gamma {g}, seed {seed}, chunks P={P}"
+                        + (f" (weak scaling: 2^28 points and 4096 chunks per GPU)" if weak else ""),
+            "n": n, "avg_degree": d, "gamma": g, "seed": seed, "chunks": P, "parallelism": f"chunk-shard x{world}",
+            "l2": "inputs larger than L2: every step regenerates the full point set (~64 B/point in HBM)"}
+
+
+def parity_block(name, wl, result, cpu_result=None):
+    n, P = wl[0], wl[4]
+    g = golden_row(name, n, P)
+    out = {}
+    if g is not None:
+        want = {"edges": g["edges"], "fingerprint": g["fingerprint"], "comps": g["comps"]}
+        out["golden"] = {"source": f"tests/golden/stats.json row {g['name']} (the reference run by make_golden.py)",
+                         "expected": want, "equal": all(result[k] == want[k] for k in want)}
+    if cpu_result is not None:
+        out["cpu_baseline_equal"] = all(result[k] == cpu_result[k] for k in ("edges", "fingerprint", "comps"))
+    out["equal"] = all(v["equal"] if isinstance(v, dict) else v for v in out.values()) if out else None
+    return out
+
+
+def run_reference(args, name, wl, world, rank):
     if rank != 0:
         return 0
+    n, d, g, seed, P, _ = wl
     cores = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        cpu_reference_run(cfg)
-    tot_edges, tot_s = 0, 0.0
+    budget_s = float(os.environ.get("RHG_REF_BUDGET_S", "150"))
+    st, wall = cpu_reference_run(n, d, g, seed, P)  # warm-up (page cache, thread pool); one is enough on a CPU
+    secs, steps_run = [], 0
+    t_start = time.perf_counter()
     for _ in range(args.steps):
-        st, wall = cpu_reference_run(cfg)
-        tot_edges += st["edges"]
-        tot_s += st["seconds"]
-    v = tot_edges / tot_s
-    n, d, g, seed, P = cfg
+        st, wall = cpu_reference_run(n, d, g, seed, P)
+        secs.append(st["seconds"])
+        steps_run += 1
+        if time.perf_counter() - t_start + st["seconds"] > budget_s:
+            break
+    v = st["edges"] * len(secs) / sum(secs)
+    result = {"edges": st["edges"], "fingerprint": st["fingerprint"], "comps": st["comps"]}
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded model sampler)",
-            "config": workload_config(args.config, cfg, world),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
-                             "sample": f"full {args.config} graph per step (RunStats.seconds), "
-                                       f"GenOptions.workers = hardware_concurrency"},
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / len(secs), "higher_is_better": True,
+            "scaling": "weak" if wl[5] else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded model sampler)", "config": workload_config(name, wl, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "cpu": cpu_model(), "kind": "reference",
+                             "sample": f"full {name} graph per step (RunStats.seconds), GenOptions.workers = "
+                                       f"hardware_concurrency; {steps_run} of {args.steps} steps timed "
+                                       f"(budget {budget_s:.0f} s), median {statistics.median(secs):.3f} s"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "result": {"edges": st["edges"], "fingerprint": st["fingerprint"], "comps": st["comps"]}}
+            "result": result, "parity": parity_block(name, wl, result)}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def workload_config(name, cfg, world):
-    n, d, g, seed, P = cfg
-    return {"workload": f"{name}: threshold RHG n={n}, avg degree {d:g}, gamma {g}, seed {seed}, chunks P={P}",
-            "n": n, "avg_degree": d, "gamma": g, "seed": seed, "chunks": P, "parallelism": f"chunk-shard x{world}",
-            "l2": "inputs larger than L2: every step regenerates the full point set (~64 B/point in HBM)"}
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(args):
+    """--gpus N without torchrun: re-launch under torchrun, one rank per GPU."""
+    one_gpu = os.environ.get("RHG_BENCH_ONE_GPU") == "1"
+    if args.impl == "ours" and not one_gpu:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}", file=sys.stderr,
+                  flush=True)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -190,23 +273,31 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: cfg2 at --gpus 1, cfg3 (strong scaling) at --gpus > 1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     world, rank, local = dist_env()
-    cfg = CONFIGS[args.config]
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr, flush=True)
+        return 2
+    name = args.config or ("cfg2" if world == 1 else "cfg3")
+    wl = workload(name, world)
     if args.impl == "reference":
-        return run_reference(args, cfg, world, rank)
+        return run_reference(args, name, wl, world, rank)
 
     import torch
     import torch.distributed as dist
     import paper_1710_07565_b200 as rhg
 
     # RHG_BENCH_ONE_GPU=1: functional check of the N-rank path on a 1-GPU box (every rank on
-    # cuda:0, gloo for the counter all-reduce); its timings are not scaling numbers
+    # cuda:0; NCCL cannot put two ranks on one GPU, so the counters go through gloo in Python);
+    # its timings are not scaling numbers
     one_gpu = os.environ.get("RHG_BENCH_ONE_GPU") == "1"
     if one_gpu:
         local = 0
@@ -216,7 +307,13 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n, d, g, seed, P = cfg
+            # the library's own communicator: rank 0's NCCL id, broadcast over the torch group
+            uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(rhg.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(uid, 0)
+            rhg.attach_comm(world, rank, bytes(uid.cpu().numpy().tobytes()), device=local)
+    n, d, g, seed, P, weak = wl
     params = rhg.ModelParams.from_avg_degree(n, rhg.alpha_from_gamma(g), d, seed, P)
     opts = rhg.GenOptions(device=local, rank=rank, world=world)
 
@@ -226,17 +323,23 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    from paper_1710_07565_b200.distributed import ShardResult, reduce_shards
+
+    def step():
+        st = rhg.generate_stats(params, opts)
+        if world > 1 and one_gpu:  # the per-step counter reduction (gloo stands in for the device collective)
+            gr = reduce_shards(ShardResult(st.total.edges, st.total.fingerprint, st.total.comps), device="cpu")
+            st.total.edges, st.total.fingerprint, st.total.comps = gr.edges, gr.fingerprint, gr.comps
+        return st
+
     for _ in range(args.warmup):
-        rhg.generate_stats(params, opts)
+        step()
     barrier()
-    dev_ms, wall_s, launches, h2d, d2h = 0.0, 0.0, 0, 0, 0
-    edges_ms = 0.0
-    pairs_ms = 0.0
-    stream_comps = 0
+    dev_ms, wall_s, launches, h2d, d2h, edges_ms, pairs_ms, stream_comps = 0.0, 0.0, 0, 0, 0, 0.0, 0.0, 0
     with Clocks(local) as clk:
         for _ in range(args.steps):
             t = time.perf_counter()
-            st = rhg.generate_stats(params, opts)
+            st = step()
             wall_s += time.perf_counter() - t
             dev_ms += st.device_ms
             edges_ms += st.edges_ms
@@ -246,60 +349,64 @@ def main():
             h2d += st.h2d_bytes
             d2h += st.d2h_bytes
     barrier()
-    # whole-graph counters: wrapping u64 sums over shards (the one collective)
-    from paper_1710_07565_b200.distributed import ShardResult, reduce_shards
-    cdev = "cpu" if one_gpu else "cuda"
-    g = reduce_shards(ShardResult(st.total.edges, st.total.fingerprint, st.total.comps, dev_ms), device=cdev)
-    edges, fp, comps = g.edges, g.fingerprint, g.comps
-    tm = torch.tensor([wall_s, edges_ms], dtype=torch.float64, device=cdev)
+    edges, fp, comps = st.total.edges, st.total.fingerprint, st.total.comps  # whole graph (reduced every step)
+    tm = torch.tensor([dev_ms, wall_s, edges_ms], dtype=torch.float64, device="cpu" if one_gpu else "cuda")
     if world > 1:
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-    dev_ms, wall_s, edges_ms = g.max_device_ms, float(tm[0]), float(tm[1])
+    dev_ms, wall_s, edges_ms = float(tm[0]), float(tm[1]), float(tm[2])
     value = edges * args.steps / (dev_ms * 1e-3)
     e2e = edges * args.steps / wall_s
     if rank == 0:
         ops, lat, _ = rhg.fp64_peak(local)
-        # SURVEY §8(d): algorithmic FP64-pipe work = 8 per reference predicate test
+        # SURVEY 8(d): algorithmic FP64-pipe work = 8 per reference predicate test
         # (5 DMUL + 2 DADD + 1 DSETP).  Dominant kernel: the slab join (sparse
         # engine) - its own tests (stream_comps, this rank) over its own launch time
         # (CUDA events around the launch on the library stream).
         achieved = 8.0 * stream_comps / (pairs_ms * 1e-3) / 1e12 if pairs_ms > 0 else 0.0
-        edge_phase = 8.0 * comps * args.steps / (edges_ms * 1e-3) / 1e12
         peak = ops / 1e12
         tr = traffic_from_profile()
+        result = {"edges": edges, "fingerprint": fp, "comps": comps}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded model sampler)",
-                "config": workload_config(args.config, cfg, world),
+                "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded model sampler)",
+                "config": workload_config(name, wl, world),
                 "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                         "d2h_bytes_per_step": d2h // args.steps},
                 "gpu_launches": launches,
                 "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak,
                              "traffic": tr.get("dram_bytes_per_launch") if tr else None,
-                             "kernel": "sparse engine: slab_kernel (+ its small tail_kernel), CUDA events around the two launches",
+                             "kernel": "sparse engine: slab_kernel (+ its small tail_kernel), CUDA events around "
+                                       "the launches",
                              "kernel_ms": pairs_ms / args.steps,
                              "kernel_tests_per_launch": stream_comps / args.steps,
                              "peak_source": "measured live: non-FMA DMUL+DADD rate (rhg_fp64_peak)",
                              "work": "8 FP64-pipe ops per reference predicate test (SURVEY 8(d)) x the kernel's tests",
                              "dmul_latency_cycles": lat, "kernel_profile": kernel_profile()},
-                "fp64_roofline_frac_edge_phase": edge_phase / peak,
-                "fp64_roofline_frac_whole_step": (8.0 * comps * args.steps / (dev_ms * 1e-3)) / ops,
+                "fp64_roofline_frac_edge_phase": (8.0 * comps * args.steps / (edges_ms * 1e-3)) / ops / world,
+                "fp64_roofline_frac_whole_step": (8.0 * comps * args.steps / (dev_ms * 1e-3)) / ops / world,
                 "clocks": clk.summary(),
-                "result": {"edges": edges, "fingerprint": fp, "comps": comps,
-                           "W_ops_per_edge": 8.0 * comps / max(edges, 1)}}
+                "collective": ("one ncclAllReduce(uint64, 9 counters) per step inside the timed region"
+                               if world > 1 and not one_gpu else
+                               "gloo all-reduce per step (RHG_BENCH_ONE_GPU functional mode)" if world > 1 else None),
+                "result": dict(result, W_ops_per_edge=8.0 * comps / max(edges, 1))}
+        cpu_res = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                stc, wall = cpu_reference_run(cfg)
-                line["cpu_baseline"] = {"value": stc["edges"] / stc["seconds"], "unit": UNIT,
-                                        "cores": os.cpu_count() or 1, "kind": "reference",
-                                        "sample": f"one full {args.config} generate_stats (oracle/_ref, all host "
-                                                  f"threads), {stc['seconds']:.2f} s",
-                                        "result": {"edges": stc["edges"], "fingerprint": stc["fingerprint"],
-                                                   "comps": stc["comps"]}}
+                runs = [cpu_reference_run(n, d, g, seed, P) for _ in range(3)]
+                secs = sorted(r[0]["seconds"] for r in runs)
+                stc = runs[0][0]
+                cpu_res = {"edges": stc["edges"], "fingerprint": stc["fingerprint"], "comps": stc["comps"]}
+                line["cpu_baseline"] = {"value": stc["edges"] / secs[1], "unit": UNIT,
+                                        "cores": os.cpu_count() or 1, "cpu": cpu_model(), "kind": "reference",
+                                        "sample": f"full {name} generate_stats (oracle/_ref, all host threads), "
+                                                  f"median of 3 runs: {secs[1]:.3f} s ({', '.join(f'{x:.3f}' for x in secs)})",
+                                        "result": cpu_res}
             except Exception as e:  # noqa: BLE001 - report, do not fail the bench
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1,
                                         "kind": "reference", "sample": f"unavailable: {e}"}
+        line["parity"] = parity_block(name, wl, result, cpu_res)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -12,6 +12,8 @@
  *   ModelParams::from_avg_degree  geometry.hpp:69-72      rhg_params_from_avg_degree
  *   make_layout                   partition.hpp:233-240   rhg_layout (host only)
  *   GenOptions                    generator.hpp:27-32     rhg_create(device) / rhg_shard
+ *   GenOptions.workers -> GPUs    generator.hpp:245-268   rhg_create_multi (one process, N GPUs, NCCL)
+ *     (one process per GPU)                               rhg_nccl_unique_id + rhg_attach_comm
  *   RunStats                      generator.hpp:34-46     rhg_run_stats
  *   generate_stats(params, opts,  generator.hpp:219-291   rhg_generate_stats
  *                  degrees*)
@@ -42,7 +44,7 @@
 extern "C" {
 #endif
 
-#define RHG_ABI_VERSION 5
+#define RHG_ABI_VERSION 6
 #define RHG_MAX_ANNULI 64 /* layouts with more annuli are rejected (RHG_INVALID_ARGUMENT) */
 
 enum {
@@ -105,7 +107,23 @@ typedef struct {
     uint64_t annulus_edges[RHG_MAX_ANNULI];
     uint64_t annulus_comps[RHG_MAX_ANNULI];
     uint64_t annulus_vertices[RHG_MAX_ANNULI];
+    /* >= 1: edges / fingerprint / comps (and the per-family and per-annulus counters) are the
+     * WHOLE graph's: this call ended with the NCCL all-reduce over `reduced_world` shards
+     * (device_ms includes it).  0: no collective ran; the counters are this shard's. */
+    uint32_t reduced_world, pad2_;
 } rhg_run_stats;
+
+/* Host-side shard plan (no device needed): rank r of `world` owns engines (angular chunks)
+ * [chunk_begin, chunk_end), draws its owned streaming points, the halo chunk's points
+ * (regenerated from the hash seeds, no communication) and every global point. */
+typedef struct {
+    uint32_t chunk_begin, chunk_end;
+    uint64_t owned_points;   /* streaming points of the owned chunks                */
+    uint64_t halo_points;    /* streaming points of chunk chunk_end mod P (the halo)  */
+    uint64_t global_points;  /* clique + global annuli (every rank draws them)       */
+    uint64_t sampled_points; /* owned + halo + global                                */
+    uint64_t device_point_bytes; /* approximate device bytes of the point arrays      */
+} rhg_shard_info;
 
 /* Host point arrays in vertex-id order (n entries each; any may be NULL
  * where a call documents it as optional). */
@@ -143,6 +161,24 @@ int rhg_layout(const rhg_params* params, uint32_t* n_annuli, uint32_t* first_str
 typedef struct rhg_ctx rhg_ctx;
 int rhg_create(int device, rhg_ctx** out);
 void rhg_destroy(rhg_ctx* ctx);
+
+/* Multi-GPU, one process (GenOptions.workers mapped to GPUs, generator.hpp:27-32,
+ * 245-268): one sub-context, stream and host thread per device and an NCCL communicator over
+ * them (ncclCommInitAll).  rhg_generate_stats / rhg_count_edges_from_points on such a context
+ * (shard NULL or {0, 1}) run shard {g, n_devices} on device g, end with one
+ * ncclAllReduce(ncclUint64, sum) of the counters and return the whole graph
+ * (reduced_world = n_devices; device_ms = the slowest device; degrees = summed).  Other calls
+ * use devices[0].  Materialised edge streams need a single-device context. */
+int rhg_create_multi(int n_devices, const int* devices, rhg_ctx** out);
+/* Number of devices a context drives (1 for rhg_create). */
+int rhg_context_devices(const rhg_ctx* ctx, int* n_devices);
+/* Multi-GPU, one process per GPU: rank 0 creates an id (128 bytes), the caller distributes
+ * it (e.g. a torch.distributed broadcast), every rank attaches it to its context.  Shard calls
+ * with shard {rank, world} then end with the counter all-reduce and return the whole graph. */
+int rhg_nccl_unique_id(uint8_t* id);
+int rhg_attach_comm(rhg_ctx* ctx, uint32_t world, uint32_t rank, const uint8_t* id);
+/* The shard plan of `shard` (host only): owned chunks and point counts. */
+int rhg_shard_extent(const rhg_params* params, const rhg_shard* shard, rhg_shard_info* out);
 
 /* generator.hpp:219-291 generate_stats.  `degrees` (optional, u32[n],
  * host) receives exact per-vertex degrees of the edges this shard emits. */

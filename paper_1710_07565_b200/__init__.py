@@ -13,6 +13,7 @@ librhg_b200.so (C ABI, include/rhg_b200.h) on the GPU; there is no CPU path.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import math
 import threading
@@ -26,7 +27,7 @@ from ._native import RHG_OK, RhgCudaError, check, lib
 
 __all__ = ["alpha_from_gamma", "gamma_from_alpha", "radial_const_from_avg_degree", "radius_from_size",
            "expected_avg_degree", "ModelParams", "AnnulusLayout", "make_layout", "GenOptions", "ChunkStats", "RunStats", "generate_stats",
-           "sample_points", "sample_uniforms", "fp64_peak", "count_edges_from_points", "Points", "RhgCudaError", "two_pi"]
+           "sample_points", "sample_uniforms", "fp64_peak", "count_edges_from_points", "Points", "RhgCudaError", "two_pi", "libm_eval", "LIBM_FUNCTIONS", "nccl_unique_id", "attach_comm", "shard_extent", "ShardExtent"]
 
 two_pi = 6.283185307179586476925286766559  # geometry.hpp:11
 
@@ -127,6 +128,9 @@ class GenOptions:
     device: int = 0
     rank: int = 0
     world: int = 1
+    # GenOptions.workers mapped to GPUs (generator.hpp:245-268): a tuple of several devices runs
+    # the whole graph on all of them from this process (rhg_create_multi; NCCL all-reduce)
+    devices: Optional[tuple] = None
 
 
 @dataclass
@@ -167,6 +171,7 @@ class RunStats:
     pairs_ms: float = 0.0
     stream_comps: int = 0
     dense_comps: int = 0
+    reduced_world: int = 0  # >= 1: counters are the whole graph's (NCCL all-reduce over that many shards)
     degrees: Optional[np.ndarray] = None
 
     def avg_degree(self) -> float:
@@ -187,30 +192,58 @@ class RunStats:
                    global_comps=s.global_comps, device_ms=s.device_ms, sample_ms=s.sample_ms, edges_ms=s.edges_ms,
                    host_ms=s.host_ms, kernel_launches=s.kernel_launches, device_bytes=s.device_bytes,
                    h2d_bytes=s.h2d_bytes, d2h_bytes=s.d2h_bytes, pairs_ms=s.pairs_ms,
-                   stream_comps=s.stream_comps, dense_comps=s.dense_comps)
+                   stream_comps=s.stream_comps, dense_comps=s.dense_comps, reduced_world=s.reduced_world)
 
 
 class _Context:
-    """One rhg_ctx (CUDA stream + device buffers) per device, reused."""
+    """One rhg_ctx (CUDA streams + device buffers) per device -- or per device tuple for a
+    multi-GPU context -- reused across calls.  A context is not re-entrant (rhg_b200.h), so
+    every library call holds the context's lock (ctypes releases the GIL during the call)."""
 
     _lock = threading.Lock()
     _ctx: dict = {}
 
     @classmethod
-    def get(cls, device: int) -> C.c_void_p:
+    def _key(cls, opts) -> tuple:
+        if isinstance(opts, int):
+            return (int(opts),)
+        if opts.devices:  # a multi-GPU context, even over one device
+            return ("multi",) + tuple(int(d) for d in opts.devices)
+        return (int(opts.device),)
+
+    @classmethod
+    def _entry(cls, key: tuple):
         with cls._lock:
-            h = cls._ctx.get(device)
-            if h is None:
+            e = cls._ctx.get(key)
+            if e is None:
                 h = C.c_void_p()
-                check(lib().rhg_create(int(device), C.byref(h)))
-                cls._ctx[device] = h
-            return h
+                if key[0] != "multi":
+                    check(lib().rhg_create(key[0], C.byref(h)))
+                else:
+                    devs = key[1:]
+                    arr = (C.c_int * len(devs))(*devs)
+                    check(lib().rhg_create_multi(len(devs), arr, C.byref(h)))
+                e = (h, threading.Lock())
+                cls._ctx[key] = e
+            return e
+
+    @classmethod
+    def get(cls, opts) -> C.c_void_p:
+        return cls._entry(cls._key(opts))[0]
+
+    @classmethod
+    @contextlib.contextmanager
+    def use(cls, opts):
+        h, lk = cls._entry(cls._key(opts))
+        with lk:
+            yield h
 
     @classmethod
     def release_all(cls):
         with cls._lock:
-            for h in cls._ctx.values():
-                lib().rhg_destroy(h)
+            for h, lk in cls._ctx.values():
+                with lk:
+                    lib().rhg_destroy(h)
             cls._ctx.clear()
 
 
@@ -222,14 +255,52 @@ def generate_stats(params: ModelParams, opts: GenOptions = GenOptions(), degrees
     """generator.hpp:219-291: edge count, wrapping Σ(u+v) fingerprint and
     distance computations of the graph (or of this shard), on the GPU.  With
     degrees=True, RunStats.degrees is the exact u32 per-vertex degree."""
-    ctx = _Context.get(opts.device)
     st = _native.rhg_run_stats()
     deg = np.zeros(params.n, np.uint32) if degrees else None
-    check(lib().rhg_generate_stats(ctx, C.byref(params._c()), C.byref(_shard(opts)), C.byref(st),
-                                   deg.ctypes.data_as(C.POINTER(C.c_uint32)) if degrees else None))
+    with _Context.use(opts) as ctx:
+        check(lib().rhg_generate_stats(ctx, C.byref(params._c()), C.byref(_shard(opts)), C.byref(st),
+                                       deg.ctypes.data_as(C.POINTER(C.c_uint32)) if degrees else None))
     out = RunStats._from_c(st)
     out.degrees = deg
     return out
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for attach_comm; create it on rank 0 and share it."""
+    buf = (C.c_uint8 * 128)()
+    check(lib().rhg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def attach_comm(world: int, rank: int, uid: bytes, device: int = 0) -> None:
+    """Give this process's context on `device` an NCCL communicator (rank of world, one process
+    per GPU).  Afterwards generate_stats with GenOptions(rank=rank, world=world) ends with the
+    device-side counter all-reduce and returns the whole graph (RunStats.reduced_world = world)."""
+    if len(uid) != 128:
+        raise ValueError("attach_comm: the NCCL unique id has 128 bytes")
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    with _Context.use(device) as ctx:
+        check(lib().rhg_attach_comm(ctx, int(world), int(rank), buf))
+
+
+@dataclass
+class ShardExtent:
+    """The host-side shard plan (rhg_shard_extent): owned engines (angular chunks) and points."""
+    chunk_begin: int
+    chunk_end: int
+    owned_points: int
+    halo_points: int
+    global_points: int
+    sampled_points: int
+    device_point_bytes: int
+
+
+def shard_extent(params: ModelParams, rank: int = 0, world: int = 1) -> ShardExtent:
+    """Which chunks and how many points rank `rank` of `world` draws (no GPU needed)."""
+    out = _native.rhg_shard_info()
+    check(lib().rhg_shard_extent(C.byref(params._c()), C.byref(_native.rhg_shard(int(rank), int(world))),
+                                 C.byref(out)))
+    return ShardExtent(*[int(getattr(out, f)) for f, _ in _native.rhg_shard_info._fields_])
 
 
 @dataclass
@@ -262,18 +333,18 @@ class Points:
 
 def sample_points(params: ModelParams, opts: GenOptions = GenOptions()) -> Points:
     """The device sampler's point set (ChunkPointSource streams, sweep.hpp:102-141)."""
-    ctx = _Context.get(opts.device)
     pts = Points(*[np.empty(params.n, np.float64) for _ in Points.FIELDS])
-    check(lib().rhg_sample_points(ctx, C.byref(params._c()), C.byref(pts._c())))
+    with _Context.use(opts) as ctx:
+        check(lib().rhg_sample_points(ctx, C.byref(params._c()), C.byref(pts._c())))
     return pts
 
 
 def sample_uniforms(params: ModelParams, opts: GenOptions = GenOptions()):
     """Raw MT19937-64 uniforms of every point's (angle, radius) streams, id order."""
-    ctx = _Context.get(opts.device)
     ua, ur = np.empty(params.n, np.float64), np.empty(params.n, np.float64)
-    check(lib().rhg_sample_uniforms(ctx, C.byref(params._c()), ua.ctypes.data_as(_native.P_f64),
-                                    ur.ctypes.data_as(_native.P_f64)))
+    with _Context.use(opts) as ctx:
+        check(lib().rhg_sample_uniforms(ctx, C.byref(params._c()), ua.ctypes.data_as(_native.P_f64),
+                                        ur.ctypes.data_as(_native.P_f64)))
     return ua, ur
 
 
@@ -309,7 +380,6 @@ def count_edges_from_points(params: ModelParams, points, opts: GenOptions = GenO
                             degrees: bool = False) -> RunStats:
     """Parity hook: run the device edge kernels on a given point set (any
     object with the Points fields; r optional)."""
-    ctx = _Context.get(opts.device)
     pts = Points(*[getattr(points, k, None) for k in Points.FIELDS])
     for k in Points.FIELDS:
         a = getattr(pts, k)
@@ -317,9 +387,10 @@ def count_edges_from_points(params: ModelParams, points, opts: GenOptions = GenO
             raise ValueError(f"count_edges_from_points: field {k} must have n entries")
     st = _native.rhg_run_stats()
     deg = np.zeros(params.n, np.uint32) if degrees else None
-    check(lib().rhg_count_edges_from_points(ctx, C.byref(params._c()), C.byref(_shard(opts)),
-                                            C.byref(pts._c()), C.byref(st),
-                                            deg.ctypes.data_as(C.POINTER(C.c_uint32)) if degrees else None))
+    with _Context.use(opts) as ctx:
+        check(lib().rhg_count_edges_from_points(ctx, C.byref(params._c()), C.byref(_shard(opts)),
+                                                C.byref(pts._c()), C.byref(st),
+                                                deg.ctypes.data_as(C.POINTER(C.c_uint32)) if degrees else None))
     out = RunStats._from_c(st)
     out.degrees = deg
     return out
@@ -330,7 +401,11 @@ def count_edges_from_points(params: ModelParams, points, opts: GenOptions = GenO
 # generate(params, opts, edge sink)) and its file formats (io.hpp:20-96).
 
 def _edges_call(fn, params: ModelParams, opts: GenOptions, *pre):
-    ctx = _Context.get(opts.device)
+    with _Context.use(opts) as ctx:
+        return _edges_call_locked(ctx, fn, params, opts, *pre)
+
+
+def _edges_call_locked(ctx, fn, params: ModelParams, opts: GenOptions, *pre):
     st = _native.rhg_run_stats()
     m = C.c_uint64(0)
     est = expected_avg_degree(params.C, params.alpha) * params.n / 2.0 / max(1, opts.world)
@@ -405,14 +480,14 @@ def naive_edges(points, R: float, device: int = 0) -> np.ndarray:
     r = np.ascontiguousarray(points.r, np.float64)
     th = np.ascontiguousarray(points.theta, np.float64)
     n = len(r)
-    ctx = _Context.get(device)
     m = C.c_uint64(0)
     P64 = C.POINTER(C.c_uint64)
-    check(lib().rhg_naive_edges(ctx, n, float(R), r.ctypes.data_as(_native.P_f64), th.ctypes.data_as(_native.P_f64),
-                                None, 0, C.byref(m)))
-    buf = np.empty((m.value, 2), np.uint64)
-    check(lib().rhg_naive_edges(ctx, n, float(R), r.ctypes.data_as(_native.P_f64), th.ctypes.data_as(_native.P_f64),
-                                buf.ctypes.data_as(P64), m.value, C.byref(m)))
+    with _Context.use(device) as ctx:
+        check(lib().rhg_naive_edges(ctx, n, float(R), r.ctypes.data_as(_native.P_f64),
+                                    th.ctypes.data_as(_native.P_f64), None, 0, C.byref(m)))
+        buf = np.empty((m.value, 2), np.uint64)
+        check(lib().rhg_naive_edges(ctx, n, float(R), r.ctypes.data_as(_native.P_f64),
+                                    th.ctypes.data_as(_native.P_f64), buf.ctypes.data_as(P64), m.value, C.byref(m)))
     return buf
 
 

@@ -33,7 +33,13 @@ class rhg_run_stats(C.Structure):
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("pairs_ms", C.c_double),
                 ("stream_comps", C.c_uint64), ("dense_comps", C.c_uint64),
                 ("per_annulus", C.c_uint32), ("pad_", C.c_uint32), ("annulus_edges", C.c_uint64 * 64), ("annulus_comps", C.c_uint64 * 64),
-                ("annulus_vertices", C.c_uint64 * 64)]
+                ("annulus_vertices", C.c_uint64 * 64), ("reduced_world", C.c_uint32), ("pad2_", C.c_uint32)]
+
+
+class rhg_shard_info(C.Structure):
+    _fields_ = [("chunk_begin", C.c_uint32), ("chunk_end", C.c_uint32), ("owned_points", C.c_uint64),
+                ("halo_points", C.c_uint64), ("global_points", C.c_uint64), ("sampled_points", C.c_uint64),
+                ("device_point_bytes", C.c_uint64)]
 
 
 P_f64 = C.POINTER(C.c_double)
@@ -53,7 +59,8 @@ EXPORTS = ["rhg_last_error", "rhg_abi_version", "rhg_alpha_from_gamma", "rhg_rad
            "rhg_sample_points", "rhg_sample_uniforms", "rhg_count_edges_from_points",
            "rhg_fp64_peak", "rhg_generate_edges", "rhg_edges_from_points", "rhg_write_edges_text", "rhg_write_edges_binary",
            "rhg_read_edges_binary", "rhg_io_last_error", "rhg_naive_edges", "rhg_powerlaw_mle", "rhg_layout",
-           "rhg_libm_eval"]
+           "rhg_libm_eval", "rhg_create_multi", "rhg_context_devices", "rhg_nccl_unique_id", "rhg_attach_comm",
+           "rhg_shard_extent"]
 
 _lib = None
 
@@ -99,6 +106,11 @@ def lib():
     L.rhg_layout.argtypes = [C.POINTER(rhg_params), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), P_u64, P_u64,
                              P_u64, C.POINTER(C.c_uint8)]
     L.rhg_libm_eval.argtypes = [C.c_int, C.c_int, P_f64, P_f64, P_f64, C.c_uint64]
+    L.rhg_create_multi.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]
+    L.rhg_context_devices.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
+    L.rhg_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+    L.rhg_attach_comm.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint8)]
+    L.rhg_shard_extent.argtypes = [C.POINTER(rhg_params), C.POINTER(rhg_shard), C.POINTER(rhg_shard_info)]
     _lib = L
     return L
 

@@ -5,6 +5,13 @@
 // H2D copy of all tables -> sampler kernels -> cell index -> edge kernels ->
 // one D2H copy of the counters.  All device work is on the context's stream,
 // timed with CUDA events on that stream.
+//
+// Multi-GPU: a context may carry an NCCL communicator (rhg_attach_comm:
+// one process per GPU; rhg_create_multi: one process, one sub-context and host thread
+// per GPU).  A shard call on such a context ends with ONE ncclAllReduce(ncclUint64, sum)
+// of its counters on the context's stream, inside the timed region, so every rank
+// returns the whole graph's (edges, fingerprint, comps).  NCCL is dlopen'ed on first
+// use: single-GPU use has no NCCL dependency.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -14,7 +21,11 @@
 #include <new>
 #include <string>
 #include <queue>
+#include <thread>
 #include <vector>
+
+#include <dlfcn.h>
+#include <nccl.h> // types and prototypes only: the library is dlopen'ed (nccl_api)
 
 #include "../../include/rhg_b200.h"
 #include "device.cuh"
@@ -88,7 +99,8 @@ struct HostPinned {
     void ensure(std::size_t bytes) {
         if (bytes <= cap) return;
         if (p) cudaFreeHost(p);
-        p = nullptr;
+        p   = nullptr;
+        cap = 0;
         CK(cudaMallocHost(&p, bytes));
         cap = bytes;
     }
@@ -101,6 +113,43 @@ double ms_between(cudaEvent_t a, cudaEvent_t b) {
     CK(cudaEventElapsedTime(&ms, a, b));
     return ms;
 }
+
+// NCCL entry points, resolved from libnccl.so.2 on first use (the copy torch already
+// loaded, if any: same soname).
+struct NcclApi {
+    void* h = nullptr;
+    decltype(&ncclGetUniqueId)    get_unique_id = nullptr;
+    decltype(&ncclCommInitRank)   comm_init_rank = nullptr;
+    decltype(&ncclCommInitAll)    comm_init_all = nullptr;
+    decltype(&ncclAllReduce)      all_reduce = nullptr;
+    decltype(&ncclCommDestroy)    comm_destroy = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+};
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        for (const char* name: {"libnccl.so.2", "libnccl.so"})
+            if ((a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!a.h) return a;
+        a.get_unique_id  = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(a.h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(a.h, "ncclCommInitRank"));
+        a.comm_init_all  = reinterpret_cast<decltype(a.comm_init_all)>(dlsym(a.h, "ncclCommInitAll"));
+        a.all_reduce     = reinterpret_cast<decltype(a.all_reduce)>(dlsym(a.h, "ncclAllReduce"));
+        a.comm_destroy   = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(a.h, "ncclCommDestroy"));
+        a.error_string   = reinterpret_cast<decltype(a.error_string)>(dlsym(a.h, "ncclGetErrorString"));
+        return a;
+    }();
+    if (!api.h || !api.get_unique_id || !api.comm_init_rank || !api.comm_init_all || !api.all_reduce ||
+        !api.comm_destroy || !api.error_string)
+        throw CudaError("rhg: NCCL (libnccl.so.2) is not available for multi-GPU contexts");
+    return api;
+}
+
+#define NK(x)                                                                                             \
+    do {                                                                                                  \
+        ncclResult_t r_ = (x);                                                                            \
+        if (r_ != ncclSuccess) throw CudaError(std::string(#x) + ": " + nccl_api().error_string(r_));   \
+    } while (0)
 
 } // namespace
 
@@ -118,6 +167,12 @@ struct rhg_ctx {
     DevBuf       ebuf, ecount, ekeys, esort; // materialised edges (rhg_generate_edges)
     DevBuf       lam_tmp;
     HostPinned   staging, staging2, readback; // table parts 1 and 2, counter readback
+    // multi-GPU: a communicator over `comm_world` ranks (this context = rank comm_rank); shard
+    // calls with shard {comm_rank, comm_world} all-reduce their counters through it
+    ncclComm_t    comm       = nullptr;
+    std::uint32_t comm_world = 1, comm_rank = 0;
+    // rhg_create_multi: one sub-context per device (each with its comm); calls fan out to them
+    std::vector<rhg_ctx*> subs;
 };
 
 namespace {
@@ -749,6 +804,15 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     fin.finish = true;
     launch_edges(e, fin, ctx->stream, launches);
     CK(cudaGetLastError());
+    const bool reduce = ctx->comm && pl.world == ctx->comm_world && pl.rank == ctx->comm_rank;
+    if (reduce) { // the one collective of the shard plan: wrapping u64 sums of the counters
+        const NcclApi& N = nccl_api();
+        NK(N.all_reduce(ctx->counters.p, ctx->counters.p, 3 * sizeof(Counters) / 8, ncclUint64, ncclSum, ctx->comm,
+                        ctx->stream));
+        if (degrees || sink)
+            NK(N.all_reduce(e.ann_ctr, e.ann_ctr, 2 * kMaxAnnuli, ncclUint64, ncclSum, ctx->comm, ctx->stream));
+    }
+    out->reduced_world = reduce ? pl.world : 0u;
     CK(cudaEventRecord(ctx->ev[2], ctx->stream));
     ctx->readback.ensure(4096);
     auto* hc = static_cast<Counters*>(ctx->readback.p);
@@ -820,6 +884,66 @@ Params to_params(const rhg_params* p) {
 
 using Clock = std::chrono::steady_clock;
 
+// A multi-GPU context (rhg_create_multi) computes the whole graph: sub-context g runs shard
+// {g, G} from its own host thread (its plan, uploads and launches overlap the others'), ends
+// with the NCCL all-reduce of the counters, and the results merge here: counters are the
+// (identical) reduced whole-graph values, times the max over devices, sizes and per-shard
+// vertex counts the sum, degrees the sum of the shards' partial degrees.
+template <typename Run>
+void multi_dispatch(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, rhg_run_stats* out,
+                    std::uint32_t* degrees, EdgeSink* sink, Run run) {
+    if (shard && !(shard->rank == 0 && shard->world == 1))
+        throw InvalidArgument("rhg: a multi-GPU context generates the whole graph (shard must be NULL or {0, 1})");
+    if (sink) throw InvalidArgument("rhg: materialised edge streams need a single-device context");
+    if (!params) throw InvalidArgument("rhg: params is null");
+    const auto          t0 = Clock::now();
+    const std::uint32_t G  = std::uint32_t(ctx->subs.size());
+    std::vector<rhg_run_stats>              outs(G);
+    std::vector<std::vector<std::uint32_t>> deg(degrees ? G : 0);
+    std::vector<std::string>                err(G);
+    std::vector<int>                        code(G, RHG_OK);
+    std::vector<std::thread>                th;
+    for (std::uint32_t g = 0; g < G; ++g)
+        th.emplace_back([&, g] {
+            if (degrees) deg[g].assign(params->n, 0u);
+            code[g] = guarded([&] {
+                const rhg_shard sh{g, G};
+                run(ctx->subs[g], &sh, &outs[g], degrees ? deg[g].data() : nullptr);
+            });
+            if (code[g] != RHG_OK) err[g] = g_err;
+        });
+    for (auto& t: th) t.join();
+    for (std::uint32_t g = 0; g < G; ++g)
+        if (code[g] != RHG_OK) {
+            const std::string m = "device " + std::to_string(ctx->subs[g]->device) + ": " + err[g];
+            if (code[g] == RHG_INVALID_ARGUMENT) throw InvalidArgument(m);
+            if (code[g] == RHG_CUDA) throw CudaError(m);
+            if (code[g] == RHG_NOMEM) throw std::bad_alloc();
+            throw Invariant(m);
+        }
+    *out = outs[0];
+    for (std::uint32_t g = 1; g < G; ++g) {
+        const rhg_run_stats& o = outs[g];
+        out->device_ms = std::max(out->device_ms, o.device_ms), out->sample_ms = std::max(out->sample_ms, o.sample_ms);
+        out->edges_ms = std::max(out->edges_ms, o.edges_ms), out->host_ms = std::max(out->host_ms, o.host_ms);
+        out->pairs_ms = std::max(out->pairs_ms, o.pairs_ms);
+        out->kernel_launches += o.kernel_launches, out->device_bytes += o.device_bytes;
+        out->h2d_bytes += o.h2d_bytes, out->d2h_bytes += o.d2h_bytes;
+        out->streaming_vertices += o.streaming_vertices;
+        for (int a = 0; a < RHG_MAX_ANNULI; ++a) out->annulus_vertices[a] += o.annulus_vertices[a];
+    }
+    if (degrees)
+        for (std::uint64_t v = 0; v < params->n; ++v) {
+            std::uint32_t d = 0;
+            for (std::uint32_t g = 0; g < G; ++g) d += deg[g][v];
+            degrees[v] = d;
+        }
+    out->seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+// single-device entry points on a multi-GPU context use its first device
+rhg_ctx* primary(rhg_ctx* c) { return c && !c->subs.empty() ? c->subs[0] : c; }
+
 } // namespace
 
 extern "C" {
@@ -887,13 +1011,20 @@ int rhg_create(int device, rhg_ctx** out) {
 
 void rhg_destroy(rhg_ctx* c) {
     if (!c) return;
+    if (!c->subs.empty()) { // a multi-GPU context owns its per-device sub-contexts
+        for (rhg_ctx* s: c->subs) rhg_destroy(s);
+        delete c;
+        return;
+    }
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->side);
     for (DevBuf* b: {&c->beta, &c->hw, &c->rec0, &c->rec1, &c->rec2, &c->r_out, &c->beta_raw, &c->tables, &c->cells,
                      &c->counters, &c->degrees, &c->dbg, &c->nid, &c->lcells, &c->s_beta,
-                     &c->s_hw, &c->s_lt, &c->s_rec1, &c->s_rec2, &c->gsort, &c->gbuf})
+                     &c->s_hw, &c->s_lt, &c->s_rec1, &c->s_rec2, &c->gsort, &c->gbuf, &c->tables2, &c->lam_tmp,
+                     &c->ebuf, &c->ecount, &c->ekeys, &c->esort})
         b->release();
+    if (c->comm) nccl_api().comm_destroy(c->comm);
     if (c->staging.p) cudaFreeHost(c->staging.p);
     if (c->staging2.p) cudaFreeHost(c->staging2.p);
     if (c->readback.p) cudaFreeHost(c->readback.p);
@@ -909,6 +1040,83 @@ void rhg_destroy(rhg_ctx* c) {
     for (auto& e: c->tl_pool) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     delete c;
+}
+
+int rhg_create_multi(int n_devices, const int* devices, rhg_ctx** out) {
+    return guarded([&] {
+        if (!out) throw InvalidArgument("rhg_create_multi: out is null");
+        *out = nullptr;
+        if (n_devices < 1 || !devices) throw InvalidArgument("rhg_create_multi: need n_devices >= 1 devices");
+        for (int i = 0; i < n_devices; ++i)
+            for (int j = 0; j < i; ++j)
+                if (devices[i] == devices[j]) throw InvalidArgument("rhg_create_multi: a device is listed twice");
+        const NcclApi&          N = nccl_api();
+        std::vector<ncclComm_t> comms(n_devices, nullptr);
+        auto*                   m = new rhg_ctx;
+        try {
+            for (int i = 0; i < n_devices; ++i) {
+                rhg_ctx* sub = nullptr;
+                if (rhg_create(devices[i], &sub) != RHG_OK) throw CudaError(g_err);
+                m->subs.push_back(sub);
+            }
+            NK(N.comm_init_all(comms.data(), n_devices, devices));
+            for (int i = 0; i < n_devices; ++i)
+                m->subs[i]->comm = comms[i], m->subs[i]->comm_world = std::uint32_t(n_devices),
+                m->subs[i]->comm_rank = std::uint32_t(i);
+        } catch (...) {
+            rhg_destroy(m);
+            throw;
+        }
+        m->device = devices[0];
+        *out      = m;
+    });
+}
+
+int rhg_context_devices(const rhg_ctx* ctx, int* n_devices) {
+    return guarded([&] {
+        if (!ctx || !n_devices) throw InvalidArgument("rhg_context_devices: null argument");
+        *n_devices = ctx->subs.empty() ? 1 : int(ctx->subs.size());
+    });
+}
+
+int rhg_nccl_unique_id(uint8_t* id) {
+    return guarded([&] {
+        if (!id) throw InvalidArgument("rhg_nccl_unique_id: id is null");
+        ncclUniqueId u;
+        NK(nccl_api().get_unique_id(&u));
+        std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+    });
+}
+
+int rhg_attach_comm(rhg_ctx* ctx, uint32_t world, uint32_t rank, const uint8_t* id) {
+    return guarded([&] {
+        if (!ctx || !id) throw InvalidArgument("rhg_attach_comm: null argument");
+        if (!ctx->subs.empty()) throw InvalidArgument("rhg_attach_comm: a multi-GPU context has its communicators");
+        if (world < 1 || rank >= world) throw InvalidArgument("rhg_attach_comm: rank must lie in [0, world)");
+        if (ctx->comm) throw InvalidArgument("rhg_attach_comm: the context already has a communicator");
+        CK(cudaSetDevice(ctx->device));
+        ncclUniqueId u;
+        std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+        ncclComm_t c = nullptr;
+        NK(nccl_api().comm_init_rank(&c, int(world), u, int(rank)));
+        ctx->comm = c, ctx->comm_world = world, ctx->comm_rank = rank;
+    });
+}
+
+int rhg_shard_extent(const rhg_params* params, const rhg_shard* shard, rhg_shard_info* out) {
+    return guarded([&] {
+        if (!out) throw InvalidArgument("rhg_shard_extent: out is null");
+        const Plan pl = make_plan_head(to_params(params), shard);
+        std::memset(out, 0, sizeof *out);
+        out->chunk_begin = pl.e0, out->chunk_end = pl.e1;
+        for (std::uint32_t i = pl.L.first_streaming; i < pl.L.count; ++i) {
+            out->owned_points += pl.ann[i].halo - pl.ann[i].off;
+            out->halo_points += pl.ann[i].end - pl.ann[i].halo;
+        }
+        out->global_points = pl.n_glob;
+        out->sampled_points = pl.total;
+        out->device_point_bytes = pl.total * 136; // sampler arrays + the lambda-sorted SoA (DESIGN 3)
+    });
 }
 
 namespace {
@@ -970,6 +1178,7 @@ int rhg_generate_stats(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
 
 int rhg_naive_edges(rhg_ctx* ctx, std::uint64_t n, double R, const double* r, const double* theta,
                     std::uint64_t* edges, std::uint64_t cap, std::uint64_t* n_edges) {
+    ctx = primary(ctx);
     return guarded([&] {
         if (!ctx || !n_edges || (n && (!r || !theta))) throw InvalidArgument("rhg_naive_edges: null argument");
         if (n > 100000) throw InvalidArgument("naive_edges: refusing quadratic work above n = 100000");
@@ -1014,6 +1223,13 @@ int rhg_count_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rh
 namespace {
 void generate_impl(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, rhg_run_stats* out,
                    std::uint32_t* degrees, EdgeSink* sink) {
+    if (ctx && !ctx->subs.empty()) {
+        multi_dispatch(ctx, params, shard, out, degrees, sink,
+                       [&](rhg_ctx* sub, const rhg_shard* sh, rhg_run_stats* o, std::uint32_t* deg) {
+                           generate_impl(sub, params, sh, o, deg, nullptr);
+                       });
+        return;
+    }
     {
         if (!ctx || !out) throw InvalidArgument("rhg_generate_stats: null argument");
         const auto t0 = Clock::now();
@@ -1063,6 +1279,7 @@ void generate_impl(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shar
 } // namespace
 
 int rhg_sample_points(rhg_ctx* ctx, const rhg_params* params, rhg_points* o) {
+    ctx = primary(ctx);
     return guarded([&] {
         if (!ctx || !o || !o->beta || !o->r || !o->theta || !o->half_width || !o->coth_r || !o->inv_sinh_r ||
             !o->cos_theta || !o->sin_theta)
@@ -1103,6 +1320,7 @@ int rhg_sample_points(rhg_ctx* ctx, const rhg_params* params, rhg_points* o) {
 }
 
 int rhg_sample_uniforms(rhg_ctx* ctx, const rhg_params* params, double* u_angle, double* u_radius) {
+    ctx = primary(ctx);
     return guarded([&] {
         if (!ctx || !u_angle || !u_radius) throw InvalidArgument("rhg_sample_uniforms: null argument");
         CK(cudaSetDevice(ctx->device));
@@ -1131,6 +1349,13 @@ int rhg_sample_uniforms(rhg_ctx* ctx, const rhg_params* params, double* u_angle,
 namespace {
 void from_points_impl(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, const rhg_points* pts,
                       rhg_run_stats* out, std::uint32_t* degrees, EdgeSink* sink) {
+    if (ctx && !ctx->subs.empty()) {
+        multi_dispatch(ctx, params, shard, out, degrees, sink,
+                       [&](rhg_ctx* sub, const rhg_shard* sh, rhg_run_stats* o, std::uint32_t* deg) {
+                           from_points_impl(sub, params, sh, pts, o, deg, nullptr);
+                       });
+        return;
+    }
     {
         if (!ctx || !out || !pts || !pts->beta || !pts->theta || !pts->half_width || !pts->coth_r ||
             !pts->inv_sinh_r || !pts->cos_theta || !pts->sin_theta)

@@ -43,7 +43,7 @@ def test_library_is_sm100a():
 
 
 def test_abi_version():
-    assert _native.lib().rhg_abi_version() == 5
+    assert _native.lib().rhg_abi_version() == 6
 
 
 def test_params_mirror_oracle(oracle):
@@ -75,3 +75,12 @@ def test_no_gpu_fails_loudly():
     p = rhg.ModelParams.from_avg_degree(1000, 1.0, 8.0, 1, 2)
     with pytest.raises(rhg.RhgCudaError):
         rhg.generate_stats(p)
+
+
+def test_multi_context_rejects_duplicates_and_needs_gpus():
+    p = rhg.ModelParams.from_avg_degree(1000, 0.8, 8.0, 1, 4)
+    with pytest.raises(ValueError, match="twice"):
+        rhg.generate_stats(p, rhg.GenOptions(devices=(0, 0)))
+    if not torch.cuda.is_available():
+        with pytest.raises(rhg.RhgCudaError):
+            rhg.generate_stats(p, rhg.GenOptions(devices=(0, 1)))

@@ -56,3 +56,32 @@ def test_gloo_shards_reduce_to_whole(oracle, world, P):
 def test_shard_validation(oracle):
     with pytest.raises(ValueError, match="rank"):
         oracle.generate_stats_shard(1000, 1.0, 1.0, 1, 4, 2, 2)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_shard_plan_partitions_the_graph(oracle, world):
+    """rhg_shard_extent (host plan, no GPU): the ranks' engine ranges tile [0, P), their owned
+    streaming points add up to every streaming point, each rank's halo is the first chunk of
+    the next rank's range, and every rank draws all global points (generator.hpp:58-104)."""
+    import paper_1710_07565_b200 as rhg
+    n, d, alpha, seed, P = 300000, 16.0, 0.8, 3, 16
+    p = rhg.ModelParams.from_avg_degree(n, alpha, d, seed, P)
+    L = oracle.layout(n, alpha, p.C, seed, P)
+    ext = [rhg.shard_extent(p, r, world) for r in range(world)]
+    assert ext[0].chunk_begin == 0 and ext[-1].chunk_end == P
+    assert all(a.chunk_end == b.chunk_begin for a, b in zip(ext, ext[1:]))
+    streaming = L.chunk_counts[L.first_streaming:]
+    n_glob = int(L.counts[:L.first_streaming].sum())
+    assert sum(e.owned_points for e in ext) == n - n_glob
+    for e in ext:
+        assert e.global_points == n_glob
+        assert e.owned_points == int(streaming[:, e.chunk_begin:e.chunk_end].sum())
+        assert e.halo_points == int(streaming[:, e.chunk_end % P].sum())
+        assert e.sampled_points == e.owned_points + e.halo_points + e.global_points
+
+
+def test_shard_plan_rejects_bad_rank():
+    import paper_1710_07565_b200 as rhg
+    p = rhg.ModelParams.from_avg_degree(1000, 0.8, 8.0, 1, 4)
+    with pytest.raises(ValueError, match="rank"):
+        rhg.shard_extent(p, 2, 2)
