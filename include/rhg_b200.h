@@ -240,6 +240,27 @@ int rhg_powerlaw_mle(const uint32_t* degrees, uint64_t n, uint32_t d_min, double
 /* message of the last failed edge-file / analytics call (this thread) */
 const char* rhg_io_last_error(void);
 
+/* Predicate audit (north_star / SURVEY 8(c) "borderline pairs"): one generate_stats of `shard` in
+ * which the slab join (the only engine that does not evaluate the reference predicate
+ * sweep.hpp:531-533 directly) also evaluates it, in FP64 and the reference's order, for every
+ * pair its FP32 pre-filter decided.  disagreements must be 0 (a decided pair whose FP32 sign
+ * differs from the reference's); max_err_over_tau is the largest |D32 - D64| / tau seen (< 1:
+ * the pre-filter's error bound held, DESIGN 4.1).  The other engines evaluate the reference
+ * predicate itself, so their device decisions equal the reference's by construction.
+ * stats receives the call's RunStats (counters unchanged by the audit). */
+typedef struct {
+    uint64_t slab_pairs;          /* pairs tested by the slab join                             */
+    uint64_t prefilter_decided;   /* ... decided by the FP32 pre-filter                        */
+    uint64_t exact_recheck;       /* ... left to the exact FP64 predicate near the threshold    */
+    uint64_t exact_only;          /* ... in groups whose windows run the exact predicate only  */
+    uint64_t disagreements;       /* pre-filter decisions != reference predicate (must be 0)   */
+    uint64_t noise_band_pairs;    /* slab pairs with |lhs - rhs| < 1e-15 (rounding-noise band) */
+    uint64_t exact_engine_pairs;  /* pairs of the engines that evaluate the predicate directly */
+    double max_err_over_tau;      /* max |D32 - D64| / tau over pre-filter decisions           */
+} rhg_audit_report;
+int rhg_audit_predicate(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, rhg_audit_report* out,
+                        rhg_run_stats* stats);
+
 /* Diagnostic (not part of the reference interface): measured non-FMA FP64
  * DMUL+DADD instruction rate of `device` (the edge kernels' roofline
  * denominator) and the dependent-DMUL latency in SM cycles. */

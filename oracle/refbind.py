@@ -12,6 +12,7 @@ does.
 from __future__ import annotations
 
 import ctypes as C
+import ctypes as C_
 import os
 from dataclasses import dataclass
 
@@ -234,6 +235,11 @@ class OrcStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class OrcBorder(C.Structure):
+    _fields_ = [(k, u64) for k in ("comps", "edges", "band_pairs", "flips_to_edge", "flips_to_nonedge",
+                                   "border_pairs", "listed")] + [("max_flip_dmr", f64), ("seconds", f64)]
+
+
 class Oracle(_Base):
     """The plain-C restatement (oracle/rhg_oracle.c)."""
 
@@ -259,7 +265,22 @@ class Oracle(_Base):
             C.POINTER(OrcStats), P_u32]
         L.orc_generate_stats_shard.argtypes = [u64, f64, f64, u64, u32, u32, u32, u32, C.POINTER(OrcStats)]
         L.orc_libm_eval.argtypes = [C.c_int, P_f64, P_f64, P_f64, u64, u32]
+        L.orc_borderline.argtypes = [u64, f64, f64, u64, u32, u32, u32, u32, f64, u64, C.POINTER(OrcBorder), P_u64,
+                                     P_u64, P_f64, P_u8]
         L.orc_libm_eval.restype = None
+
+    def borderline(self, n, alpha, C, seed, P, rank=0, world=1, band=1e-13, cap=10000, threads=0):
+        """Threshold-borderline audit of shard (rank, world) (orc_borderline): counts and the
+        listed pairs (u, v, d - R, reference decision) with |d - R| < 1e-12 in binary128."""
+        out = OrcBorder()
+        u, v = np.zeros(cap, np.uint64), np.zeros(cap, np.uint64)
+        dmr, dec = np.zeros(cap, np.float64), np.zeros(cap, np.uint8)
+        self._check(self.L.orc_borderline(n, alpha, C, seed, P, rank, world, threads, band, cap, C_.byref(out),
+                                          _p(u, P_u64), _p(v, P_u64), _p(dmr, P_f64), _p(dec, P_u8)))
+        k = out.listed
+        rep = {f: getattr(out, f) for f, _ in OrcBorder._fields_}
+        rep["pairs"] = [(int(u[i]), int(v[i]), float(dmr[i]), bool(dec[i])) for i in range(k)]
+        return rep
 
     def libm_eval(self, fn: int, x: np.ndarray, y: np.ndarray | None = None, threads: int | None = None):
         """Host glibc exp/log/log1p/acosh/acos/pow/sin/cos (fn 0..7) elementwise."""

@@ -17,6 +17,7 @@
 
 #include <math.h>
 #include <pthread.h>
+#include <quadmath.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -785,6 +786,51 @@ static void draw_point(engine* e, asweep* a, src_t* src, int local) {
     activate(e, a, &t);
     enqueue_node(e, a, &nd);
 }
+/* threshold-borderline audit (orc_borderline; NULL/0 when off) */
+static struct {
+    int on;
+    double band;
+    const double *r, *theta;
+    __float128 R, coshR;
+    uint64_t band_pairs, to_edge, to_nonedge, border, cap, listed;
+    double max_flip_dmr; /* largest |d - R| of a pair whose decision flips */
+    uint64_t *u, *v;
+    double* dmr;
+    uint8_t* dec;
+    pthread_mutex_t mu;
+} g_bd;
+
+/* geometry.hpp:117-123 in binary128 for a pair whose FP64 predicate value is within the band */
+static void border_check(uint64_t a, uint64_t b, double lhs, double rhs, double cab, double iab, int ref_edge) {
+    const double scale = fabs(lhs) + fabs(cab) + fabs(iab) + 1.0;
+    if (!(fabs(lhs - rhs) <= g_bd.band * scale)) return;
+    __atomic_fetch_add(&g_bd.band_pairs, 1, __ATOMIC_RELAXED);
+    const double ra = g_bd.r[a], rb = g_bd.r[b];
+    const __float128 r1 = ra < rb ? ra : rb, r2 = ra < rb ? rb : ra;
+    const __float128 dth = fabsq((__float128)g_bd.theta[a] - (__float128)g_bd.theta[b]);
+    const __float128 arg = coshq(r2 - r1) + (1 - cosq(dth)) * sinhq(r1) * sinhq(r2);
+    const int exact_edge = arg < g_bd.coshR;
+    if (exact_edge != ref_edge) {
+        __atomic_fetch_add(exact_edge ? &g_bd.to_edge : &g_bd.to_nonedge, 1, __ATOMIC_RELAXED);
+        const double dmr = fabs((double)(acoshq(arg < 1 ? 1 : arg) - g_bd.R));
+        pthread_mutex_lock(&g_bd.mu);
+        if (dmr > g_bd.max_flip_dmr) g_bd.max_flip_dmr = dmr;
+        pthread_mutex_unlock(&g_bd.mu);
+    }
+    if (fabsq(arg / g_bd.coshR - 1) < 1e-9Q) {
+        const double dmr = (double)(acoshq(arg < 1 ? 1 : arg) - g_bd.R);
+        if (fabs(dmr) < 1e-12) {
+            __atomic_fetch_add(&g_bd.border, 1, __ATOMIC_RELAXED);
+            pthread_mutex_lock(&g_bd.mu);
+            if (g_bd.listed < g_bd.cap) {
+                const uint64_t k = g_bd.listed++;
+                g_bd.u[k] = a < b ? a : b, g_bd.v[k] = a < b ? b : a, g_bd.dmr[k] = dmr, g_bd.dec[k] = (uint8_t)ref_edge;
+            }
+            pthread_mutex_unlock(&g_bd.mu);
+        }
+    }
+}
+
 /* sweep.hpp:509-543 — the predicate, evaluated in the reference's order */
 static void match_node(engine* e, asweep* a, const ntok* nd) {
     active_t* act = &a->act;
@@ -802,6 +848,9 @@ static void match_node(engine* e, asweep* a, const ntok* nd) {
         if (e->mat) __atomic_fetch_add(&e->mat[(size_t)act->home[i] * e->L->count + nd->annulus], 1, __ATOMIC_RELAXED);
         const double lhs = act->cs[i] * nd->cs + act->sn[i] * nd->sn;
         const double rhs = act->coth[i] * nd->coth - cosh_R * act->inv[i] * nd->inv;
+        if (g_bd.on)
+            border_check(act->id[i], nd->id, lhs, rhs, act->coth[i] * nd->coth, cosh_R * act->inv[i] * nd->inv,
+                         lhs > rhs);
         if (lhs > rhs) {
             const uint64_t u = act->id[i] < nd->id ? act->id[i] : nd->id;
             const uint64_t v = act->id[i] < nd->id ? nd->id : act->id[i];
@@ -907,6 +956,8 @@ static void global_unit_rows(unit_job* j) {
             ++j->gst.comps;
             const double lhs = P->cs[i] * P->cs[k] + P->sn[i] * P->sn[k];
             const double rhs = P->coth[i] * P->coth[k] - cosh_R * P->inv[i] * P->inv[k];
+            if (g_bd.on)
+                border_check(i, k, lhs, rhs, P->coth[i] * P->coth[k], cosh_R * P->inv[i] * P->inv[k], lhs > rhs);
             if (lhs > rhs) {
                 ++j->gst.edges;
                 j->gst.fp += i + k;
@@ -1076,6 +1127,44 @@ int orc_generate_stats_shard(uint64_t n, double alpha, double C, uint64_t seed, 
     pts_t P = {buf, NULL, buf + n, buf + 2 * n, buf + 3 * n, buf + 4 * n, buf + 5 * n, buf + 6 * n};
     draw_all(&L, &P, threads);
     rc = run_units_shard(&L, &P, threads, out, NULL, rank, world);
+    free(buf);
+    layout_free(&L);
+    out->seconds = now_s() - t0;
+    return rc;
+}
+
+/* Threshold-borderline audit of shard (rank, world): see rhg_oracle.h.  Not re-entrant. */
+int orc_borderline(uint64_t n, double alpha, double C, uint64_t seed, uint32_t chunks, uint32_t rank, uint32_t world,
+                   uint32_t threads, double band, uint64_t cap, orc_border* out, uint64_t* u, uint64_t* v,
+                   double* d_minus_R, uint8_t* ref_edge) {
+    if (world < 1 || rank >= world) return fail(ORC_INVALID_ARGUMENT, "shard: rank must lie in [0, world)");
+    const double t0 = now_s();
+    layout_t L;
+    int rc = make_layout(&L, n, alpha, C, seed, chunks);
+    if (rc) {
+        layout_free(&L);
+        return rc;
+    }
+    double* buf = malloc(8 * n * sizeof(double));
+    if (!buf) {
+        layout_free(&L);
+        return fail(ORC_NOMEM, "oracle: out of memory");
+    }
+    pts_t P = {buf, buf + 7 * n, buf + n, buf + 2 * n, buf + 3 * n, buf + 4 * n, buf + 5 * n, buf + 6 * n};
+    draw_all(&L, &P, threads);
+    memset(&g_bd, 0, sizeof g_bd);
+    pthread_mutex_init(&g_bd.mu, NULL);
+    g_bd.band = band, g_bd.r = P.r, g_bd.theta = P.theta, g_bd.R = L.R, g_bd.coshR = coshq((__float128)L.R);
+    g_bd.cap = cap, g_bd.u = u, g_bd.v = v, g_bd.dmr = d_minus_R, g_bd.dec = ref_edge;
+    g_bd.on = 1;
+    orc_stats st;
+    rc = run_units_shard(&L, &P, threads, &st, NULL, rank, world);
+    g_bd.on = 0;
+    memset(out, 0, sizeof *out);
+    out->comps = st.comps, out->edges = st.edges;
+    out->band_pairs = g_bd.band_pairs, out->flips_to_edge = g_bd.to_edge, out->flips_to_nonedge = g_bd.to_nonedge;
+    out->border_pairs = g_bd.border, out->listed = g_bd.listed, out->max_flip_dmr = g_bd.max_flip_dmr;
+    pthread_mutex_destroy(&g_bd.mu);
     free(buf);
     layout_free(&L);
     out->seconds = now_s() - t0;

@@ -79,6 +79,26 @@ int orc_generate_stats_shard(uint64_t n, double alpha, double C, uint64_t seed, 
 int orc_comps_matrix(uint64_t n, double alpha, double C, uint64_t seed, uint32_t chunks, uint32_t threads,
                      uint64_t* mat);
 
+/* Threshold-borderline audit of one engine shard (north_star): every pair the
+ * reference tests whose predicate value |lhs - rhs| lies within band x (its terms' magnitude)
+ * -- the only pairs whose decision FP64 rounding can flip -- is re-decided with the exact
+ * distance test d < R of geometry.hpp:117-123 evaluated in binary128 from (r, theta).
+ * flips_* count decisions that differ (informational: the reference's own rounding);
+ * border_pairs those with |d - R| < 1e-12, listed (u, v, d - R, reference decision) up to cap. */
+typedef struct {
+    uint64_t comps, edges;
+    uint64_t band_pairs;       /* pairs re-decided in binary128                          */
+    uint64_t flips_to_edge;    /* binary128: edge, reference predicate: no edge          */
+    uint64_t flips_to_nonedge; /* binary128: no edge, reference predicate: edge          */
+    uint64_t border_pairs;     /* |d - R| < 1e-12 (binary128)                            */
+    uint64_t listed;
+    double max_flip_dmr;       /* largest |d - R| among the flipped pairs                */
+    double seconds;
+} orc_border;
+int orc_borderline(uint64_t n, double alpha, double C, uint64_t seed, uint32_t chunks, uint32_t rank, uint32_t world,
+                   uint32_t threads, double band, uint64_t cap, orc_border* out, uint64_t* u, uint64_t* v,
+                   double* d_minus_R, uint8_t* ref_edge);
+
 /* The HOST glibc routines the reference calls, elementwise (the checker of
  * rhg_libm_eval): fn 0 exp, 1 log, 2 log1p, 3 acosh, 4 acos, 5 pow(x, y),
  * 6 / 7 sin / cos from one sincos call (what gcc -O3 makes of sweep.hpp:138-139). */

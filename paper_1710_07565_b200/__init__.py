@@ -27,7 +27,7 @@ from ._native import RHG_OK, RhgCudaError, check, lib
 
 __all__ = ["alpha_from_gamma", "gamma_from_alpha", "radial_const_from_avg_degree", "radius_from_size",
            "expected_avg_degree", "ModelParams", "AnnulusLayout", "make_layout", "GenOptions", "ChunkStats", "RunStats", "generate_stats",
-           "sample_points", "sample_uniforms", "fp64_peak", "count_edges_from_points", "Points", "RhgCudaError", "two_pi", "libm_eval", "LIBM_FUNCTIONS", "nccl_unique_id", "attach_comm", "shard_extent", "ShardExtent"]
+           "sample_points", "sample_uniforms", "fp64_peak", "count_edges_from_points", "Points", "RhgCudaError", "two_pi", "libm_eval", "LIBM_FUNCTIONS", "nccl_unique_id", "attach_comm", "shard_extent", "ShardExtent", "audit_predicate"]
 
 two_pi = 6.283185307179586476925286766559  # geometry.hpp:11
 
@@ -263,6 +263,18 @@ def generate_stats(params: ModelParams, opts: GenOptions = GenOptions(), degrees
     out = RunStats._from_c(st)
     out.degrees = deg
     return out
+
+
+def audit_predicate(params: ModelParams, opts: GenOptions = GenOptions()):
+    """Predicate audit (rhg_audit_predicate): one generate_stats in which the slab join also
+    evaluates the reference predicate (sweep.hpp:531-533) for every pair its FP32 pre-filter
+    decided.  Returns (report dict, RunStats); report["disagreements"] must be 0."""
+    rep = _native.rhg_audit_report()
+    st = _native.rhg_run_stats()
+    with _Context.use(opts) as ctx:
+        check(lib().rhg_audit_predicate(ctx, C.byref(params._c()), C.byref(_shard(opts)), C.byref(rep),
+                                        C.byref(st)))
+    return {f: getattr(rep, f) for f, _ in _native.rhg_audit_report._fields_}, RunStats._from_c(st)
 
 
 def nccl_unique_id() -> bytes:

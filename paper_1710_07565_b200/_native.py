@@ -36,6 +36,12 @@ class rhg_run_stats(C.Structure):
                 ("annulus_vertices", C.c_uint64 * 64), ("reduced_world", C.c_uint32), ("pad2_", C.c_uint32)]
 
 
+class rhg_audit_report(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("slab_pairs", "prefilter_decided", "exact_recheck", "exact_only",
+                                          "disagreements", "noise_band_pairs", "exact_engine_pairs")] + [
+        ("max_err_over_tau", C.c_double)]
+
+
 class rhg_shard_info(C.Structure):
     _fields_ = [("chunk_begin", C.c_uint32), ("chunk_end", C.c_uint32), ("owned_points", C.c_uint64),
                 ("halo_points", C.c_uint64), ("global_points", C.c_uint64), ("sampled_points", C.c_uint64),
@@ -60,7 +66,7 @@ EXPORTS = ["rhg_last_error", "rhg_abi_version", "rhg_alpha_from_gamma", "rhg_rad
            "rhg_fp64_peak", "rhg_generate_edges", "rhg_edges_from_points", "rhg_write_edges_text", "rhg_write_edges_binary",
            "rhg_read_edges_binary", "rhg_io_last_error", "rhg_naive_edges", "rhg_powerlaw_mle", "rhg_layout",
            "rhg_libm_eval", "rhg_create_multi", "rhg_context_devices", "rhg_nccl_unique_id", "rhg_attach_comm",
-           "rhg_shard_extent"]
+           "rhg_shard_extent", "rhg_audit_predicate"]
 
 _lib = None
 
@@ -110,6 +116,8 @@ def lib():
     L.rhg_context_devices.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
     L.rhg_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
     L.rhg_attach_comm.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint8)]
+    L.rhg_audit_predicate.argtypes = [C.c_void_p, C.POINTER(rhg_params), C.POINTER(rhg_shard),
+                                      C.POINTER(rhg_audit_report), C.POINTER(rhg_run_stats)]
     L.rhg_shard_extent.argtypes = [C.POINTER(rhg_params), C.POINTER(rhg_shard), C.POINTER(rhg_shard_info)]
     _lib = L
     return L

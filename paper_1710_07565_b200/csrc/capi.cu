@@ -165,7 +165,8 @@ struct rhg_ctx {
     DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, tables2, cells, counters, degrees, dbg, nid;
     DevBuf       lcells, s_beta, s_hw, s_lt, s_rec1, s_rec2, gsort, gbuf;
     DevBuf       ebuf, ecount, ekeys, esort; // materialised edges (rhg_generate_edges)
-    DevBuf       lam_tmp;
+    DevBuf       lam_tmp, audit;
+    bool         audit_on = false;            // rhg_audit_predicate in progress
     HostPinned   staging, staging2, readback; // table parts 1 and 2, counter readback
     // multi-GPU: a communicator over `comm_world` ranks (this context = rank comm_rank); shard
     // calls with shard {comm_rank, comm_world} all-reduce their counters through it
@@ -460,6 +461,7 @@ void plan_edges(Plan& pl) {
         pl.slab_prefix[j + 1]   = pl.slab_prefix[j] + (own + kSlabNodes - 1) / kSlabNodes;
     }
     pl.n_slabs = pl.slab_prefix[K];
+
     { // slabs in angular order across targets (requests are re-read from L2 by the next target's
       // slab), wave-1 targets first: a counting sort on (wave, angle bucket) - the order only
       // shapes cache locality
@@ -742,6 +744,11 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         CK(cudaMemsetAsync(ctx->dbg.p, 0, kDbgSlots * sizeof(unsigned long long), ctx->stream));
         e.dbg = ctx->dbg.as<unsigned long long>();
     }
+    if (ctx->audit_on) { // rhg_audit_predicate: the slab join runs its MODE 3 instance
+        ctx->audit.ensure(kAuditSlots * sizeof(unsigned long long));
+        CK(cudaMemsetAsync(ctx->audit.p, 0, kAuditSlots * sizeof(unsigned long long), ctx->stream));
+        e.audit = ctx->audit.as<unsigned long long>();
+    }
     e.ann_blk = t.ann_blk;
     e.gen = gen ? 1 : 0;
     e.mark = timeline_of(ctx);
@@ -1021,7 +1028,7 @@ void rhg_destroy(rhg_ctx* c) {
     cudaStreamSynchronize(c->side);
     for (DevBuf* b: {&c->beta, &c->hw, &c->rec0, &c->rec1, &c->rec2, &c->r_out, &c->beta_raw, &c->tables, &c->cells,
                      &c->counters, &c->degrees, &c->dbg, &c->nid, &c->lcells, &c->s_beta,
-                     &c->s_hw, &c->s_lt, &c->s_rec1, &c->s_rec2, &c->gsort, &c->gbuf, &c->tables2, &c->lam_tmp,
+                     &c->s_hw, &c->s_lt, &c->s_rec1, &c->s_rec2, &c->gsort, &c->gbuf, &c->tables2, &c->lam_tmp, &c->audit,
                      &c->ebuf, &c->ecount, &c->ekeys, &c->esort})
         b->release();
     if (c->comm) nccl_api().comm_destroy(c->comm);
@@ -1148,6 +1155,32 @@ void deliver_edges(rhg_ctx* ctx, const rhg_params* params, const EdgeSink& sink,
     CK(cudaStreamSynchronize(ctx->stream));
 }
 } // namespace
+
+int rhg_audit_predicate(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, rhg_audit_report* out,
+                        rhg_run_stats* stats) {
+    ctx = primary(ctx);
+    return guarded([&] {
+        if (!ctx || !out || !stats) throw InvalidArgument("rhg_audit_predicate: null argument");
+        struct Reset {
+            rhg_ctx* c;
+            ~Reset() { c->audit_on = false; }
+        } reset{ctx};
+        ctx->audit_on = true;
+        generate_impl(ctx, params, shard, stats, nullptr, nullptr);
+        unsigned long long h[kAuditSlots];
+        CK(cudaMemcpy(h, ctx->audit.p, sizeof h, cudaMemcpyDeviceToHost));
+        std::memset(out, 0, sizeof *out);
+        out->prefilter_decided = h[0], out->exact_recheck = h[1], out->exact_only = h[2];
+        out->disagreements = h[3];
+        float ratio = 0.0f;
+        const std::uint32_t bits = std::uint32_t(h[4]);
+        std::memcpy(&ratio, &bits, 4);
+        out->max_err_over_tau = ratio;
+        out->noise_band_pairs = h[5];
+        out->slab_pairs = h[0] + h[1] + h[2];
+        out->exact_engine_pairs = stats->comps - out->slab_pairs;
+    });
+}
 
 int rhg_generate_edges(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, rhg_run_stats* out,
                        std::uint64_t* edges, std::uint64_t cap, std::uint64_t* n_edges) {

@@ -562,6 +562,8 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     SlabRow64* const    rows64  = S.rows64[warp];
     std::uint32_t       acc_e = 0, acc_c = 0; // per-thread totals of one slab fit 32 bits
     unsigned long long  acc_fp = 0;
+    unsigned long long  au_decided = 0, au_recheck = 0, au_exact = 0, au_disagree = 0, au_noise = 0; // MODE 3
+    float               au_ratio = 0.0f;
     int ri = 0; // run of group gi: last ri with run_g[ri] <= gi (gi only grows)
     for (std::uint32_t gi = warp; gi < ngroups; gi += kSlabThreads / 32) {
         while (S.run_g[ri + 1] <= gi) ++ri;
@@ -673,7 +675,22 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                     const float         D  = P - M;
                     const float         tau = fmaf(fabsf(df), q.w, fmaf(P + M, 1.4e-6f, __uint_as_float(u.x)));
                     bool                e  = D > 0.0f;
-                    if (!(fabsf(D) > tau) || fabsf(df) > kPreMaxDelta) { // near the threshold: exact FP64
+                    const bool          undecided = !(fabsf(D) > tau) || fabsf(df) > kPreMaxDelta;
+                    if constexpr (MODE == 3) { // audit: every pre-filter decision against the reference predicate
+                        const SlabRow64& R   = rows64[o];
+                        const double2    n1  = node_r1(k), n2 = node_r2(k);
+                        const double     lhs = fadd(fmul(R.cs, n1.x), fmul(R.sn, n1.y));
+                        const double     rhs = fsub(fmul(R.coth, n2.x), fmul(R.rci, n2.y));
+                        const double     d64 = fsub(lhs, rhs);
+                        if (undecided) ++au_recheck;
+                        else {
+                            ++au_decided;
+                            au_disagree += e != (lhs > rhs);
+                            au_ratio = fmaxf(au_ratio, float(fabs(double(D) - d64)) / tau);
+                        }
+                        au_noise += fabs(d64) < 1e-15;
+                    }
+                    if (undecided) { // near the threshold: exact FP64
                         const SlabRow64& R = rows64[o];
                         e = edge_test(R.cs, R.sn, R.coth, R.rci, node_r1(k), node_r2(k));
                         if (A.dbg) atomicAdd(&A.dbg[17], 1ull);
@@ -697,6 +714,12 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                         q0 = r64[2 * o], q1 = r64[2 * o + 1], u = ru[2 * o + 1];
                     }
                     const std::uint32_t k = u.z + t;
+                    if constexpr (MODE == 3) {
+                        const double2 n1 = node_r1(k), n2 = node_r2(k);
+                        ++au_exact;
+                        au_noise += fabs(fsub(fadd(fmul(q0.x, n1.x), fmul(q0.y, n1.y)),
+                                              fsub(fmul(q1.x, n2.x), fmul(q1.y, n2.y)))) < 1e-15;
+                    }
                     if (edge_test(q0.x, q0.y, q1.x, q1.y, node_r1(k), node_r2(k))) {
                         const std::uint32_t nid = __float_as_uint(S.nd[k].w);
                         sum += nid + u.y, ++cnt;
@@ -715,7 +738,15 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     }
     Acc acc;
     acc.edges = acc_e, acc.comps = acc_c, acc.fp = acc_fp;
-    flush<MODE != 0>(acc, A, 0, lane, j);
+    flush<MODE == 1 || MODE == 2>(acc, A, 0, lane, j);
+    if constexpr (MODE == 3) {
+        if (au_decided) atomicAdd(&A.audit[0], au_decided);
+        if (au_recheck) atomicAdd(&A.audit[1], au_recheck);
+        if (au_exact) atomicAdd(&A.audit[2], au_exact);
+        if (au_disagree) atomicAdd(&A.audit[3], au_disagree);
+        if (au_ratio > 0.0f) atomicMax(&A.audit[4], static_cast<unsigned long long>(__float_as_uint(au_ratio)));
+        if (au_noise) atomicAdd(&A.audit[5], au_noise);
+    }
 }
 
 // Pairs the slab join leaves out: halo requests (Foreign replica) x owned
@@ -1555,9 +1586,11 @@ void launch_slab(const EdgeArgs& a, unsigned n, int mode, cudaStream_t st) {
         cudaFuncSetAttribute(slab_kernel<0, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(slab_kernel<1, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(slab_kernel<2, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(slab_kernel<3, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    if (mode == 2) slab_kernel<2, NT, MINB><<<n, NT, smem, st>>>(a);
+    if (mode == 3) slab_kernel<3, NT, MINB><<<n, NT, smem, st>>>(a);
+    else if (mode == 2) slab_kernel<2, NT, MINB><<<n, NT, smem, st>>>(a);
     else if (mode == 1) slab_kernel<1, NT, MINB><<<n, NT, smem, st>>>(a);
     else slab_kernel<0, NT, MINB><<<n, NT, smem, st>>>(a);
 }
@@ -1595,9 +1628,10 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         // memory, so 31.5 KB of shared memory per CTA): measured best at cfg2 (x4 with the node
         // doubles staged, 64 registers: 3.96 -> 3.80 ms/step; x5 3.87; x7 4.13, spills), also
         // cfg3 / cfg4 (-1.6% / -3.4%); RHG_SLAB_CFG selects the others for A/B runs
-        if (scfg == 4) launch_slab<256, 4>(a, n, mode, st);
-        else if (scfg == 1) launch_slab<128, 8>(a, n, mode, st);
-        else launch_slab<256, 6>(a, n, mode, st);
+        const int smode = a.audit ? 3 : mode; // the predicate audit instruments the sparse engine's pre-filter
+        if (scfg == 4) launch_slab<256, 4>(a, n, smode, st);
+        else if (scfg == 1) launch_slab<128, 8>(a, n, smode, st);
+        else launch_slab<256, 6>(a, n, smode, st);
         ++*launches;
         if (W.tail && a.n_tail) {
             RHG_LAUNCH_MODE(tail_kernel, mode, RHG_CFG(unsigned((a.n_tail + 255) / 256), 256, 0, st), a);

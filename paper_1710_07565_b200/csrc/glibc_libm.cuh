@@ -422,6 +422,7 @@ GL_FN double acos_table(double x, int32_t m, int n, int deg) {
     const double ax = (m > 0) ? x : gNeg(x);
     const double xx = gS(ax, tab_d(gl_asncs_tab, n));
     double p = tab_d(gl_asncs_tab, n + deg + 1);
+#pragma unroll 1
     for (int j = deg; j >= 2; --j) p = gF(xx, p, tab_d(gl_asncs_tab, n + j));
     p = gF(gM(xx, xx), p, tab_d(gl_asncs_tab, n + deg + 2));
     const double t = gF(xx, tab_d(gl_asncs_tab, n + 1), p);
@@ -446,12 +447,16 @@ GL_FN double gl_acos(double x) {
         const double cor = gF(-p, gM(x, x2), cor0);
         return gA(r, cor);
     }
-    if (k < 0x3fd00000) return acos_table(x, m, 11 * ((k & 0x000fffff) >> 15), 5);
-    if (k < 0x3fe00000) return acos_table(x, m, 11 * ((k & 0x000fffff) >> 14) + 352, 5);
-    if (k < 0x3fe80000) return acos_table(x, m, 12 * ((k >> 13) & 0x7f) + 1056, 6);
-    if (k < 0x3fed8000) return acos_table(x, m, 13 * ((k >> 13) & 0x7f) + 992, 7);
-    if (k < 0x3fee8000) return acos_table(x, m, 14 * ((k >> 13) & 0x7f) + 884, 8);
-    if (k < 0x3fef0000) return acos_table(x, m, 15 * ((k >> 13) & 0x7f) + 768, 9);
+    if (k < 0x3fef0000) { // one table evaluation, record base n and degree by interval
+        int n, deg;
+        if (k < 0x3fd00000) n = 11 * ((k & 0x000fffff) >> 15), deg = 5;
+        else if (k < 0x3fe00000) n = 11 * ((k & 0x000fffff) >> 14) + 352, deg = 5;
+        else if (k < 0x3fe80000) n = 12 * ((k >> 13) & 0x7f) + 1056, deg = 6;
+        else if (k < 0x3fed8000) n = 13 * ((k >> 13) & 0x7f) + 992, deg = 7;
+        else if (k < 0x3fee8000) n = 14 * ((k >> 13) & 0x7f) + 884, deg = 8;
+        else n = 15 * ((k >> 13) & 0x7f) + 768, deg = 9;
+        return acos_table(x, m, n, deg);
+    }
     if (k < 0x3ff00000) {                                             // 0.96875 <= |x| < 1
         const double z = gM((m > 0) ? gS(1.0, x) : gA(x, 1.0), 0.5);
         const uint64_t v = asu(z);

@@ -128,6 +128,7 @@ struct EdgeArgs {
     unsigned long long  edge_cap = 0;
     unsigned long long* edge_count = nullptr; // device counter of emitted edges (may exceed edge_cap)
     unsigned long long* dbg = nullptr; // optional path statistics (RHG_DEBUG_STATS=1), kDbgSlots entries
+    unsigned long long* audit = nullptr; // predicate audit (rhg_audit_predicate): kAuditSlots entries
     unsigned int*     degrees = nullptr;
 };
 
@@ -161,6 +162,11 @@ constexpr int kAnnSlots  = 64;  // spread per-annulus counter slots (folded by r
 constexpr int kTileNodes = 128; // owned nodes per dense-engine node tile (edges.cu glob_tiles_kernel; 64: 0.64 vs 0.58 ms)
 constexpr int kSlabNodes = 512; // owned nodes per slab of the slab join (edges.cu)
 constexpr int kMaxCls = 1024; // (source, radial class) segments of the dense-engine requests
+// audit layout (slab_kernel MODE 3): [0] pairs the FP32 pre-filter decided, [1] pairs it left to
+// the exact recheck, [2] pairs of exact-only groups, [3] pre-filter decisions that differ from the
+// reference predicate, [4] max |D32 - D64| / tau over decided pairs (float bits), [5] pairs with
+// |D64| below 1e-15 (the rounding-noise band of the reference predicate)
+constexpr int kAuditSlots = 8;
 // dbg layout (RHG_DEBUG_STATS=1): [0] stream (warp, target) steps, [1] staged unions, [2] per-lane
 // searches, [3] long rows, [4] flattened pairs, [5] serial pairs, [8] dense candidates loaded,
 // [9] dense (request, tile) pieces evaluated, [10] dense warps

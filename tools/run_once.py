@@ -20,4 +20,4 @@ for _ in range(reps):
     st = rhg.generate_stats(p)
 print(json.dumps({"edges": st.total.edges, "fp": st.total.fingerprint, "comps": st.total.comps,
                   "device_ms": st.device_ms, "sample_ms": st.sample_ms, "edges_ms": st.edges_ms,
-                  "launches": st.kernel_launches}))
+                  "pairs_ms": st.pairs_ms, "stream_comps": st.stream_comps, "launches": st.kernel_launches}))
