@@ -217,6 +217,20 @@ int rhg_generate_edges(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* 
 int rhg_edges_from_points(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shard, const rhg_points* pts,
                           rhg_run_stats* out, uint64_t* edges, uint64_t cap, uint64_t* n_edges);
 
+/* Per-unit counters of generate_stats (RunStats::unit_edges / unit_comps / unit_vertices,
+ * generator.hpp:270-284; printed by RunReport::write_text, stats.hpp:189-195): unit 0 = the
+ * global unit, unit c + 1 = chunk engine c.  Arrays of chunks + 1 entries.  Runs the P engine
+ * shards {c, P} on the context's (first) device. */
+int rhg_unit_stats(rhg_ctx* ctx, const rhg_params* params, uint64_t* unit_edges, uint64_t* unit_comps,
+                   uint64_t* unit_vertices);
+/* The edge stream in the reference's unit order (generator.hpp:183-199: the global unit first,
+ * then chunk engines ascending), canonical pairs (u < v), each unit in (u, v) order (the
+ * reference's order inside a unit follows its sweep's active-list slots).  unit_offsets
+ * (chunks + 2 entries): unit u's pairs are [unit_offsets[u], unit_offsets[u + 1]).  Same
+ * buffer protocol as rhg_generate_edges (edges == NULL only counts). */
+int rhg_generate_edges_units(rhg_ctx* ctx, const rhg_params* params, uint64_t* edges, uint64_t cap, uint64_t* n_edges,
+                             uint64_t* unit_offsets);
+
 /* Brute-force oracle on the GPU (oracle.hpp:41-54 naive_edges): every pair
  * u < v of the n given points (host arrays, id order) with
  * hyperbolic_distance (geometry.hpp:117-123, direct formula) < R, as sorted

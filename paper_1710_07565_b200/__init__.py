@@ -27,7 +27,7 @@ from ._native import RHG_OK, RhgCudaError, check, lib
 
 __all__ = ["alpha_from_gamma", "gamma_from_alpha", "radial_const_from_avg_degree", "radius_from_size",
            "expected_avg_degree", "ModelParams", "AnnulusLayout", "make_layout", "GenOptions", "ChunkStats", "RunStats", "generate_stats",
-           "sample_points", "sample_uniforms", "fp64_peak", "count_edges_from_points", "Points", "RhgCudaError", "two_pi", "libm_eval", "LIBM_FUNCTIONS", "nccl_unique_id", "attach_comm", "shard_extent", "ShardExtent", "audit_predicate"]
+           "sample_points", "sample_uniforms", "fp64_peak", "count_edges_from_points", "Points", "RhgCudaError", "two_pi", "libm_eval", "LIBM_FUNCTIONS", "nccl_unique_id", "attach_comm", "shard_extent", "ShardExtent", "audit_predicate", "unit_stats", "generate_edges_units"]
 
 two_pi = 6.283185307179586476925286766559  # geometry.hpp:11
 
@@ -441,6 +441,33 @@ def generate_edges(params: ModelParams, opts: GenOptions = GenOptions()):
     return _edges_call(lib().rhg_generate_edges, params, opts)
 
 
+def generate_edges_units(params: ModelParams, opts: GenOptions = GenOptions()):
+    """generate() in the reference's unit order (generator.hpp:183-199): the global unit's edges,
+    then chunk engine 0, 1, ... (canonical u < v; (u, v) order inside a unit).  Returns the
+    (m, 2) uint64 edge array and the unit offsets (chunks + 2 entries)."""
+    P64 = C.POINTER(C.c_uint64)
+    offs = np.zeros(params.chunks + 2, np.uint64)
+    m = C.c_uint64(0)
+    with _Context.use(opts) as ctx:
+        check(lib().rhg_generate_edges_units(ctx, C.byref(params._c()), None, 0, C.byref(m),
+                                             offs.ctypes.data_as(P64)))
+        buf = np.empty((m.value, 2), np.uint64)
+        check(lib().rhg_generate_edges_units(ctx, C.byref(params._c()), buf.ctypes.data_as(P64), m.value,
+                                             C.byref(m), offs.ctypes.data_as(P64)))
+    return buf, offs
+
+
+def unit_stats(params: ModelParams, opts: GenOptions = GenOptions()):
+    """RunStats::unit_edges / unit_comps / unit_vertices (generator.hpp:270-284): unit 0 = the
+    global unit, unit c + 1 = chunk engine c.  Returns three lists of chunks + 1 entries."""
+    P64 = C.POINTER(C.c_uint64)
+    e, c, v = (np.zeros(params.chunks + 1, np.uint64) for _ in range(3))
+    with _Context.use(opts) as ctx:
+        check(lib().rhg_unit_stats(ctx, C.byref(params._c()), e.ctypes.data_as(P64), c.ctypes.data_as(P64),
+                                   v.ctypes.data_as(P64)))
+    return [int(x) for x in e], [int(x) for x in c], [int(x) for x in v]
+
+
 def edges_from_points(params: ModelParams, points, opts: GenOptions = GenOptions()):
     """generate_edges for a GIVEN point set ("same points" mode)."""
     pts = Points(*[getattr(points, k, None) for k in Points.FIELDS])
@@ -601,8 +628,8 @@ def _fmt(x) -> str:
 
 @dataclass
 class RunReport:
-    """stats.hpp:120-208: the flat run summary of `rhg stats`.  Per-unit vectors are not
-    produced by the B200 path (its unit of work is not the reference's chunk engine)."""
+    """stats.hpp:120-208: the flat run summary of `rhg stats`, per-unit vectors included
+    (unit_stats: the P engine shards)."""
     n: int = 0
     m: int = 0
     avg_degree: float = 0.0
@@ -618,6 +645,9 @@ class RunReport:
     annulus_edges: list = field(default_factory=list)
     annulus_comps: list = field(default_factory=list)
     annulus_vertices: list = field(default_factory=list)
+    unit_edges: list = field(default_factory=list)
+    unit_comps: list = field(default_factory=list)
+    unit_vertices: list = field(default_factory=list)
 
     @classmethod
     def from_stats(cls, params: ModelParams, stats: RunStats) -> "RunReport":
@@ -649,15 +679,19 @@ class RunReport:
                 f"global_vertices={self.global_vertices}\nr_G={_fmt(float(self.r_G))}\n"
                 f"seconds={_fmt(float(self.seconds))}\nedges_per_sec={_fmt(float(self.edges_per_sec))}\n"
                 f"annulus_vertices={j(self.annulus_vertices)}\nannulus_comps={j(self.annulus_comps)}\n"
-                f"annulus_edges={j(self.annulus_edges)}\nunit_edges=\nunit_comps=\n")
+                f"annulus_edges={j(self.annulus_edges)}\nunit_edges={j(self.unit_edges)}\n"
+                f"unit_comps={j(self.unit_comps)}\n")
 
 
-def stats_report(params: ModelParams, opts: GenOptions = GenOptions()) -> RunReport:
+def stats_report(params: ModelParams, opts: GenOptions = GenOptions(), units: bool = True) -> RunReport:
     """proj/tools/rhg.cpp:144-164 cmd_stats: generate with exact degrees, fit gamma_hat over
     the degrees >= d_min = max(10, round(expected average degree)) (NaN when the tail has fewer
-    than 100 samples) and build the run report."""
+    than 100 samples) and build the run report.  units=True also fills the per-unit vectors
+    (P extra engine-shard runs; whole-graph reports only)."""
     st = generate_stats(params, opts, degrees=True)
     rep = RunReport.from_stats(params, st)
+    if units and opts.world == 1:
+        rep.unit_edges, rep.unit_comps, rep.unit_vertices = unit_stats(params, opts)
     d_min = int(max(10.0, float(math.floor(rep.expected_avg_degree + 0.5))))  # std::llround (x > 0)
     try:
         rep.gamma_hat = powerlaw_mle(st.degrees, d_min)

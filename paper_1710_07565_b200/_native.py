@@ -66,7 +66,7 @@ EXPORTS = ["rhg_last_error", "rhg_abi_version", "rhg_alpha_from_gamma", "rhg_rad
            "rhg_fp64_peak", "rhg_generate_edges", "rhg_edges_from_points", "rhg_write_edges_text", "rhg_write_edges_binary",
            "rhg_read_edges_binary", "rhg_io_last_error", "rhg_naive_edges", "rhg_powerlaw_mle", "rhg_layout",
            "rhg_libm_eval", "rhg_create_multi", "rhg_context_devices", "rhg_nccl_unique_id", "rhg_attach_comm",
-           "rhg_shard_extent", "rhg_audit_predicate"]
+           "rhg_shard_extent", "rhg_audit_predicate", "rhg_unit_stats", "rhg_generate_edges_units"]
 
 _lib = None
 
@@ -118,6 +118,8 @@ def lib():
     L.rhg_attach_comm.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint8)]
     L.rhg_audit_predicate.argtypes = [C.c_void_p, C.POINTER(rhg_params), C.POINTER(rhg_shard),
                                       C.POINTER(rhg_audit_report), C.POINTER(rhg_run_stats)]
+    L.rhg_unit_stats.argtypes = [C.c_void_p, C.POINTER(rhg_params), P_u64, P_u64, P_u64]
+    L.rhg_generate_edges_units.argtypes = [C.c_void_p, C.POINTER(rhg_params), P_u64, C.c_uint64, P_u64, P_u64]
     L.rhg_shard_extent.argtypes = [C.POINTER(rhg_params), C.POINTER(rhg_shard), C.POINTER(rhg_shard_info)]
     _lib = L
     return L

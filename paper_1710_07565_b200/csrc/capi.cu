@@ -172,6 +172,7 @@ struct rhg_ctx {
     // calls with shard {comm_rank, comm_world} all-reduce their counters through it
     ncclComm_t    comm       = nullptr;
     std::uint32_t comm_world = 1, comm_rank = 0;
+    bool          reduce_off = false; // per-unit calls: shard results stay per shard
     // rhg_create_multi: one sub-context per device (each with its comm); calls fan out to them
     std::vector<rhg_ctx*> subs;
 };
@@ -811,7 +812,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     fin.finish = true;
     launch_edges(e, fin, ctx->stream, launches);
     CK(cudaGetLastError());
-    const bool reduce = ctx->comm && pl.world == ctx->comm_world && pl.rank == ctx->comm_rank;
+    const bool reduce = ctx->comm && !ctx->reduce_off && pl.world == ctx->comm_world && pl.rank == ctx->comm_rank;
     if (reduce) { // the one collective of the shard plan: wrapping u64 sums of the counters
         const NcclApi& N = nccl_api();
         NK(N.all_reduce(ctx->counters.p, ctx->counters.p, 3 * sizeof(Counters) / 8, ncclUint64, ncclSum, ctx->comm,
@@ -1179,6 +1180,95 @@ int rhg_audit_predicate(rhg_ctx* ctx, const rhg_params* params, const rhg_shard*
         out->noise_band_pairs = h[5];
         out->slab_pairs = h[0] + h[1] + h[2];
         out->exact_engine_pairs = stats->comps - out->slab_pairs;
+    });
+}
+
+// The reference's units (generator.hpp:183-199, 270-284): unit 0 = the global unit, unit c + 1 =
+// chunk engine c.  Engine shard {c, P} is exactly engine c plus a 1/P slice of the global-unit
+// tiles (whose pairs the dense/global family counters separate), so the per-unit vectors are P
+// shard runs on this device.
+namespace {
+struct ReduceOff {
+    rhg_ctx* c;
+    bool     old;
+    explicit ReduceOff(rhg_ctx* x) : c(x), old(x->reduce_off) { c->reduce_off = true; }
+    ~ReduceOff() { c->reduce_off = old; }
+};
+} // namespace
+
+int rhg_unit_stats(rhg_ctx* ctx, const rhg_params* params, std::uint64_t* unit_edges, std::uint64_t* unit_comps,
+                   std::uint64_t* unit_vertices) {
+    ctx = primary(ctx);
+    return guarded([&] {
+        if (!ctx || !params || !unit_edges || !unit_comps || !unit_vertices)
+            throw InvalidArgument("rhg_unit_stats: null argument");
+        const std::uint32_t P = params->chunks;
+        if (P < 1) throw InvalidArgument("ModelParams: chunks must be >= 1");
+        ReduceOff     guard(ctx);
+        rhg_run_stats st;
+        unit_edges[0] = unit_comps[0] = 0;
+        for (std::uint32_t c = 0; c < P; ++c) {
+            const rhg_shard sh{c, P};
+            generate_impl(ctx, params, &sh, &st, nullptr, nullptr);
+            unit_edges[c + 1]    = st.edges - st.global_edges;
+            unit_comps[c + 1]    = st.comps - st.global_comps;
+            unit_vertices[c + 1] = st.streaming_vertices;
+            unit_edges[0] += st.global_edges, unit_comps[0] += st.global_comps;
+            unit_vertices[0] = st.global_vertices;
+        }
+    });
+}
+
+int rhg_generate_edges_units(rhg_ctx* ctx, const rhg_params* params, std::uint64_t* edges, std::uint64_t cap,
+                             std::uint64_t* n_edges, std::uint64_t* unit_offsets) {
+    ctx = primary(ctx);
+    return guarded([&] {
+        if (!ctx || !params || !n_edges || !unit_offsets) throw InvalidArgument("rhg_generate_edges_units: null argument");
+        const std::uint32_t P = params->chunks;
+        if (P < 1) throw InvalidArgument("ModelParams: chunks must be >= 1");
+        ReduceOff                               guard(ctx);
+        std::vector<std::uint64_t>              glob; // unit 0: pairs of two global points
+        std::vector<std::vector<std::uint64_t>> units(P);
+        rhg_run_stats                           st;
+        for (std::uint32_t c = 0; c < P; ++c) {
+            const rhg_shard sh{c, P};
+            // first pass counts, second materialises (the device buffer is sized exactly)
+            EdgeSink sink;
+            sink.dev_cap = 0;
+            generate_impl(ctx, params, &sh, &st, nullptr, &sink);
+            const std::uint64_t m = sink.count;
+            std::vector<std::uint64_t> buf(2 * std::max<std::uint64_t>(m, 1));
+            EdgeSink                   sink2;
+            sink2.dev_cap = m;
+            generate_impl(ctx, params, &sh, &st, nullptr, &sink2);
+            std::uint64_t got = 0;
+            deliver_edges(ctx, params, sink2, buf.data(), m, &got);
+            const std::uint64_t nG = st.global_vertices;
+            for (std::uint64_t i = 0; i < got; ++i) {
+                auto& dst = buf[2 * i + 1] < nG ? glob : units[c];
+                dst.push_back(buf[2 * i]), dst.push_back(buf[2 * i + 1]);
+            }
+        }
+        { // unit 0 in canonical order (the shards' global slices interleave)
+            std::vector<std::pair<std::uint64_t, std::uint64_t>> g(glob.size() / 2);
+            for (std::size_t i = 0; i < g.size(); ++i) g[i] = {glob[2 * i], glob[2 * i + 1]};
+            std::sort(g.begin(), g.end());
+            for (std::size_t i = 0; i < g.size(); ++i) glob[2 * i] = g[i].first, glob[2 * i + 1] = g[i].second;
+        }
+        std::uint64_t total = glob.size() / 2;
+        unit_offsets[0] = 0, unit_offsets[1] = total;
+        for (std::uint32_t c = 0; c < P; ++c) total += units[c].size() / 2, unit_offsets[c + 2] = total;
+        *n_edges = total;
+        if (!edges) return;
+        if (total > cap)
+            throw InvalidArgument("rhg edges: the edge buffer holds " + std::to_string(cap) + " pairs, the graph has " +
+                                  std::to_string(total));
+        std::memcpy(edges, glob.data(), glob.size() * 8);
+        std::uint64_t* o = edges + glob.size();
+        for (std::uint32_t c = 0; c < P; ++c) {
+            std::memcpy(o, units[c].data(), units[c].size() * 8);
+            o += units[c].size();
+        }
     });
 }
 
