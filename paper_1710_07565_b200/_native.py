@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librhg_b200.so")
+# RHG_LIB_PATH: an alternative build of the same library (A/B timing experiments only)
+LIB_PATH = os.environ.get("RHG_LIB_PATH") or os.path.join(HERE, "librhg_b200.so")
 
 RHG_OK, RHG_INVALID_ARGUMENT, RHG_INVARIANT, RHG_CUDA, RHG_NOMEM = range(5)
 

@@ -442,6 +442,10 @@ __device__ __forceinline__ std::uint32_t slab_lb(const SM& S, double x, double o
 // |D32| > tau does the FP32 sign decide; otherwise (and for |Delta| > 2^-6, where
 // the truncated series is not used) the pair takes the exact FP64 predicate.
 constexpr float  kPreMaxDelta = 0.015625f;
+#ifndef RHG_SLAB_DIRECT
+#define RHG_SLAB_DIRECT 8 // groups whose lanes have <= this many pairs each skip the flattening (measured 0 / 2 / 4 / 8 / 16 / 32: cfg4 slab 19.2 / 18.8 / 18.4 / 18.2 / 18.5 / 18.8 ms, cfg2 1.58 / 1.57 / 1.55 / 1.55 / 1.56 / 1.58)
+#endif
+constexpr int kSlabDirect = RHG_SLAB_DIRECT;
 constexpr double kPreMinS     = 4e-14; // groups whose windows give S below this skip the pre-filter
 
 struct __align__(16) SlabRow32 { // one request with pairs in the slab (rows of a group are compacted)
@@ -611,6 +615,47 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                     atomicAdd(&A.dbg[12], (unsigned long long)__popc(nz)), atomicAdd(&A.dbg[own ? 15 : 16], 1ull);
         }
         if (nz == 0) continue;
+        // narrow windows (every lane <= kSlabDirect pairs): each lane tests its own pairs with
+        // its request in registers -- no prefix sum, row table or row search
+        if (MODE != 3 && !(A.ablate & 2) && __reduce_max_sync(kFull, len) <= std::uint32_t(kSlabDirect)) {
+            acc_c += len;
+            if (len) {
+                const double2            r1  = A.s_rec1[pc];
+                const double             rci = fmul(A.cosh_R, r2.y);
+                const unsigned long long idp = A.s_id[pc];
+                const std::uint64_t      base_j_ = base_j;
+                std::uint32_t            cnt = 0;
+                unsigned long long       sum = 0;
+                const float              lamf = float(fsub(lam, lam_first));
+                const float              ed   = 5.9604645e-8f * (fabsf(lamf) + span) + 1.5e-15f;
+                const float              qm = float(fsub(r2.x, 1.0)), qr = float(rci);
+                for (std::uint32_t k = l0; k < l1; ++k) {
+                    const float4 nd = S.nd[k];
+                    bool         e;
+                    if (fp64) e = edge_test(r1.x, r1.y, r2.x, rci, node_r1(k), node_r2(k));
+                    else {
+                        const float df  = nd.x - lamf;
+                        const float y2  = df * df;
+                        const float Sv  = y2 * fmaf(y2, -1.0f / 24.0f, 0.5f);
+                        const float P   = qr * nd.z;
+                        const float M   = fmaf(qm, nd.y, qm + nd.y) + Sv;
+                        const float D   = P - M;
+                        const float tau = fmaf(fabsf(df), 1.3f * ed + 3e-15f, fmaf(P + M, 1.4e-6f, 1.3f * ed * ed + 2e-15f));
+                        e = D > 0.0f;
+                        if (!(fabsf(D) > tau) || fabsf(df) > kPreMaxDelta)
+                            e = edge_test(r1.x, r1.y, r2.x, rci, node_r1(k), node_r2(k));
+                    }
+                    if (e) {
+                        const unsigned long long nid = base_j_ + __float_as_uint(nd.w);
+                        sum += nid + idp, ++cnt;
+                        if (MODE == 1) atomicAdd(&A.degrees[idp], 1u), atomicAdd(&A.degrees[nid], 1u);
+                        if (MODE == 2) emit_edge(A, idp, nid);
+                    }
+                }
+                acc_e += cnt, acc_fp += sum;
+            }
+            continue;
+        }
         // flattened pair list over the warp: pair t belongs to the row whose prefix covers it
         std::uint32_t incl = len;
 #pragma unroll
