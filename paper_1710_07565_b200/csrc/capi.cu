@@ -792,6 +792,12 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     d1.global_unit = true;
     EdgeWave s1; // wave 1 slab join (tail pairs too when there is no wave 2)
     s1.slab_begin = 0, s1.slab_end = split ? pl.n_slabs1 : pl.n_slabs;
+    // a wave is "exact" when the own-window bound of its largest target annulus lies below the
+    // pre-filter's FP64 floor (slab_kernel's kPreMinS = 4e-14 on S = h^2 / 2)
+    auto exact_wave = [&](std::uint32_t j) {
+        return j < K && j >= fs && pl.hbound[std::size_t(j) * K + j] < std::sqrt(2.0 * 4e-14);
+    };
+    s1.exact_slabs = exact_wave(jw - 1);
     s1.tail = !split, s1.ev0 = ctx->evw[0], s1.ev1 = ctx->evw[1];
     fork_to(ctx->stream, dst);
     launch_edges(e, d1, dst, launches);
@@ -803,6 +809,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         d2.j0 = int(jw), d2.j1 = int(K), d2.tile_warps = pl.gt_prefix[K] - pl.gt_prefix[jw];
         EdgeWave s2;
         s2.slab_begin = pl.n_slabs1, s2.slab_end = pl.n_slabs;
+        s2.exact_slabs = exact_wave(K - 1);
         s2.tail = true, s2.ev0 = ctx->evw[2], s2.ev1 = ctx->evw[3];
         launch_edges(e, d2, dst, launches);
         launch_edges(e, s2, ctx->stream, launches);

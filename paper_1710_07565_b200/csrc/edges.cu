@@ -417,12 +417,38 @@ __device__ __forceinline__ std::uint32_t slab_bucket(double x, double org, doubl
     return std::uint32_t(t);
 }
 template <class SM>
-__device__ __forceinline__ std::uint32_t slab_lb(const SM& S, double x, double org, double inv_w) {
+__device__ __forceinline__ std::uint32_t slab_lb(const SM& S, const double* lam, double x, double org, double inv_w) {
     const std::uint32_t b = slab_bucket(x, org, inv_w);
     std::uint32_t       k = S.bstart[b];
     const std::uint32_t e = S.bstart[b + 1];
-    while (k < e && S.lam[k] < x) ++k;
+    while (k < e && lam[k] < x) ++k;
     return k;
+}
+
+// ---- TMA bulk copies (cp.async.bulk global -> shared, completion on an mbarrier) ----
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+// bytes: a multiple of 16; src and dst 16-byte aligned
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, unsigned bytes, std::uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned phase) {
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n}"
+                 ::"r"(smem_addr(bar)), "r"(phase)
+                 : "memory");
 }
 
 // FP32 pre-filter of the reference predicate (sweep.hpp:531-533), exact by
@@ -473,7 +499,8 @@ struct SlabNodes64<false> {};
 template <int NT, bool R12 = true>
 struct SlabSmem : SlabNodes64<R12> {
     float4             nd[kSlab];         // (lambda - lam_first, coth - 1, 1 / sinh, id offset bits)
-    double             lam[kSlab];
+    double             lam[kSlab + 2];    // node lambdas from index `sh` (TMA needs 16-byte alignment)
+    std::uint64_t      bar;               // completion of the slab's bulk copies
     std::uint16_t      bstart[kSlab + 1]; // bucket b: first local node with bucket(lambda) >= b
     SlabRow32          rows[NT / 32][32];
     SlabRow64          rows64[NT / 32][32];
@@ -504,20 +531,44 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
         if constexpr (kR12) return S.r2[k];
         else return A.s_rec2[N0 + k];
     };
-    const double             lam_first = A.s_lam[N0];
-    const double             lam_last  = A.s_lam[N0 + m - 1];
-    // warp 0 finds the slab's request runs (cell-table lookups) while warps 1.. stage the nodes
+    // The slab's node data arrive by TMA bulk copies (one elected thread, completion on an
+    // mbarrier) into shared memory: lambda into its final place, (coth, 1/sinh) and ids into the
+    // group-row buffers (free until the groups start), the exact-path doubles (R12) into place.
+    // 8-byte arrays start at the even index N0 & ~1 (16-byte alignment): element i at [sh + i].
+    const std::uint32_t sh   = std::uint32_t(N0 & 1u);
+    const std::uint32_t n8   = (m + sh + 1u) & ~1u; // 8-byte elements copied (reads < s_lam + n_ext + 2)
+    double2* const      st_r2 = [&]() -> double2* {
+        if constexpr (kR12) return S.r2;
+        else return reinterpret_cast<double2*>(&S.rows[0][0]);
+    }();
+    unsigned long long* const st_id = reinterpret_cast<unsigned long long*>(&S.rows64[0][0]);
+    static_assert(sizeof(S.rows) >= kSlab * sizeof(double2) && sizeof(S.rows64) >= (kSlab + 2) * 8,
+                  "the row buffers hold the staged node records");
+    if (threadIdx.x == 0) {
+        mbar_init(&S.bar, 1);
+        const unsigned bytes = n8 * 8 * 2 + m * 16 * (kR12 ? 2 : 1);
+        mbar_expect_tx(&S.bar, bytes);
+        bulk_copy_g2s(S.lam, A.s_lam + (N0 - sh), n8 * 8, &S.bar);
+        bulk_copy_g2s(st_id, A.s_id + (N0 - sh), n8 * 8, &S.bar);
+        bulk_copy_g2s(st_r2, A.s_rec2 + N0, m * 16, &S.bar);
+        if constexpr (kR12) bulk_copy_g2s(&S.r1[0], A.s_rec1 + N0, m * 16, &S.bar);
+    }
+    const double* const slam      = S.lam + sh;
+    const double        lam_first = A.s_lam[N0];
+    const double        lam_last  = A.s_lam[N0 + m - 1];
+    // warp 0 finds the slab's request runs (cell-table lookups) while warps 1.. build the node
+    // records and bucket starts from the staged data
     const double inv_w = lam_last > lam_first ? double(kSlab - 1) / (lam_last - lam_first) : 0.0;
     const float  span  = float(fsub(lam_last, lam_first)) * 1.0001f;
-    if (warp != 0) { // staging + bucket starts (cell_fill pattern; the predecessor's lambda from L1)
+    __syncthreads(); // the mbarrier is initialised before anyone waits on it
+    if (warp != 0) { // node records + bucket starts (cell_fill pattern)
+        mbar_wait(&S.bar, 0);
         for (std::uint32_t i = threadIdx.x - 32; i < m; i += kSlabThreads - 32) {
-            const double  l  = A.s_lam[N0 + i];
-            const double  lp = i ? A.s_lam[N0 + i - 1] : 0.0;
-            const double2 r2 = A.s_rec2[N0 + i];
-            S.lam[i] = l;
-            if constexpr (kR12) S.r1[i] = A.s_rec1[N0 + i], S.r2[i] = r2;
+            const double  l  = slam[i];
+            const double  lp = i ? slam[i - 1] : 0.0;
+            const double2 r2 = st_r2[i];
             S.nd[i]  = make_float4(float(fsub(l, lam_first)), float(fsub(r2.x, 1.0)), float(r2.y),
-                                   __uint_as_float(std::uint32_t(A.s_id[N0 + i] - base_j)));
+                                   __uint_as_float(std::uint32_t(st_id[sh + i] - base_j)));
             const std::uint32_t b  = slab_bucket(l, lam_first, inv_w);
             const std::int32_t  bp = i ? std::int32_t(slab_bucket(lp, lam_first, inv_w)) : -1;
             for (std::int32_t c = bp + 1; c <= std::int32_t(b); ++c) S.bstart[c] = std::uint16_t(i);
@@ -594,7 +645,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
         }
         std::uint32_t l0 = 0, l1 = 0;
         if (valid && hi > lo && hi > lam_first && lo <= lam_last) {
-            l0 = slab_lb(S, lo, lam_first, inv_w), l1 = slab_lb(S, hi, lam_first, inv_w);
+            l0 = slab_lb(S, slam, lo, lam_first, inv_w), l1 = slab_lb(S, slam, hi, lam_first, inv_w);
             if (own) {
                 const std::uint32_t wl = std::uint32_t(Aa.wrap > N0 ? (Aa.wrap - N0 < m ? Aa.wrap - N0 : m) : 0);
                 if (p + 1 > N0 && l0 < std::uint32_t(p + 1 - N0)) l0 = std::uint32_t(p + 1 - N0 < m ? p + 1 - N0 : m);
@@ -1674,8 +1725,11 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         // doubles staged, 64 registers: 3.96 -> 3.80 ms/step; x5 3.87; x7 4.13, spills), also
         // cfg3 / cfg4 (-1.6% / -3.4%); RHG_SLAB_CFG selects the others for A/B runs
         const int smode = a.audit ? 3 : mode; // the predicate audit instruments the sparse engine's pre-filter
-        if (scfg == 4) launch_slab<256, 4>(a, n, smode, st);
-        else if (scfg == 1) launch_slab<128, 8>(a, n, smode, st);
+        // waves whose windows lie below the FP64 rounding floor of the pre-filter (outer annuli at
+        // R >~ 35: cfg4, cfg5) run the exact predicate on most pairs: 4 CTAs/SM with the node
+        // doubles staged by TMA (measured cfg4 slab 17.5 -> 16.6 ms, cfg5 86 -> 78; cfg2 / cfg3
+        // keep 6 CTAs/SM without them: 1.52 vs 1.55 ms, 8.22 vs 8.42 ms)
+        if (scfg == 4 || (scfg == 0 && W.exact_slabs)) launch_slab<256, 4>(a, n, smode, st);
         else launch_slab<256, 6>(a, n, smode, st);
         ++*launches;
         if (W.tail && a.n_tail) {

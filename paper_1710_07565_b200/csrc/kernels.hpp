@@ -140,6 +140,7 @@ struct EdgeWave {
     int           j0 = 0, j1 = 0;                 // target annuli of the dense rows / node tiles
     std::uint64_t tile_warps = 0;                 // gt_prefix[j1] - gt_prefix[j0]
     std::uint64_t slab_begin = 0, slab_end = 0;   // slab-join CTAs (slab_tab range)
+    bool          exact_slabs = false;            // the wave's slabs are mostly exact-predicate pairs
     bool          global_unit = false, tail = false, finish = false;
     cudaEvent_t   ev0 = nullptr, ev1 = nullptr;   // optional: time the wave's sparse engine
 };
