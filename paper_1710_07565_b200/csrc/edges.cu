@@ -1018,6 +1018,11 @@ __global__ void __launch_bounds__(1024) req_segments_kernel(EdgeArgs A) {
 // Bucket starts of every segment: gbk[bk_off[c] + b] = first sorted position
 // of segment c whose quantised angle falls in bucket >= b (cell_fill pattern;
 // the angles are the low 32 bits of the sort keys).
+// Pass 1, one thread per sorted request s: the bucket entries (b(s-1), b(s)] hold s when that
+// run is short (the common case for a whole graph); longer runs -- the head and tail of a
+// shard's segments, whose requests span 1/N of the circle, and the gap wrapped requests leave --
+// stay 0xffffffff for pass 2.
+constexpr std::int64_t kBucketRun = 32;
 __global__ void req_buckets_kernel(EdgeArgs A, const unsigned long long* keys) {
     const std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (s >= A.n_req) return;
@@ -1032,11 +1037,35 @@ __global__ void req_buckets_kernel(EdgeArgs A, const unsigned long long* keys) {
     std::uint32_t*      tab = A.gbk + A.bk_off[c];
     const std::int64_t  b   = std::int64_t(std::uint32_t(keys[s]) >> sh);
     const std::int64_t  bp  = s > A.cseg[c] ? std::int64_t(std::uint32_t(keys[s - 1]) >> sh) : -1;
-    for (std::int64_t k = bp + 1; k <= b; ++k) tab[k] = std::uint32_t(s);
+    if (b - bp <= kBucketRun)
+        for (std::int64_t k = bp + 1; k <= b; ++k) tab[k] = std::uint32_t(s);
     if (s + 1 == A.cseg[c + 1]) { // last of the segment: the tail buckets hold the segment end
         const std::int64_t nb = std::int64_t(1) << (32 - sh);
-        for (std::int64_t k = b + 1; k <= nb; ++k) tab[k] = std::uint32_t(s + 1);
+        if (nb - b <= kBucketRun)
+            for (std::int64_t k = b + 1; k <= nb; ++k) tab[k] = std::uint32_t(s + 1);
     }
+}
+// Pass 2, one thread per bucket entry: entries pass 1 left empty get the first position of
+// their segment whose key bucket is >= b (binary search; the last entry b = nb holds the end).
+__global__ void __launch_bounds__(256) req_bucket_runs_kernel(EdgeArgs A, const unsigned long long* keys) {
+    const int           ncls = *A.n_cls < kMaxCls ? *A.n_cls : kMaxCls;
+    const std::uint64_t g    = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (ncls <= 0 || g >= A.bk_off[ncls] || A.gbk[g] != 0xffffffffu) return;
+    int c = 0, hc = ncls - 1; // last segment with bk_off[c] <= g
+    while (c < hc) {
+        const int mid = (c + hc + 1) >> 1;
+        if (A.bk_off[mid] <= g) c = mid;
+        else hc = mid - 1;
+    }
+    const std::uint32_t sh = A.bk_shift[c];
+    const std::uint64_t b  = g - A.bk_off[c];
+    std::uint32_t       lo = A.cseg[c], hi = A.cseg[c + 1];
+    while (lo < hi) {
+        const std::uint32_t mid = (lo + hi) >> 1;
+        if (std::uint64_t(std::uint32_t(keys[mid]) >> sh) < b) lo = mid + 1;
+        else hi = mid;
+    }
+    A.gbk[g] = lo;
 }
 
 // Sorted copies of the dense-engine requests (one gather pass, so the rows
@@ -1658,10 +1687,13 @@ void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, 
                     st);
     req_marks_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kout);
     req_segments_kernel<<<1, 1024, 0, st>>>(a);
+    const std::size_t nbk = 2 * n + 65 * std::size_t(kMaxCls); // bound on the bucket entries
+    cudaMemsetAsync(a.gbk, 0xff, nbk * sizeof(std::uint32_t), st);
     req_buckets_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kout);
+    req_bucket_runs_kernel<<<unsigned((nbk + 255) / 256), 256, 0, st>>>(a, kout);
     a.gperm = perm;
     req_gather_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a);
-    *launches += 6;
+    *launches += 7;
     a.mark("dense_prep", st);
 }
 
