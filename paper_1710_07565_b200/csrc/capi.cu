@@ -240,6 +240,33 @@ struct Plan {
     double                  sub_ms[4] = {0, 0, 0, 0}; // RHG_TIMELINE: plan phases after the layout
 };
 
+// LSD radix sort of u64 keys on bits [lo_bit, 64), stable (keys equal there keep their order):
+// 16-bit digits, constant digits skipped.  std::sort of the 1.2e5 job keys at cfg4 took 10 ms.
+void radix_sort_keys(std::vector<std::uint64_t>& key, int lo_bit) {
+    if (key.size() < 8192) { // the digit histograms would cost more than the comparisons
+        std::stable_sort(key.begin(), key.end(), [lo_bit](std::uint64_t x, std::uint64_t y) {
+            return (x >> lo_bit) < (y >> lo_bit);
+        });
+        return;
+    }
+    std::vector<std::uint64_t> tmp(key.size());
+    std::vector<std::uint32_t> cnt(1u << 16);
+    for (int sh = lo_bit; sh < 64; sh += 16) {
+        const int           bits = std::min(16, 64 - sh);
+        const std::uint64_t mask = (std::uint64_t(1) << bits) - 1;
+        std::fill(cnt.begin(), cnt.begin() + (std::size_t(1) << bits), 0u);
+        for (std::uint64_t k: key) ++cnt[(k >> sh) & mask];
+        if (cnt[(key.empty() ? 0 : (key[0] >> sh) & mask)] == key.size()) continue; // one digit value
+        std::uint32_t run = 0;
+        for (std::size_t d = 0; d < (std::size_t(1) << bits); ++d) {
+            const std::uint32_t c = cnt[d];
+            cnt[d] = run, run += c;
+        }
+        for (std::uint64_t k: key) tmp[cnt[(k >> sh) & mask]++] = k;
+        key.swap(tmp);
+    }
+}
+
 // Expected number of annulus-j nodes in the window of an annulus-a request
 // at a's median radius (density ~ sinh(alpha r)); same-annulus windows count
 // half (dedup).  Only chooses the engine for (a, j); never affects results.
@@ -274,13 +301,21 @@ double half_width_bound(const Layout& L, std::uint32_t a, std::uint32_t j) {
 }
 
 Plan make_plan_head(const Params& P, const rhg_shard* shard) {
-    Plan       pl;
-    const auto tl0 = std::chrono::steady_clock::now();
-    pl.L           = make_layout(P);
-    pl.layout_ms   = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count();
-    const Layout&       L = pl.L;
+    Plan                pl;
+    const auto          tl0 = std::chrono::steady_clock::now();
     const std::uint32_t W = shard ? shard->world : 1, r = shard ? shard->rank : 0;
     if (W < 1 || r >= W) throw InvalidArgument("rhg_shard: rank must lie in [0, world)");
+    if (P.chunks < 1) throw InvalidArgument("ModelParams: chunk count must be >= 1");
+    {   // a shard's layout splits only its own streaming chunks and the halo chunk
+        const std::uint32_t e0 = std::uint32_t(std::uint64_t(P.chunks) * r / W);
+        const std::uint32_t e1 = std::uint32_t(std::uint64_t(P.chunks) * (r + 1) / W);
+        ChunkNeed           need;
+        if (e1 < P.chunks) need.lo[0] = e0, need.hi[0] = e1 + 1, need.n = 1;
+        else need.lo[0] = e0, need.hi[0] = P.chunks, need.lo[1] = 0, need.hi[1] = 1, need.n = 2;
+        pl.L = make_layout(P, W > 1 ? &need : nullptr);
+    }
+    pl.layout_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count();
+    const Layout&       L  = pl.L;
     const std::uint32_t Pc = L.chunks;
     pl.rank = r, pl.world = W;
     pl.e0 = std::uint32_t(std::uint64_t(Pc) * r / W);
@@ -377,7 +412,7 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
             key[k] = (std::uint64_t(w2) << 63) | ((((std::uint64_t(1) << 39) - 1) - c) << 24) | k;
             pl.wave2_jobs += w2;
         }
-        std::sort(key.begin(), key.end());
+        radix_sort_keys(key, 24); // the index bits are already in order: a stable sort of the rest
         pl.job_order.resize(key.size());
         for (std::uint32_t k = 0; k < key.size(); ++k) pl.job_order[k] = std::uint32_t(key[k] & 0xffffffu);
     }
@@ -393,8 +428,12 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
         const std::uint32_t j0 = wv ? std::uint32_t(pl.jobs.size() - pl.wave2_jobs) : 0;
         const std::uint32_t j1 = wv ? std::uint32_t(pl.jobs.size()) : std::uint32_t(pl.jobs.size() - pl.wave2_jobs);
         if (j1 <= j0) continue;
-        std::uint64_t sum = 0, mx = 0;
-        for (std::uint32_t k = j0; k < j1; ++k) sum += pl.jobs[pl.job_order[k]].count, mx = std::max(mx, pl.jobs[pl.job_order[k]].count);
+        std::vector<std::uint64_t> cnt(j1 - j0); // counts in job order (contiguous for the packing loop)
+        std::uint64_t              sum = 0, mx = 0;
+        for (std::uint32_t k = j0; k < j1; ++k) {
+            const std::uint64_t c = pl.jobs[pl.job_order[k]].count;
+            cnt[k - j0] = c, sum += c, mx = std::max(mx, c);
+        }
         const std::uint64_t nb = std::min<std::uint64_t>(j1 - j0, mx ? (sum + mx - 1) / mx + (sum + 7 * mx) / (8 * mx) : 1);
         // min-heap on (load, bin) in a flat array; bin ids per job, then a stable counting sort
         // (per-bin vectors cost more in allocations than the packing itself)
@@ -403,13 +442,22 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
         if (nb >= (1u << 24)) throw InvalidArgument("rhg: too many sampler streams");
         for (std::uint32_t b = 0; b < nb; ++b) heap[b] = b; // load 0
         std::vector<std::uint32_t> bin_of(j1 - j0), fill(nb + 1, 0);
-        for (std::uint32_t k = j0; k < j1; ++k) { // job_order is by descending count inside a wave
+        // many streams (large P): a boustrophedon deal of the descending job list (O(1) per job;
+        // the heap's LPT took 3.6 ms for the 1.2e5 streams of cfg4), else LPT
+        const bool snake = j1 - j0 > 16384;
+        for (std::uint32_t k = j0; snake && k < j1; ++k) {
+            const std::uint64_t q = (k - j0) % nb, pass = (k - j0) / nb;
+            const std::uint32_t b = std::uint32_t(pass & 1 ? nb - 1 - q : q);
+            bin_of[k - j0]        = b;
+            ++fill[b + 1];
+        }
+        for (std::uint32_t k = j0; !snake && k < j1; ++k) { // job_order is by descending count inside a wave
             const std::uint64_t top = heap[0];
             const std::uint32_t b   = std::uint32_t(top & 0xffffffu);
             bin_of[k - j0]          = b;
             ++fill[b + 1];
             // + per-stream pipeline fill / seeding
-            const std::uint64_t v = top + ((pl.jobs[pl.job_order[k]].count + 1250) << 24);
+            const std::uint64_t v = top + ((cnt[k - j0] + 1250) << 24);
             std::size_t         h = 0;
             for (;;) { // sift the grown root down
                 std::size_t c = 2 * h + 1;
@@ -1122,6 +1170,9 @@ int rhg_shard_extent(const rhg_params* params, const rhg_shard* shard, rhg_shard
     return guarded([&] {
         if (!out) throw InvalidArgument("rhg_shard_extent: out is null");
         const Plan pl = make_plan_head(to_params(params), shard);
+        if (const char* v = std::getenv("RHG_TIMELINE"); v && v[0] == '1')
+            std::fprintf(stderr, "RHG_HOST plan head: layout=%.3f jobs=%.3f bins=%.3f ms\n", pl.layout_ms, pl.sub_ms[0],
+                         pl.sub_ms[1]);
         std::memset(out, 0, sizeof *out);
         out->chunk_begin = pl.e0, out->chunk_end = pl.e1;
         for (std::uint32_t i = pl.L.first_streaming; i < pl.L.count; ++i) {

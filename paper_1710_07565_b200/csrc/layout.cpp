@@ -241,12 +241,35 @@ void split_chunk_range(std::uint64_t seed, std::uint32_t annulus, std::uint64_t 
         out[lo] = total;
         return;
     }
+    if (total == 0) { // binomial(0, p) = 0 for every node below: nothing to draw
+        for (std::uint32_t c = lo; c < hi; ++c) out[c] = 0;
+        return;
+    }
     const std::uint32_t mid = lo + (hi - lo + 1) / 2;
     const double        ml = double(mid - lo), mr = double(hi - mid);
     Mt64                s(derive_seed3(seed, kPhaseChunks, annulus, node));
     const std::uint64_t left = binomial(total, ml / (ml + mr), s); // rng.hpp:197-204
     split_chunk_range(seed, annulus, left, lo, mid, 2 * node, out);
     split_chunk_range(seed, annulus, total - left, mid, hi, 2 * node + 1, out);
+}
+
+// The same tree, descending only into subtrees that hold needed chunks; `before` is the number
+// of the annulus's points in chunks below lo, so base[c] is chunk c's offset in the annulus.
+void split_chunk_partial(std::uint64_t seed, std::uint32_t annulus, std::uint64_t total, std::uint32_t lo,
+                         std::uint32_t hi, std::uint64_t node, const ChunkNeed& need, std::uint64_t before,
+                         std::uint64_t* out, std::uint64_t* base) {
+    if (!need.meets(lo, hi)) return;
+    if (hi - lo == 1 || total == 0) {
+        for (std::uint32_t c = lo; c < hi; ++c)
+            if (need.has(c)) out[c] = c == lo ? total : 0, base[c] = before + (c == lo ? 0 : total);
+        return;
+    }
+    const std::uint32_t mid = lo + (hi - lo + 1) / 2;
+    const double        ml = double(mid - lo), mr = double(hi - mid);
+    Mt64                s(derive_seed3(seed, kPhaseChunks, annulus, node));
+    const std::uint64_t left = binomial(total, ml / (ml + mr), s); // rng.hpp:197-204
+    split_chunk_partial(seed, annulus, left, lo, mid, 2 * node, need, before, out, base);
+    split_chunk_partial(seed, annulus, total - left, mid, hi, 2 * node + 1, need, before + left, out, base);
 }
 
 } // namespace
@@ -277,7 +300,7 @@ Params::Params(std::uint64_t n_, double alpha_, double C_, std::uint64_t seed_, 
     if (chunks < 1) throw InvalidArgument("ModelParams: chunk count must be >= 1");
 }
 
-Layout make_layout(const Params& p) {
+Layout make_layout(const Params& p, const ChunkNeed* need) {
     Layout L;
     L.n = p.n, L.seed = p.seed, L.chunks = p.chunks, L.alpha = p.alpha, L.R = p.R;
     L.cosh_R = std::cosh(p.R);
@@ -337,6 +360,26 @@ Layout make_layout(const Params& p) {
         }
         L.counts[L.count - 1] = remaining;
     }
+    // classify, partition.hpp:195-217
+    L.classes.assign(L.count, 1);
+    L.first_streaming       = L.count;
+    const double chunk_width = kTwoPi / double(p.chunks);
+    for (std::uint32_t i = 0; i < L.count; ++i) {
+        if (i == 0 && L.has_clique) {
+            L.classes[i] = 0;
+            continue;
+        }
+        const double l     = L.lower[i];
+        const double width = l > 0.0 ? 2.0 * angular_deviation(l, l, p.R) : kTwoPi;
+        if (width <= chunk_width) {
+            L.classes[i] = 2;
+            if (L.first_streaming == L.count) L.first_streaming = i;
+        }
+    }
+    for (std::uint32_t i = L.first_streaming; i < L.count; ++i)
+        if (L.classes[i] != 2) throw Invariant("classify: streaming annuli are not contiguous");
+    L.r_G = L.first_streaming < L.count ? L.lower[L.first_streaming] : p.R;
+
     L.chunk_counts.assign(std::size_t(L.count) * p.chunks, 0);
     // The per-annulus binomial trees are independent (every split node has its own seed path),
     // and so are the subtrees below any node: the first levels are split here, and the
@@ -359,7 +402,9 @@ Layout make_layout(const Params& p) {
         const int         levels = threads > 1 ? 3 : 0;
         std::vector<Task> per(std::size_t(L.count) << levels);
         std::vector<int>  nper(L.count, 0);
-        run(L.count, [&](std::uint32_t i) {
+        // with `need`, streaming annuli take the partial traversal below instead
+        const std::uint32_t nfull = need ? L.first_streaming : L.count;
+        run(nfull, [&](std::uint32_t i) {
             std::vector<Task> cur{{i, 0, p.chunks, L.counts[i], 1}};
             for (int level = 0; level < levels; ++level) {
                 std::vector<Task> next;
@@ -381,7 +426,7 @@ Layout make_layout(const Params& p) {
             nper[i] = int(cur.size());
         });
         std::vector<Task> tasks;
-        for (std::uint32_t i = 0; i < L.count; ++i)
+        for (std::uint32_t i = 0; i < nfull; ++i)
             for (int k = 0; k < nper[i]; ++k) tasks.push_back(per[(std::size_t(i) << levels) + k]);
         std::sort(tasks.begin(), tasks.end(), [](const Task& x, const Task& y) { return x.total > y.total; });
         // phase 2: the subtrees
@@ -390,36 +435,32 @@ Layout make_layout(const Params& p) {
             split_chunk_range(p.seed, t.annulus, t.total, t.lo, t.hi, t.node,
                               L.chunk_counts.data() + std::size_t(t.annulus) * p.chunks);
         });
+        if (need) { // streaming annuli: only the shard's chunks (relative id bases into id_base)
+            L.id_base.assign(std::size_t(L.count) * p.chunks, 0);
+            run(L.count - nfull, [&](std::uint32_t k) {
+                const std::uint32_t i = nfull + k;
+                split_chunk_partial(p.seed, i, L.counts[i], 0, p.chunks, 1, *need, 0,
+                                    L.chunk_counts.data() + std::size_t(i) * p.chunks,
+                                    L.id_base.data() + std::size_t(i) * p.chunks);
+            });
+        }
     }
 
-    // classify, partition.hpp:195-217
-    L.classes.assign(L.count, 1);
-    L.first_streaming       = L.count;
-    const double chunk_width = kTwoPi / double(p.chunks);
+    // assign_vertex_ids, partition.hpp:220-231 (annulus-major, chunk-minor)
+    if (!need) L.id_base.assign(std::size_t(L.count) * p.chunks, 0);
+    std::uint64_t next = 0;
     for (std::uint32_t i = 0; i < L.count; ++i) {
-        if (i == 0 && L.has_clique) {
-            L.classes[i] = 0;
+        if (need && i >= L.first_streaming) { // partial: bases relative to the annulus start
+            for (std::uint32_t c = 0; c < p.chunks; ++c)
+                if (need->has(c) || c == 0) L.id_base[std::size_t(i) * p.chunks + c] += next;
+            next += L.counts[i];
             continue;
         }
-        const double l     = L.lower[i];
-        const double width = l > 0.0 ? 2.0 * angular_deviation(l, l, p.R) : kTwoPi;
-        if (width <= chunk_width) {
-            L.classes[i] = 2;
-            if (L.first_streaming == L.count) L.first_streaming = i;
-        }
-    }
-    for (std::uint32_t i = L.first_streaming; i < L.count; ++i)
-        if (L.classes[i] != 2) throw Invariant("classify: streaming annuli are not contiguous");
-    L.r_G = L.first_streaming < L.count ? L.lower[L.first_streaming] : p.R;
-
-    // assign_vertex_ids, partition.hpp:220-231
-    L.id_base.assign(std::size_t(L.count) * p.chunks, 0);
-    std::uint64_t next = 0;
-    for (std::uint32_t i = 0; i < L.count; ++i)
         for (std::uint32_t c = 0; c < p.chunks; ++c) {
             L.id_base[std::size_t(i) * p.chunks + c] = next;
             next += L.chunk_counts[std::size_t(i) * p.chunks + c];
         }
+    }
     if (next != p.n) throw Invariant("assign_vertex_ids: counts do not sum to n");
     return L;
 }

@@ -67,9 +67,29 @@ struct Layout { // partition.hpp:22-82
     }
 };
 
+// Streaming-annulus chunks a shard needs (its owned chunks and the halo chunk): at most two
+// ranges [lo, hi).  Counts and id bases of the other streaming chunks are left 0 (the
+// reference computes every count with independent per-node seeds, so the needed ones are
+// the same either way); global annuli always get every chunk.
+struct ChunkNeed {
+    std::uint32_t lo[2] = {0, 0}, hi[2] = {0, 0};
+    int           n = 0;
+    bool          has(std::uint32_t c) const {
+        for (int k = 0; k < n; ++k)
+            if (c >= lo[k] && c < hi[k]) return true;
+        return false;
+    }
+    bool meets(std::uint32_t a, std::uint32_t b) const { // [a, b) intersects a needed range
+        for (int k = 0; k < n; ++k)
+            if (a < hi[k] && lo[k] < b) return true;
+        return false;
+    }
+};
+
 // partition.hpp:233-240 make_layout (cell grids are graph-neutral and the
-// device builds its own candidate index, so they are not reproduced).
-Layout make_layout(const Params& p);
+// device builds its own candidate index, so they are not reproduced).  With `need`, only
+// those streaming chunks are split (O(owned chunks + log P) binomial draws per annulus).
+Layout make_layout(const Params& p, const ChunkNeed* need = nullptr);
 
 // sweep.hpp:80-85
 inline double chunk_lower_bound(std::uint32_t c, std::uint32_t P) { return double(c) * (kTwoPi / double(P)); }
