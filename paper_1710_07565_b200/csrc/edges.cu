@@ -429,6 +429,13 @@ __device__ __forceinline__ std::uint32_t slab_lb(const SM& S, const double* lam,
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
+// 16-byte shared-memory load by 32-bit shared address (keeps the loop from re-deriving the
+// generic shared window base, S2R SR_CgaCtaId, on every pair under register pressure)
+__device__ __forceinline__ float4 lds128(unsigned addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -613,6 +620,15 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     }
     __syncthreads();
     const std::uint32_t ngroups = S.run_g[S.n_run];
+    // at the 40-register budget the compiler re-derives the shared window base (S2R SR_CgaCtaId)
+    // inside the pair loop: an opaque copy keeps it in a register (measured cfg3 slab 8.22 ->
+    // 8.01 ms; the 64-register exact-wave variant is faster without it: cfg4 16.6 vs 17.1)
+    unsigned nd_base = smem_addr(&S.nd[0]);
+    if constexpr (!kR12) asm volatile("mov.u32 %0, %0;" : "+r"(nd_base));
+    auto node_rec = [&](std::uint32_t k) {
+        if constexpr (kR12) return S.nd[k];
+        else return lds128(nd_base + 16u * k);
+    };
     SlabRow32* const    rows    = S.rows[warp];
     SlabRow64* const    rows64  = S.rows64[warp];
     std::uint32_t       acc_e = 0, acc_c = 0; // per-thread totals of one slab fit 32 bits
@@ -681,7 +697,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                 const float              ed   = 5.9604645e-8f * (fabsf(lamf) + span) + 1.5e-15f;
                 const float              qm = float(fsub(r2.x, 1.0)), qr = float(rci);
                 for (std::uint32_t k = l0; k < l1; ++k) {
-                    const float4 nd = S.nd[k];
+                    const float4 nd = node_rec(k);
                     bool         e;
                     if (fp64) e = edge_test(r1.x, r1.y, r2.x, rci, node_r1(k), node_r2(k));
                     else {
@@ -762,7 +778,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                         q = rf[2 * o], u = ru[2 * o + 1];
                     }
                     const std::uint32_t k  = u.z + t;
-                    const float4        nd = S.nd[k];
+                    const float4        nd = node_rec(k);
                     const float         df = nd.x - q.x;
                     const float         y2 = df * df;
                     const float         Sv = y2 * fmaf(y2, -1.0f / 24.0f, 0.5f);
