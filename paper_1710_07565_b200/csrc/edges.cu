@@ -475,6 +475,9 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned phase) {
 // |D32| > tau does the FP32 sign decide; otherwise (and for |Delta| > 2^-6, where
 // the truncated series is not used) the pair takes the exact FP64 predicate.
 constexpr float  kPreMaxDelta = 0.015625f;
+#ifndef RHG_SLAB_MINB
+#define RHG_SLAB_MINB 6 // CTAs per SM of the pre-filter slab join (40 registers)
+#endif
 #ifndef RHG_SLAB_DIRECT
 #define RHG_SLAB_DIRECT 8 // groups whose lanes have <= this many pairs each skip the flattening (measured 0 / 2 / 4 / 8 / 16 / 32: cfg4 slab 19.2 / 18.8 / 18.4 / 18.2 / 18.5 / 18.8 ms, cfg2 1.58 / 1.57 / 1.55 / 1.55 / 1.56 / 1.58)
 #endif
@@ -1788,7 +1791,7 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         // doubles staged by TMA (measured cfg4 slab 17.5 -> 16.6 ms, cfg5 86 -> 78; cfg2 / cfg3
         // keep 6 CTAs/SM without them: 1.52 vs 1.55 ms, 8.22 vs 8.42 ms)
         if (scfg == 4 || (scfg == 0 && W.exact_slabs)) launch_slab<256, 4>(a, n, smode, st);
-        else launch_slab<256, 6>(a, n, smode, st);
+        else launch_slab<256, RHG_SLAB_MINB>(a, n, smode, st);
         ++*launches;
         if (W.tail && a.n_tail) {
             RHG_LAUNCH_MODE(tail_kernel, mode, RHG_CFG(unsigned((a.n_tail + 255) / 256), 256, 0, st), a);
