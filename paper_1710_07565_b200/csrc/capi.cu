@@ -838,6 +838,11 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     EdgeWave d1; // wave 1 dense targets + the global unit
     d1.j0 = int(fs), d1.j1 = int(jw), d1.tile_warps = pl.gt_prefix[jw] - pl.gt_prefix[fs];
     d1.global_unit = true;
+    { // the average degree the model targets (geometry.hpp:26-33 inverted): wide dense windows
+        const double q    = (pl.L.alpha - 0.5) / pl.L.alpha;
+        const double dbar = std::exp(-0.5 * (pl.L.R - 2.0 * std::log(double(pl.L.n)))) / (kPi / 2.0 * q * q);
+        d1.dense_occ4     = dbar >= 128.0;
+    }
     EdgeWave s1; // wave 1 slab join (tail pairs too when there is no wave 2)
     s1.slab_begin = 0, s1.slab_end = split ? pl.n_slabs1 : pl.n_slabs;
     // a wave is "exact" when the own-window bound of its largest target annulus lies below the

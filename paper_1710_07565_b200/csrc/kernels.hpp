@@ -141,6 +141,7 @@ struct EdgeWave {
     std::uint64_t tile_warps = 0;                 // gt_prefix[j1] - gt_prefix[j0]
     std::uint64_t slab_begin = 0, slab_end = 0;   // slab-join CTAs (slab_tab range)
     bool          exact_slabs = false;            // the wave's slabs are mostly exact-predicate pairs
+    bool          dense_occ4 = false;             // node tiles at 4 CTAs/SM (wide dense windows)
     bool          global_unit = false, tail = false, finish = false;
     cudaEvent_t   ev0 = nullptr, ev1 = nullptr;   // optional: time the wave's sparse engine
 };
