@@ -1213,6 +1213,7 @@ __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
         const AnnulusDev&   Aj = A.ann[j];
         std::uint32_t       pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         double              h     = -1.0; // half-width that bounds the pieces around the key angle
+        bool                used  = u < A.n_glob; // the row is read by the node tiles (dense pairs only)
         const double2       q2 = A.g_rec[2 * s + 1];  // (coth, coshR / sinh)
         const double        inv = A.g_inv[s];
         const double4       ax  = A.g_aux[s];         // global: (theta, 0, 0, theta); streaming: (lambda, beta, hw, theta)
@@ -1257,6 +1258,7 @@ __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
         } else {
             const int a = req_annulus(A, u);
             if (j >= a && ((A.dense_mask[a] >> j) & 1ull)) {
+                used = true;
                 const AnnulusDev&   Aa = A.ann[a];
                 const std::uint64_t p  = Aa.off + (u - A.req_off[a]);
                 const bool          halo_req  = p >= Aa.halo;
@@ -1307,9 +1309,11 @@ __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
             hkey  = c0 * A.count + j;
             hbits = static_cast<unsigned long long>(__double_as_longlong(h));
         }
-        uint4* row = reinterpret_cast<uint4*>(A.g_rows + (std::uint64_t(jt) * nR + s) * 8);
-        row[0]     = make_uint4(pc[0], pc[1], pc[2], pc[3]);
-        row[1]     = make_uint4(pc[4], pc[5], pc[6], pc[7]);
+        if (used) { // rows of non-dense (source, target) pairs are never read: their segments' hmax stays 0
+            uint4* row = reinterpret_cast<uint4*>(A.g_rows + (std::uint64_t(jt) * nR + s) * 8);
+            row[0]     = make_uint4(pc[0], pc[1], pc[2], pc[3]);
+            row[1]     = make_uint4(pc[4], pc[5], pc[6], pc[7]);
+        }
     }
     // per-(segment, target) max half-width: one atomic per group of lanes sharing the key
     {   // the high word bounds the value from above (non-negative doubles order like their bits)
