@@ -843,6 +843,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         const double dbar = std::exp(-0.5 * (pl.L.R - 2.0 * std::log(double(pl.L.n)))) / (kPi / 2.0 * q * q);
         d1.dense_occ4     = dbar >= 128.0;
     }
+    const bool dense_occ4 = d1.dense_occ4;
     EdgeWave s1; // wave 1 slab join (tail pairs too when there is no wave 2)
     s1.slab_begin = 0, s1.slab_end = split ? pl.n_slabs1 : pl.n_slabs;
     // a wave is "exact" when the own-window bound of its largest target annulus lies below the
@@ -860,6 +861,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         CK(cudaStreamWaitEvent(dst, ctx->ev_late, 0));
         EdgeWave d2;
         d2.j0 = int(jw), d2.j1 = int(K), d2.tile_warps = pl.gt_prefix[K] - pl.gt_prefix[jw];
+        d2.dense_occ4 = dense_occ4;
         EdgeWave s2;
         s2.slab_begin = pl.n_slabs1, s2.slab_end = pl.n_slabs;
         s2.exact_slabs = exact_wave(K - 1);

@@ -961,13 +961,15 @@ __device__ __forceinline__ int req_annulus(const EdgeArgs& A, std::uint64_t u) {
     return lo;
 }
 
-// Sort keys: (source, radial class, theta or lambda quantised to 32 bits).
-// Source 0 = global points, a - first_streaming + 1 = streaming annulus a;
-// the class is the binary exponent of 1/sinh r halved, so the half-widths of
-// one segment differ by at most ~2x and a segment's angle-sorted run is a
-// tight candidate list for the node tiles (any order is exact: the rows carry
-// exact index ranges).
-__global__ void req_keys_kernel(EdgeArgs A, unsigned long long* keys, std::uint32_t* vals) {
+// Dense-engine request order: a counting sort by (segment, angle bucket), no general sort.
+// Key of a request: (source, radial class, theta or lambda quantised to 32 bits); source 0 =
+// global points, a - first_streaming + 1 = streaming annulus a; the class is the binary exponent
+// of 1/sinh r halved, so the half-widths of one segment = (source, class) differ by at most ~2x.
+// Segment c gets 2^lg >= max(64, size) angle buckets over [0, 2pi).  The node tiles only use
+// bucket ranges (supersets; any order inside a bucket is exact: the rows carry exact index
+// ranges), so the exclusive scan of the bucket counts IS the bucket table, and a per-bucket
+// atomic cursor places every request (replaces a 48-bit radix sort, 6 passes).
+__global__ void req_keys_kernel(EdgeArgs A, unsigned long long* keys) {
     const std::uint64_t u = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (u >= A.n_req) return;
     double   th, inv;
@@ -984,53 +986,59 @@ __global__ void req_keys_kernel(EdgeArgs A, unsigned long long* keys, std::uint3
     const unsigned      cls = unsigned(static_cast<unsigned long long>(__double_as_longlong(inv)) >> 53) & 0x3ffu;
     const double        q   = th * (4294967296.0 / kTwoPiD);
     const std::uint32_t tq  = q >= 4294967295.0 ? 0xffffffffu : std::uint32_t(q);
-    keys[u]                 = (static_cast<unsigned long long>(src) << 42) | (static_cast<unsigned long long>(cls) << 32) | tq;
-    vals[u]                 = std::uint32_t(u);
+    const unsigned      seg = (src << 10) | cls;
+    keys[u]                 = (static_cast<unsigned long long>(seg) << 32) | tq;
+    // segment sizes: consecutive requests share their segment, so one atomic per distinct
+    // segment of the warp (per-request atomics on a few hot counters cost 9 ms at cfg3)
+    const unsigned same = __match_any_sync(__activemask(), seg);
+    if (int(threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&A.seg_first[seg], unsigned(__popc(same)));
 }
 
-// Start positions of the non-empty (source, class) segments in the sorted
-// keys: every segment's first position marks seg_first[segment id]
-// (req_marks_kernel), then one block compacts the table in id order into
-// cseg[0..n_cls] and lays out the angle-bucket tables.
-__global__ void req_marks_kernel(EdgeArgs A, const unsigned long long* keys) {
-    const std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (s >= A.n_req) return;
-    const unsigned long long seg = keys[s] >> 32;
-    if (s == 0 || (keys[s - 1] >> 32) != seg) A.seg_first[seg] = std::uint32_t(s);
-}
-__global__ void __launch_bounds__(1024) req_segments_kernel(EdgeArgs A) {
-    __shared__ int wsum[32];
+// One block: the non-empty segments in id order -> dense index c, start position cseg[c]
+// (exclusive prefix of the sizes), n_cls, and the bucket layout (bk_off, bk_shift).
+__global__ void __launch_bounds__(1024) req_segments_kernel(EdgeArgs A, std::uint32_t* seg_index) {
+    __shared__ int      wn[32];
+    __shared__ unsigned ws[32];
     const int      lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned nseg = unsigned(A.count - A.first_streaming + 1) << 10;
-    const unsigned per  = (nseg + 1023) / 1024; // thread t compacts ids [t per, (t + 1) per)
+    const unsigned per  = (nseg + 1023) / 1024; // thread t handles ids [t per, (t + 1) per)
     const unsigned i0   = threadIdx.x * per, i1 = i0 + per < nseg ? i0 + per : nseg;
-    int            mine = 0;
-    for (unsigned i = i0; i < i1; ++i) mine += A.seg_first[i] != 0xffffffffu;
-    int incl = mine;
+    int            mine_n = 0;
+    unsigned       mine_s = 0;
+    for (unsigned i = i0; i < i1; ++i) {
+        const unsigned c = A.seg_first[i];
+        mine_n += c != 0u, mine_s += c;
+    }
+    int      in_n = mine_n;
+    unsigned in_s = mine_s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const int x = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += x;
+        const int      x = __shfl_up_sync(kFull, in_n, o);
+        const unsigned y = __shfl_up_sync(kFull, in_s, o);
+        if (lane >= o) in_n += x, in_s += y;
     }
-    if (lane == 31) wsum[w] = incl;
+    if (lane == 31) wn[w] = in_n, ws[w] = in_s;
     __syncthreads();
-    int before = 0, total = 0;
+    int      bn = 0, total = 0;
+    unsigned bs = 0;
     for (int k = 0; k < 32; ++k) {
-        before += k < w ? wsum[k] : 0;
-        total += wsum[k];
+        bn += k < w ? wn[k] : 0, bs += k < w ? ws[k] : 0u;
+        total += wn[k];
     }
-    int idx = before + incl - mine;
-    for (unsigned i = i0; i < i1; ++i)
-        if (A.seg_first[i] != 0xffffffffu) {
-            if (idx < kMaxCls) A.cseg[idx] = A.seg_first[i];
-            ++idx;
-        }
+    int      idx = bn + in_n - mine_n;
+    unsigned pos = bs + in_s - mine_s;
+    for (unsigned i = i0; i < i1; ++i) {
+        const unsigned c = A.seg_first[i];
+        if (!c) continue;
+        seg_index[i] = unsigned(idx);
+        if (idx < kMaxCls) A.cseg[idx] = pos;
+        ++idx, pos += c;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         const int n = total < kMaxCls ? total : kMaxCls; // overflow is checked on the host via n_cls
         A.cseg[n]   = std::uint32_t(A.n_req);
         *A.n_cls    = total;
-        // angle-bucket tables: segment c gets 2^k >= max(64, size) buckets over [0, 2pi)
         std::uint32_t off = 0;
         for (int c = 0; c < n; ++c) {
             const std::uint32_t sz = A.cseg[c + 1] - A.cseg[c];
@@ -1038,63 +1046,85 @@ __global__ void __launch_bounds__(1024) req_segments_kernel(EdgeArgs A) {
             while ((1u << lg) < sz && lg < 24) ++lg;
             A.bk_off[c]   = off;
             A.bk_shift[c] = std::uint32_t(32 - lg);
-            off += (1u << lg) + 1;
+            off += (1u << lg) + 1; // the extra entry holds the segment end
         }
         A.bk_off[n] = off;
     }
 }
 
-// Bucket starts of every segment: gbk[bk_off[c] + b] = first sorted position
-// of segment c whose quantised angle falls in bucket >= b (cell_fill pattern;
-// the angles are the low 32 bits of the sort keys).
-// Pass 1, one thread per sorted request s: the bucket entries (b(s-1), b(s)] hold s when that
-// run is short (the common case for a whole graph); longer runs -- the head and tail of a
-// shard's segments, whose requests span 1/N of the circle, and the gap wrapped requests leave --
-// stay 0xffffffff for pass 2.
-constexpr std::int64_t kBucketRun = 32;
-__global__ void req_buckets_kernel(EdgeArgs A, const unsigned long long* keys) {
-    const std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (s >= A.n_req) return;
-    const int ncls = *A.n_cls < kMaxCls ? *A.n_cls : kMaxCls;
-    int       c = 0, hc = ncls - 1; // segment of s
-    while (c < hc) {
-        const int mid = (c + hc + 1) >> 1;
-        if (A.cseg[mid] <= s) c = mid;
-        else hc = mid - 1;
+__device__ __forceinline__ long long req_bucket(const EdgeArgs& A, unsigned long long key, const std::uint32_t* seg_index) {
+    const unsigned c = seg_index[unsigned(key >> 32)];
+    if (c >= unsigned(kMaxCls)) return -1;
+    return (long long)(A.bk_off[c] + (std::uint32_t(key) >> A.bk_shift[c]));
+}
+__global__ void req_bucket_count_kernel(EdgeArgs A, const unsigned long long* keys, const std::uint32_t* seg_index,
+                                        std::uint32_t* bcount) {
+    const std::uint64_t u = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (u >= A.n_req) return;
+    const long long g = req_bucket(A, keys[u], seg_index);
+    if (g >= 0) atomicAdd(&bcount[g], 1u);
+}
+__global__ void req_scatter_kernel(EdgeArgs A, const unsigned long long* keys, const std::uint32_t* seg_index,
+                                   std::uint32_t* cursor, std::uint32_t* perm) {
+    const std::uint64_t u = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (u >= A.n_req) return;
+    const long long g = req_bucket(A, keys[u], seg_index);
+    if (g >= 0) perm[atomicAdd(&cursor[g], 1u)] = std::uint32_t(u);
+}
+
+// Exclusive scan of n u32 (three passes): 2048-entry blocks, their sums (one block), the add.
+constexpr int kScanItems = 8;
+__global__ void __launch_bounds__(256) scan_blocks_kernel(const std::uint32_t* in, std::uint32_t* out,
+                                                          std::uint32_t* bsum, std::size_t n) {
+    __shared__ std::uint32_t wsum[8];
+    const int         lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const std::size_t i0   = (std::size_t(blockIdx.x) * 256 + threadIdx.x) * kScanItems;
+    std::uint32_t     v[kScanItems], t = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) v[k] = i0 + k < n ? in[i0 + k] : 0u, t += v[k];
+    std::uint32_t incl = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const std::uint32_t x = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += x;
     }
-    const std::uint32_t sh  = A.bk_shift[c];
-    std::uint32_t*      tab = A.gbk + A.bk_off[c];
-    const std::int64_t  b   = std::int64_t(std::uint32_t(keys[s]) >> sh);
-    const std::int64_t  bp  = s > A.cseg[c] ? std::int64_t(std::uint32_t(keys[s - 1]) >> sh) : -1;
-    if (b - bp <= kBucketRun)
-        for (std::int64_t k = bp + 1; k <= b; ++k) tab[k] = std::uint32_t(s);
-    if (s + 1 == A.cseg[c + 1]) { // last of the segment: the tail buckets hold the segment end
-        const std::int64_t nb = std::int64_t(1) << (32 - sh);
-        if (nb - b <= kBucketRun)
-            for (std::int64_t k = b + 1; k <= nb; ++k) tab[k] = std::uint32_t(s + 1);
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    std::uint32_t before = 0, tot = 0;
+    for (int k = 0; k < 8; ++k) before += k < w ? wsum[k] : 0u, tot += wsum[k];
+    std::uint32_t run = before + incl - t;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+        if (i0 + k < n) out[i0 + k] = run, run += v[k];
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(1024) scan_sums_kernel(std::uint32_t* bsum, unsigned nb) {
+    __shared__ std::uint32_t wsum[32];
+    const int      lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned per  = (nb + 1023) / 1024, i0 = threadIdx.x * per, i1 = i0 + per < nb ? i0 + per : nb;
+    std::uint32_t  t = 0;
+    for (unsigned i = i0; i < i1; ++i) t += bsum[i];
+    std::uint32_t incl = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const std::uint32_t x = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += x;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    std::uint32_t before = 0;
+    for (int k = 0; k < 32; ++k) before += k < w ? wsum[k] : 0u;
+    std::uint32_t run = before + incl - t;
+    for (unsigned i = i0; i < i1; ++i) {
+        const std::uint32_t x = bsum[i];
+        bsum[i]               = run, run += x;
     }
 }
-// Pass 2, one thread per bucket entry: entries pass 1 left empty get the first position of
-// their segment whose key bucket is >= b (binary search; the last entry b = nb holds the end).
-__global__ void __launch_bounds__(256) req_bucket_runs_kernel(EdgeArgs A, const unsigned long long* keys) {
-    const int           ncls = *A.n_cls < kMaxCls ? *A.n_cls : kMaxCls;
-    const std::uint64_t g    = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (ncls <= 0 || g >= A.bk_off[ncls] || A.gbk[g] != 0xffffffffu) return;
-    int c = 0, hc = ncls - 1; // last segment with bk_off[c] <= g
-    while (c < hc) {
-        const int mid = (c + hc + 1) >> 1;
-        if (A.bk_off[mid] <= g) c = mid;
-        else hc = mid - 1;
-    }
-    const std::uint32_t sh = A.bk_shift[c];
-    const std::uint64_t b  = g - A.bk_off[c];
-    std::uint32_t       lo = A.cseg[c], hi = A.cseg[c + 1];
-    while (lo < hi) {
-        const std::uint32_t mid = (lo + hi) >> 1;
-        if (std::uint64_t(std::uint32_t(keys[mid]) >> sh) < b) lo = mid + 1;
-        else hi = mid;
-    }
-    A.gbk[g] = lo;
+__global__ void scan_add_kernel(std::uint32_t* out, std::uint32_t* cursor, const std::uint32_t* bsum, std::size_t n) {
+    const std::size_t i = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const std::uint32_t v = out[i] + bsum[i / (256 * kScanItems)];
+    out[i] = v, cursor[i] = v;
 }
 
 // Sorted copies of the dense-engine requests (one gather pass, so the rows
@@ -1703,35 +1733,34 @@ void launch_cell_index(const EdgeArgs& a0, std::uint32_t blk_begin, std::uint32_
 
 void launch_sort_globals(EdgeArgs& a, void* scratch, std::size_t scratch_bytes, std::size_t* need, cudaStream_t st,
                          std::uint64_t* launches) {
-    // scratch: keys_in | keys_out | vals_in | perm(out) | cub temp
-    const std::size_t n   = a.n_req;
-    const std::size_t a8  = (n * 8 + 255) & ~std::size_t(255);
-    const std::size_t a4  = (n * 4 + 255) & ~std::size_t(255);
-    std::size_t       tmp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, static_cast<const unsigned long long*>(nullptr),
-                                    static_cast<unsigned long long*>(nullptr),
-                                    static_cast<const std::uint32_t*>(nullptr), static_cast<std::uint32_t*>(nullptr),
-                                    int(n), 0, 48, st);
-    *need = 2 * a8 + 2 * a4 + tmp + 256;
+    // scratch: keys | perm (the sorted order) | bucket counts, then cursors | block sums | segment index
+    const std::size_t n    = a.n_req;
+    const std::size_t nbk  = 2 * n + 65 * std::size_t(kMaxCls); // bound on the bucket entries
+    const std::size_t nsum = (nbk + 256 * kScanItems - 1) / (256 * kScanItems);
+    const std::size_t nseg = std::size_t(a.count - a.first_streaming + 1) << 10;
+    auto              al   = [](std::size_t x) { return (x + 255) & ~std::size_t(255); };
+    const std::size_t o_pm = al(n * 8), o_bc = o_pm + al(n * 4), o_bs = o_bc + al(nbk * 4), o_si = o_bs + al(nsum * 4);
+    *need = o_si + al(nseg * 4) + 256;
     if (!scratch || scratch_bytes < *need || n == 0) return;
-    char*               p    = static_cast<char*>(scratch);
-    unsigned long long* kin  = reinterpret_cast<unsigned long long*>(p);
-    unsigned long long* kout = reinterpret_cast<unsigned long long*>(p + a8);
-    std::uint32_t*      vin  = reinterpret_cast<std::uint32_t*>(p + 2 * a8);
-    std::uint32_t*      perm = reinterpret_cast<std::uint32_t*>(p + 2 * a8 + a4);
-    req_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kin, vin);
-    cub::DeviceRadixSort::SortPairs(p + 2 * a8 + 2 * a4, tmp, kin, kout, vin, perm, int(n), 0, 48, st);
-    cudaMemsetAsync(a.seg_first, 0xff, (std::size_t(a.count - a.first_streaming + 1) << 10) * sizeof(std::uint32_t),
-                    st);
-    req_marks_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kout);
-    req_segments_kernel<<<1, 1024, 0, st>>>(a);
-    const std::size_t nbk = 2 * n + 65 * std::size_t(kMaxCls); // bound on the bucket entries
-    cudaMemsetAsync(a.gbk, 0xff, nbk * sizeof(std::uint32_t), st);
-    req_buckets_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a, kout);
-    req_bucket_runs_kernel<<<unsigned((nbk + 255) / 256), 256, 0, st>>>(a, kout);
+    char*               p      = static_cast<char*>(scratch);
+    unsigned long long* keys   = reinterpret_cast<unsigned long long*>(p);
+    std::uint32_t*      perm   = reinterpret_cast<std::uint32_t*>(p + o_pm);
+    std::uint32_t*      bcount = reinterpret_cast<std::uint32_t*>(p + o_bc);
+    std::uint32_t*      bsum   = reinterpret_cast<std::uint32_t*>(p + o_bs);
+    std::uint32_t*      segix  = reinterpret_cast<std::uint32_t*>(p + o_si);
+    const unsigned      g      = unsigned((n + 255) / 256);
+    cudaMemsetAsync(a.seg_first, 0, nseg * sizeof(std::uint32_t), st);
+    cudaMemsetAsync(bcount, 0, nbk * sizeof(std::uint32_t), st);
+    req_keys_kernel<<<g, 256, 0, st>>>(a, keys);
+    req_segments_kernel<<<1, 1024, 0, st>>>(a, segix);
+    req_bucket_count_kernel<<<g, 256, 0, st>>>(a, keys, segix, bcount);
+    scan_blocks_kernel<<<unsigned(nsum), 256, 0, st>>>(bcount, a.gbk, bsum, nbk);
+    scan_sums_kernel<<<1, 1024, 0, st>>>(bsum, unsigned(nsum));
+    scan_add_kernel<<<unsigned((nbk + 255) / 256), 256, 0, st>>>(a.gbk, bcount, bsum, nbk);
+    req_scatter_kernel<<<g, 256, 0, st>>>(a, keys, segix, bcount, perm);
     a.gperm = perm;
-    req_gather_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(a);
-    *launches += 7;
+    req_gather_kernel<<<g, 256, 0, st>>>(a);
+    *launches += 8;
     a.mark("dense_prep", st);
 }
 
@@ -1786,6 +1815,11 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
                 if (mode == 2) glob_tiles_kernel<2, RHG_TILES_MINB1><<<g, 256, 0, st>>>(a);
                 else if (mode == 1) glob_tiles_kernel<1, RHG_TILES_MINB1><<<g, 256, 0, st>>>(a);
                 else glob_tiles_kernel<0, RHG_TILES_MINB1><<<g, 256, 0, st>>>(a);
+            }
+            else if (W.dense_occ4) { // wave 2, wide windows
+                if (mode == 2) glob_tiles_kernel<2, 4><<<g, 256, 0, st>>>(a);
+                else if (mode == 1) glob_tiles_kernel<1, 4><<<g, 256, 0, st>>>(a);
+                else glob_tiles_kernel<0, 4><<<g, 256, 0, st>>>(a);
             }
             else if (mode == 2) glob_tiles_kernel<2, 3><<<g, 256, 0, st>>>(a);
             else if (mode == 1) glob_tiles_kernel<1, 3><<<g, 256, 0, st>>>(a);
