@@ -1244,9 +1244,14 @@ __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
         std::uint32_t       pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         double              h     = -1.0; // half-width that bounds the pieces around the key angle
         bool                used  = u < A.n_glob; // the row is read by the node tiles (dense pairs only)
-        const double2       q2 = A.g_rec[2 * s + 1];  // (coth, coshR / sinh)
-        const double        inv = A.g_inv[s];
-        const double4       ax  = A.g_aux[s];         // global: (theta, 0, 0, theta); streaming: (lambda, beta, hw, theta)
+        const int           a_req = used ? -1 : req_annulus(A, u);
+        if (!used) used = j >= a_req && ((A.dense_mask[a_req] >> j) & 1ull);
+        // the request records only for rows that are used (most (request, target) pairs of a wave
+        // are sparse or below the request's annulus)
+        const double2 q2  = used ? A.g_rec[2 * s + 1] : make_double2(0.0, 0.0); // (coth, coshR / sinh)
+        const double  inv = used ? A.g_inv[s] : 0.0;
+        const double4 ax  = used ? A.g_aux[s] : make_double4(0.0, 0.0, 0.0, 0.0); // global: (theta, 0, 0, theta);
+                                                                                  // streaming: (lambda, beta, hw, theta)
         if (u < A.n_glob) {
             const double th = ax.x;
             if (Aj.halo > Aj.off) {
@@ -1286,9 +1291,8 @@ __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
                 }
             }
         } else {
-            const int a = req_annulus(A, u);
-            if (j >= a && ((A.dense_mask[a] >> j) & 1ull)) {
-                used = true;
+            const int a = a_req;
+            if (used) {
                 const AnnulusDev&   Aa = A.ann[a];
                 const std::uint64_t p  = Aa.off + (u - A.req_off[a]);
                 const bool          halo_req  = p >= Aa.halo;
