@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                 r0 = A.lcellstart[Aa.cell_off + cellf(Aa, lam_first - hb)];
                 r1 = A.lcellstart[Aa.cell_off + cellf(Aa, lam_last + hb) + 1];
                 if (a == j && r1 > Aa.wrap) r1 = Aa.wrap; // own annulus: unwrapped requests only
-                if (a == j && r1 > N0 + m - 1) r1 = N0 + m - 1; // own requests past the slab: no node after them
+                if (a == j && r1 > N0) r1 = N0; // own requests inside the slab: the own pass below
                 if (r1 < r0) r1 = r0;
             }
             const std::uint32_t ng = std::uint32_t((r1 - r0 + 31) / 32);
@@ -639,6 +639,147 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     unsigned long long  au_decided = 0, au_recheck = 0, au_exact = 0, au_disagree = 0, au_noise = 0; // MODE 3
     float               au_ratio = 0.0f;
     int ri = 0; // run of group gi: last ri with run_g[ri] <= gi (gi only grows)
+    // ---- own pass: requests of the target annulus inside the slab (p = N0 + i, unwrapped). Their
+    // pairs are the slab nodes after them up to lower_bound(beta + 2 hw) (the requests before the
+    // slab run through the groups below). Everything but (beta, hw) is staged, so a request costs
+    // two coalesced loads and a short scan; the pairs of all requests are then flattened over the
+    // whole CTA (one packed prefix sum also compacts the requests with pairs), so every thread
+    // gets the same share.
+    {
+        const std::uint32_t wl  = std::uint32_t(Aj.wrap > N0 ? (Aj.wrap - N0 < m ? Aj.wrap - N0 : m) : 0);
+        const bool          on  = ((A.src_mask[j] >> j) & 1ull) && !(A.ablate & 5);
+        const std::uint32_t nrq = on ? wl : 0u; // requests p < min(wrap, halo)
+        static_assert(2 * kSlabThreads >= kSlab, "two requests per thread cover the slab");
+        std::uint32_t len[2] = {0u, 0u};
+        bool          fpw[2] = {false, false};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const std::uint32_t i = 2 * threadIdx.x + h;
+            if (i < nrq) {
+                const double  b  = A.s_beta[N0 + i], hw = A.s_hw[N0 + i];
+                const double  hi = fadd(b, fmul(2.0, hw));
+                std::uint32_t k  = i + 1;
+#pragma unroll 1
+                for (int it = 0; it < 4 && k < m && slam[k] < hi; ++it) ++k;
+                if (k < m && slam[k] < hi) k = slab_lb(S, slam, hi, lam_first, inv_w);
+                const std::uint32_t l1 = k < wl ? k : wl;
+                len[h] = l1 > i + 1 ? l1 - (i + 1) : 0u;
+                fpw[h] = 0.5 * hw * hw < kPreMinS;
+            }
+        }
+        // packed inclusive scan: pairs << 10 | requests with pairs (<= 130816 pairs, <= 512 requests)
+        __shared__ std::uint32_t wsum[kSlabThreads / 32];
+        const std::uint32_t      x0 = (len[0] << 10) + (len[0] > 0) + (len[1] << 10) + (len[1] > 0);
+        std::uint32_t            x  = x0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const std::uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        std::uint32_t wb = 0, X = 0;
+#pragma unroll
+        for (int w = 0; w < kSlabThreads / 32; ++w) wb += w < warp ? wsum[w] : 0u, X += wsum[w];
+        // compacted request table in the staged-id buffer (free once the node records exist):
+        // (inclusive pair prefix, node of pair t = pad + t, float rci, request | fp64 flag << 31)
+        uint4* const  crow = reinterpret_cast<uint4*>(st_id);
+        static_assert(sizeof(S.rows64) >= kSlab * sizeof(uint4), "the compacted requests fit the row buffer");
+        std::uint32_t pe = (wb + x - x0) >> 10, ce = (wb + x - x0) & 1023u;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const std::uint32_t i = 2 * threadIdx.x + h;
+            if (len[h]) {
+                const float rcif = float(fmul(A.cosh_R, st_r2[i].y));
+                crow[ce] = make_uint4(pe + len[h], i + 1 - pe, __float_as_uint(rcif), i | (fpw[h] ? 0x80000000u : 0u));
+                pe += len[h], ++ce;
+            }
+        }
+        __syncthreads();
+        const std::uint32_t T = X >> 10, nne = X & 1023u;
+        acc_c += threadIdx.x == 0 ? T : 0u;
+        const std::uint32_t c  = ((T + kSlabThreads - 1) / kSlabThreads) | 1u;
+        std::uint32_t       t  = threadIdx.x * c;
+        const std::uint32_t te = t + c < T ? t + c : T;
+        if (t < te && !(A.ablate & 2)) {
+            std::uint32_t o = 0, ho = nne - 1; // first request whose inclusive prefix exceeds t
+            while (o < ho) {
+                const std::uint32_t mid = (o + ho) >> 1;
+                if (crow[mid].x > t) ho = mid;
+                else o = mid + 1;
+            }
+            uint4  cr = crow[o];
+            float4 qr = S.nd[cr.w & 0x7fffffffu]; // (lamf, m, 1 / sinh, id offset) of the request
+            float  e1f, c0f;
+            auto   tau_coef = [&]() {
+                const float ed = 5.9604645e-8f * (fabsf(qr.x) + span) + 1.5e-15f;
+                e1f = 1.3f * ed + 3e-15f, c0f = 1.3f * ed * ed + 2e-15f;
+            };
+            tau_coef();
+            // the reference predicate for request i, node k (request doubles: staged or global)
+            auto d64 = [&](std::uint32_t i, std::uint32_t k, double& lhs, double& rhs) {
+                const double2 q1 = [&]() {
+                    if constexpr (kR12) return S.r1[i];
+                    else return A.s_rec1[N0 + i];
+                }();
+                const double2 q2 = st_r2[i], n1 = node_r1(k), n2 = st_r2[k];
+                lhs = fadd(fmul(q1.x, n1.x), fmul(q1.y, n1.y));
+                rhs = fsub(fmul(q2.x, n2.x), fmul(fmul(A.cosh_R, q2.y), n2.y));
+            };
+            std::uint32_t      cnt = 0;
+            unsigned long long sum = 0;
+            for (; t < te; ++t) {
+                if (t >= cr.x) { // next request (compacted: every entry has pairs)
+                    cr = crow[++o];
+                    qr = S.nd[cr.w & 0x7fffffffu];
+                    tau_coef();
+                }
+                const std::uint32_t i  = cr.w & 0x7fffffffu;
+                const std::uint32_t k  = cr.y + t;
+                const float4        nd = node_rec(k);
+                bool                e;
+                if (cr.w >> 31) { // window below the pre-filter's floor: exact predicate only
+                    double lhs, rhs;
+                    d64(i, k, lhs, rhs);
+                    e = lhs > rhs;
+                    if constexpr (MODE == 3) ++au_exact, au_noise += fabs(fsub(lhs, rhs)) < 1e-15;
+                } else {
+                    const float df  = nd.x - qr.x;
+                    const float y2  = df * df;
+                    const float Sv  = y2 * fmaf(y2, -1.0f / 24.0f, 0.5f);
+                    const float P   = __uint_as_float(cr.z) * nd.z;
+                    const float M   = fmaf(qr.y, nd.y, qr.y + nd.y) + Sv;
+                    const float D   = P - M;
+                    const float tau = fmaf(fabsf(df), e1f, fmaf(P + M, 1.4e-6f, c0f));
+                    e                    = D > 0.0f;
+                    const bool undecided = !(fabsf(D) > tau) || fabsf(df) > kPreMaxDelta;
+                    if (undecided || MODE == 3) {
+                        double lhs, rhs;
+                        d64(i, k, lhs, rhs);
+                        if constexpr (MODE == 3) { // audit: every pre-filter decision against the reference predicate
+                            if (undecided) ++au_recheck;
+                            else {
+                                ++au_decided;
+                                au_disagree += e != (lhs > rhs);
+                                au_ratio = fmaxf(au_ratio, float(fabs(double(D) - fsub(lhs, rhs))) / tau);
+                            }
+                            au_noise += fabs(fsub(lhs, rhs)) < 1e-15;
+                        }
+                        if (undecided) e = lhs > rhs;
+                    }
+                }
+                if (e) {
+                    const std::uint32_t nid = __float_as_uint(nd.w), qid = __float_as_uint(qr.w);
+                    sum += nid + qid, ++cnt;
+                    if (MODE == 1) atomicAdd(&A.degrees[base_j + qid], 1u), atomicAdd(&A.degrees[base_j + nid], 1u);
+                    if (MODE == 2) emit_edge(A, base_j + qid, base_j + nid);
+                }
+            }
+            acc_e += cnt;
+            acc_fp += sum + static_cast<unsigned long long>(cnt) * (2 * base_j);
+        }
+        __syncthreads(); // the group rows below overwrite the staged (coth, 1/sinh) buffer
+    }
     for (std::uint32_t gi = warp; gi < ngroups; gi += kSlabThreads / 32) {
         while (S.run_g[ri + 1] <= gi) ++ri;
         const int           a   = S.run_a[ri];
@@ -648,7 +789,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
         if ((A.ablate & 8) && !own) continue;
         const std::uint64_t g    = S.run_r0[ri] + std::uint64_t(gi - S.run_g[ri]) * 32;
         const std::uint64_t R1   = S.run_r0[ri] + std::uint64_t(S.run_g[ri + 1] - S.run_g[ri]) * 32; // group end bound
-        const std::uint64_t Rend = own ? (Aa.wrap < Aa.halo ? Aa.wrap : Aa.halo) : Aa.halo;
+        const std::uint64_t Rend = own ? (Aa.wrap < N0 ? Aa.wrap : N0) : Aa.halo; // own: requests before the slab
         const std::uint64_t p     = g + std::uint64_t(lane);
         const bool          valid = p < R1 && p < Rend;
         const std::uint64_t pc    = valid ? p : g;
@@ -690,9 +831,13 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
         const bool          fp64 = __any_sync(kFull, len > 0 && 0.5 * hwin * hwin < kPreMinS);
         if (A.dbg) { // slab-join path statistics (RHG_DEBUG_STATS=1)
             const unsigned nv = __popc(__ballot_sync(kFull, valid));
+            const unsigned sl = __reduce_add_sync(kFull, len);
             if (lane == 0)
                 atomicAdd(&A.dbg[10], 1ull), atomicAdd(&A.dbg[11], (unsigned long long)nv),
-                    atomicAdd(&A.dbg[12], (unsigned long long)__popc(nz)), atomicAdd(&A.dbg[own ? 15 : 16], 1ull);
+                    atomicAdd(&A.dbg[12], (unsigned long long)__popc(nz)), atomicAdd(&A.dbg[own ? 15 : 16], 1ull),
+                    atomicAdd(&A.dbg[own ? 18 : 21], (unsigned long long)nv),
+                    atomicAdd(&A.dbg[own ? 19 : 22], (unsigned long long)__popc(nz)),
+                    atomicAdd(&A.dbg[own ? 20 : 23], (unsigned long long)sl);
         }
         if (nz == 0) continue;
         // narrow windows (every lane <= kSlabDirect pairs): each lane tests its own pairs with
