@@ -795,31 +795,53 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
         const std::uint64_t pc    = valid ? p : g;
         const double2       r2  = A.s_rec2[pc];
         const double        lam = A.s_lam[pc];
-        double              lo, hi, hw_own = 0.0, h_oth = 0.0;
+        double        lo = 0.0, hi = 0.0, hw_own = 0.0, h_oth = 0.0;
+        std::uint32_t l0 = 0, l1 = 0;
         if (own) {
             const double b = A.s_beta[pc], hw = A.s_hw[pc];
             lo = b, hi = fadd(b, fmul(2.0, hw)), hw_own = hw;
-        } else {
-            const double h = half_width_in(Aj, r2.x, r2.y);
-            lo = fsub(lam, h), hi = fadd(lam, h), h_oth = h;
-        }
-        std::uint32_t l0 = 0, l1 = 0;
-        if (valid && hi > lo && hi > lam_first && lo <= lam_last) {
-            if (own) {
-                // own window: the nodes after p, i.e. from index p + 1 (lower_bound(beta) never lies
-                // past it), up to lower_bound(beta + 2 hw): a short linear scan from there covers
-                // the narrow windows of the outer annuli, the bucket search the rest (measured slab
-                // ms: cfg2 1.49 -> 1.47, cfg4 16.6 -> 16.0, cfg5 78.3 -> 76.9; the same scan for the
-                // other targets' window ends was slower: cfg2 1.52, cfg4 16.5)
+            if (valid && hi > lo && hi > lam_first && lo <= lam_last) {
+                // own window (requests before the slab): the slab's nodes up to lower_bound(beta + 2 hw):
+                // a short linear scan covers the narrow windows of the outer annuli, the bucket search
+                // the rest (measured slab ms: cfg2 1.49 -> 1.47, cfg4 16.6 -> 16.0, cfg5 78.3 -> 76.9)
                 const std::uint32_t wl = std::uint32_t(Aa.wrap > N0 ? (Aa.wrap - N0 < m ? Aa.wrap - N0 : m) : 0);
-                l0 = p + 1 > N0 ? std::uint32_t(p + 1 - N0 < m ? p + 1 - N0 : m) : 0u;
-                std::uint32_t k = l0;
+                std::uint32_t       k  = 0;
 #pragma unroll 1
                 for (int it = 0; it < 4 && k < m && slam[k] < hi; ++it) ++k;
                 if (k < m && slam[k] < hi) k = slab_lb(S, slam, hi, lam_first, inv_w);
                 l1 = k < wl ? k : wl;
-            } else {
-                l0 = slab_lb(S, slam, lo, lam_first, inv_w), l1 = slab_lb(S, slam, hi, lam_first, inv_w);
+            }
+        } else if (valid) {
+            // window half-width in j (sweep.hpp:60-67, 365-370): h = acos(arg), arg rounded as the
+            // reference does. For arg in [1/2, 1) a float estimate hf = 2 asin(sqrt((1 - arg) / 2))
+            // (1 - arg exact) is within 1e-6 of glibc's acos relatively; the window ends are
+            // bracketed with a 1e-5 margin and glibc's acos runs only when a slab node falls inside
+            // a bracket (the exact ends could then differ from the estimate's).
+            double arg = 0.0, h = kPiD;
+            bool   fast = false;
+            if (Aj.lower > 0.0) {
+                arg = fsub(fmul(r2.x, Aj.coth_lower), fmul(Aj.cris, r2.y));
+                if (arg >= 1.0) h = 0.0;
+                else if (arg > -1.0) {
+                    fast = arg >= 0.5 && fsub(1.0, arg) >= 1e-30;
+                    if (!fast) h = gl::gl_acos(arg);
+                }
+            }
+            if (fast) {
+                const float  hf = 2.0f * asinf(sqrtf(float(fsub(1.0, arg)) * 0.5f));
+                const double hl = fmul(double(hf), 1.0 - 1e-5), hh = fmul(double(hf), 1.0 + 1e-5);
+                const double lo_a = fsub(lam, hh), lo_b = fsub(lam, hl), hi_a = fadd(lam, hl), hi_b = fadd(lam, hh);
+                h_oth = hf;
+                if (hi_b > lam_first && lo_a <= lam_last) {
+                    l0 = slab_lb(S, slam, lo_a, lam_first, inv_w), l1 = slab_lb(S, slam, hi_a, lam_first, inv_w);
+                    if ((l0 < m && slam[l0] < lo_b) || (l1 < m && slam[l1] < hi_b)) fast = false, h = gl::gl_acos(arg);
+                }
+            }
+            if (!fast) {
+                lo = fsub(lam, h), hi = fadd(lam, h), h_oth = h;
+                l0 = l1 = 0;
+                if (hi > lo && hi > lam_first && lo <= lam_last)
+                    l0 = slab_lb(S, slam, lo, lam_first, inv_w), l1 = slab_lb(S, slam, hi, lam_first, inv_w);
             }
         }
         const std::uint32_t len = l1 > l0 ? l1 - l0 : 0u;
