@@ -229,6 +229,8 @@ struct Plan {
     std::uint64_t              n_req = 0;
     std::vector<std::uint32_t> ann_blk;     // 256-point blocks per streaming annulus (prefix, count + 1)
     std::vector<unsigned long long> src_mask; // [count] bit a: (a, j) runs on the slab join
+    std::vector<uint4>              row_tasks;   // dense rows: (j | source << 16, s0, s1, first block), by target j
+    std::vector<std::uint32_t>      row_task_j;  // [count + 1] first task of target j
     std::vector<double>        hbound;      // [count * count] half-width bound of a's requests in j
     std::vector<std::uint64_t> slab_prefix; // [count + 1] slabs (1024 owned nodes) before annulus j
     std::vector<unsigned long long> slab_tab; // [n_slabs] (j << 32) | slab index, angle-interleaved
@@ -510,6 +512,28 @@ void plan_edges(Plan& pl) {
         pl.slab_prefix[j + 1]   = pl.slab_prefix[j] + (own + kSlabNodes - 1) / kSlabNodes;
     }
     pl.n_slabs = pl.slab_prefix[K];
+    // dense rows: per target j the sorted-request ranges whose rows the node tiles read (the
+    // global points, and each dense source annulus a <= j: its requests are one contiguous range
+    // of the (source, class, angle) order, [req_off[a], req_off[a] + its points))
+    pl.row_tasks.clear();
+    pl.row_task_j.assign(K + 1, 0);
+    {
+        std::uint32_t blk = 0;
+        auto          add = [&](std::uint32_t j, std::uint32_t src, std::uint64_t s0, std::uint64_t s1) {
+            if (s1 <= s0) return;
+            pl.row_tasks.push_back(make_uint4(j | (src << 16), std::uint32_t(s0), std::uint32_t(s1), blk));
+            blk += std::uint32_t((s1 - s0 + 255) / 256);
+        };
+        for (std::uint32_t j = 0; j < K; ++j) {
+            pl.row_task_j[j] = std::uint32_t(pl.row_tasks.size());
+            if (j < L.first_streaming || !pl.n_req) continue;
+            add(j, 0xffffu, 0, pl.n_glob);
+            for (std::uint32_t a = L.first_streaming; a <= j; ++a)
+                if ((pl.dense_mask[a] >> j) & 1ull) add(j, a, pl.req_off[a], pl.req_off[a] + (pl.ann[a].end - pl.ann[a].off));
+        }
+        pl.row_task_j[K] = std::uint32_t(pl.row_tasks.size());
+        pl.row_tasks.push_back(make_uint4(0, 0, 0, blk)); // sentinel: total blocks
+    }
 
     { // slabs in angular order across targets (requests are re-read from L2 by the next target's
       // slab), wave-1 targets first: a counting sort on (wave, angle bucket) - the order only
@@ -593,6 +617,7 @@ struct Tables {
     std::uint32_t*      ann_blk;
     std::uint64_t*      pseg;
     unsigned long long* src_mask;
+    uint4*              row_tasks;
     double*             hbound;
     unsigned long long* slab_tab;
     std::uint64_t*      tail_prefix;
@@ -642,11 +667,12 @@ void upload_tables_edges(rhg_ctx* ctx, const Plan& pl, Tables& t, std::uint64_t*
     std::vector<void*> d;
     upload_part(ctx, 1,
                 {blob(pl.gt_prefix), blob(pl.src_mask), blob(pl.hbound), blob(pl.slab_tab), blob(pl.tail_prefix),
-                 blob(pl.tail_lam)},
+                 blob(pl.tail_lam), blob(pl.row_tasks)},
                 d, h2d);
     t.gt_prefix = static_cast<std::uint64_t*>(d[0]), t.src_mask = static_cast<unsigned long long*>(d[1]);
     t.hbound = static_cast<double*>(d[2]), t.slab_tab = static_cast<unsigned long long*>(d[3]);
     t.tail_prefix = static_cast<std::uint64_t*>(d[4]), t.tail_lam = static_cast<double*>(d[5]);
+    t.row_tasks = static_cast<uint4*>(d[6]);
 }
 Tables upload_tables(rhg_ctx* ctx, const Plan& pl, std::uint64_t* h2d = nullptr) {
     Tables t{};
@@ -764,6 +790,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         e.bk_off    = reinterpret_cast<std::uint32_t*>(ctx->counters.as<char>() + o_bkoff);
         e.bk_shift  = reinterpret_cast<std::uint32_t*>(ctx->counters.as<char>() + o_bksh);
         e.gt_prefix = t.gt_prefix, e.glob_tile_warps = pl.gtwarps;
+        e.row_tasks = t.row_tasks;
         e.n_req = pl.n_req, e.req_off = t.req_off, e.dense_mask = t.dense_mask;
     }
     e.ann_rw = t.ann;
@@ -838,6 +865,11 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     EdgeWave d1; // wave 1 dense targets + the global unit
     d1.j0 = int(fs), d1.j1 = int(jw), d1.tile_warps = pl.gt_prefix[jw] - pl.gt_prefix[fs];
     d1.global_unit = true;
+    auto row_range = [&](EdgeWave& w) { // the wave's dense-row tasks and their blocks
+        w.row_t0 = pl.row_task_j[w.j0], w.row_t1 = pl.row_task_j[w.j1];
+        w.row_b0 = pl.row_tasks[w.row_t0].w, w.row_nb = pl.row_tasks[w.row_t1].w - w.row_b0;
+    };
+    row_range(d1);
     { // the average degree the model targets (geometry.hpp:26-33 inverted): wide dense windows
         const double q    = (pl.L.alpha - 0.5) / pl.L.alpha;
         const double dbar = std::exp(-0.5 * (pl.L.R - 2.0 * std::log(double(pl.L.n)))) / (kPi / 2.0 * q * q);
@@ -862,6 +894,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         EdgeWave d2;
         d2.j0 = int(jw), d2.j1 = int(K), d2.tile_warps = pl.gt_prefix[K] - pl.gt_prefix[jw];
         d2.dense_occ4 = dense_occ4;
+        row_range(d2);
         EdgeWave s2;
         s2.slab_begin = pl.n_slabs1, s2.slab_end = pl.n_slabs;
         s2.exact_slabs = exact_wave(K - 1);

@@ -1395,30 +1395,33 @@ __global__ void __launch_bounds__(256) deferred_kernel(EdgeArgs A) {
 template <int MODE>
 __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
     const std::uint64_t nR  = A.n_req;
-    const int           nst = A.j1 - A.j0; // targets of this wave
-    const std::uint64_t idx = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool          ok  = idx < nR * std::uint64_t(nst);
+    // task of this block (uniform search over the wave's tasks): target j, source, request range
+    const std::uint32_t b = A.row_b0 + blockIdx.x;
+    std::uint32_t       t0 = A.row_t0, t1 = A.row_t1 - 1; // last task with first block <= b
+    while (t0 < t1) {
+        const std::uint32_t mid = (t0 + t1 + 1) >> 1;
+        if (A.row_tasks[mid].w <= b) t0 = mid;
+        else t1 = mid - 1;
+    }
+    const uint4         task = A.row_tasks[t0];
+    const std::uint64_t s    = task.y + std::uint64_t(b - task.w) * blockDim.x + threadIdx.x;
+    const bool          ok   = s < task.z;
+    const int           j    = int(task.x & 0xffffu);
     Acc                 acc;
     int                 hkey  = -1;
     unsigned long long  hbits = 0;
     if (ok) {
-        const int           jw = int(idx / nR);
-        const std::uint64_t s  = idx - std::uint64_t(jw) * nR;
-        const int           j  = A.j0 + jw;
         const int           jt = j - A.first_streaming;
         const std::uint32_t u  = A.g_u[s];
         const AnnulusDev&   Aj = A.ann[j];
         std::uint32_t       pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         double              h     = -1.0; // half-width that bounds the pieces around the key angle
-        bool                used  = u < A.n_glob; // the row is read by the node tiles (dense pairs only)
-        const int           a_req = used ? -1 : req_annulus(A, u);
-        if (!used) used = j >= a_req && ((A.dense_mask[a_req] >> j) & 1ull);
-        // the request records only for rows that are used (most (request, target) pairs of a wave
-        // are sparse or below the request's annulus)
-        const double2 q2  = used ? A.g_rec[2 * s + 1] : make_double2(0.0, 0.0); // (coth, coshR / sinh)
-        const double  inv = used ? A.g_inv[s] : 0.0;
-        const double4 ax  = used ? A.g_aux[s] : make_double4(0.0, 0.0, 0.0, 0.0); // global: (theta, 0, 0, theta);
-                                                                                  // streaming: (lambda, beta, hw, theta)
+        // every task row is read by the node tiles: the global points, and the dense (source, j) pairs
+        const bool          used  = true;
+        const int           a_req = (task.x >> 16) == 0xffffu ? -1 : int(task.x >> 16);
+        const double2 q2  = A.g_rec[2 * s + 1]; // (coth, coshR / sinh)
+        const double  inv = A.g_inv[s];
+        const double4 ax  = A.g_aux[s]; // global: (theta, 0, 0, theta); streaming: (lambda, beta, hw, theta)
         if (u < A.n_glob) {
             const double th = ax.x;
             if (Aj.halo > Aj.off) {
@@ -1525,7 +1528,7 @@ __global__ void __launch_bounds__(256) req_rows_kernel(EdgeArgs A) {
     }
     if constexpr (MODE != 0) { // the rows' comps per target annulus (lanes of one target reduce together;
                                // compiled out of the counters-only kernel, where it also miscompiled)
-        const int      jj  = ok ? A.j0 + int(idx / nR) : -1;
+        const int      jj  = ok ? j : -1;
         const unsigned grp = __match_any_sync(kFull, jj);
         const unsigned cs  = __reduce_add_sync(grp, unsigned(acc.comps));
         if (jj >= 0 && cs && int(threadIdx.x & 31) == __ffs(grp) - 1) {
@@ -1971,9 +1974,11 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
     EdgeArgs   a   = a0;
     a.j0 = W.j0, a.j1 = W.j1, a.slab0 = W.slab_begin;
     if (W.j1 > W.j0 && a.n_req && a.first_streaming < a.count) {
-        const std::uint64_t rows = a.n_req * std::uint64_t(W.j1 - W.j0);
-        RHG_LAUNCH_MODE(req_rows_kernel, mode, RHG_CFG(unsigned((rows + 255) / 256), 256, 0, st), a);
-        ++*launches;
+        a.row_t0 = W.row_t0, a.row_t1 = W.row_t1, a.row_b0 = W.row_b0;
+        if (W.row_nb) {
+            RHG_LAUNCH_MODE(req_rows_kernel, mode, RHG_CFG(W.row_nb, 256, 0, st), a);
+            ++*launches;
+        }
         a.mark("rows", st);
         const std::uint64_t tw = W.tile_warps;
         if (tw) {

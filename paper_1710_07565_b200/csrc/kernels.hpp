@@ -82,6 +82,8 @@ struct EdgeArgs {
     std::uint64_t     n_req = 0;
     const std::uint64_t* req_off = nullptr;      // [count] first unified index of streaming annulus a
     const unsigned long long* dense_mask = nullptr; // [count] bit j: (a, j) runs on the dense engine
+    const uint4*      row_tasks = nullptr;  // dense rows: (j | source << 16, s0, s1, first block) by target
+    std::uint32_t     row_t0 = 0, row_t1 = 0, row_b0 = 0; // this wave's tasks / first block
     double2*          g_rec = nullptr;     // [2 n_req] sorted requests: (cos, sin), (coth, coshR/sinh)
     double*           g_theta = nullptr;   // [n_req] key angle (theta, or lambda mod 2pi), sorted per segment
     std::uint32_t*    g_id = nullptr;      // [n_req] vertex id
@@ -142,6 +144,8 @@ struct EdgeWave {
     std::uint64_t slab_begin = 0, slab_end = 0;   // slab-join CTAs (slab_tab range)
     bool          exact_slabs = false;            // the wave's slabs are mostly exact-predicate pairs
     bool          dense_occ4 = false;             // node tiles at 4 CTAs/SM (wide dense windows)
+    std::uint32_t row_t0 = 0, row_t1 = 0;         // dense-row tasks of the targets [j0, j1)
+    std::uint32_t row_b0 = 0, row_nb = 0;         // their first block and block count
     bool          global_unit = false, tail = false, finish = false;
     cudaEvent_t   ev0 = nullptr, ev1 = nullptr;   // optional: time the wave's sparse engine
 };
