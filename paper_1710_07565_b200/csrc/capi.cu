@@ -761,8 +761,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     {   // global requests: theta-sorted records and window-piece rows
         const std::size_t nG  = std::max<std::uint64_t>(pl.n_req, 1);
         const std::size_t nst = pl.L.count - pl.L.first_streaming;
-        const std::size_t o_th = align256(2 * nG * sizeof(double2));
-        const std::size_t o_id = o_th + align256(nG * sizeof(double));
+        const std::size_t o_id = align256(2 * nG * sizeof(double2));
         const std::size_t o_rw = o_id + align256(nG * sizeof(std::uint32_t));
         const std::size_t o_bk = o_rw + align256(std::max<std::size_t>(nst, 1) * nG * 8 * sizeof(std::uint32_t));
         const std::size_t o_iv = o_bk + align256((2 * nG + 65 * std::size_t(kMaxCls)) * sizeof(std::uint32_t));
@@ -775,7 +774,6 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         e.deferred = reinterpret_cast<uint4*>(ctx->gbuf.as<char>() + o_df);
         char* g     = ctx->gbuf.as<char>();
         e.g_rec     = reinterpret_cast<double2*>(g);
-        e.g_theta   = reinterpret_cast<double*>(g + o_th);
         e.g_id      = reinterpret_cast<std::uint32_t*>(g + o_id);
         e.g_rows    = reinterpret_cast<std::uint32_t*>(g + o_rw);
         e.gbk       = reinterpret_cast<std::uint32_t*>(g + o_bk);

@@ -1296,34 +1296,30 @@ __global__ void scan_add_kernel(std::uint32_t* out, std::uint32_t* cursor, const
 
 // Sorted copies of the dense-engine requests (one gather pass, so the rows
 // and tile kernels read them coalesced): (cos, sin), (coth, coshR / sinh),
-// 1 / sinh, key angle, id, unified index, and (lambda or theta, beta, hw, theta).
+// 1 / sinh, id, unified index, and (lambda or theta, beta, hw, theta).
 __global__ void req_gather_kernel(EdgeArgs A) {
     const std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (s >= A.n_req) return;
     const std::uint32_t u = A.gperm[s];
     double2             r1, r2;
     double4             ax;
-    double              key;
     unsigned long long  id;
     if (u < A.n_glob) {
         const std::uint64_t g = A.n_ext + u;
         r1 = A.rec1[g], r2 = A.rec2[g];
         const double th = A.rec0[g].y;
-        ax = make_double4(th, 0.0, 0.0, th), key = th, id = u;
+        ax = make_double4(th, 0.0, 0.0, th), id = u;
     } else {
         const int           a = req_annulus(A, u);
         const std::uint64_t p = A.ann[a].off + (u - A.req_off[a]);
         r1 = A.s_rec1[p], r2 = A.s_rec2[p];
         const double lam = A.s_lam[p];
-        ax  = make_double4(lam, A.s_beta[p], A.s_hw[p], A.s_theta[p]);
-        key = lam;
-        while (key >= kTwoPiD) key -= kTwoPiD;
+        ax = make_double4(lam, A.s_beta[p], A.s_hw[p], A.s_theta[p]);
         id = A.s_id[p];
     }
     A.g_rec[2 * s]     = r1;
     A.g_rec[2 * s + 1] = make_double2(r2.x, fmul(A.cosh_R, r2.y));
     A.g_inv[s]         = r2.y;
-    A.g_theta[s]       = key;
     A.g_id[s]          = std::uint32_t(id);
     A.g_u[s]           = u;
     A.g_aux[s]         = ax;

@@ -85,7 +85,6 @@ struct EdgeArgs {
     const uint4*      row_tasks = nullptr;  // dense rows: (j | source << 16, s0, s1, first block) by target
     std::uint32_t     row_t0 = 0, row_t1 = 0, row_b0 = 0; // this wave's tasks / first block
     double2*          g_rec = nullptr;     // [2 n_req] sorted requests: (cos, sin), (coth, coshR/sinh)
-    double*           g_theta = nullptr;   // [n_req] key angle (theta, or lambda mod 2pi), sorted per segment
     std::uint32_t*    g_id = nullptr;      // [n_req] vertex id
     double*           g_inv = nullptr;     // [n_req] 1 / sinh r
     std::uint32_t*    g_u = nullptr;       // [n_req] unified request index
