@@ -159,7 +159,7 @@ struct rhg_ctx {
     cudaEvent_t  ev[6]{};
     cudaEvent_t  fork = nullptr, join = nullptr; // timing-free events for the side stream
     cudaEvent_t  ev_pow = nullptr, ev_late = nullptr; // the wave-2 chains (late stream)
-    cudaEvent_t  evw[4]{};                            // sparse-engine timing of the two edge waves
+    cudaEvent_t  evw[6]{};                            // sparse-engine timing: the two waves' slab joins, the side tail
     std::vector<std::pair<std::string, cudaEvent_t>> tl; // RHG_TIMELINE marks of the current call
     std::vector<cudaEvent_t> tl_pool;
     DevBuf       beta, hw, rec0, rec1, rec2, r_out, beta_raw, tables, tables2, cells, counters, degrees, dbg, nid;
@@ -860,9 +860,23 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         CK(cudaEventRecord(ctx->fork, from));
         CK(cudaStreamWaitEvent(to, ctx->fork, 0));
     };
-    EdgeWave d1; // wave 1 dense targets + the global unit
+    // the small independent kernels (global unit, tail pairs) run on ctx->side beside the big
+    // ones (their last-wave tails overlap): the global unit needs only the global points, so it
+    // starts with the sort phase; the tail pairs start with wave 2's slab join
+    const char* ss   = std::getenv("RHG_SIDE_SMALL"); // A/B: 0 off, 1 global unit only, 2 tail only, 3 both
+    const int   ssv  = ss ? std::atoi(ss) : 3;
+    const bool  side_small = !conc && ssv != 0;
+    const bool  side_glob = side_small && (ssv & 1), side_tail = side_small && (ssv & 2);
+    bool        tail_timed = false; // the tail pairs ran (and were timed) on ctx->side
+    if (side_glob) {
+        fork_to(ctx->stream, ctx->side);
+        EdgeWave g;
+        g.global_unit = true;
+        launch_edges(e, g, ctx->side, launches);
+    }
+    EdgeWave d1; // wave 1 dense targets (+ the global unit)
     d1.j0 = int(fs), d1.j1 = int(jw), d1.tile_warps = pl.gt_prefix[jw] - pl.gt_prefix[fs];
-    d1.global_unit = true;
+    d1.global_unit = !side_glob;
     auto row_range = [&](EdgeWave& w) { // the wave's dense-row tasks and their blocks
         w.row_t0 = pl.row_task_j[w.j0], w.row_t1 = pl.row_task_j[w.j1];
         w.row_b0 = pl.row_tasks[w.row_t0].w, w.row_nb = pl.row_tasks[w.row_t1].w - w.row_b0;
@@ -896,11 +910,22 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         EdgeWave s2;
         s2.slab_begin = pl.n_slabs1, s2.slab_end = pl.n_slabs;
         s2.exact_slabs = exact_wave(K - 1);
-        s2.tail = true, s2.ev0 = ctx->evw[2], s2.ev1 = ctx->evw[3];
-        launch_edges(e, d2, dst, launches);
+        s2.tail = !side_tail, s2.ev0 = ctx->evw[2], s2.ev1 = ctx->evw[3];
+        if (side_small && (ssv & 4)) { // A/B: wave 2's dense engine beside its slab join
+            fork_to(ctx->stream, ctx->side);
+            launch_edges(e, d2, ctx->side, launches);
+        } else launch_edges(e, d2, dst, launches);
+        if (side_tail) { // the tail pairs beside wave 2's slab join
+            fork_to(ctx->stream, ctx->side);
+            EdgeWave t;
+            t.tail = true, t.ev0 = ctx->evw[4], t.ev1 = ctx->evw[5];
+            launch_edges(e, t, ctx->side, launches);
+            tail_timed = pl.n_tail > 0;
+        }
         launch_edges(e, s2, ctx->stream, launches);
     }
     fork_to(dst, ctx->stream); // join
+    if (side_small) fork_to(ctx->side, ctx->stream);
     EdgeWave fin;
     fin.finish = true;
     launch_edges(e, fin, ctx->stream, launches);
@@ -957,6 +982,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     const bool split_used = split_wave && pl.wave_j < pl.L.count;
     if (pl.n_slabs1 || !split_used) out->pairs_ms += (split_used ? pl.n_slabs1 : pl.n_slabs) ? ms_between(ctx->evw[0], ctx->evw[1]) : 0.0;
     if (split_used && pl.n_slabs > pl.n_slabs1) out->pairs_ms += ms_between(ctx->evw[2], ctx->evw[3]);
+    if (tail_timed) out->pairs_ms += ms_between(ctx->evw[4], ctx->evw[5]); // the tail beside wave 2 (its own duration)
     out->d2h_bytes += 3 * sizeof(Counters) + (degrees ? pl.L.n * sizeof(unsigned) : 0);
 }
 

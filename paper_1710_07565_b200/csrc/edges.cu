@@ -2023,8 +2023,10 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         if (W.ev1) cudaEventRecord(W.ev1, st); // sparse engine of this wave (slab join [+ tail])
         a.mark("slab(+tail)", st);
     } else if (W.tail && a.n_tail) {
+        if (W.ev0) cudaEventRecord(W.ev0, st);
         RHG_LAUNCH_MODE(tail_kernel, mode, RHG_CFG(unsigned((a.n_tail + 255) / 256), 256, 0, st), a);
         ++*launches;
+        if (W.ev1) cudaEventRecord(W.ev1, st);
     }
     if (W.global_unit && a.gg_tile_end > a.gg_tile_begin) {
         const std::uint64_t nT     = (a.n_glob + kGGTile - 1) / kGGTile;
