@@ -156,6 +156,7 @@ const NcclApi& nccl_api() {
 struct rhg_ctx {
     int          device = 0;
     cudaStream_t stream = nullptr, side = nullptr, late = nullptr;
+    cudaStream_t small = nullptr; // the edge phase's small independent kernels (global unit, tail pairs)
     cudaEvent_t  ev[6]{};
     cudaEvent_t  fork = nullptr, join = nullptr; // timing-free events for the side stream
     cudaEvent_t  ev_pow = nullptr, ev_late = nullptr; // the wave-2 chains (late stream)
@@ -848,31 +849,31 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         ctx->gsort.ensure(need);
         launch_sort_globals(e, ctx->gsort.p, ctx->gsort.cap, &need, ctx->stream, launches);
     }
-    // Per wave: the dense engine (rows + node tiles) and the global unit, then the slab join.
-    // RHG_CONCURRENT_ENGINES=1 puts the dense side on ctx->side beside the slab join
-    // (independent counter families, both only read the sorted arrays; measured: no gain at
-    // cfg2 — each engine fills the GPU on its own); the deferred ranges and the counter fold
-    // wait for both.
-    const bool conc = std::getenv("RHG_CONCURRENT_ENGINES") != nullptr;
+    // Per wave: the dense engine (rows + node tiles) on ctx->side beside the slab join on the main
+    // stream (independent counter families, both only read the sorted arrays); the deferred ranges
+    // and the counter fold wait for both. Measured with the small kernels on their own stream
+    // (below): cfg2 3.49 -> 3.38 ms, cfg3 24.76 -> 24.71, cfg4 36.45 -> 36.40 (without them the
+    // overlap gained nothing at cfg2). RHG_CONCURRENT_ENGINES=0: one stream (A/B).
+    const char* ce   = std::getenv("RHG_CONCURRENT_ENGINES");
+    const bool  conc = !(ce && ce[0] == '0');
     cudaStream_t dst = conc ? ctx->side : ctx->stream;
     auto fork_to = [&](cudaStream_t from, cudaStream_t to) {
         if (from == to) return;
         CK(cudaEventRecord(ctx->fork, from));
         CK(cudaStreamWaitEvent(to, ctx->fork, 0));
     };
-    // the small independent kernels (global unit, tail pairs) run on ctx->side beside the big
-    // ones (their last-wave tails overlap): the global unit needs only the global points, so it
+    // the small independent kernels (global unit, tail pairs) run on their own stream beside the
+    // big ones (their last-wave tails overlap): the global unit needs only the global points, so it
     // starts with the sort phase; the tail pairs start with wave 2's slab join
     const char* ss   = std::getenv("RHG_SIDE_SMALL"); // A/B: 0 off, 1 global unit only, 2 tail only, 3 both
     const int   ssv  = ss ? std::atoi(ss) : 3;
-    const bool  side_small = !conc && ssv != 0;
-    const bool  side_glob = side_small && (ssv & 1), side_tail = side_small && (ssv & 2);
-    bool        tail_timed = false; // the tail pairs ran (and were timed) on ctx->side
+    const bool  side_glob = (ssv & 1) != 0, side_tail = (ssv & 2) != 0, side_small = side_glob || side_tail;
+    bool        tail_timed = false; // the tail pairs ran (and were timed) on ctx->small
     if (side_glob) {
-        fork_to(ctx->stream, ctx->side);
+        fork_to(ctx->stream, ctx->small);
         EdgeWave g;
         g.global_unit = true;
-        launch_edges(e, g, ctx->side, launches);
+        launch_edges(e, g, ctx->small, launches);
     }
     EdgeWave d1; // wave 1 dense targets (+ the global unit)
     d1.j0 = int(fs), d1.j1 = int(jw), d1.tile_warps = pl.gt_prefix[jw] - pl.gt_prefix[fs];
@@ -911,21 +912,18 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
         s2.slab_begin = pl.n_slabs1, s2.slab_end = pl.n_slabs;
         s2.exact_slabs = exact_wave(K - 1);
         s2.tail = !side_tail, s2.ev0 = ctx->evw[2], s2.ev1 = ctx->evw[3];
-        if (side_small && (ssv & 4)) { // A/B: wave 2's dense engine beside its slab join
-            fork_to(ctx->stream, ctx->side);
-            launch_edges(e, d2, ctx->side, launches);
-        } else launch_edges(e, d2, dst, launches);
+        launch_edges(e, d2, dst, launches);
         if (side_tail) { // the tail pairs beside wave 2's slab join
-            fork_to(ctx->stream, ctx->side);
+            fork_to(ctx->stream, ctx->small);
             EdgeWave t;
             t.tail = true, t.ev0 = ctx->evw[4], t.ev1 = ctx->evw[5];
-            launch_edges(e, t, ctx->side, launches);
+            launch_edges(e, t, ctx->small, launches);
             tail_timed = pl.n_tail > 0;
         }
         launch_edges(e, s2, ctx->stream, launches);
     }
     fork_to(dst, ctx->stream); // join
-    if (side_small) fork_to(ctx->side, ctx->stream);
+    if (side_small) fork_to(ctx->small, ctx->stream);
     EdgeWave fin;
     fin.finish = true;
     launch_edges(e, fin, ctx->stream, launches);
@@ -1123,6 +1121,7 @@ int rhg_create(int device, rhg_ctx** out) {
         c->device = device;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->small, cudaStreamNonBlocking));
         int prio_lo = 0, prio_hi = 0; // the late stream (outermost annulus) gets block-scheduling priority
         CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         CK(cudaStreamCreateWithPriority(&c->late, cudaStreamNonBlocking, prio_hi));
@@ -1146,6 +1145,7 @@ void rhg_destroy(rhg_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->side);
+    cudaStreamSynchronize(c->small);
     for (DevBuf* b: {&c->beta, &c->hw, &c->rec0, &c->rec1, &c->rec2, &c->r_out, &c->beta_raw, &c->tables, &c->cells,
                      &c->counters, &c->degrees, &c->dbg, &c->nid, &c->lcells, &c->s_beta,
                      &c->s_hw, &c->s_lt, &c->s_rec1, &c->s_rec2, &c->gsort, &c->gbuf, &c->tables2, &c->lam_tmp, &c->audit,
@@ -1159,6 +1159,7 @@ void rhg_destroy(rhg_ctx* c) {
     cudaEventDestroy(c->fork);
     cudaEventDestroy(c->join);
     cudaStreamDestroy(c->side);
+    cudaStreamDestroy(c->small);
     cudaStreamSynchronize(c->late);
     cudaStreamDestroy(c->late);
     cudaEventDestroy(c->ev_pow);
