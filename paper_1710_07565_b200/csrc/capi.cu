@@ -157,6 +157,7 @@ struct rhg_ctx {
     int          device = 0;
     cudaStream_t stream = nullptr, side = nullptr, late = nullptr;
     cudaStream_t small = nullptr; // the edge phase's small independent kernels (global unit, tail pairs)
+    cudaStream_t dense = nullptr; // the edge phase's dense engine (beside the slab join on `stream`)
     cudaEvent_t  ev[6]{};
     cudaEvent_t  fork = nullptr, join = nullptr; // timing-free events for the side stream
     cudaEvent_t  ev_pow = nullptr, ev_late = nullptr; // the wave-2 chains (late stream)
@@ -856,7 +857,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     // overlap gained nothing at cfg2). RHG_CONCURRENT_ENGINES=0: one stream (A/B).
     const char* ce   = std::getenv("RHG_CONCURRENT_ENGINES");
     const bool  conc = !(ce && ce[0] == '0');
-    cudaStream_t dst = conc ? ctx->side : ctx->stream;
+    cudaStream_t dst = conc ? ctx->dense : ctx->stream;
     auto fork_to = [&](cudaStream_t from, cudaStream_t to) {
         if (from == to) return;
         CK(cudaEventRecord(ctx->fork, from));
@@ -1125,6 +1126,10 @@ int rhg_create(int device, rhg_ctx** out) {
         int prio_lo = 0, prio_hi = 0; // the late stream (outermost annulus) gets block-scheduling priority
         CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         CK(cudaStreamCreateWithPriority(&c->late, cudaStreamNonBlocking, prio_hi));
+        {
+            const char* dp = std::getenv("RHG_DENSE_PRIO"); // A/B: block-scheduling priority of the dense engine
+            CK(cudaStreamCreateWithPriority(&c->dense, cudaStreamNonBlocking, dp && dp[0] == '1' ? prio_hi : prio_lo));
+        }
         CK(cudaEventCreateWithFlags(&c->ev_pow, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_late, cudaEventDisableTiming));
         for (auto& e: c->evw) CK(cudaEventCreate(&e));
@@ -1146,6 +1151,7 @@ void rhg_destroy(rhg_ctx* c) {
     cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->side);
     cudaStreamSynchronize(c->small);
+    cudaStreamSynchronize(c->dense);
     for (DevBuf* b: {&c->beta, &c->hw, &c->rec0, &c->rec1, &c->rec2, &c->r_out, &c->beta_raw, &c->tables, &c->cells,
                      &c->counters, &c->degrees, &c->dbg, &c->nid, &c->lcells, &c->s_beta,
                      &c->s_hw, &c->s_lt, &c->s_rec1, &c->s_rec2, &c->gsort, &c->gbuf, &c->tables2, &c->lam_tmp, &c->audit,
@@ -1160,6 +1166,7 @@ void rhg_destroy(rhg_ctx* c) {
     cudaEventDestroy(c->join);
     cudaStreamDestroy(c->side);
     cudaStreamDestroy(c->small);
+    cudaStreamDestroy(c->dense);
     cudaStreamSynchronize(c->late);
     cudaStreamDestroy(c->late);
     cudaEventDestroy(c->ev_pow);
