@@ -160,6 +160,7 @@ struct rhg_ctx {
     cudaStream_t dense = nullptr; // the edge phase's dense engine (beside the slab join on `stream`)
     cudaEvent_t  ev[6]{};
     cudaEvent_t  fork = nullptr, join = nullptr; // timing-free events for the side stream
+    cudaEvent_t  ev_glob = nullptr, ev_gz = nullptr; // global points sampled / counters zeroed (small stream)
     cudaEvent_t  ev_pow = nullptr, ev_late = nullptr; // the wave-2 chains (late stream)
     cudaEvent_t  evw[6]{};                            // sparse-engine timing: the two waves' slab joins, the side tail
     std::vector<std::pair<std::string, cudaEvent_t>> tl; // RHG_TIMELINE marks of the current call
@@ -219,9 +220,11 @@ struct Plan {
     std::vector<StreamJob>  jobs;
     std::vector<std::uint32_t> job_order;   // wave-1 jobs then wave-2 jobs, grouped by chain bin
     std::vector<std::uint32_t> chain_bins;  // bin b runs job_order[chain_bins[b], chain_bins[b + 1])
-    std::uint32_t              chain_bins1 = 0; // wave-1 bins (wave-2 bins follow)
+    std::uint32_t              chain_bins1 = 0; // global-annulus + wave-1 bins (wave-2 bins follow)
+    std::uint32_t              chain_bins_g = 0; // global-annulus bins (they come first)
     std::uint32_t              wave_j = 0;  // first annulus of wave 2 (count: no split)
     int                        wave2_jobs = 0;
+    int                        glob_jobs = 0;     // jobs of the global annuli (the last entries of `jobs`)
     std::uint64_t              n_slabs1 = 0; // slabs of wave-1 targets (they come first in slab_tab)
     std::vector<std::uint64_t> gt_prefix;   // dense-engine warps (512-node owned strips) before annulus j
     std::vector<std::uint64_t> gseg;        // global-point annulus offsets (segments of the theta sort)
@@ -403,18 +406,21 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
             if (!dense_src) pl.wave_j = L.count - w2;
         }
     }
-    // job order: wave 1 then wave 2, each by descending count, ties by job index (a stable
-    // sort), as one u64 key per job: wave bit | complemented count (< 2^39) | index (< 2^24)
+    // job order: the global annuli's jobs, wave 1, wave 2, each by descending count, ties by job
+    // index (a stable sort), as one u64 key per job: class (2 bits) | complemented count (< 2^38) |
+    // index (< 2^24)
     if (pl.jobs.size() >= (std::size_t(1) << 24)) throw InvalidArgument("rhg: too many sampler streams");
     {
         std::vector<std::uint64_t> key(pl.jobs.size());
-        pl.wave2_jobs = 0;
+        pl.wave2_jobs = 0, pl.glob_jobs = 0;
         for (std::uint32_t k = 0; k < key.size(); ++k) {
-            const StreamJob&    J  = pl.jobs[k];
-            const bool          w2 = J.annulus >= pl.wave_j && J.annulus < L.count;
-            const std::uint64_t c  = std::min<std::uint64_t>(J.count, (std::uint64_t(1) << 39) - 1);
-            key[k] = (std::uint64_t(w2) << 63) | ((((std::uint64_t(1) << 39) - 1) - c) << 24) | k;
-            pl.wave2_jobs += w2;
+            const StreamJob&    J   = pl.jobs[k];
+            const bool          w2  = J.annulus >= pl.wave_j && J.annulus < L.count;
+            const bool          gl  = J.annulus < L.first_streaming;
+            const std::uint64_t cls = gl ? 0 : w2 ? 2 : 1;
+            const std::uint64_t c   = std::min<std::uint64_t>(J.count, (std::uint64_t(1) << 38) - 1);
+            key[k] = (cls << 62) | ((((std::uint64_t(1) << 38) - 1) - c) << 24) | k;
+            pl.wave2_jobs += w2, pl.glob_jobs += gl;
         }
         radix_sort_keys(key, 24); // the index bits are already in order: a stable sort of the rest
         pl.job_order.resize(key.size());
@@ -427,11 +433,16 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
     // so few chain warps share an SM (their shared-memory traffic, not the DMUL latency,
     // is what slows a chain that shares its SM with many others)
     pl.chain_bins.assign(1, 0);
-    pl.chain_bins1 = 0;
-    for (int wv = 0; wv < 2; ++wv) {
-        const std::uint32_t j0 = wv ? std::uint32_t(pl.jobs.size() - pl.wave2_jobs) : 0;
-        const std::uint32_t j1 = wv ? std::uint32_t(pl.jobs.size()) : std::uint32_t(pl.jobs.size() - pl.wave2_jobs);
-        if (j1 <= j0) continue;
+    pl.chain_bins1 = pl.chain_bins_g = 0;
+    for (int wv = 0; wv < 3; ++wv) { // classes: global annuli, wave 1, wave 2
+        const std::uint32_t nj = std::uint32_t(pl.jobs.size()), ng = std::uint32_t(pl.glob_jobs);
+        const std::uint32_t j0 = wv == 0 ? 0 : wv == 1 ? ng : nj - std::uint32_t(pl.wave2_jobs);
+        const std::uint32_t j1 = wv == 0 ? ng : wv == 1 ? nj - std::uint32_t(pl.wave2_jobs) : nj;
+        if (j1 <= j0) {
+            if (wv == 0) pl.chain_bins_g = 0;
+            if (wv <= 1) pl.chain_bins1 = std::uint32_t(pl.chain_bins.size() - 1);
+            continue;
+        }
         std::vector<std::uint64_t> cnt(j1 - j0); // counts in job order (contiguous for the packing loop)
         std::uint64_t              sum = 0, mx = 0;
         for (std::uint32_t k = j0; k < j1; ++k) {
@@ -480,7 +491,8 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
         }
         std::copy(ordered.begin(), ordered.end(), pl.job_order.begin() + j0);
         for (std::uint32_t b = 0; b < nb; ++b) pl.chain_bins.push_back(j0 + fill[b + 1]);
-        if (!wv) pl.chain_bins1 = std::uint32_t(nb);
+        if (wv == 0) pl.chain_bins_g = std::uint32_t(nb);
+        if (wv <= 1) pl.chain_bins1 = std::uint32_t(pl.chain_bins.size() - 1);
     }
     pl.sub_ms[1] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl1).count();
     if (pl.n_ext >= (std::uint64_t(1) << 32) || pl.n_req >= (std::uint64_t(1) << 31) || L.n >= (std::uint64_t(1) << 32))
@@ -720,7 +732,7 @@ struct EdgeSink {
 };
 
 void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out, std::uint32_t* degrees,
-               bool gen, bool split_wave, std::uint64_t* launches, EdgeSink* sink = nullptr) {
+               bool gen, bool split_wave, std::uint64_t* launches, EdgeSink* sink = nullptr, bool glob_small = false) {
     const std::uint32_t K         = pl.L.count;
     const std::size_t   o_dmax    = align256(3 * sizeof(Counters));
     const std::size_t   o_hmax    = o_dmax + align256(K * sizeof(unsigned long long));
@@ -731,7 +743,12 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     const std::size_t   o_ann     = o_slots + align256(3 * kSlots * sizeof(SlotCounter));
     const std::size_t   cnt_bytes = o_ann + align256(std::size_t(kAnnSlots) * 2 * kMaxAnnuli * sizeof(unsigned long long)) + 256;
     ctx->counters.ensure(cnt_bytes);
-    CK(cudaMemsetAsync(ctx->counters.p, 0, cnt_bytes, ctx->stream));
+    if (glob_small) { // the global points were sampled on ctx->small: zero the counters there, so the
+                      // global unit can start right after them; the main stream waits for the zeroing
+        CK(cudaMemsetAsync(ctx->counters.p, 0, cnt_bytes, ctx->small));
+        CK(cudaEventRecord(ctx->ev_gz, ctx->small));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_gz, 0));
+    } else CK(cudaMemsetAsync(ctx->counters.p, 0, cnt_bytes, ctx->stream));
     ctx->cells.ensure(std::max<std::uint64_t>(pl.ncells, 1) * sizeof(std::uint64_t));
     if (degrees) {
         ctx->degrees.ensure(pl.L.n * sizeof(unsigned));
@@ -871,7 +888,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     const bool  side_glob = (ssv & 1) != 0, side_tail = (ssv & 2) != 0, side_small = side_glob || side_tail;
     bool        tail_timed = false; // the tail pairs ran (and were timed) on ctx->small
     if (side_glob) {
-        fork_to(ctx->stream, ctx->small);
+        if (!glob_small) fork_to(ctx->stream, ctx->small);
         EdgeWave g;
         g.global_unit = true;
         launch_edges(e, g, ctx->small, launches);
@@ -1136,6 +1153,8 @@ int rhg_create(int device, rhg_ctx** out) {
         for (auto& e: c->ev) CK(cudaEventCreate(&e));
         CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_glob, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_gz, cudaEventDisableTiming));
         *out = c;
     });
 }
@@ -1164,6 +1183,8 @@ void rhg_destroy(rhg_ctx* c) {
     for (auto& e: c->ev) cudaEventDestroy(e);
     cudaEventDestroy(c->fork);
     cudaEventDestroy(c->join);
+    cudaEventDestroy(c->ev_glob);
+    cudaEventDestroy(c->ev_gz);
     cudaStreamDestroy(c->side);
     cudaStreamDestroy(c->small);
     cudaStreamDestroy(c->dense);
@@ -1507,6 +1528,14 @@ void generate_impl(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shar
         const char* ns    = std::getenv("RHG_NO_WAVES"); // A/B switch for timing experiments
         const bool  split = pl.wave_j < pl.L.count && !(ns && ns[0] == '1');
         if (split) sa.wave2_jobs = pl.wave2_jobs, sa.late = ctx->late, sa.ev_pow = ctx->ev_pow, sa.ev_late = ctx->ev_late;
+        const char* gs    = std::getenv("RHG_GLOB_STREAM"); // A/B switch: 0 = global points with wave 1
+        const bool  gsplit = split && pl.glob_jobs > 0 && pl.chain_bins_g > 0 && pl.n_glob > 0 && !(gs && gs[0] == '0');
+        if (gsplit) {
+            sa.glob = ctx->small, sa.ev_glob = ctx->ev_glob;
+            sa.chain_bins_g = int(pl.chain_bins_g), sa.glob_job0 = int(pl.jobs.size()) - pl.glob_jobs;
+            if (pl.jobs[std::size_t(sa.glob_job0)].annulus >= pl.L.first_streaming)
+                throw Invariant("plan: the global annuli's jobs are not the last ones");
+        }
         launch_sampler(sa, ctx->stream, &launches);
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         { // the edge-phase plan is built and staged while the device samples
@@ -1515,7 +1544,7 @@ void generate_impl(rhg_ctx* ctx, const rhg_params* params, const rhg_shard* shar
             upload_tables_edges(ctx, pl, t, &out->h2d_bytes);
             host_ms += std::chrono::duration<double, std::milli>(Clock::now() - t2).count();
         }
-        run_edges(ctx, pl, t, out, degrees, true, split, &launches, sink);
+        run_edges(ctx, pl, t, out, degrees, true, split, &launches, sink, gsplit);
         fill_common(pl, out);
         out->sample_ms       = ms_between(ctx->ev[0], ctx->ev[1]);
         out->edges_ms        = ms_between(ctx->ev[1], ctx->ev[2]);

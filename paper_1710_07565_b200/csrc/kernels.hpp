@@ -44,6 +44,11 @@ struct SamplerArgs {
     int               wave2_jobs = 0;     // the last wave2_jobs entries of job_order chain on `late`
     cudaStream_t      late = nullptr;
     cudaEvent_t       ev_pow = nullptr, ev_late = nullptr; // pow done (main) / wave-2 chains done (late)
+    // the global annuli's points on their own stream (generate mode): their bins come first
+    // (chain_bins_g), their jobs last in `jobs` ([glob_job0, njobs)); ev_glob marks them sampled
+    cudaStream_t      glob = nullptr;
+    cudaEvent_t       ev_glob = nullptr;
+    int               chain_bins_g = 0, glob_job0 = 0;
 };
 
 void launch_sampler(const SamplerArgs& a, cudaStream_t st, std::uint64_t* launches);

@@ -145,9 +145,9 @@ __device__ __forceinline__ int pseg_find(const std::uint64_t* __restrict__ pseg,
     return lo;
 }
 __global__ void point_radial_kernel(const std::uint64_t* __restrict__ pseg, int nseg, const AnnulusDev* __restrict__ ann,
-                                    double alpha, std::uint64_t total, double* __restrict__ hw_out,
+                                    double alpha, std::uint64_t first, std::uint64_t total, double* __restrict__ hw_out,
                                     double2* __restrict__ rec2, double* __restrict__ r_out) {
-    const std::uint64_t i0 = std::uint64_t(blockIdx.x) * blockDim.x;
+    const std::uint64_t i0 = first + std::uint64_t(blockIdx.x) * blockDim.x; // points [first, total)
     const std::uint64_t i  = i0 + threadIdx.x;
     __shared__ int           s_a;
     __shared__ std::uint64_t s_end;
@@ -343,6 +343,11 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
     }
     const bool split = S.wave2_jobs && S.late;
     const int  nb1   = split ? S.chain_bins1 : S.chain_bins_total;
+    // the global annuli (few, short streams) on their own stream: their points are ready long
+    // before the streaming chains finish, so the global unit runs during the chain phase
+    const bool gsplit = split && S.glob && S.ev_glob && S.side && S.glob_job0 < S.njobs && S.chain_bins_g > 0 &&
+                        S.total > S.angular_from;
+    const int  njs    = gsplit ? S.glob_job0 : S.njobs; // the side stream's radius streams
     if (split && S.chain_bins_total > nb1) {
         cudaEventRecord(S.ev_pow, st);
         cudaStreamWaitEvent(S.late, S.ev_pow, 0);
@@ -352,17 +357,35 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
         S.mark("chain_wave2(late)", S.late);
         ++*launches;
     }
-    mt_uniforms_kernel<<<S.njobs, kMtThreads, 0, side>>>(S.jobs, S.njobs, S.beta, S.hw, 2, S.seed);
+    if (gsplit) {
+        cudaStreamWaitEvent(S.glob, S.ev_fork, 0);
+        const int ng = S.njobs - S.glob_job0;
+        mt_uniforms_kernel<<<ng, kMtThreads, 0, S.glob>>>(S.jobs + S.glob_job0, ng, S.beta, S.hw, 2, S.seed);
+        angle_side_kernel<<<S.chain_bins_g, 32 * kAngWarps, 0, S.glob>>>(S.jobs, S.chain_bins, S.chain_bins_g,
+                                                                         S.job_order, S.beta, S.seed);
+        const std::uint64_t first = S.angular_from;
+        point_radial_kernel<<<unsigned((S.total - first + 255) / 256), 256, 0, S.glob>>>(
+            S.pseg, S.npseg, S.ann, S.alpha, first, S.total, S.hw, S.rec2, S.r_out);
+        point_angular_kernel<<<unsigned((S.total - first + 255) / 256), 256, 0, S.glob>>>(
+            S.jobs, S.njobs, first, S.total, S.beta, S.hw, S.rec0, S.rec1, S.beta_unlifted_out);
+        cudaEventRecord(S.ev_glob, S.glob);
+        S.mark("global_points", S.glob);
+        *launches += 4;
+    }
+    mt_uniforms_kernel<<<njs, kMtThreads, 0, side>>>(S.jobs, njs, S.beta, S.hw, 2, S.seed);
     S.mark("mt_radii", side);
     // the radius attributes run beside the angle side (measured at cfg2: serialising them after
     // the wave-1 chains is slower — the wave-1 sort then waits for the whole radius side — and
     // so is splitting them by wave: the GPU is saturated either way)
-    point_radial_kernel<<<unsigned((S.total + 255) / 256), 256, 0, side>>>(S.pseg, S.npseg, S.ann, S.alpha, S.total,
+    const std::uint64_t rad_end = gsplit ? S.angular_from : S.total;
+    point_radial_kernel<<<unsigned((rad_end + 255) / 256), 256, 0, side>>>(S.pseg, S.npseg, S.ann, S.alpha, 0, rad_end,
                                                                           S.hw, S.rec2, S.r_out);
     S.mark("radial", side);
     *launches += 2;
-    if (nb1) {
-        angle_side_kernel<<<nb1, 32 * kAngWarps, 0, st>>>(S.jobs, S.chain_bins, nb1, S.job_order, S.beta, S.seed);
+    const int nbw = gsplit ? S.chain_bins_g : 0; // the main stream's wave-1 bins
+    if (nb1 > nbw) {
+        angle_side_kernel<<<nb1 - nbw, 32 * kAngWarps, 0, st>>>(S.jobs, S.chain_bins + nbw, nb1 - nbw, S.job_order,
+                                                               S.beta, S.seed);
         ++*launches;
     }
     S.mark("chain_wave1", st);
@@ -372,10 +395,11 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
     }
     // generate mode: streaming points get their frames in the sort phase (edges.cu rank_kernel, angular_scatter_point)
     const std::uint64_t first = S.angular_from;
-    if (S.total > first)
+    if (S.total > first && !gsplit) {
         point_angular_kernel<<<unsigned((S.total - first + 255) / 256), 256, 0, st>>>(
             S.jobs, S.njobs, first, S.total, S.beta, S.hw, S.rec0, S.rec1, S.beta_unlifted_out);
-    *launches += 1;
+        *launches += 1;
+    }
 }
 
 void launch_mt_uniforms(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launches) {
