@@ -855,11 +855,16 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     launch_cell_index(e, pl.ann_blk[fs], pl.ann_blk[jw], int(fs), int(jw), gen, ctx->stream, launches);
     if (split) { // wave 2's sort phase right after its chains, beside wave 1 (needs the radius side
                  // and this call's zeroed counters / dmax table from the main stream)
+        // on ctx->side (normal priority; measured cfg2 3.41 -> 3.35 ms): on the high-priority late
+        // stream it held back wave 1's edge work. RHG_SORT2_SIDE=0: the late stream (A/B)
+        const char*  s2s = std::getenv("RHG_SORT2_SIDE");
+        cudaStream_t s2  = s2s && s2s[0] == '0' ? ctx->late : ctx->side;
         CK(cudaEventRecord(ctx->fork, ctx->stream));
-        CK(cudaStreamWaitEvent(ctx->late, ctx->fork, 0));
-        CK(cudaStreamWaitEvent(ctx->late, ctx->join, 0));
-        launch_cell_index(e, pl.ann_blk[jw], pl.ann_blk[K], int(jw), int(K), gen, ctx->late, launches);
-        CK(cudaEventRecord(ctx->ev_late, ctx->late));
+        CK(cudaStreamWaitEvent(s2, ctx->fork, 0));
+        CK(cudaStreamWaitEvent(s2, ctx->join, 0));
+        if (s2 != ctx->late) CK(cudaStreamWaitEvent(s2, ctx->ev_late, 0)); // the wave-2 chains
+        launch_cell_index(e, pl.ann_blk[jw], pl.ann_blk[K], int(jw), int(K), gen, s2, launches);
+        CK(cudaEventRecord(ctx->ev_late, s2));
     }
     if (pl.n_req && fs < K) { // dense-engine requests in (source, class, angle) order
         std::size_t need = 0;
