@@ -743,16 +743,14 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     const std::size_t   o_ann     = o_slots + align256(3 * kSlots * sizeof(SlotCounter));
     const std::size_t   cnt_bytes = o_ann + align256(std::size_t(kAnnSlots) * 2 * kMaxAnnuli * sizeof(unsigned long long)) + 256;
     ctx->counters.ensure(cnt_bytes);
-    if (glob_small) { // the global points were sampled on ctx->small: zero the counters there, so the
-                      // global unit can start right after them; the main stream waits for the zeroing
-        CK(cudaMemsetAsync(ctx->counters.p, 0, cnt_bytes, ctx->small));
-        CK(cudaEventRecord(ctx->ev_gz, ctx->small));
-        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_gz, 0));
-    } else CK(cudaMemsetAsync(ctx->counters.p, 0, cnt_bytes, ctx->stream));
+    // the global points sampled on ctx->small: every output the kernels accumulate into is zeroed
+    // there, so the global unit can start right after them; the main stream waits for the zeroing
+    cudaStream_t zs = glob_small ? ctx->small : ctx->stream;
+    CK(cudaMemsetAsync(ctx->counters.p, 0, cnt_bytes, zs));
     ctx->cells.ensure(std::max<std::uint64_t>(pl.ncells, 1) * sizeof(std::uint64_t));
     if (degrees) {
         ctx->degrees.ensure(pl.L.n * sizeof(unsigned));
-        CK(cudaMemsetAsync(ctx->degrees.p, 0, pl.L.n * sizeof(unsigned), ctx->stream));
+        CK(cudaMemsetAsync(ctx->degrees.p, 0, pl.L.n * sizeof(unsigned), zs));
     }
     EdgeArgs e;
     e.ann = t.ann, e.count = int(K), e.first_streaming = int(pl.L.first_streaming);
@@ -825,7 +823,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     if (sink) {
         ctx->ebuf.ensure(std::max<std::uint64_t>(sink->dev_cap, 1) * sizeof(ulonglong2));
         ctx->ecount.ensure(256);
-        CK(cudaMemsetAsync(ctx->ecount.p, 0, 8, ctx->stream));
+        CK(cudaMemsetAsync(ctx->ecount.p, 0, 8, zs));
         e.edge_out = ctx->ebuf.as<ulonglong2>(), e.edge_cap = sink->dev_cap;
         e.edge_count = ctx->ecount.as<unsigned long long>();
     }
@@ -834,12 +832,12 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     const bool  dbg     = dbg_env && dbg_env[0] == '1';
     if (dbg) {
         ctx->dbg.ensure(kDbgSlots * sizeof(unsigned long long));
-        CK(cudaMemsetAsync(ctx->dbg.p, 0, kDbgSlots * sizeof(unsigned long long), ctx->stream));
+        CK(cudaMemsetAsync(ctx->dbg.p, 0, kDbgSlots * sizeof(unsigned long long), zs));
         e.dbg = ctx->dbg.as<unsigned long long>();
     }
     if (ctx->audit_on) { // rhg_audit_predicate: the slab join runs its MODE 3 instance
         ctx->audit.ensure(kAuditSlots * sizeof(unsigned long long));
-        CK(cudaMemsetAsync(ctx->audit.p, 0, kAuditSlots * sizeof(unsigned long long), ctx->stream));
+        CK(cudaMemsetAsync(ctx->audit.p, 0, kAuditSlots * sizeof(unsigned long long), zs));
         e.audit = ctx->audit.as<unsigned long long>();
     }
     e.ann_blk = t.ann_blk;
@@ -849,6 +847,10 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     // pl.wave_j (sort phase, dense prep, rows / node tiles / slabs of those targets, the global
     // unit) overlaps the outermost annulus's chains on ctx->late; wave 2 = the outermost annulus
     // after ev_late, then the tail pairs, the deferred ranges and the counter fold.
+    if (glob_small) {
+        CK(cudaEventRecord(ctx->ev_gz, ctx->small));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_gz, 0));
+    }
     const std::uint32_t fs = pl.L.first_streaming;
     const bool          split = split_wave && pl.wave_j < K;
     const std::uint32_t jw    = split ? pl.wave_j : K;
