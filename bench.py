@@ -350,6 +350,23 @@ def main():
             d2h += st.d2h_bytes
     barrier()
     edges, fp, comps = st.total.edges, st.total.fingerprint, st.total.comps  # whole graph (reduced every step)
+    # the sparse engine alone (untimed, after the timed region): the edge phase on one stream, so its
+    # kernels do not share the SMs with the dense engine / global unit / tail as in the timed steps
+    iso_ms, iso_tests = 0.0, 0
+    if rank == 0 and world == 1:
+        saved = {k: os.environ.get(k) for k in ("RHG_CONCURRENT_ENGINES", "RHG_SIDE_SMALL")}
+        os.environ["RHG_CONCURRENT_ENGINES"], os.environ["RHG_SIDE_SMALL"] = "0", "0"
+        try:
+            for _ in range(3):
+                si = step()
+                iso_ms += si.pairs_ms
+                iso_tests += si.stream_comps
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
     tm = torch.tensor([dev_ms, wall_s, edges_ms], dtype=torch.float64, device="cpu" if one_gpu else "cuda")
     if world > 1:
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
@@ -377,13 +394,19 @@ def main():
                 "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak,
                              "traffic": tr.get("dram_bytes_per_launch") if tr else None,
-                             "kernel": "sparse engine: slab_kernel (+ its small tail_kernel), CUDA events around "
-                                       "the launches",
+                             "kernel": "sparse engine: slab_kernel (+ its small tail_kernel, on its own stream: its "
+                                       "own duration added), CUDA events around the launches; in the timed steps the "
+                                       "dense engine runs beside it on the same SMs (see 'isolated')",
                              "kernel_ms": pairs_ms / args.steps,
                              "kernel_tests_per_launch": stream_comps / args.steps,
                              "peak_source": "measured live: non-FMA DMUL+DADD rate (rhg_fp64_peak)",
                              "work": "8 FP64-pipe ops per reference predicate test (SURVEY 8(d)) x the kernel's tests",
-                             "dmul_latency_cycles": lat, "kernel_profile": kernel_profile()},
+                             "dmul_latency_cycles": lat, "kernel_profile": kernel_profile(),
+                             "isolated": ({"kernel_ms": iso_ms / 3, "achieved": 8.0 * iso_tests / (iso_ms * 1e-3) / 1e12,
+                                           "frac": 8.0 * iso_tests / (iso_ms * 1e-3) / ops,
+                                           "note": "3 untimed steps after the timed region with the edge phase on one "
+                                                   "stream (RHG_CONCURRENT_ENGINES=0, RHG_SIDE_SMALL=0)"}
+                                          if iso_ms > 0 else None)},
                 "fp64_roofline_frac_edge_phase": (8.0 * comps * args.steps / (edges_ms * 1e-3)) / ops / world,
                 "fp64_roofline_frac_whole_step": (8.0 * comps * args.steps / (dev_ms * 1e-3)) / ops / world,
                 "clocks": clk.summary(),
