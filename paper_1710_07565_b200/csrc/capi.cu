@@ -385,12 +385,20 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
     pl.pseg.push_back(pl.total << 8);
     // (annulus, target) pairs whose windows hold >= kDenseMin nodes on average run on the dense
     // engine (node tiles x streamed requests); the rest on the slab join (96: measured optimum band 64..128 at cfg2)
+    // the engine threshold (chooses the engine, never the result): 96 nodes, doubled for graphs whose
+    // average degree is >= 128 (wide windows everywhere: with the dense engine beside the slab join,
+    // moving the 96..192-node windows to the slab join balances the two; measured cfg3 24.56 ->
+    // 22.48 ms, cfg2 unchanged at 96, worse above 128); RHG_DENSE_MIN overrides (A/B)
+    const double dbar_model = std::exp(-0.5 * (L.R - 2.0 * std::log(double(L.n)))) /
+                              (kPi / 2.0 * ((L.alpha - 0.5) / L.alpha) * ((L.alpha - 0.5) / L.alpha));
+    const char*  dmv       = std::getenv("RHG_DENSE_MIN");
+    const double dense_min = dmv ? std::atof(dmv) : kDenseMin * (dbar_model >= 128.0 ? 2.0 : 1.0);
     pl.dense_mask.assign(L.count, 0ull);
     pl.req_off.assign(L.count, 0);
     pl.n_req = pl.n_glob;
     for (std::uint32_t a = L.first_streaming; a < L.count; ++a) {
         for (std::uint32_t j = a; j < L.count && j < 64; ++j)
-            if (expected_window_nodes(L, a, j) >= kDenseMin) pl.dense_mask[a] |= 1ull << j;
+            if (expected_window_nodes(L, a, j) >= dense_min) pl.dense_mask[a] |= 1ull << j;
         pl.req_off[a] = pl.n_req;
         if (pl.dense_mask[a]) pl.n_req += pl.ann[a].end - pl.ann[a].off;
     }
