@@ -768,7 +768,11 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                         if (undecided) e = lhs > rhs;
                     }
                 }
-                if (e) {
+                if constexpr (MODE == 0) { // branch-free accumulation (the counters-only kernel)
+                    const std::uint32_t nid = __float_as_uint(nd.w), qid = __float_as_uint(qr.w);
+                    sum += e ? static_cast<unsigned long long>(nid + qid) : 0ull;
+                    cnt += e;
+                } else if (e) {
                     const std::uint32_t nid = __float_as_uint(nd.w), qid = __float_as_uint(qr.w);
                     sum += nid + qid, ++cnt;
                     if (MODE == 1) atomicAdd(&A.degrees[base_j + qid], 1u), atomicAdd(&A.degrees[base_j + nid], 1u);
@@ -892,7 +896,10 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                         if (!(fabsf(D) > tau) || fabsf(df) > kPreMaxDelta)
                             e = edge_test(r1.x, r1.y, r2.x, rci, node_r1(k), node_r2(k));
                     }
-                    if (e) {
+                    if constexpr (MODE == 0) { // branch-free accumulation (the counters-only kernel)
+                        sum += e ? base_j_ + __float_as_uint(nd.w) + idp : 0ull;
+                        cnt += e;
+                    } else if (e) {
                         const unsigned long long nid = base_j_ + __float_as_uint(nd.w);
                         sum += nid + idp, ++cnt;
                         if (MODE == 1) atomicAdd(&A.degrees[idp], 1u), atomicAdd(&A.degrees[nid], 1u);
@@ -987,9 +994,13 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                         e = edge_test(R.cs, R.sn, R.coth, R.rci, node_r1(k), node_r2(k));
                         if (A.dbg) atomicAdd(&A.dbg[17], 1ull);
                     }
-                    if (e) {
+                    if constexpr (MODE == 0) { // branch-free accumulation (the counters-only kernel)
                         const std::uint32_t nid = __float_as_uint(nd.w);
-                        sum += nid + u.y, ++cnt; // < 2^32: a shard holds < 2^31 points
+                        sum += e ? static_cast<unsigned long long>(nid + u.y) : 0ull; // < 2^32: a shard holds < 2^31 points
+                        cnt += e;
+                    } else if (e) {
+                        const std::uint32_t nid = __float_as_uint(nd.w);
+                        sum += nid + u.y, ++cnt;
                         if (MODE == 1) {
                             atomicAdd(&A.degrees[base_a + u.y], 1u);
                             atomicAdd(&A.degrees[base_j + nid], 1u);
