@@ -245,6 +245,32 @@ def run_reference(args, name, wl, world, rank):
     return 0
 
 
+# SURVEY 8(d) per-point figures (the cost at small average degree is per point): HBM bytes per
+# sampled point that the pipeline's passes must move (DESIGN 8): radius uniforms 8 + radius
+# attributes 40 + beta 8 (sampler), beta cells 28 + rank / scatter 128 + lambda cells 12 (sort
+# phase), slab staging 32 + own-window (beta, hw) 16 (sparse engine)
+DESIGN_BYTES_PER_POINT = 8 + 40 + 8 + 28 + 128 + 12 + 32 + 16
+
+
+def per_point_block(params, rank, world, step_ms, sample_ms):
+    import paper_1710_07565_b200 as rhg
+    pts = rhg.shard_extent(params, rank, world).sampled_points
+    peak = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak = float(json.load(f)["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        pass
+    gbs = pts * DESIGN_BYTES_PER_POINT / (step_ms * 1e-3) / 1e9 if step_ms > 0 else 0.0
+    return {"points_sampled_per_rank": pts,
+            "points_per_s": pts / (step_ms * 1e-3) if step_ms > 0 else 0.0,
+            "sampler_points_per_s": pts / (sample_ms * 1e-3) if sample_ms > 0 else 0.0,
+            "design_hbm_bytes_per_point": DESIGN_BYTES_PER_POINT,
+            "design_hbm_GBps": gbs,
+            "hbm_peak_GBps": peak, "hbm_frac": gbs / peak if peak else None,
+            "note": "rank 0's shard; sampler rate over the main stream's sampler phase (chains + radius side)"}
+
+
 def free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -336,6 +362,7 @@ def main():
         step()
     barrier()
     dev_ms, wall_s, launches, h2d, d2h, edges_ms, pairs_ms, stream_comps = 0.0, 0.0, 0, 0, 0, 0.0, 0.0, 0
+    sample_ms = 0.0
     with Clocks(local) as clk:
         for _ in range(args.steps):
             t = time.perf_counter()
@@ -343,6 +370,7 @@ def main():
             wall_s += time.perf_counter() - t
             dev_ms += st.device_ms
             edges_ms += st.edges_ms
+            sample_ms += st.sample_ms
             pairs_ms += st.pairs_ms
             stream_comps += st.stream_comps
             launches += st.kernel_launches
@@ -409,6 +437,7 @@ def main():
                                           if iso_ms > 0 else None)},
                 "fp64_roofline_frac_edge_phase": (8.0 * comps * args.steps / (edges_ms * 1e-3)) / ops / world,
                 "fp64_roofline_frac_whole_step": (8.0 * comps * args.steps / (dev_ms * 1e-3)) / ops / world,
+                "per_point": per_point_block(params, rank, world, dev_ms / args.steps, sample_ms / args.steps),
                 "clocks": clk.summary(),
                 "collective": ("one ncclAllReduce(uint64, 9 counters) per step inside the timed region"
                                if world > 1 and not one_gpu else
