@@ -910,7 +910,7 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     }
     EdgeWave d1; // wave 1 dense targets (+ the global unit)
     d1.j0 = int(fs), d1.j1 = int(jw), d1.tile_warps = pl.gt_prefix[jw] - pl.gt_prefix[fs];
-    d1.global_unit = !side_glob;
+    d1.global_unit = !side_glob, d1.first_wave = true;
     auto row_range = [&](EdgeWave& w) { // the wave's dense-row tasks and their blocks
         w.row_t0 = pl.row_task_j[w.j0], w.row_t1 = pl.row_task_j[w.j1];
         w.row_b0 = pl.row_tasks[w.row_t0].w, w.row_nb = pl.row_tasks[w.row_t1].w - w.row_b0;

@@ -1581,9 +1581,9 @@ __device__ __forceinline__ std::uint32_t gtheta_lb(const double* th, std::uint32
 // MINB: CTAs per SM the register budget targets (measured cfg2: wave 1's targets 0.40 ms at 2,
 // 0.43 at 3 with small spills; wave 2's outermost target 0.18 at 2, 0.15 at 3)
 #ifndef RHG_TILES_MINB1
-#define RHG_TILES_MINB1 2 // node tiles of wave 1 (measured cfg2: 2 -> 0.40 ms, 3 -> 0.43; step 3.73 / 3.78 / 3.79 ms
-                          // at 2 / 3 / 4, cfg3 29.39 / 28.68 / 28.23: EdgeWave::dense_occ4 picks 4 for
-                          // average degrees >= 128, whose dense windows are wide)
+#define RHG_TILES_MINB1 3 // node tiles of wave 1 (measured cfg2, dense engine alone: 2 -> 0.40 ms, 3 -> 0.43; beside
+                          // the slab join on its own stream 3 is better: step 3.35 -> 3.28 ms at cfg2, cfg4 36.7 ->
+                          // 36.4, cfg5 165.6 -> 163.5; EdgeWave::dense_occ4 picks 4 for average degrees >= 128)
 #endif
 template <int MODE, int MINB = 2>
 __global__ void __launch_bounds__(256, MINB) glob_tiles_kernel(EdgeArgs A) {
@@ -1990,11 +1990,11 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         const std::uint64_t tw = W.tile_warps;
         if (tw) {
             const unsigned g = unsigned((tw + 7) / 8);
-            if (W.global_unit && W.dense_occ4) { // wave 1, wide windows: 4 CTAs/SM (64 registers)
+            if (W.first_wave && W.dense_occ4) { // wave 1, wide windows: 4 CTAs/SM (64 registers)
                 if (mode == 2) glob_tiles_kernel<2, 4><<<g, 256, 0, st>>>(a);
                 else if (mode == 1) glob_tiles_kernel<1, 4><<<g, 256, 0, st>>>(a);
                 else glob_tiles_kernel<0, 4><<<g, 256, 0, st>>>(a);
-            } else if (W.global_unit) { // wave 1
+            } else if (W.first_wave) { // wave 1
                 if (mode == 2) glob_tiles_kernel<2, RHG_TILES_MINB1><<<g, 256, 0, st>>>(a);
                 else if (mode == 1) glob_tiles_kernel<1, RHG_TILES_MINB1><<<g, 256, 0, st>>>(a);
                 else glob_tiles_kernel<0, RHG_TILES_MINB1><<<g, 256, 0, st>>>(a);

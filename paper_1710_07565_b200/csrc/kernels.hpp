@@ -148,6 +148,7 @@ struct EdgeWave {
     std::uint64_t slab_begin = 0, slab_end = 0;   // slab-join CTAs (slab_tab range)
     bool          exact_slabs = false;            // the wave's slabs are mostly exact-predicate pairs
     bool          dense_occ4 = false;             // node tiles at 4 CTAs/SM (wide dense windows)
+    bool          first_wave = false;             // wave 1's dense targets (node-tile launch bounds)
     std::uint32_t row_t0 = 0, row_t1 = 0;         // dense-row tasks of the targets [j0, j1)
     std::uint32_t row_b0 = 0, row_nb = 0;         // their first block and block count
     bool          global_unit = false, tail = false, finish = false;
