@@ -217,10 +217,22 @@ __device__ __forceinline__ void angular_scatter_point(const EdgeArgs& A, const A
     A.s_beta[d]     = bf;
     A.s_hw[d]       = h;
     A.s_lam[d]      = fadd(bf, h);
-    A.s_theta[d]    = th;
+    if (A.lift_part && i >= J.halo) A.s_theta[d] = th; // elsewhere theta follows from lambda (theta_of)
     A.s_rec1[d]     = make_double2(cs, sn);
     A.s_rec2[d]     = A.rec2[i];
     A.s_id[d]       = i + static_cast<unsigned long long>(i < J.halo ? J.dlt0 : J.dlt1);
+}
+
+// theta of sorted point k (sweep.hpp:135-139): in generate mode an unlifted point's lambda is
+// fl(beta + hw) itself, so theta = lambda, or fl(lambda - 2pi) from 2pi on, exactly as the angular
+// step computes it; only the lifted halo block (k >= lift_from) and same-points runs store it.
+__device__ __forceinline__ double theta_of(const EdgeArgs& A, std::uint64_t k, std::uint64_t lift_from) {
+    if (!A.gen || k >= lift_from) return A.s_theta[k];
+    const double l = A.s_lam[k];
+    return l >= kTwoPiD ? fsub(l, kTwoPiD) : l;
+}
+__device__ __forceinline__ std::uint64_t lift_from(const EdgeArgs& A, const AnnulusDev& J) {
+    return A.lift_part ? J.halo : ~std::uint64_t(0);
 }
 
 // Exact rank of point i by (lambda, beta-order index) inside its block; in the
@@ -370,7 +382,7 @@ struct SRow { // one request as the cooperative loop reads it (broadcast from sh
 // need the full (theta, id) dedup (sweep.hpp:517-526).
 template <int MODE>
 __device__ __forceinline__ void serial_range(const EdgeArgs& A, const SRow& q, double theta, bool dedup,
-                                             std::uint64_t k0, std::uint64_t k1, Acc& acc) {
+                                             std::uint64_t k0, std::uint64_t k1, std::uint64_t lift, Acc& acc) {
     for (std::uint64_t k = k0; k < k1; k += 4) { // four independent nodes in flight
         double2            n1[4], n2[4];
         unsigned long long nid[4];
@@ -379,7 +391,7 @@ __device__ __forceinline__ void serial_range(const EdgeArgs& A, const SRow& q, d
         for (int u = 0; u < 4; ++u) {
             const std::uint64_t kk = k + u < k1 ? k + u : k;
             n1[u] = A.s_rec1[kk], n2[u] = A.s_rec2[kk], nid[u] = A.s_id[kk];
-            tq[u] = dedup ? A.s_theta[kk] : 0.0;
+            tq[u] = dedup ? theta_of(A, kk, lift) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1080,7 +1092,7 @@ __global__ void __launch_bounds__(256) tail_kernel(EdgeArgs A) {
             const double2 r1 = A.s_rec1[p], r2 = A.s_rec2[p];
             SRow          q;
             q.cs = r1.x, q.sn = r1.y, q.coth = r2.x, q.rci = fmul(A.cosh_R, r2.y), q.id = A.s_id[p], q.pad = 0;
-            const double             theta = A.s_theta[p];
+            const double             theta = theta_of(A, p, lift_from(A, Aa));
             const unsigned long long srcm  = ~A.dense_mask[a];
             for (int j = a; j < A.count; ++j) {
                 const AnnulusDev& Aj = A.ann[j];
@@ -1108,11 +1120,11 @@ __global__ void __launch_bounds__(256) tail_kernel(EdgeArgs A) {
                         if (p >= Aa.wrap) owned_range(A, Aj, lo, hi, g0, g1);
                         else g0 = Aj.wrap, g1 = lower_bound_owned(A, Aj, hi); // wrapped nodes
                     }
-                    if (g1 > g0) serial_range<MODE>(A, q, theta, own, g0, g1, acc);
+                    if (g1 > g0) serial_range<MODE>(A, q, theta, own, g0, g1, lift_from(A, Aj), acc);
                 }
                 if (!halo_req && Aj.end > Aj.halo && hi > A.s_lam[Aj.halo] && lo <= A.s_lam[Aj.end - 1]) {
                     const std::uint64_t h0 = lower_bound_halo(A, Aj, lo), h1 = lower_bound_halo(A, Aj, hi);
-                    if (h1 > h0) serial_range<MODE>(A, q, theta, own, h0, h1, acc);
+                    if (h1 > h0) serial_range<MODE>(A, q, theta, own, h0, h1, lift_from(A, Aj), acc);
                 }
                 ann_add<MODE != 0>(SA, j, acc.edges - e0, acc.comps - c0);
             }
@@ -1325,7 +1337,7 @@ __global__ void req_gather_kernel(EdgeArgs A) {
         const std::uint64_t p = A.ann[a].off + (u - A.req_off[a]);
         r1 = A.s_rec1[p], r2 = A.s_rec2[p];
         const double lam = A.s_lam[p];
-        ax = make_double4(lam, A.s_beta[p], A.s_hw[p], A.s_theta[p]);
+        ax = make_double4(lam, A.s_beta[p], A.s_hw[p], theta_of(A, p, lift_from(A, A.ann[a])));
         id = A.s_id[p];
     }
     A.g_rec[2 * s]     = r1;
@@ -1364,26 +1376,25 @@ __global__ void __launch_bounds__(256) deferred_kernel(EdgeArgs A) {
         SRow          q;
         q.cs = q1.x, q.sn = q1.y, q.coth = q2.x, q.rci = q2.y, q.id = A.g_id[E.x], q.pad = 0;
         const double theta = A.g_aux[E.x].w;
+        int          j     = A.first_streaming; // the range's annulus: the one whose extended block holds node E.y
+        for (int base = 0; base < A.count; base += 32) {
+            const int      a = base + lane;
+            const unsigned m = __ballot_sync(kFull, a < A.count && a >= A.first_streaming && A.ann[a].off <= E.y);
+            if (m) j = base + 31 - __clz(m);
+        }
+        const std::uint64_t lift = lift_from(A, A.ann[j]);
         for (std::uint64_t k = E.y + std::uint64_t(lane); k < E.z; k += 32) {
             const unsigned long long nid = A.s_id[k];
             bool                     in  = true;
             if (E.w) {
-                const double tq = A.s_theta[k];
+                const double tq = theta_of(A, k, lift);
                 in              = nid != q.id && (theta < tq || (theta == tq && q.id < nid));
             }
             if (!in) continue;
             acc.comps += 1;
             count_edge<MODE>(A, edge_test(q.cs, q.sn, q.coth, q.rci, A.s_rec1[k], A.s_rec2[k]), q.id, nid, acc);
         }
-        { // the range's annulus: the one whose extended block holds node E.y
-            int j = A.first_streaming;
-            for (int base = 0; base < A.count; base += 32) {
-                const int      a = base + lane;
-                const unsigned m = __ballot_sync(kFull, a < A.count && a >= A.first_streaming && A.ann[a].off <= E.y);
-                if (m) j = base + 31 - __clz(m);
-            }
-            ann_add<MODE != 0>(SA, j, acc.edges - e0, acc.comps - c0);
-        }
+        ann_add<MODE != 0>(SA, j, acc.edges - e0, acc.comps - c0);
     }
     flush(acc, A, 1, lane);
     __syncthreads();
