@@ -142,7 +142,7 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 // Fill a cell-start table: entries (kp, k] = i.  The tail after the last
 // point, (k_last, ncells] = end, is filled in parallel by cell_tail_kernel.
 __device__ __forceinline__ void cell_fill(std::uint64_t* tab, std::int64_t kp, std::uint32_t k, std::uint64_t i) {
-    for (std::int64_t c = kp + 1; c <= std::int64_t(k); ++c) tab[c] = i;
+    for (std::uint32_t c = std::uint32_t(kp + 1); c <= k; ++c) tab[c] = i; // kp >= -1: kp + 1 >= 0
 }
 
 // ---------------------------------------------------------------- sort ---
