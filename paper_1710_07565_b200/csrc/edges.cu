@@ -180,14 +180,16 @@ __global__ void __launch_bounds__(256, RHG_RANK_MINB) beta_cells_kernel(EdgeArgs
         hwbits     = static_cast<unsigned long long>(__double_as_longlong(hi)); // hw >= +0
         A.lam_tmp[i] = GEN ? fadd(bi, hi) : A.rec0[i].x; // engine-frame lambda, read by rank_kernel
     }
-    __shared__ unsigned long long wmax[8]; // one atomic per block (all its points share the annulus)
-    const unsigned long long m = warp_max_u64(hwbits);
-    if (lane == 0) wmax[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long b = 0;
-        for (int w = 0; w < int(blockDim.x >> 5); ++w) b = wmax[w] > b ? wmax[w] : b;
-        if (b) atomicMax(&A.dmax_bits[j], b);
+    if constexpr (!GEN) { // same-points runs: the annulus's largest uploaded half-width, measured
+        __shared__ unsigned long long wmax[8]; // one atomic per block (all its points share the annulus)
+        const unsigned long long m = warp_max_u64(hwbits);
+        if (lane == 0) wmax[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long b = 0;
+            for (int w = 0; w < int(blockDim.x >> 5); ++w) b = wmax[w] > b ? wmax[w] : b;
+            if (b) atomicMax(&A.dmax_bits[j], b);
+        }
     }
 }
 
@@ -249,7 +251,11 @@ __global__ void __launch_bounds__(256, RHG_RANK_MINB) rank_kernel(EdgeArgs A) {
     const bool          hb = i >= J.halo;
     const std::uint64_t bs = hb ? J.halo : J.off, be = hb ? J.end : J.halo;
     const double        li = A.lam_tmp[i];
-    const double        dm = __longlong_as_double(static_cast<long long>(A.dmax_bits[j]));
+    // the annulus's largest half-width: in generate mode the host bound at its lower radius
+    // (half-widths fall with the radius; hbound carries a 1e-6 relative margin over the device's
+    // rounding), in same-points runs the measured maximum
+    const double        dm = GEN ? A.hbound[std::size_t(j) * A.count + j]
+                                 : __longlong_as_double(static_cast<long long>(A.dmax_bits[j]));
     std::uint64_t       k0 = A.cellstart[J.cell_off + cellf(J, fsub(fsub(li, dm), 1e-12))];
     std::uint64_t       k1 = A.cellstart[J.cell_off + cellf(J, li) + 1];
     k0 = k0 < bs ? bs : k0;
