@@ -30,8 +30,9 @@
  * Every call returns RHG_OK (0) or an error code; rhg_last_error() gives the
  * thread-local message.  The reference's std::invalid_argument maps to
  * RHG_INVALID_ARGUMENT, std::logic_error (sweep invariants) to RHG_INVARIANT.
- * A context owns one CUDA device, one stream and its device buffers; it is
- * not re-entrant.  There is no CPU fallback: without a usable sm_100 device
+ * A context owns one CUDA device, its streams (five, ordered by events: DESIGN.md
+ * section 2) and its device buffers; it is not re-entrant (one call at a time per
+ * context).  There is no CPU fallback: without a usable sm_100 device
  * rhg_create fails with RHG_CUDA.
  */
 #ifndef RHG_B200_H
