@@ -869,6 +869,13 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     }
     e.ann_blk = t.ann_blk;
     e.gen = gen ? 1 : 0;
+    { // the rank window holds ~ the average degree's worth of points: below ~100 the galloping
+      // searches beat the beta-cell pass (measured cfg4 35.1 -> 33.5 ms; cfg3 at d = 256 22.1 -> 24.0)
+        const double q    = (pl.L.alpha - 0.5) / pl.L.alpha;
+        const double dbar = std::exp(-0.5 * (pl.L.R - 2.0 * std::log(double(pl.L.n)))) / (kPi / 2.0 * q * q);
+        const char*  rg   = std::getenv("RHG_RANK_GALLOP"); // A/B: 0 / 1 force
+        e.rank_gallop     = gen && (rg ? rg[0] == '1' : dbar < 100.0) ? 1 : 0;
+    }
     e.mark = timeline_of(ctx);
     // Two waves when the sampler split its chains (generate mode): wave 1 = every annulus below
     // pl.wave_j (sort phase, dense prep, rows / node tiles / slabs of those targets, the global

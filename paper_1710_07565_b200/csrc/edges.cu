@@ -250,19 +250,54 @@ __global__ void __launch_bounds__(256, RHG_RANK_MINB) rank_kernel(EdgeArgs A) {
     if (i >= J.end) return;
     const bool          hb = i >= J.halo;
     const std::uint64_t bs = hb ? J.halo : J.off, be = hb ? J.end : J.halo;
-    const double        li = A.lam_tmp[i];
     // the annulus's largest half-width: in generate mode the host bound at its lower radius
     // (half-widths fall with the radius; hbound carries a 1e-6 relative margin over the device's
     // rounding), in same-points runs the measured maximum
     const double        dm = GEN ? A.hbound[std::size_t(j) * A.count + j]
                                  : __longlong_as_double(static_cast<long long>(A.dmax_bits[j]));
-    std::uint64_t       k0 = A.cellstart[J.cell_off + cellf(J, fsub(fsub(li, dm), 1e-12))];
-    std::uint64_t       k1 = A.cellstart[J.cell_off + cellf(J, li) + 1];
-    k0 = k0 < bs ? bs : k0;
-    k1 = k1 > be ? be : k1;
+    std::uint64_t       k0, k1;
+    double              li;
+    if (GEN && A.rank_gallop) {
+        // no beta-cell table: the window's ends by galloping searches over the block's sorted
+        // frame betas from i itself (the window holds ~d points), lambdas computed in place
+        li = fadd(frame_beta<true>(A, J, i), A.hw[i]);
+        const double  lo = fsub(fsub(li, dm), 1e-12);
+        std::uint64_t h = i, l = bs, step = 1; // beta(h) >= lo; find the first index >= lo
+        for (;;) {
+            if (h - bs <= step) { l = bs; break; }
+            const std::uint64_t c = h - step;
+            if (frame_beta<true>(A, J, c) < lo) { l = c + 1; break; } // beta(c) < lo: the answer is in (c, h]
+            h = c, step <<= 1;
+        }
+        while (l < h) { // first index in [l, h] with beta >= lo (beta(h) >= lo)
+            const std::uint64_t mid = (l + h) >> 1;
+            if (frame_beta<true>(A, J, mid) < lo) l = mid + 1;
+            else h = mid;
+        }
+        k0 = l;
+        std::uint64_t a = i, b = be; step = 1; // beta(a) <= li; find the first index > a with beta > li
+        for (;;) {
+            const std::uint64_t c = a + step;
+            if (c >= be) { b = be; break; }
+            if (frame_beta<true>(A, J, c) > li) { b = c; break; }
+            a = c, step <<= 1;
+        }
+        while (a + 1 < b) { // beta(a) <= li < beta(b) (b = be: past the end)
+            const std::uint64_t mid = (a + b) >> 1;
+            if (frame_beta<true>(A, J, mid) > li) b = mid;
+            else a = mid;
+        }
+        k1 = b;
+    } else { // the beta-cell table and lambdas of beta_cells_kernel
+        li = A.lam_tmp[i];
+        k0 = A.cellstart[J.cell_off + cellf(J, fsub(fsub(li, dm), 1e-12))];
+        k1 = A.cellstart[J.cell_off + cellf(J, li) + 1];
+        k0 = k0 < bs ? bs : k0;
+        k1 = k1 > be ? be : k1;
+    }
     std::uint64_t rank = k0 - bs;
     for (std::uint64_t k = k0; k < k1; ++k) {
-        const double lk = A.lam_tmp[k];
+        const double lk = GEN && A.rank_gallop ? fadd(frame_beta<true>(A, J, k), A.hw[k]) : A.lam_tmp[k];
         rank += (lk < li) || (lk == li && k < i);
     }
     // the point goes straight to its sorted slot (measured cfg2: rank 0.20 + scatter 0.31 ms
@@ -274,6 +309,12 @@ __global__ void __launch_bounds__(256, RHG_RANK_MINB) rank_kernel(EdgeArgs A) {
 // Lambda-cell starts of every owned block, and the first owned index with
 // lambda >= 2pi (wrapped points: theta = lambda - 2pi there).
 __global__ void __launch_bounds__(256) lambda_cells_kernel(EdgeArgs A) {
+    if (blockIdx.x == 0 && A.blk0 == 0 && A.gen && A.rank_gallop && int(threadIdx.x) < A.count &&
+        int(threadIdx.x) >= A.first_streaming) {
+        const AnnulusDev& E = A.ann[threadIdx.x]; // empty owned blocks: [off, off] (beta_cells does it otherwise)
+        if (E.halo == E.off)
+            for (std::uint32_t k = 0; k <= E.ncells; ++k) A.lcellstart[E.cell_off + k] = E.off;
+    }
     std::uint64_t i;
     const int     j = block_annulus(A, i);
     AnnulusDev&   J = A.ann_rw[j];
@@ -1915,16 +1956,22 @@ void launch_cell_index(const EdgeArgs& a0, std::uint32_t blk_begin, std::uint32_
     const std::uint32_t nblocks = blk_end - blk_begin;
     const unsigned      g = unsigned(nblocks ? nblocks : 1); // >= 1: block 0 of wave 1 initialises empty annuli
     const dim3          tails(64, unsigned(j_end - j_begin));
-    if (gen) beta_cells_kernel<true><<<g, 256, 0, st>>>(a);
-    else beta_cells_kernel<false><<<g, 256, 0, st>>>(a);
-    cell_tail_kernel<<<tails, 256, 0, st>>>(a, 0);
-    *launches += 2;
+    const bool gallop = gen && a.rank_gallop;
+    if (!gallop) { // galloping ranks search the sorted betas themselves (rank_kernel)
+        if (gen) beta_cells_kernel<true><<<g, 256, 0, st>>>(a);
+        else beta_cells_kernel<false><<<g, 256, 0, st>>>(a);
+        cell_tail_kernel<<<tails, 256, 0, st>>>(a, 0);
+        *launches += 2;
+    }
     if (nblocks) {
         if (gen) rank_kernel<true><<<g, 256, 0, st>>>(a);
         else rank_kernel<false><<<g, 256, 0, st>>>(a);
+        ++*launches;
+    }
+    if (nblocks || gallop) { // galloping: block 0 of wave 1 also initialises the empty annuli's tables
         lambda_cells_kernel<<<g, 256, 0, st>>>(a);
         cell_tail_kernel<<<tails, 256, 0, st>>>(a, 1);
-        *launches += 3;
+        *launches += 2;
     }
     a0.mark("sort_phase", st);
 }

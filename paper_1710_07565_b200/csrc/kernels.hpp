@@ -104,6 +104,7 @@ struct EdgeArgs {
     std::uint64_t     glob_tile_warps = 0;
     const std::uint32_t* ann_blk = nullptr; // [count + 1] prefix of 256-point blocks per streaming annulus
     unsigned long long* dmax_bits = nullptr; // per annulus, max half-width (bits)
+    int               rank_gallop = 0;      // generate mode, small windows: rank by galloping (no beta cells)
     double            cosh_R = 1.0;
     double            chunk0_upper = 0.0; // chunk_upper_bound(0, P)
     int               lift_part = 0;      // shard owns engine P-1 (halo = lifted chunk 0)
