@@ -242,7 +242,7 @@ __device__ __forceinline__ std::uint64_t lift_from(const EdgeArgs& A, const Annu
 // (lambda, id).  Only points whose beta lies in [lambda_i - dmax, lambda_i]
 // can compare either way: everything before that window is smaller
 // (lambda <= beta + dmax), everything after is larger (lambda >= beta).
-template <bool GEN>
+template <bool GEN, bool GALLOP = false>
 __global__ void __launch_bounds__(256, RHG_RANK_MINB) rank_kernel(EdgeArgs A) {
     std::uint64_t       i;
     const int           j = block_annulus(A, i);
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256, RHG_RANK_MINB) rank_kernel(EdgeArgs A) {
                                  : __longlong_as_double(static_cast<long long>(A.dmax_bits[j]));
     std::uint64_t       k0, k1;
     double              li;
-    if (GEN && A.rank_gallop) {
+    if constexpr (GALLOP) {
         // no beta-cell table: the window's ends by galloping searches over the block's sorted
         // frame betas from i itself (the window holds ~d points), lambdas computed in place
         li = fadd(frame_beta<true>(A, J, i), A.hw[i]);
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(256, RHG_RANK_MINB) rank_kernel(EdgeArgs A) {
     }
     std::uint64_t rank = k0 - bs;
     for (std::uint64_t k = k0; k < k1; ++k) {
-        const double lk = GEN && A.rank_gallop ? fadd(frame_beta<true>(A, J, k), A.hw[k]) : A.lam_tmp[k];
+        const double lk = GALLOP ? fadd(frame_beta<true>(A, J, k), A.hw[k]) : A.lam_tmp[k];
         rank += (lk < li) || (lk == li && k < i);
     }
     // the point goes straight to its sorted slot (measured cfg2: rank 0.20 + scatter 0.31 ms
@@ -1964,7 +1964,8 @@ void launch_cell_index(const EdgeArgs& a0, std::uint32_t blk_begin, std::uint32_
         *launches += 2;
     }
     if (nblocks) {
-        if (gen) rank_kernel<true><<<g, 256, 0, st>>>(a);
+        if (gallop) rank_kernel<true, true><<<g, 256, 0, st>>>(a);
+        else if (gen) rank_kernel<true><<<g, 256, 0, st>>>(a);
         else rank_kernel<false><<<g, 256, 0, st>>>(a);
         ++*launches;
     }

@@ -67,6 +67,9 @@ __device__ __forceinline__ void mt_twist_to(const std::uint64_t* __restrict__ A,
 #define RHG_MT_THREADS 320 // measured cfg2: 160 -> 4.12 ms/step, 320 -> 4.07
 #endif
 constexpr int kMtThreads = RHG_MT_THREADS; // >= 156: one state word per thread and twist phase
+// radius streams from which mt_radial_kernel runs (measured cfg3 22.13 -> 22.02 ms, cfg4 33.55 ->
+// 33.20, cfg5 155.9 -> 154.1; cfg2's 832 long streams: 3.20 -> 3.58 fused)
+constexpr int kFusedRadialJobs = 4096;
 
 // One CTA per (stream, {angles, radii}): thread 0 seeds ([rand.predef]
 // seeding recurrence, serial by definition); then per 312-word block the
@@ -144,6 +147,21 @@ __device__ __forceinline__ int pseg_find(const std::uint64_t* __restrict__ pseg,
     }
     return lo;
 }
+// The radius-only attributes of one point from its radius uniform u (partition.hpp:64-70,
+// sweep.hpp:121-134).
+__device__ __forceinline__ void radial_point(const AnnulusDev& A, double alpha, double u, double& hw, double2& rec2,
+                                             double& r) {
+    const double c = fadd(A.cal, fmul(u, fsub(A.cau, A.cal)));
+    r              = __ddiv_rn(gl::gl_acosh(c < 1.0 ? 1.0 : c), alpha);
+    r              = r > 1e-12 ? r : 1e-12;
+    const double ex   = gl::gl_exp(r);
+    const double mex  = __ddiv_rn(1.0, ex);
+    const double sh   = fmul(0.5, fsub(ex, mex));
+    const double coth = __ddiv_rn(fmul(0.5, fadd(ex, mex)), sh);
+    const double inv  = __ddiv_rn(1.0, sh);
+    hw                = A.lower > 0.0 ? request_half_width(coth, inv, A.coth_lower, A.cris) : kPiD;
+    rec2              = make_double2(coth, inv);
+}
 __global__ void point_radial_kernel(const std::uint64_t* __restrict__ pseg, int nseg, const AnnulusDev* __restrict__ ann,
                                     double alpha, std::uint64_t first, std::uint64_t total, double* __restrict__ hw_out,
                                     double2* __restrict__ rec2, double* __restrict__ r_out) {
@@ -157,20 +175,69 @@ __global__ void point_radial_kernel(const std::uint64_t* __restrict__ pseg, int 
     }
     __syncthreads();
     if (i >= total) return;
-    const int         a = i < s_end ? s_a : int(pseg[pseg_find(pseg, nseg, i)] & 0xffu);
-    const AnnulusDev& A = ann[a];
-    const double      u = hw_out[i];
-    const double      c = fadd(A.cal, fmul(u, fsub(A.cau, A.cal)));
-    double            r = __ddiv_rn(gl::gl_acosh(c < 1.0 ? 1.0 : c), alpha);
-    r                   = r > 1e-12 ? r : 1e-12;
-    const double ex   = gl::gl_exp(r);
-    const double mex  = __ddiv_rn(1.0, ex);
-    const double sh   = fmul(0.5, fsub(ex, mex));
-    const double coth = __ddiv_rn(fmul(0.5, fadd(ex, mex)), sh);
-    const double inv  = __ddiv_rn(1.0, sh);
-    hw_out[i]         = A.lower > 0.0 ? request_half_width(coth, inv, A.coth_lower, A.cris) : kPiD;
-    rec2[i]           = make_double2(coth, inv);
+    const int a = i < s_end ? s_a : int(pseg[pseg_find(pseg, nseg, i)] & 0xffu);
+    double    hw, r;
+    double2   q;
+    radial_point(ann[a], alpha, hw_out[i], hw, q, r);
+    hw_out[i] = hw;
+    rec2[i]   = q;
     if (r_out) r_out[i] = r;
+}
+
+// The radius side of one stream in one CTA for many short streams (small average degree, large
+// P): mt_uniforms_kernel's radius stream (seed {4, annulus, chunk}) with each tempered block turned
+// straight into the radius attributes, so the uniforms never go through HBM and the attributes'
+// FP64 work overlaps other streams' twists (few long streams leave it latency-bound: cfg2).
+__global__ void __launch_bounds__(kMtThreads) mt_radial_kernel(const StreamJob* __restrict__ jobs, int njobs,
+                                                               const AnnulusDev* __restrict__ ann, double alpha,
+                                                               double* __restrict__ hw_out, double2* __restrict__ rec2,
+                                                               double* __restrict__ r_out, std::uint64_t seed) {
+    __shared__ std::uint64_t st[2][kMtN];
+    const int t = threadIdx.x;
+    if (int(blockIdx.x) >= njobs) return;
+    const StreamJob&    J = jobs[blockIdx.x];
+    const std::uint64_t n = J.count;
+    if (n == 0) return;
+    const AnnulusDev& A = ann[J.annulus];
+    if (t == 0) {
+        std::uint64_t x = stream_seed(seed, 4, J.annulus, J.chunk); // kPhaseRadii
+        st[0][0]        = x;
+        for (int i = 1; i < kMtN; ++i) {
+            x        = 6364136223846793005ull * (x ^ (x >> 62)) + std::uint64_t(i);
+            st[0][i] = x;
+        }
+    }
+    __syncthreads();
+    const std::uint64_t nblk = (n + kMtN - 1) / kMtN;
+    for (std::uint64_t k = 0; k <= nblk; ++k) {
+        const std::uint64_t* S = st[k & 1];       // the state after k twists (block k - 1)
+        std::uint64_t*       B = st[(k + 1) & 1]; // block k
+        std::uint64_t        w = 0, idx = 0;
+        bool                 have = false;
+        if (k > 0) { // this thread's word of block k - 1 (read before the state is rewritten)
+            idx  = (k - 1) * kMtN + std::uint64_t(t);
+            have = t < kMtN && idx < n;
+            if (have) w = S[t];
+        }
+        if (k < nblk) {
+            if (t < kMtN - kMtM) B[t] = mt_mix(S[t], S[t + 1], S[t + kMtM]);
+            __syncthreads();
+            if (t < kMtN - kMtM) {
+                const int i = kMtN - kMtM + t;
+                B[i] = i < kMtN - 1 ? mt_mix(S[i], S[i + 1], B[t]) : mt_mix(S[kMtN - 1], B[0], B[kMtM - 1]);
+            }
+        }
+        __syncthreads();
+        if (have) {
+            double  hw, r;
+            double2 q;
+            radial_point(A, alpha, double(mt_temper(w) >> 11) * 0x1.0p-53, hw, q, r);
+            const std::uint64_t i = J.out_off + idx;
+            hw_out[i] = hw;
+            rec2[i]   = q;
+            if (r_out) r_out[i] = r;
+        }
+    }
 }
 
 // The whole angle side of one chain bin in one CTA (rng.hpp:58-69 + 209-244):
@@ -372,16 +439,24 @@ void launch_sampler(const SamplerArgs& S, cudaStream_t st, std::uint64_t* launch
         S.mark("global_points", S.glob);
         *launches += 4;
     }
-    mt_uniforms_kernel<<<njs, kMtThreads, 0, side>>>(S.jobs, njs, S.beta, S.hw, 2, S.seed);
-    S.mark("mt_radii", side);
     // the radius attributes run beside the angle side (measured at cfg2: serialising them after
     // the wave-1 chains is slower — the wave-1 sort then waits for the whole radius side — and
-    // so is splitting them by wave: the GPU is saturated either way)
-    const std::uint64_t rad_end = gsplit ? S.angular_from : S.total;
-    point_radial_kernel<<<unsigned((rad_end + 255) / 256), 256, 0, side>>>(S.pseg, S.npseg, S.ann, S.alpha, 0, rad_end,
-                                                                          S.hw, S.rec2, S.r_out);
+    // so is splitting them by wave: the GPU is saturated either way). Many short streams (large P):
+    // uniforms and attributes fused per stream (RHG_MT_RADIAL=0 / 1 forces either)
+    const char* fr    = std::getenv("RHG_MT_RADIAL");
+    const bool  fused = fr ? fr[0] == '1' : njs >= kFusedRadialJobs;
+    if (fused) {
+        mt_radial_kernel<<<njs, kMtThreads, 0, side>>>(S.jobs, njs, S.ann, S.alpha, S.hw, S.rec2, S.r_out, S.seed);
+        *launches += 1;
+    } else {
+        mt_uniforms_kernel<<<njs, kMtThreads, 0, side>>>(S.jobs, njs, S.beta, S.hw, 2, S.seed);
+        S.mark("mt_radii", side);
+        const std::uint64_t rad_end = gsplit ? S.angular_from : S.total;
+        point_radial_kernel<<<unsigned((rad_end + 255) / 256), 256, 0, side>>>(S.pseg, S.npseg, S.ann, S.alpha, 0,
+                                                                              rad_end, S.hw, S.rec2, S.r_out);
+        *launches += 2;
+    }
     S.mark("radial", side);
-    *launches += 2;
     const int nbw = gsplit ? S.chain_bins_g : 0; // the main stream's wave-1 bins
     if (nb1 > nbw) {
         angle_side_kernel<<<nb1 - nbw, 32 * kAngWarps, 0, st>>>(S.jobs, S.chain_bins + nbw, nb1 - nbw, S.job_order,
