@@ -255,50 +255,42 @@ __global__ void __launch_bounds__(256, RHG_RANK_MINB) rank_kernel(EdgeArgs A) {
     // rounding), in same-points runs the measured maximum
     const double        dm = GEN ? A.hbound[std::size_t(j) * A.count + j]
                                  : __longlong_as_double(static_cast<long long>(A.dmax_bits[j]));
-    std::uint64_t       k0, k1;
+    std::uint64_t       rank;
     double              li;
     if constexpr (GALLOP) {
-        // no beta-cell table: the window's ends by galloping searches over the block's sorted
-        // frame betas from i itself (the window holds ~d points), lambdas computed in place
-        li = fadd(frame_beta<true>(A, J, i), A.hw[i]);
-        const double  lo = fsub(fsub(li, dm), 1e-12);
-        std::uint64_t h = i, l = bs, step = 1; // beta(h) >= lo; find the first index >= lo
-        for (;;) {
-            if (h - bs <= step) { l = bs; break; }
-            const std::uint64_t c = h - step;
-            if (frame_beta<true>(A, J, c) < lo) { l = c + 1; break; } // beta(c) < lo: the answer is in (c, h]
-            h = c, step <<= 1;
+        // no beta-cell table: walk the window outwards from i itself (it holds ~d points, and
+        // every one of them is compared anyway), lambdas computed in place; the block's points
+        // are all lifted or none (the lifted halo block), so the frame shift is one flag
+        const bool lift = A.lift_part && hb;
+        auto       fb   = [&](std::uint64_t k) {
+            const double b = A.beta[k];
+            return lift ? fadd(b, kTwoPiD) : b;
+        };
+        li              = fadd(fb(i), A.hw[i]);
+        const double lo = fsub(fsub(li, dm), 1e-12);
+        rank            = 0;
+        for (std::uint64_t k = i; k > bs;) { // beta(k) < lo: k and everything before it is smaller
+            --k;
+            const double b = fb(k);
+            if (b < lo) { rank += k - bs + 1; break; }
+            rank += fadd(b, A.hw[k]) <= li; // k < i: ties count
         }
-        while (l < h) { // first index in [l, h] with beta >= lo (beta(h) >= lo)
-            const std::uint64_t mid = (l + h) >> 1;
-            if (frame_beta<true>(A, J, mid) < lo) l = mid + 1;
-            else h = mid;
+        for (std::uint64_t k = i + 1; k < be; ++k) { // beta(k) > li: k and everything after is larger
+            const double b = fb(k);
+            if (b > li) break;
+            rank += fadd(b, A.hw[k]) < li;
         }
-        k0 = l;
-        std::uint64_t a = i, b = be; step = 1; // beta(a) <= li; find the first index > a with beta > li
-        for (;;) {
-            const std::uint64_t c = a + step;
-            if (c >= be) { b = be; break; }
-            if (frame_beta<true>(A, J, c) > li) { b = c; break; }
-            a = c, step <<= 1;
-        }
-        while (a + 1 < b) { // beta(a) <= li < beta(b) (b = be: past the end)
-            const std::uint64_t mid = (a + b) >> 1;
-            if (frame_beta<true>(A, J, mid) > li) b = mid;
-            else a = mid;
-        }
-        k1 = b;
     } else { // the beta-cell table and lambdas of beta_cells_kernel
-        li = A.lam_tmp[i];
-        k0 = A.cellstart[J.cell_off + cellf(J, fsub(fsub(li, dm), 1e-12))];
-        k1 = A.cellstart[J.cell_off + cellf(J, li) + 1];
-        k0 = k0 < bs ? bs : k0;
-        k1 = k1 > be ? be : k1;
-    }
-    std::uint64_t rank = k0 - bs;
-    for (std::uint64_t k = k0; k < k1; ++k) {
-        const double lk = GALLOP ? fadd(frame_beta<true>(A, J, k), A.hw[k]) : A.lam_tmp[k];
-        rank += (lk < li) || (lk == li && k < i);
+        li               = A.lam_tmp[i];
+        std::uint64_t k0 = A.cellstart[J.cell_off + cellf(J, fsub(fsub(li, dm), 1e-12))];
+        std::uint64_t k1 = A.cellstart[J.cell_off + cellf(J, li) + 1];
+        k0               = k0 < bs ? bs : k0;
+        k1               = k1 > be ? be : k1;
+        rank             = k0 - bs;
+        for (std::uint64_t k = k0; k < k1; ++k) {
+            const double lk = A.lam_tmp[k];
+            rank += (lk < li) || (lk == li && k < i);
+        }
     }
     // the point goes straight to its sorted slot (measured cfg2: rank 0.20 + scatter 0.31 ms
     // as two kernels through a permutation array -> 0.41 ms fused)
@@ -1957,7 +1949,7 @@ void launch_cell_index(const EdgeArgs& a0, std::uint32_t blk_begin, std::uint32_
     const unsigned      g = unsigned(nblocks ? nblocks : 1); // >= 1: block 0 of wave 1 initialises empty annuli
     const dim3          tails(64, unsigned(j_end - j_begin));
     const bool gallop = gen && a.rank_gallop;
-    if (!gallop) { // galloping ranks search the sorted betas themselves (rank_kernel)
+    if (!gallop) { // walking ranks scan the sorted betas around each point themselves (rank_kernel)
         if (gen) beta_cells_kernel<true><<<g, 256, 0, st>>>(a);
         else beta_cells_kernel<false><<<g, 256, 0, st>>>(a);
         cell_tail_kernel<<<tails, 256, 0, st>>>(a, 0);
