@@ -891,10 +891,13 @@ void run_edges(rhg_ctx* ctx, const Plan& pl, const Tables& t, rhg_run_stats* out
     launch_cell_index(e, pl.ann_blk[fs], pl.ann_blk[jw], int(fs), int(jw), gen, ctx->stream, launches);
     if (split) { // wave 2's sort phase right after its chains, beside wave 1 (needs the radius side
                  // and this call's zeroed counters / dmax table from the main stream)
-        // on ctx->side (normal priority; measured cfg2 3.41 -> 3.35 ms): on the high-priority late
-        // stream it held back wave 1's edge work. RHG_SORT2_SIDE=0: the late stream (A/B)
+        // small graphs: on ctx->side (normal priority; measured cfg2 3.41 -> 3.35 ms): on the
+        // high-priority late stream it held back wave 1's edge work; from n = 2^25 on the late
+        // stream (wave 2 then starts earlier: cfg4 32.36 -> 32.03 ms, cfg5 148.2 -> 146.8, cfg3
+        // 22.03 -> 21.97; cfg2 3.08 -> 3.12). RHG_SORT2_SIDE=0 / 1 forces the late / side stream (A/B)
         const char*  s2s = std::getenv("RHG_SORT2_SIDE");
-        cudaStream_t s2  = s2s && s2s[0] == '0' ? ctx->late : ctx->side;
+        const bool   s2l = s2s ? s2s[0] == '0' : pl.L.n >= (std::uint64_t(1) << 25);
+        cudaStream_t s2  = s2l ? ctx->late : ctx->side;
         CK(cudaEventRecord(ctx->fork, ctx->stream));
         CK(cudaStreamWaitEvent(s2, ctx->fork, 0));
         CK(cudaStreamWaitEvent(s2, ctx->join, 0));
