@@ -487,6 +487,11 @@ __device__ __forceinline__ float4 lds128(unsigned addr) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ uint4 lds128u(unsigned addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -533,7 +538,8 @@ constexpr float  kPreMaxDelta = 0.015625f;
 #define RHG_SLAB_DIRECT 8 // groups whose lanes have <= this many pairs each skip the flattening (measured 0 / 2 / 4 / 8 / 16 / 32: cfg4 slab 19.2 / 18.8 / 18.4 / 18.2 / 18.5 / 18.8 ms, cfg2 1.58 / 1.57 / 1.55 / 1.55 / 1.56 / 1.58)
 #endif
 constexpr int kSlabDirect = RHG_SLAB_DIRECT;
-constexpr double kPreMinS     = 4e-14; // groups whose windows give S below this skip the pre-filter
+constexpr double kPreMinS     = 4e-14;
+constexpr unsigned long long kCntOne = 1ull << 42; // packed edge count unit (flattened pair loop) // groups whose windows give S below this skip the pre-filter
 
 struct __align__(16) SlabRow32 { // one request with pairs in the slab (rows of a group are compacted)
     float         lamf;  // lambda_r - lam_first (float)
@@ -576,6 +582,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
     constexpr int kSlabThreads = NT;
     extern __shared__ __align__(16) unsigned char slab_raw[];
     constexpr bool           kR12 = MINB < 5; // exact-path node doubles in shared memory
+    constexpr bool           kLean = !kR12;   // the 40-register instance (register-saving code forms)
     SlabSmem<NT, kR12>&      S    = *reinterpret_cast<SlabSmem<NT, kR12>*>(slab_raw);
     const int                lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned long long sl   = A.slab_tab[A.slab0 + blockIdx.x]; // (j << 32) | slab index in j, angle order per wave
@@ -759,11 +766,23 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                 if (crow[mid].x > t) ho = mid;
                 else o = mid + 1;
             }
-            uint4  cr = crow[o];
-            float4 qr = S.nd[cr.w & 0x7fffffffu]; // (lamf, m, 1 / sinh, id offset) of the request
+            // 40-register instance (kLean): the request table's address in a register, and tau
+            // coefficients for the whole pass -- the requests lie inside the slab, |lamf| <= span, so the
+            // per-request bound ed(|lamf| + span) is at most ed(2 span) (a larger tau only sends more pairs
+            // to the exact predicate); recomputing them per request cost 14 divergent instructions on
+            // every request change there. The 64-register instance keeps per-request coefficients
+            // (measured: the lean form costs it 0.8 ms at cfg4).
+            unsigned cb = smem_addr(crow);
+            if constexpr (kLean) asm volatile("mov.u32 %0, %0;" : "+r"(cb));
+            auto   crow_at = [&](std::uint32_t r) {
+                if constexpr (kLean) return lds128u(cb + 16u * r);
+                else return crow[r];
+            };
+            uint4  cr = crow_at(o);
+            float4 qr = node_rec(cr.w & 0x7fffffffu); // (lamf, m, 1 / sinh, id offset) of the request
             float  e1f, c0f;
             auto   tau_coef = [&]() {
-                const float ed = 5.9604645e-8f * (fabsf(qr.x) + span) + 1.5e-15f;
+                const float ed = 5.9604645e-8f * ((kLean ? 2.0f * span : fabsf(qr.x) + span)) + 1.5e-15f;
                 e1f = 1.3f * ed + 3e-15f, c0f = 1.3f * ed * ed + 2e-15f;
             };
             tau_coef();
@@ -781,9 +800,9 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
             unsigned long long sum = 0;
             for (; t < te; ++t) {
                 if (t >= cr.x) { // next request (compacted: every entry has pairs)
-                    cr = crow[++o];
-                    qr = S.nd[cr.w & 0x7fffffffu];
-                    tau_coef();
+                    cr = crow_at(++o);
+                    qr = node_rec(cr.w & 0x7fffffffu);
+                    if constexpr (!kLean) tau_coef();
                 }
                 const std::uint32_t i  = cr.w & 0x7fffffffu;
                 const std::uint32_t k  = cr.y + t;
@@ -819,7 +838,11 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                         if (undecided) e = lhs > rhs;
                     }
                 }
-                if constexpr (MODE == 0) { // branch-free accumulation (the counters-only kernel)
+                if constexpr (MODE == 0 && kLean) { // counters-only kernel: the edge count rides in bits 42..
+                    // of the id sum (a thread runs <= 512 pairs here: id sums < 2^41), one predicated add
+                    const std::uint32_t nid = __float_as_uint(nd.w), qid = __float_as_uint(qr.w);
+                    if (e) sum += static_cast<unsigned long long>(nid + qid) + kCntOne;
+                } else if constexpr (MODE == 0) { // branch-free accumulation
                     const std::uint32_t nid = __float_as_uint(nd.w), qid = __float_as_uint(qr.w);
                     sum += e ? static_cast<unsigned long long>(nid + qid) : 0ull;
                     cnt += e;
@@ -830,6 +853,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                     if (MODE == 2) emit_edge(A, base_j + qid, base_j + nid);
                 }
             }
+            if constexpr (MODE == 0 && kLean) cnt = std::uint32_t(sum >> 42), sum &= kCntOne - 1;
             acc_e += cnt;
             acc_fp += sum + static_cast<unsigned long long>(cnt) * (2 * base_j);
         }
@@ -921,7 +945,53 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
         // its request in registers -- no prefix sum, row table or row search
         if (MODE != 3 && !(A.ablate & 2) && __reduce_max_sync(kFull, len) <= std::uint32_t(kSlabDirect)) {
             acc_c += len;
-            if (len) {
+            if (kLean && len) {
+                const unsigned long long idp = A.s_id[pc];
+                std::uint32_t            cnt = 0;
+                unsigned long long       sum = 0; // node-id offsets from base_j
+                // the exact predicate of request pc and node k; the request's doubles are re-read
+                // (L1/L2) rather than held across the loop: at the 40-register budget holding them
+                // made the compiler re-derive the float request terms on every pair
+                auto exact = [&](std::uint32_t k) {
+                    const double2 q1 = A.s_rec1[pc], q2 = A.s_rec2[pc];
+                    return edge_test(q1.x, q1.y, q2.x, fmul(A.cosh_R, q2.y), node_r1(k), node_r2(k));
+                };
+                auto count = [&](bool e, float ndw) {
+                    if constexpr (MODE == 0) { // the edge count rides in bits 42.. of the sum (<= 8 pairs)
+                        if (e) sum += static_cast<unsigned long long>(__float_as_uint(ndw)) + kCntOne;
+                    } else if (e) {
+                        const unsigned long long nid = base_j + __float_as_uint(ndw);
+                        sum += __float_as_uint(ndw), ++cnt;
+                        if (MODE == 1) atomicAdd(&A.degrees[idp], 1u), atomicAdd(&A.degrees[nid], 1u);
+                        if (MODE == 2) emit_edge(A, idp, nid);
+                    }
+                };
+                if (fp64) { // every pair exact (request doubles re-read: measured faster here, cfg2 3.10 -> 3.07 ms)
+                    for (std::uint32_t k = l0; k < l1; ++k) count(exact(k), node_rec(k).w);
+                } else {
+                    const float lamf = float(fsub(lam, lam_first));
+                    const float ed   = 5.9604645e-8f * (fabsf(lamf) + span) + 1.5e-15f;
+                    const float qm = float(fsub(r2.x, 1.0)), qr = float(fmul(A.cosh_R, r2.y));
+                    const float e1 = 1.3f * ed + 3e-15f, c0 = 1.3f * ed * ed + 2e-15f;
+                    for (std::uint32_t k = l0; k < l1; ++k) {
+                        const float4 nd  = node_rec(k);
+                        const float  df  = nd.x - lamf;
+                        const float  y2  = df * df;
+                        const float  Sv  = y2 * fmaf(y2, -1.0f / 24.0f, 0.5f);
+                        const float  P   = qr * nd.z;
+                        const float  M   = fmaf(qm, nd.y, qm + nd.y) + Sv;
+                        const float  D   = P - M;
+                        const float  tau = fmaf(fabsf(df), e1, fmaf(P + M, 1.4e-6f, c0));
+                        bool         e   = D > 0.0f;
+                        if (!(fabsf(D) > tau) || fabsf(df) > kPreMaxDelta) e = exact(k);
+                        count(e, nd.w);
+                    }
+                }
+                if constexpr (MODE == 0) cnt = std::uint32_t(sum >> 42), sum &= kCntOne - 1;
+                acc_e += cnt, acc_fp += sum + static_cast<unsigned long long>(cnt) * (base_j + idp);
+            }
+            // the 64-register instance: the request in registers (its base form measured faster there)
+            if (!kLean && len) {
                 const double2            r1  = A.s_rec1[pc];
                 const double             rci = fmul(A.cosh_R, r2.y);
                 const unsigned long long idp = A.s_id[pc];
@@ -1003,17 +1073,30 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                 if (rows[mid].incl > t) ho = mid;
                 else o = mid + 1;
             }
-            const float4* rf = reinterpret_cast<const float4*>(rows); // row o: rf[2 o] floats, ru[2 o + 1]
+            // row o: floats at rb + 32 o, words at rb + 32 o + 16. In the 40-register instance the warp's
+            // row-table address is kept in a register (opaque copy): re-deriving it on every row change
+            // (S2R SR_CgaCtaId + 8 instructions, divergent) cost 6 % of its instructions at cfg2
+            unsigned rb = smem_addr(rows);
+            if constexpr (kLean) asm volatile("mov.u32 %0, %0;" : "+r"(rb));
+            const float4* rf = reinterpret_cast<const float4*>(rows);
             const uint4*  ru = reinterpret_cast<const uint4*>(rows);
-            float4        q  = rf[2 * o];     // (lamf, m, rcif, e1)
-            uint4         u  = ru[2 * o + 1]; // (c0 bits, qoff, pad, incl)
+            auto row_f = [&](std::uint32_t r) {
+                if constexpr (kLean) return lds128(rb + 32u * r);
+                else return rf[2 * r];
+            };
+            auto row_u = [&](std::uint32_t r) {
+                if constexpr (kLean) return lds128u(rb + 32u * r + 16u);
+                else return ru[2 * r + 1];
+            };
+            float4        q  = row_f(o); // (lamf, m, rcif, e1)
+            uint4         u  = row_u(o); // (c0 bits, qoff, pad, incl)
             std::uint32_t cnt = 0;
             unsigned long long sum = 0;
             if (!fp64) {
                 for (; t < te; ++t) {
                     if (t >= u.w) { // next row
                         ++o;
-                        q = rf[2 * o], u = ru[2 * o + 1];
+                        q = row_f(o), u = row_u(o);
                     }
                     const std::uint32_t k  = u.z + t;
                     const float4        nd = node_rec(k);
@@ -1045,9 +1128,13 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                         e = edge_test(R.cs, R.sn, R.coth, R.rci, node_r1(k), node_r2(k));
                         if (A.dbg) atomicAdd(&A.dbg[17], 1ull);
                     }
-                    if constexpr (MODE == 0) { // branch-free accumulation (the counters-only kernel)
+                    if constexpr (MODE == 0 && kLean) { // counters-only kernel: the edge count rides in bits 42..
+                        // of the id sum (a lane runs <= 513 pairs of a group: id sums < 2^41), one predicated add
                         const std::uint32_t nid = __float_as_uint(nd.w);
-                        sum += e ? static_cast<unsigned long long>(nid + u.y) : 0ull; // < 2^32: a shard holds < 2^31 points
+                        if (e) sum += static_cast<unsigned long long>(nid + u.y) + kCntOne; // < 2^32: a shard holds < 2^31 points
+                    } else if constexpr (MODE == 0) { // branch-free accumulation
+                        const std::uint32_t nid = __float_as_uint(nd.w);
+                        sum += e ? static_cast<unsigned long long>(nid + u.y) : 0ull;
                         cnt += e;
                     } else if (e) {
                         const std::uint32_t nid = __float_as_uint(nd.w);
@@ -1059,6 +1146,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
                         if (MODE == 2) emit_edge(A, base_a + u.y, base_j + nid);
                     }
                 }
+                if constexpr (MODE == 0 && kLean) cnt = std::uint32_t(sum >> 42), sum &= kCntOne - 1;
             } else { // windows so narrow that the FP64 rounding noise dominates: exact predicate only
                 const double2* r64 = reinterpret_cast<const double2*>(rows64);
                 double2        q0 = r64[2 * o], q1 = r64[2 * o + 1]; // (cs, sn), (coth, rci)
