@@ -538,6 +538,10 @@ constexpr float  kPreMaxDelta = 0.015625f;
 #define RHG_SLAB_DIRECT 8 // groups whose lanes have <= this many pairs each skip the flattening (measured 0 / 2 / 4 / 8 / 16 / 32: cfg4 slab 19.2 / 18.8 / 18.4 / 18.2 / 18.5 / 18.8 ms, cfg2 1.58 / 1.57 / 1.55 / 1.55 / 1.56 / 1.58)
 #endif
 constexpr int kSlabDirect = RHG_SLAB_DIRECT;
+#ifndef RHG_SLAB_DIRECT_LEAN
+#define RHG_SLAB_DIRECT_LEAN 20 // the 40-register instance's cheaper direct loop (measured 8 / 12 / 16 / 20 / 28 / 40: cfg2 3.052 / 3.047 / 3.040 / 3.031 / 3.030 / 3.036 ms; cfg3 flat to 20, +0.1 % at 28)
+#endif
+constexpr int kSlabDirectLean = RHG_SLAB_DIRECT_LEAN;
 constexpr double kPreMinS     = 4e-14;
 constexpr unsigned long long kCntOne = 1ull << 42; // packed edge count unit (flattened pair loop) // groups whose windows give S below this skip the pre-filter
 
@@ -943,7 +947,7 @@ __global__ void __launch_bounds__(NT, MINB) slab_kernel(EdgeArgs A) {
         if (nz == 0) continue;
         // narrow windows (every lane <= kSlabDirect pairs): each lane tests its own pairs with
         // its request in registers -- no prefix sum, row table or row search
-        if (MODE != 3 && !(A.ablate & 2) && __reduce_max_sync(kFull, len) <= std::uint32_t(kSlabDirect)) {
+        if (MODE != 3 && !(A.ablate & 2) && __reduce_max_sync(kFull, len) <= std::uint32_t(kLean ? kSlabDirectLean : kSlabDirect)) {
             acc_c += len;
             if (kLean && len) {
                 const unsigned long long idp = A.s_id[pc];
