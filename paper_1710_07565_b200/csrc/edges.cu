@@ -1722,6 +1722,9 @@ __device__ __forceinline__ std::uint32_t gtheta_lb(const double* th, std::uint32
 // warp sweeps the entries (32-node slices outside an entry are skipped).
 // MINB: CTAs per SM the register budget targets (measured cfg2: wave 1's targets 0.40 ms at 2,
 // 0.43 at 3 with small spills; wave 2's outermost target 0.18 at 2, 0.15 at 3)
+#ifndef RHG_TILES_MINB2
+#define RHG_TILES_MINB2 3 // node tiles of wave 2 (narrow windows; measured 2 / 3: cfg2 3.045 / 3.030 ms, cfg4 32.37 / 31.99)
+#endif
 #ifndef RHG_TILES_MINB1
 #define RHG_TILES_MINB1 3 // node tiles of wave 1 (measured cfg2, dense engine alone: 2 -> 0.40 ms, 3 -> 0.43; beside
                           // the slab join on its own stream 3 is better: step 3.35 -> 3.28 ms at cfg2, cfg4 36.7 ->
@@ -2153,9 +2156,9 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
                 else if (mode == 1) glob_tiles_kernel<1, 4><<<g, 256, 0, st>>>(a);
                 else glob_tiles_kernel<0, 4><<<g, 256, 0, st>>>(a);
             }
-            else if (mode == 2) glob_tiles_kernel<2, 3><<<g, 256, 0, st>>>(a);
-            else if (mode == 1) glob_tiles_kernel<1, 3><<<g, 256, 0, st>>>(a);
-            else glob_tiles_kernel<0, 3><<<g, 256, 0, st>>>(a);
+            else if (mode == 2) glob_tiles_kernel<2, RHG_TILES_MINB2><<<g, 256, 0, st>>>(a);
+            else if (mode == 1) glob_tiles_kernel<1, RHG_TILES_MINB2><<<g, 256, 0, st>>>(a);
+            else glob_tiles_kernel<0, RHG_TILES_MINB2><<<g, 256, 0, st>>>(a);
             ++*launches;
             a.mark("tiles", st);
         }
