@@ -1722,6 +1722,9 @@ __device__ __forceinline__ std::uint32_t gtheta_lb(const double* th, std::uint32
 // warp sweeps the entries (32-node slices outside an entry are skipped).
 // MINB: CTAs per SM the register budget targets (measured cfg2: wave 1's targets 0.40 ms at 2,
 // 0.43 at 3 with small spills; wave 2's outermost target 0.18 at 2, 0.15 at 3)
+#ifndef RHG_TILES_MINB_WIDE
+#define RHG_TILES_MINB_WIDE 4 // node tiles for wide dense windows (average degree >= 128; measured 3 / 4 / 5: cfg3 22.08 / 21.73 / 25.53 ms)
+#endif
 #ifndef RHG_TILES_MINB2
 #define RHG_TILES_MINB2 3 // node tiles of wave 2 (narrow windows; measured 2 / 3: cfg2 3.045 / 3.030 ms, cfg4 32.37 / 31.99)
 #endif
@@ -2143,18 +2146,18 @@ void launch_edges(const EdgeArgs& a0, const EdgeWave& W, cudaStream_t st, std::u
         if (tw) {
             const unsigned g = unsigned((tw + 7) / 8);
             if (W.first_wave && W.dense_occ4) { // wave 1, wide windows: 4 CTAs/SM (64 registers)
-                if (mode == 2) glob_tiles_kernel<2, 4><<<g, 256, 0, st>>>(a);
-                else if (mode == 1) glob_tiles_kernel<1, 4><<<g, 256, 0, st>>>(a);
-                else glob_tiles_kernel<0, 4><<<g, 256, 0, st>>>(a);
+                if (mode == 2) glob_tiles_kernel<2, RHG_TILES_MINB_WIDE><<<g, 256, 0, st>>>(a);
+                else if (mode == 1) glob_tiles_kernel<1, RHG_TILES_MINB_WIDE><<<g, 256, 0, st>>>(a);
+                else glob_tiles_kernel<0, RHG_TILES_MINB_WIDE><<<g, 256, 0, st>>>(a);
             } else if (W.first_wave) { // wave 1
                 if (mode == 2) glob_tiles_kernel<2, RHG_TILES_MINB1><<<g, 256, 0, st>>>(a);
                 else if (mode == 1) glob_tiles_kernel<1, RHG_TILES_MINB1><<<g, 256, 0, st>>>(a);
                 else glob_tiles_kernel<0, RHG_TILES_MINB1><<<g, 256, 0, st>>>(a);
             }
             else if (W.dense_occ4) { // wave 2, wide windows
-                if (mode == 2) glob_tiles_kernel<2, 4><<<g, 256, 0, st>>>(a);
-                else if (mode == 1) glob_tiles_kernel<1, 4><<<g, 256, 0, st>>>(a);
-                else glob_tiles_kernel<0, 4><<<g, 256, 0, st>>>(a);
+                if (mode == 2) glob_tiles_kernel<2, RHG_TILES_MINB_WIDE><<<g, 256, 0, st>>>(a);
+                else if (mode == 1) glob_tiles_kernel<1, RHG_TILES_MINB_WIDE><<<g, 256, 0, st>>>(a);
+                else glob_tiles_kernel<0, RHG_TILES_MINB_WIDE><<<g, 256, 0, st>>>(a);
             }
             else if (mode == 2) glob_tiles_kernel<2, RHG_TILES_MINB2><<<g, 256, 0, st>>>(a);
             else if (mode == 1) glob_tiles_kernel<1, RHG_TILES_MINB2><<<g, 256, 0, st>>>(a);
