@@ -409,7 +409,10 @@ Plan make_plan_head(const Params& P, const rhg_shard* shard) {
     pl.wave_j = L.count;
     {
         const char*         wv = std::getenv("RHG_WAVE2_ANNULI"); // A/B switch: outer annuli in wave 2
+        // small average degree at >= 2^28 points (cfg4's weak-scaling family): four outer annuli
+        // (measured cfg4 2 / 3 / 4: 32.00 / 31.84 / 31.78 ms; cfg3 keeps two: 21.73 vs 21.77-22.03 with three)
         const std::uint32_t w2 = wv ? std::uint32_t(std::max(1, std::atoi(wv)))
+                                    : (L.n >= (std::uint64_t(1) << 28) && dbar_model < 8.0) ? kWave2Annuli + 3
                                     : (L.n >= (std::uint64_t(1) << 25) ? kWave2Annuli + 1 : kWave2Annuli);
         if (L.count >= L.first_streaming + 1 + w2 && pl.T > 0) {
             bool dense_src = false;
