@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kMtThreads) mt_radial_kernel(const StreamJob* 
 // of after two full-array kernels.  Same arithmetic, same order as the separate
 // mt_uniforms / point_pow / sorted_chain kernels.
 #ifndef RHG_ANG_WARPS
-#define RHG_ANG_WARPS 8 // measured: 6 -> 4.35 ms, 8 -> 4.31, 10 -> 4.34, 12 -> 4.34 (cfg2 step)
+#define RHG_ANG_WARPS 8 // measured: 6 -> 4.35 ms, 8 -> 4.31, 10 -> 4.34, 12 -> 4.34 (cfg2 step, round 1); round 2: 6 / 8 / 12 / 16 -> cfg4 32.10 / 31.77 / 33.66 / 36.02 ms
 #endif
 constexpr int kAngWarps = RHG_ANG_WARPS; // warp 0: chain, warp kMtWarp: MT, the others: pow factors
 #ifndef RHG_MT_WARP
